@@ -1,0 +1,141 @@
+"""CPU oracle for Self-Convolution block matching -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package. The product path
+(``paper_2006_13714_b200``) never imports it and shares no code with it.
+
+``oracle.c`` is the plain brute-force definition (Eq. 3, restricted
+to the window of footnote 2, channels summed as in Eq. 12,
+PAPER.md:540-547); see its header for the readings it follows. Pins:
+tests/test_oracle.py (hand-worked fixture, closed forms, invariants, exhaustive
+8x8 vs an independent numpy brute force, torch conv2d special case).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+U8, F32, F64 = 0, 1, 2
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc -O2 -fopenmp, no intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-std=c11",
+                               _SRC, "-o", _LIB, "-lm"])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        vp, i32p, dp = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double)
+        ci = ctypes.c_int
+        L.sco_bm_rows.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, vp, ci]
+        L.sco_bm.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, vp, ci]
+        L.sco_bm_dense.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, dp, ci]
+        L.sco_norm_map.argtypes = [vp, ci, ci, ci, ci, ci, dp]
+        L.sco_selfconv.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, dp]
+        L.sco_num_threads.restype = ci
+        _lib = L
+    return _lib
+
+
+def _dtype_code(a: np.ndarray) -> int:
+    if a.dtype == np.uint8:
+        return U8
+    if a.dtype == np.float32:
+        return F32
+    if a.dtype == np.float64:
+        return F64
+    raise TypeError(f"oracle: unsupported dtype {a.dtype}")
+
+
+def grid(H: int, W: int, b: int, s: int):
+    return (H - b) // s + 1, (W - b) // s + 1
+
+
+def bm(img: np.ndarray, b: int, s: int, Wn: int, K: int, *, images=None, rows=None,
+       nthreads: int = 0):
+    """Brute-force BM. img: [N, C, H, W] (or [C,H,W] / [H,W]) uint8/float32/float64.
+
+    Returns (idx int32 [n, refs, K], dist int32 (uint8 input) or float64 [n, refs, K]).
+    ``images=(i0, i1)`` and ``rows=(iy0, iy1)`` restrict to a subset (reference-grid rows).
+    """
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None, None]
+    elif a.ndim == 3:
+        a = a[None]
+    N, C, H, W = a.shape
+    ny, nx = grid(H, W, b, s)
+    i0, i1 = images if images is not None else (0, N)
+    r0, r1 = rows if rows is not None else (0, ny)
+    n = i1 - i0
+    refs = (r1 - r0) * nx
+    idx = np.empty((n, refs, K), dtype=np.int32)
+    code = _dtype_code(a)
+    dist = np.empty((n, refs, K), dtype=np.int32 if code == U8 else np.float64)
+    rc = lib().sco_bm_rows(a.ctypes.data, code, C, H, W, b, s, Wn, K, i0, i1, r0, r1,
+                           idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                           dist.ctypes.data, nthreads)
+    if rc != 0:
+        raise ValueError("oracle.bm: invalid arguments")
+    return idx, dist
+
+
+def bm_dense(img: np.ndarray, b: int, s: int, Wn: int, nthreads: int = 0) -> np.ndarray:
+    """Every window distance of one image [C,H,W]: [refs, Wn*Wn] float64, -1 where clipped."""
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None]
+    C, H, W = a.shape
+    ny, nx = grid(H, W, b, s)
+    out = np.empty((ny * nx, Wn * Wn), dtype=np.float64)
+    rc = lib().sco_bm_dense(a.ctypes.data, _dtype_code(a), C, H, W, b, s, Wn,
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), nthreads)
+    if rc != 0:
+        raise ValueError("oracle.bm_dense: invalid arguments")
+    return out
+
+
+def norm_map(img: np.ndarray, b: int) -> np.ndarray:
+    """h_X (.) h_X over valid positions, channels summed: [(H-b+1), (W-b+1)] float64."""
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None]
+    C, H, W = a.shape
+    out = np.empty((H - b + 1, W - b + 1), dtype=np.float64)
+    rc = lib().sco_norm_map(a.ctypes.data, _dtype_code(a), C, H, W, b,
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if rc != 0:
+        raise ValueError("oracle.norm_map: invalid arguments")
+    return out
+
+
+def selfconv(img: np.ndarray, b: int, ry: int, rx: int) -> np.ndarray:
+    """Eq. 5 Self-Convolution map C_i for the reference at (ry, rx): [(H-b+1), (W-b+1)]."""
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None]
+    C, H, W = a.shape
+    out = np.empty((H - b + 1, W - b + 1), dtype=np.float64)
+    rc = lib().sco_selfconv(a.ctypes.data, _dtype_code(a), C, H, W, b, ry, rx,
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if rc != 0:
+        raise ValueError("oracle.selfconv: invalid arguments")
+    return out
+
+
+def num_threads() -> int:
+    return int(lib().sco_num_threads())

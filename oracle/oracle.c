@@ -1,0 +1,262 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU block matching (TEST INFRASTRUCTURE ONLY).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load this library. The product path (paper_2006_13714_b200/) never does,
+ * and this file shares no code, header, table or helper with it.
+ *
+ * What it computes is the plain definition the paper proves Self-Convolution reaches
+ * exactly (Theorem 1, proof PAPER.md:468-521; Lemma 2):
+ *
+ *   Euclidean block matching, Eq. 3:
+ *       S_i = argmin_{|S| <= K} sum_{j in S} ||X_j - X_i||_F^2
+ *   restricted to the search window Omega_i (footnote 2), with the
+ *   multi-channel distance summed over channels (Eq. 12's S(.)).
+ *
+ * Readings of the paper:
+ *   R1 window = Wn x Wn candidate top-left offsets dy,dx in [lo, hi],
+ *      lo = -floor(Wn/2), hi = Wn-1-floor(Wn/2), centred on the reference's top-left;
+ *   R3 window clipped to valid positions [0,H-b] x [0,W-b];
+ *   R5 reference grid {0, s, 2s, ...} <= H-b (and W-b), raster order, images outermost;
+ *   R6 every candidate position (candidate stride 1);
+ *   R7 ties broken by (distance, idx) lexicographic, idx = cy*W + cx (pixel raster);
+ *   R8 K smallest distances (= K largest values of b_i);
+ *   R9 fewer than K candidates: idx = -1, dist = INT32_MAX (u8) / +inf (float).
+ *
+ * Arithmetic: distances by DIRECT differences (not the identity), int64 for uint8
+ * input, double for float/double input. A full sort of every window candidate per
+ * reference (qsort), first K kept. OpenMP over references only; the result does not
+ * depend on the thread count.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define SCO_U8 0
+#define SCO_F32 1
+#define SCO_F64 2
+
+typedef struct {
+    double d;
+    int64_t di; /* exact integer distance for u8 */
+    int32_t idx;
+} sco_key;
+
+static double px(const void* img, int dtype, size_t off) {
+    if (dtype == SCO_U8) return (double)((const uint8_t*)img)[off];
+    if (dtype == SCO_F32) return (double)((const float*)img)[off];
+    return ((const double*)img)[off];
+}
+
+static int cmp_key_int(const void* a, const void* b) {
+    const sco_key* x = (const sco_key*)a;
+    const sco_key* y = (const sco_key*)b;
+    if (x->di != y->di) return x->di < y->di ? -1 : 1;
+    return (x->idx > y->idx) - (x->idx < y->idx);
+}
+
+static int cmp_key_dbl(const void* a, const void* b) {
+    const sco_key* x = (const sco_key*)a;
+    const sco_key* y = (const sco_key*)b;
+    if (x->d != y->d) return x->d < y->d ? -1 : 1;
+    return (x->idx > y->idx) - (x->idx < y->idx);
+}
+
+/* Reference grid size along one axis (R5). */
+static int grid_n(int extent, int b, int s) { return (extent - b) / s + 1; }
+
+/* ||X_c - X_r||_F^2 by direct differences, summed over channels (Eq. 3 + Eq. 12). */
+static void patch_dist(const void* img, int dtype, int C, int H, int W, int b,
+                       int ry, int rx, int cy, int cx, int64_t* di, double* d) {
+    if (dtype == SCO_U8) {
+        const uint8_t* p = (const uint8_t*)img;
+        int64_t acc = 0;
+        for (int c = 0; c < C; ++c)
+            for (int l = 0; l < b; ++l)
+                for (int m = 0; m < b; ++m) {
+                    size_t base = (size_t)c * H * W;
+                    int64_t v = (int64_t)p[base + (size_t)(ry + l) * W + rx + m] -
+                                (int64_t)p[base + (size_t)(cy + l) * W + cx + m];
+                    acc += v * v;
+                }
+        *di = acc;
+        *d = (double)acc;
+    } else {
+        double acc = 0.0;
+        for (int c = 0; c < C; ++c)
+            for (int l = 0; l < b; ++l)
+                for (int m = 0; m < b; ++m) {
+                    size_t base = (size_t)c * H * W;
+                    double v = px(img, dtype, base + (size_t)(ry + l) * W + rx + m) -
+                               px(img, dtype, base + (size_t)(cy + l) * W + cx + m);
+                    acc += v * v;
+                }
+        *di = 0;
+        *d = acc;
+    }
+}
+
+/*
+ * Brute-force BM for images [img_begin, img_end) and reference-grid rows [iy_begin, iy_end)
+ * of each image. Outputs are [n_img][n_rows * n_ref_x][K] in reference raster order:
+ * idx_out int32; dist_out int32 (u8 input) or double (float input).
+ * Returns 0 on success, -1 on bad arguments.
+ */
+int sco_bm_rows(const void* imgs, int dtype, int C, int H, int W, int b, int s, int Wn, int K,
+                int img_begin, int img_end, int iy_begin, int iy_end,
+                int32_t* idx_out, void* dist_out, int nthreads) {
+    if (!imgs || !idx_out || !dist_out || b < 1 || s < 1 || Wn < 1 || K < 1 || C < 1 ||
+        H < b || W < b || img_end < img_begin)
+        return -1;
+    const int ny = grid_n(H, b, s), nx = grid_n(W, b, s);
+    if (iy_begin < 0 || iy_end > ny || iy_end < iy_begin) return -1;
+    const int lo = -(Wn / 2), hi = Wn - 1 - Wn / 2;
+    const int rows = iy_end - iy_begin;
+    const long long refs_per_img = (long long)rows * nx;
+    const long long total = refs_per_img * (img_end - img_begin);
+    const size_t img_elems = (size_t)C * H * W;
+    const size_t esz = dtype == SCO_U8 ? 1 : dtype == SCO_F32 ? 4 : 8;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+
+#pragma omp parallel
+    {
+        sco_key* keys = (sco_key*)malloc(sizeof(sco_key) * (size_t)Wn * (size_t)Wn);
+#pragma omp for schedule(dynamic, 16)
+        for (long long t = 0; t < total; ++t) {
+            const int n = img_begin + (int)(t / refs_per_img);
+            const long long j = t % refs_per_img;
+            const int iy = iy_begin + (int)(j / nx), ix = (int)(j % nx);
+            const int ry = iy * s, rx = ix * s;
+            const void* img = (const char*)imgs + (size_t)n * img_elems * esz;
+            /* R1 + R3: clipped window of candidate top-left positions. */
+            const int cy0 = ry + lo < 0 ? 0 : ry + lo;
+            const int cy1 = ry + hi > H - b ? H - b : ry + hi;
+            const int cx0 = rx + lo < 0 ? 0 : rx + lo;
+            const int cx1 = rx + hi > W - b ? W - b : rx + hi;
+            int cnt = 0;
+            for (int cy = cy0; cy <= cy1; ++cy)
+                for (int cx = cx0; cx <= cx1; ++cx) {
+                    patch_dist(img, dtype, C, H, W, b, ry, rx, cy, cx, &keys[cnt].di, &keys[cnt].d);
+                    keys[cnt].idx = cy * W + cx;
+                    ++cnt;
+                }
+            qsort(keys, (size_t)cnt, sizeof(sco_key), dtype == SCO_U8 ? cmp_key_int : cmp_key_dbl);
+            const long long o = t * K;
+            for (int k = 0; k < K; ++k) {
+                if (k < cnt) {
+                    idx_out[o + k] = keys[k].idx;
+                    if (dtype == SCO_U8) ((int32_t*)dist_out)[o + k] = (int32_t)keys[k].di;
+                    else ((double*)dist_out)[o + k] = keys[k].d;
+                } else {
+                    idx_out[o + k] = -1;
+                    if (dtype == SCO_U8) ((int32_t*)dist_out)[o + k] = INT32_MAX;
+                    else ((double*)dist_out)[o + k] = INFINITY;
+                }
+            }
+        }
+        free(keys);
+    }
+    return 0;
+}
+
+/* All references of all n_img images. */
+int sco_bm(const void* imgs, int dtype, int n_img, int C, int H, int W, int b, int s, int Wn,
+           int K, int32_t* idx_out, void* dist_out, int nthreads) {
+    if (H < b || s < 1) return -1;
+    return sco_bm_rows(imgs, dtype, C, H, W, b, s, Wn, K, 0, n_img, 0, grid_n(H, b, s),
+                       idx_out, dist_out, nthreads);
+}
+
+/*
+ * Every window distance (debug / cross-term check): dist_all[n_refs][Wn*Wn], slot
+ * (dy-lo)*Wn + (dx-lo); clipped slots hold -1. One image.
+ */
+int sco_bm_dense(const void* img, int dtype, int C, int H, int W, int b, int s, int Wn,
+                 double* dist_all, int nthreads) {
+    if (!img || !dist_all || b < 1 || s < 1 || Wn < 1 || H < b || W < b) return -1;
+    const int ny = grid_n(H, b, s), nx = grid_n(W, b, s);
+    const int lo = -(Wn / 2);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel for schedule(dynamic, 16)
+    for (long long t = 0; t < (long long)ny * nx; ++t) {
+        const int ry = (int)(t / nx) * s, rx = (int)(t % nx) * s;
+        for (int a = 0; a < Wn; ++a)
+            for (int c = 0; c < Wn; ++c) {
+                const int cy = ry + lo + a, cx = rx + lo + c;
+                double* out = &dist_all[t * Wn * Wn + (long long)a * Wn + c];
+                if (cy < 0 || cx < 0 || cy > H - b || cx > W - b) {
+                    *out = -1.0;
+                    continue;
+                }
+                int64_t di;
+                patch_dist(img, dtype, C, H, W, b, ry, rx, cy, cx, &di, out);
+            }
+    }
+    return 0;
+}
+
+/*
+ * h_X (.) h_X: ||X_j||_F^2 for every valid position j (used in Lemma 2),
+ * summed over channels; by direct summation. out[(H-b+1)*(W-b+1)] (double).
+ */
+int sco_norm_map(const void* img, int dtype, int C, int H, int W, int b, double* out) {
+    if (!img || !out || b < 1 || H < b || W < b) return -1;
+    const int My = H - b + 1, Mx = W - b + 1;
+    for (int y = 0; y < My; ++y)
+        for (int x = 0; x < Mx; ++x) {
+            double acc = 0.0;
+            for (int c = 0; c < C; ++c)
+                for (int l = 0; l < b; ++l)
+                    for (int m = 0; m < b; ++m) {
+                        double v = px(img, dtype, (size_t)c * H * W + (size_t)(y + l) * W + x + m);
+                        acc += v * v;
+                    }
+            out[(size_t)y * Mx + x] = acc;
+        }
+    return 0;
+}
+
+/*
+ * Self-Convolution, Eq. 5 summed over channels (Eq. 12):
+ *   C_i(q, r) = sum_{c,l,m} X_i(l, m) X(q + l, r + m)   (0-based)
+ * for the reference patch at (ry, rx), over the whole image: out[(H-b+1)*(W-b+1)].
+ */
+int sco_selfconv(const void* img, int dtype, int C, int H, int W, int b, int ry, int rx,
+                 double* out) {
+    if (!img || !out || b < 1 || H < b || W < b || ry < 0 || rx < 0 || ry > H - b || rx > W - b)
+        return -1;
+    const int My = H - b + 1, Mx = W - b + 1;
+    for (int q = 0; q < My; ++q)
+        for (int r = 0; r < Mx; ++r) {
+            double acc = 0.0;
+            for (int c = 0; c < C; ++c)
+                for (int l = 0; l < b; ++l)
+                    for (int m = 0; m < b; ++m) {
+                        size_t base = (size_t)c * H * W;
+                        acc += px(img, dtype, base + (size_t)(ry + l) * W + rx + m) *
+                               px(img, dtype, base + (size_t)(q + l) * W + r + m);
+                    }
+            out[(size_t)q * Mx + r] = acc;
+        }
+    return 0;
+}
+
+int sco_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,291 @@
+"""T0: pin the CPU oracle to things other than itself (no GPU needed).
+
+Pins:
+* hand-worked 3x3 example (tests/golden/worked_3x3.json; Eq. 5, Lemma 2, Theorem 1);
+* Lemma 2 identity: norm map + ||X_i||^2 - 2 C_i == direct-difference distances, exactly
+  in integers (proof PAPER.md:426-439);
+* closed forms: b=1, Wn=1, constant image, periodic tiling, duplicated channels;
+* invariants: d >= 0, self-distance 0, symmetry, constant shift, scaling, channel permutation;
+* exhaustive 8x8 sweep against an independent numpy brute force (tests/bm_numpy.py);
+* library special case: torch conv2d correlation + numpy lexsort.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.bm_numpy import bm_np
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "worked_3x3.json")
+
+
+def _rng(seed):
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+# ---------------------------------------------------------------- worked example
+def test_worked_example_maps():
+    g = json.load(open(GOLD))
+    img = np.array(g["image"], dtype=np.uint8)
+    b = g["b"]
+    np.testing.assert_array_equal(oracle.norm_map(img, b), np.array(g["norms"], float))
+    np.testing.assert_array_equal(oracle.selfconv(img, b, *g["ref"]), np.array(g["C"], float))
+    # objective of Theorem 1 item 2, b_i = C_i - 1/2 h.h, largest value = nearest
+    bi = oracle.selfconv(img, b, *g["ref"]) - 0.5 * oracle.norm_map(img, b)
+    np.testing.assert_array_equal(bi, np.array(g["b_i"], float))
+    dense = oracle.bm_dense(img, b, 1, g["window"])  # ref (0,0) is row 0; offsets -1..1
+    d00 = dense[0].reshape(3, 3)[1:, 1:]
+    np.testing.assert_array_equal(d00, np.array(g["d"], float))
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5])
+def test_worked_example_topk(K):
+    g = json.load(open(GOLD))
+    img = np.array(g["image"], dtype=np.uint8)
+    idx, dist = oracle.bm(img, g["b"], 2, g["window"], K)  # stride 2: only ref (0,0)
+    assert idx.shape == (1, 1, K)
+    np.testing.assert_array_equal(idx[0, 0], g["topk"][str(K)]["idx"])
+    np.testing.assert_array_equal(dist[0, 0], g["topk"][str(K)]["dist"])
+
+
+def test_value_not_magnitude_selection():
+    # b_i = [23, 21, 5, -9]: the K=3 set is {0,1,3}; magnitude selection would pick 4.
+    g = json.load(open(GOLD))
+    img = np.array(g["image"], dtype=np.uint8)
+    idx, _ = oracle.bm(img, 2, 2, 3, 3)
+    assert 4 not in idx[0, 0].tolist()
+
+
+# ---------------------------------------------------------------- Lemma 2 identity
+@pytest.mark.parametrize("C,b,s,Wn", [(1, 8, 4, 21), (1, 7, 1, 9), (3, 5, 2, 11), (4, 8, 3, 13)])
+def test_lemma2_identity_exact(C, b, s, Wn):
+    rng = _rng(10 + C + b)
+    H, W = 29, 35
+    img = rng.integers(0, 256, size=(C, H, W), dtype=np.uint8)
+    dense = oracle.bm_dense(img, b, s, Wn)
+    nm = oracle.norm_map(img, b)
+    lo = -(Wn // 2)
+    ny, nx = oracle.grid(H, W, b, s)
+    for t in range(0, ny * nx, max(1, (ny * nx) // 17)):
+        ry, rx = (t // nx) * s, (t % nx) * s
+        Ci = oracle.selfconv(img, b, ry, rx)
+        for a in range(Wn):
+            for c in range(Wn):
+                cy, cx = ry + lo + a, rx + lo + c
+                v = dense[t, a * Wn + c]
+                if cy < 0 or cx < 0 or cy > H - b or cx > W - b:
+                    assert v == -1.0
+                    continue
+                assert v == nm[cy, cx] + nm[ry, rx] - 2.0 * Ci[cy, cx]
+
+
+def test_lemma2_identity_after_shift():
+    # shifting u8 by -128 leaves every distance unchanged (d is a difference, Eq. 3)
+    rng = _rng(3)
+    img = rng.integers(0, 256, size=(1, 20, 24), dtype=np.uint8)
+    a = oracle.bm_dense(img, 6, 2, 7)
+    b = oracle.bm_dense(img.astype(np.float64) - 128.0, 6, 2, 7)
+    np.testing.assert_array_equal(a, b)
+
+
+# ---------------------------------------------------------------- closed forms
+def test_b1_closed_form():
+    rng = _rng(5)
+    img = rng.integers(0, 256, size=(1, 12, 13), dtype=np.uint8)
+    dense = oracle.bm_dense(img, 1, 1, 5)
+    x = img[0].astype(np.int64)
+    for t in range(12 * 13):
+        ry, rx = divmod(t, 13)
+        for a in range(5):
+            for c in range(5):
+                cy, cx = ry - 2 + a, rx - 2 + c
+                v = dense[t, a * 5 + c]
+                if 0 <= cy < 12 and 0 <= cx < 13:
+                    assert v == (x[ry, rx] - x[cy, cx]) ** 2
+                else:
+                    assert v == -1
+
+
+def test_window_one_is_self_only():
+    rng = _rng(6)
+    img = rng.random((2, 15, 17)).astype(np.float32)
+    idx, dist = oracle.bm(img, 4, 3, 1, 3)
+    ny, nx = oracle.grid(15, 17, 4, 3)
+    for t in range(ny * nx):
+        ry, rx = (t // nx) * 3, (t % nx) * 3
+        assert idx[0, t].tolist() == [ry * 17 + rx, -1, -1]
+        assert dist[0, t, 0] == 0.0 and np.isinf(dist[0, t, 1:]).all()
+
+
+@pytest.mark.parametrize("H,W,b,s,Wn,K", [(20, 23, 4, 3, 7, 10), (16, 16, 8, 4, 21, 16), (9, 30, 3, 2, 6, 40)])
+def test_constant_image(H, W, b, s, Wn, K):
+    img = np.full((1, H, W), 77, dtype=np.uint8)
+    idx, dist = oracle.bm(img, b, s, Wn, K)
+    lo, hi = -(Wn // 2), Wn - 1 - Wn // 2
+    ny, nx = oracle.grid(H, W, b, s)
+    for t in range(ny * nx):
+        ry, rx = (t // nx) * s, (t % nx) * s
+        cands = sorted(cy * W + cx
+                       for cy in range(max(0, ry + lo), min(H - b, ry + hi) + 1)
+                       for cx in range(max(0, rx + lo), min(W - b, rx + hi) + 1))
+        want = (cands + [-1] * K)[:K]
+        assert idx[0, t].tolist() == want
+        assert all(d == 0 for d, i in zip(dist[0, t], want) if i >= 0)
+
+
+def test_periodic_tiling_zero_distances():
+    P, b = 8, 6
+    rng = _rng(8)
+    motif = rng.integers(0, 256, size=(P, P), dtype=np.uint8)
+    img = np.tile(motif, (5, 5))[None]  # 40x40
+    dense = oracle.bm_dense(img, b, 2, 17)
+    ny, nx = oracle.grid(40, 40, b, 2)
+    for t in range(ny * nx):
+        for a in range(17):
+            for c in range(17):
+                v = dense[t, a * 17 + c]
+                if v < 0:
+                    continue
+                dy, dx = a - 8, c - 8
+                if dy % P == 0 and dx % P == 0:
+                    assert v == 0
+                else:
+                    assert v > 0  # random motif: no other exact repeats at these sizes
+
+
+def test_duplicated_channels_scale_distance():
+    rng = _rng(9)
+    one = rng.integers(0, 256, size=(1, 22, 19), dtype=np.uint8)
+    three = np.repeat(one, 3, axis=0)
+    i1, d1 = oracle.bm(one, 5, 2, 9, 12)
+    i3, d3 = oracle.bm(three, 5, 2, 9, 12)
+    np.testing.assert_array_equal(i1, i3)
+    np.testing.assert_array_equal(d3, 3 * d1)
+
+
+# ---------------------------------------------------------------- invariants
+def test_nonnegative_and_self_zero():
+    rng = _rng(11)
+    img = rng.random((2, 25, 21))
+    dense = oracle.bm_dense(img, 5, 3, 9)
+    assert (dense[dense != -1] >= 0).all()
+    ny, nx = oracle.grid(25, 21, 5, 3)
+    assert (dense[:, 4 * 9 + 4] == 0).all()  # centre slot = self
+
+
+def test_symmetry_odd_window():
+    rng = _rng(12)
+    img = rng.integers(0, 256, size=(1, 18, 20), dtype=np.uint8)
+    b, Wn = 4, 7
+    dense = oracle.bm_dense(img, b, 1, Wn)
+    nx = 20 - b + 1
+    r = Wn // 2
+    for t in range(dense.shape[0]):
+        ry, rx = divmod(t, nx)
+        for a in range(Wn):
+            for c in range(Wn):
+                v = dense[t, a * Wn + c]
+                if v < 0:
+                    continue
+                cy, cx = ry + a - r, rx + c - r
+                u = (cy * nx + cx)
+                back = dense[u, (ry - cy + r) * Wn + (rx - cx + r)]
+                assert back == v
+
+
+def test_shift_and_scale_invariance():
+    rng = _rng(13)
+    x = rng.integers(0, 100, size=(1, 17, 19)).astype(np.float64)
+    base = oracle.bm(x, 5, 2, 9, 10)
+    shifted = oracle.bm(x + 37.0, 5, 2, 9, 10)
+    scaled = oracle.bm(2.0 * x, 5, 2, 9, 10)
+    np.testing.assert_array_equal(base[0], shifted[0])
+    np.testing.assert_array_equal(base[1], shifted[1])
+    np.testing.assert_array_equal(base[0], scaled[0])
+    np.testing.assert_array_equal(4.0 * base[1], scaled[1])
+
+
+def test_channel_permutation_invariance():
+    rng = _rng(14)
+    x = rng.random((4, 16, 18)).astype(np.float32)
+    a = oracle.bm(x, 4, 2, 7, 9)
+    b = oracle.bm(x[[2, 0, 3, 1]], 4, 2, 7, 9)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_allclose(a[1], b[1], rtol=1e-12)
+
+
+def test_thread_count_independent():
+    rng = _rng(15)
+    x = rng.integers(0, 4, size=(2, 1, 24, 26), dtype=np.uint8)  # many ties
+    a = oracle.bm(x, 4, 1, 9, 20, nthreads=1)
+    b = oracle.bm(x, 4, 1, 9, 20, nthreads=4)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_rows_subset_matches_full():
+    rng = _rng(16)
+    x = rng.integers(0, 256, size=(3, 1, 30, 28), dtype=np.uint8)
+    full = oracle.bm(x, 6, 3, 11, 8)
+    ny, nx = oracle.grid(30, 28, 6, 3)
+    part = oracle.bm(x, 6, 3, 11, 8, images=(1, 3), rows=(2, 5))
+    np.testing.assert_array_equal(part[0], full[0][1:3, 2 * nx:5 * nx])
+    np.testing.assert_array_equal(part[1], full[1][1:3, 2 * nx:5 * nx])
+
+
+# ---------------------------------------------------------------- exhaustive 8x8
+def test_exhaustive_8x8_u8():
+    rng = _rng(17)
+    img = rng.integers(0, 6, size=(1, 8, 8), dtype=np.uint8)  # small range -> ties exercised
+    for b in range(1, 9):
+        for s in range(1, 5):
+            for Wn in range(1, 18):
+                Kmax = min(Wn, 9 - b) ** 2
+                for K in sorted({1, max(1, Kmax // 2), Kmax, Kmax + 2}):
+                    i_o, d_o = oracle.bm(img, b, s, Wn, K)
+                    i_n, d_n = bm_np(img[0], b, s, Wn, K)
+                    np.testing.assert_array_equal(i_o[0], i_n, err_msg=f"b={b} s={s} Wn={Wn} K={K}")
+                    np.testing.assert_array_equal(d_o[0], d_n, err_msg=f"b={b} s={s} Wn={Wn} K={K}")
+
+
+def test_exhaustive_8x8_float_multichannel():
+    rng = _rng(18)
+    img = rng.random((3, 8, 8)).astype(np.float32)
+    for b in range(1, 9):
+        for s in (1, 3):
+            for Wn in (1, 2, 5, 8, 17):
+                K = min(Wn, 9 - b) ** 2
+                i_o, d_o = oracle.bm(img, b, s, Wn, K)
+                i_n, d_n = bm_np(img, b, s, Wn, K)
+                np.testing.assert_array_equal(i_o[0], i_n)
+                np.testing.assert_allclose(d_o[0], d_n, rtol=1e-12, atol=0)
+
+
+# ---------------------------------------------------------------- library special case
+def test_torch_conv2d_special_case():
+    torch = pytest.importorskip("torch")
+    import torch.nn.functional as F
+    rng = _rng(19)
+    C, H, W, b, s, Wn, K = 2, 33, 37, 6, 3, 13, 11
+    img = rng.random((C, H, W))
+    x = torch.from_numpy(img)[None]  # [1,C,H,W] float64
+    norms = F.conv2d(x * x, torch.ones(1, C, b, b, dtype=torch.float64))[0, 0].numpy()
+    i_o, d_o = oracle.bm(img, b, s, Wn, K)
+    ny, nx = oracle.grid(H, W, b, s)
+    lo, hi = -(Wn // 2), Wn - 1 - Wn // 2
+    for t in range(ny * nx):
+        ry, rx = (t // nx) * s, (t % nx) * s
+        w = x[:, :, ry:ry + b, rx:rx + b]
+        corr = F.conv2d(x, w)[0, 0].numpy()  # torch conv2d is correlation (footnote 1)
+        d = norms + norms[ry, rx] - 2.0 * corr
+        ys = np.arange(max(0, ry + lo), min(H - b, ry + hi) + 1)
+        xs = np.arange(max(0, rx + lo), min(W - b, rx + hi) + 1)
+        cy, cx = np.meshgrid(ys, xs, indexing="ij")
+        dd = d[cy, cx].ravel()
+        ii = (cy * W + cx).ravel()
+        # direct identity in float64 has rounding; compare sets/order on well-separated keys
+        order = np.lexsort((ii, np.round(dd, 9)))[:K]
+        np.testing.assert_array_equal(i_o[0, t], ii[order])
+        np.testing.assert_allclose(d_o[0, t], dd[order], rtol=1e-9, atol=1e-9)
