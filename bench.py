@@ -1,0 +1,327 @@
+"""Benchmark: Self-Convolution block matching on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path (norm map -> cross term -> distance assembly ->
+top-K -> output tables) over the config's batch, inputs resident in HBM.
+Default workload: config c5 (64 uint8 1080x1920 frames, b=8, s=4, Wn=33, K=16), the
+config the metric's 1/2/4/8-GPU scaling is quoted on; its frames are sharded across ranks
+(strong scaling: the 64-frame batch is fixed). Under torchrun each rank runs its shard;
+the timed region is bracketed by barrier + synchronize, per-step CUDA events on the run
+stream, and the max over ranks is reported. ``--impl reference`` times the CPU oracle
+(the brute-force definition, oracle/) on the host cores on a bounded sample instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate patch distances/sec"
+UNIT = "candidate distances/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.rows = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1)):
+    """Time the oracle on a bounded sample of the workload: reference rows of image 0."""
+    import oracle
+    from paper_2006_13714_b200 import synth  # noqa: F401
+    ny = (cfg.H - cfg.b) // cfg.s + 1
+    nx = (cfg.W - cfg.b) // cfg.s + 1
+    lo, hi = -(cfg.Wn // 2), cfg.Wn - 1 - cfg.Wn // 2
+
+    def pairs(r0, r1):
+        ys = [min(cfg.H - cfg.b, iy * cfg.s + hi) - max(0, iy * cfg.s + lo) + 1 for iy in range(r0, r1)]
+        xs = [min(cfg.W - cfg.b, ix * cfg.s + hi) - max(0, ix * cfg.s + lo) + 1 for ix in range(nx)]
+        return sum(ys) * sum(xs)
+
+    # calibrate on one middle row, then size the sample to ~target_s seconds
+    mid = ny // 2
+    t0 = time.perf_counter()
+    oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(mid, mid + 1))
+    dt = max(time.perf_counter() - t0, 1e-3)
+    rows = int(max(1, min(ny - mid, target_s / dt)))
+    t0 = time.perf_counter()
+    oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(mid, mid + rows))
+    dt = time.perf_counter() - t0
+    p = pairs(mid, mid + rows)
+    return {"value": p / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{cfg.name} image 0, reference rows {mid}:{mid + rows} of {ny} "
+                      f"({rows * nx} refs, {p} candidate pairs), {dt:.2f} s"}, p, dt
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from paper_2006_13714_b200 import synth
+    x = synth.make_input(cfg, n_frames=1)
+    oracle.build()
+    for _ in range(args.warmup):
+        _cpu_sample(cfg, x, target_s=1.0)
+    vals, tot_p, tot_t = [], 0, 0.0
+    last = None
+    for _ in range(args.steps):
+        last, p, dt = _cpu_sample(cfg, x, target_s=args.ref_step_s)
+        vals.append(last["value"])
+        tot_p += p
+        tot_t += dt
+    value = tot_p / tot_t
+    cpu = dict(last)
+    cpu["value"] = value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": _dtype_name(cfg),
+            "data": "synthetic", "config": _config_obj(cfg, args), "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _dtype_name(cfg):
+    return "int32" if cfg.dtype == "u8" else "f32"
+
+
+def _config_obj(cfg, args):
+    return {"workload": cfg.name, "images": cfg.N, "channels": cfg.C, "H": cfg.H, "W": cfg.W,
+            "input_dtype": "u8" if cfg.dtype == "u8" else "f32", "patch": cfg.b, "stride": cfg.s,
+            "window": cfg.Wn, "K": cfg.K, "sharding": "frames" if cfg.N > 1 else "replicas",
+            "l2": "flushed between timed steps (256 MiB write); working set > L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="also time an NCCL all-gather of the tables")
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    from paper_2006_13714_b200 import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    from paper_2006_13714_b200.bm import Plan
+
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    # shard frames (strong scaling); single-image configs run as replicas
+    if cfg.N > 1:
+        per = [cfg.N // ws + (1 if r < cfg.N % ws else 0) for r in range(ws)]
+        f0 = sum(per[:rank])
+        nloc = per[rank]
+    else:
+        f0, nloc = 0, 1
+    x_all = synth.make_input(cfg)
+    x_host = np.ascontiguousarray(x_all[f0:f0 + nloc])
+    del x_all
+    x = torch.from_numpy(x_host).cuda()
+    plan = Plan(cfg.H, cfg.W, cfg.C, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype)
+    info = plan.info()
+    idx, dst = plan.alloc_out(nloc)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        plan.run(x, out=(idx, dst))
+    torch.cuda.synchronize()
+
+    plan.set_timing(True)
+    plan.get_timing()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = plan.info()["launches"]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)  # L2 flush outside the step's events
+            starts[k].record(stream)
+            plan.run(x, out=(idx, dst))
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = plan.info()["launches"] - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tm = plan.get_timing()
+    plan.set_timing(False)
+    ms_local = float(np.mean(step_ms))
+    match_ms_local = tm["match_ms"] / max(1, args.steps)
+    norm_ms_local = tm["norm_ms"] / max(1, args.steps)
+    t = torch.tensor([ms_local, match_ms_local, norm_ms_local], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, match_ms, norm_ms = t.tolist()
+
+    pairs_per_image = info["total_candidates"]
+    n_images_total = cfg.N if cfg.N > 1 else ws
+    pairs_step = pairs_per_image * n_images_total
+    refs_step = info["n_refs"] * n_images_total
+    value = pairs_step / (ms / 1e3)
+
+    # roofline of the dominant kernel (the fused cross-term / top-K kernel)
+    peaks = _peaks()
+    macs_launch = pairs_per_image * nloc * cfg.b * cfg.b * cfg.C  # algorithmic MACs per rank-step
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if info["kernel"] == 1:
+        peak = 2.0 * peaks["bf16_tflops"]  # int8 tcgen05 = 2x the measured bf16 (guide's nominal ratio)
+        bound, unit, peak_note = "tensor", "TFLOP/s", "int8 = 2 x measured bf16 burst (MEASURED_PEAKS.json)"
+    else:
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # FP32/INT32 FMA lanes x 2 ops x max clock
+        bound, unit, peak_note = "alu", "TFLOP/s", "148 SM x 128 FMA lanes x 2 x sm_max_mhz (derived, DESIGN.md)"
+    achieved = 2.0 * macs_launch / (match_ms / 1e3) / 1e12 if match_ms > 0 else None
+    roof = {"bound": bound, "kernel": "bm_simt_kernel" if info["kernel"] == 0 else "bm_tc_i8_kernel",
+            "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "peak_source": peak_note, "kernel_ms_per_step": match_ms, "norm_ms_per_step": norm_ms,
+            "kernel_share_of_step": match_ms / ms if ms > 0 else None,
+            "algorithmic_ops_per_launch": 2.0 * macs_launch}
+
+    # end-to-end through the public API with host buffers (pinned), copies inside the timing
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(x_host).pin_memory()
+        hi = torch.empty((nloc, info["n_refs"], cfg.K), dtype=torch.int32).pin_memory()
+        hd = torch.empty((nloc, info["n_refs"], cfg.K),
+                         dtype=torch.int32 if cfg.dtype == "u8" else torch.float32).pin_memory()
+        plan.run_host(xh, out=(hi, hd))
+        e_steps = max(3, min(args.steps, 5))
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            plan.run_host(xh, out=(hi, hd))
+        e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+        te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = te.item()
+        e2e = {"value": pairs_step / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(xh.numel() * xh.element_size()) * (ws if cfg.N > 1 else 1),
+               "d2h_bytes_per_step": int(2 * hi.numel() * 4) * (ws if cfg.N > 1 else 1),
+               "steps": e_steps, "timing": "wall clock around sc_bm_run_host (synchronous), max over ranks"}
+
+    gather = None
+    if args.gather and dist:
+        gi = torch.empty((ws * idx.shape[0],) + tuple(idx.shape[1:]), dtype=idx.dtype, device="cuda")
+        gd = torch.empty_like(gi, dtype=dst.dtype)
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        dist.all_gather_into_tensor(gi, idx)
+        dist.all_gather_into_tensor(gd, dst)
+        g1.record()
+        torch.cuda.synchronize()
+        tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gather = {"ms": tg.item(), "bytes_per_rank": int(2 * gi.numel() * 4), "backend": "nccl"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu, _, _ = _cpu_sample(cfg, x_host, target_s=args.ref_step_s * 2)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if cfg.N > 1 else "weak", "vs_baseline": None,
+                "dtype": _dtype_name(cfg), "data": "synthetic", "config": _config_obj(cfg, args),
+                "ref_patches_per_s": refs_step / (ms / 1e3), "candidate_pairs_per_step": pairs_step,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk.summary(), "gather": gather,
+                "kernel": info["kernel"], "frames_per_chunk": info["frames_per_chunk"]}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

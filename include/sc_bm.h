@@ -1,0 +1,175 @@
+/*
+ * sc_bm.h -- C ABI of the B200-native Self-Convolution block-matching library (libscbm.so).
+ *
+ * The operation (arXiv 2006.13714):
+ *   For every reference patch X_i on a stride grid, find the K candidate patches X_j of
+ *   its search window with the smallest squared Euclidean distance
+ *       d_E(X_j, X_i) = ||X_j - X_i||_F^2                         (Eq. 3)
+ *   restricted to the window Omega_i (footnote 2), channels summed jointly
+ *   (Eq. 12's S(.)). The library evaluates it the paper's way:
+ *       d_E = h_X(j)^2 + ||X_i||^2 - 2 C_i(j)                     (Lemma 2)
+ *   with the norms h_X (.) h_X from an integral image of the squared image
+ *   and the cross term C_i the image self-convolved with X_i (Eq. 5);
+ *   selection keeps the K largest values of b_i = C_i - 1/2 h_X (.) h_X, i.e. the K
+ *   smallest d_E (Theorem 1, proof PAPER.md:487-502).
+ *
+ * Geometry:
+ *   reference grid  ry = 0, s, 2s, ... <= H-b;  rx = 0, s, ... <= W-b;  n_ref_y * n_ref_x refs,
+ *                   reference j = iy * n_ref_x + ix (raster), images outermost.
+ *   window          candidate top-left (cy, cx) with cy - ry, cx - rx in [lo, hi],
+ *                   lo = -floor(Wn/2), hi = Wn - 1 - floor(Wn/2), clipped to [0,H-b] x [0,W-b];
+ *                   every position (candidate stride 1).
+ *   index           idx = cy * W + cx (pixel raster of the top-left corner, per image).
+ *   order           each row of K results is sorted ascending by (distance, idx).
+ *   short windows   if a window has fewer than K candidates the tail is idx = -1 and
+ *                   dist = INT32_MAX (u8) or +inf (f32).
+ *
+ * Layouts (all row-major, contiguous):
+ *   img      [n_images][C][H][W]  uint8 (SC_DTYPE_U8) or float (SC_DTYPE_F32), planar channels.
+ *   idx_out  [n_images][n_refs][K] int32.
+ *   dist_out [n_images][n_refs][K] int32 (u8: exact integer distances) or float (f32).
+ *
+ * Ownership and threading:
+ *   The plan owns its device workspace, allocated by sc_bm_plan on the current CUDA device
+ *   and freed by sc_bm_destroy. The caller owns img / idx_out / dist_out (device memory
+ *   unless stated otherwise) and the stream. The device-pointer run calls never allocate,
+ *   never synchronise and are CUDA-graph capturable. Runs sharing one plan must be ordered
+ *   on one stream (the workspace is shared); distinct plans are independent.
+ *
+ * Errors:
+ *   Argument validation is synchronous and returns a status. Kernel launch failures return
+ *   SC_ERR_CUDA; asynchronous device faults surface at the caller's next synchronisation.
+ *   The library never prints and never exits. There is no CPU fallback: without a usable
+ *   sm_100 device sc_bm_plan returns SC_ERR_CUDA / SC_ERR_UNSUPPORTED.
+ *
+ * Numerics:
+ *   u8  : values are shifted by -128 (d is a difference, Eq. 3, so it is unchanged); the
+ *         integral image is uint32 (wrap-around, box sums exact), the cross term int32; all
+ *         distances are exact integers -- bit-identical to the definition.
+ *   f32 : values are centred by -0.5; the integral image is fp64; the cross term fp32; the
+ *         top-(K+8) survivors are re-scored by direct differences in fp32 and re-sorted.
+ *         Distances are within relative 1e-5 of the exact value (BASELINE.json north_star).
+ */
+#ifndef SC_BM_H
+#define SC_BM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SC_BM_ABI_VERSION 1
+
+typedef struct CUstream_st* sc_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum { SC_DTYPE_U8 = 0, SC_DTYPE_F32 = 1 } sc_dtype_t;
+
+typedef enum {
+    SC_OK = 0,
+    SC_ERR_INVALID_ARGUMENT = 1, /* null pointer, misaligned pointer, parameter out of range */
+    SC_ERR_UNSUPPORTED = 2,      /* valid request this build cannot serve (e.g. no sm_100 device) */
+    SC_ERR_OUT_OF_MEMORY = 3,    /* workspace allocation failed */
+    SC_ERR_CUDA = 4,             /* CUDA runtime / launch error */
+    SC_ERR_WRONG_DEVICE = 5      /* current device differs from the plan's device */
+} sc_status_t;
+
+typedef struct sc_bm_plan_s* sc_bm_plan_t;
+
+typedef struct {
+    int64_t n_ref_y, n_ref_x, n_refs;   /* reference grid per image */
+    int64_t min_candidates;             /* smallest clipped window (candidates of one ref) */
+    int64_t max_candidates;             /* largest clipped window */
+    int64_t total_candidates;           /* sum over the refs of one image: the pair count */
+    int64_t workspace_bytes;            /* device workspace owned by the plan */
+    int64_t frames_per_chunk;           /* images processed per norm->match chunk */
+    int64_t launches;                   /* kernels launched by this plan so far (counter) */
+    int32_t kernel;                     /* SC_KERNEL_* selected for the cross-term/top-K step */
+    int32_t device;                     /* CUDA device ordinal the plan is bound to */
+} sc_bm_info_t;
+
+#define SC_KERNEL_SIMT 0   /* CUDA-core FFMA / IMAD cross term + fused warp top-K */
+#define SC_KERNEL_TC_I8 1  /* tcgen05 kind::i8 cross term (TMEM) + fused top-K (u8 only) */
+
+/*
+ * Create a plan. H, W: image size (H, W >= b, H*W < 2^31); C: channels (1..8); b: patch
+ * side (1..16); stride: reference stride (>= 1); window: Wn (1..255); K: matches (1..128);
+ * dtype: SC_DTYPE_U8 or SC_DTYPE_F32. *plan_out receives the handle (NULL on failure).
+ */
+sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K,
+                       sc_dtype_t dtype, sc_bm_plan_t* plan_out);
+
+/* One image [C][H][W] -> idx_out / dist_out [n_refs][K]. Device pointers; img 16-B aligned. */
+sc_status_t sc_bm_run(sc_bm_plan_t plan, const void* img, int32_t* idx_out, void* dist_out,
+                      sc_stream_t stream);
+
+/* n_images images [n][C][H][W] -> [n][n_refs][K]. Device pointers. */
+sc_status_t sc_bm_run_batch(sc_bm_plan_t plan, const void* imgs, int64_t n_images,
+                            int32_t* idx_out, void* dist_out, sc_stream_t stream);
+
+/*
+ * Row band (the multi-GPU partitioner's spatial split): only the
+ * references of reference-grid rows [iy_begin, iy_end) of each image; idx_out / dist_out
+ * are [n_images][(iy_end - iy_begin) * n_ref_x][K]. The full image is read (replicated).
+ */
+sc_status_t sc_bm_run_rows(sc_bm_plan_t plan, const void* imgs, int64_t n_images,
+                           int32_t iy_begin, int32_t iy_end, int32_t* idx_out, void* dist_out,
+                           sc_stream_t stream);
+
+/*
+ * Same as sc_bm_run_batch but imgs / idx_out / dist_out are HOST pointers (pinned memory
+ * gives full overlap; pageable memory works but serialises the copies). The library
+ * pipelines host->device copies, matching and device->host copies over frame chunks on
+ * the given stream plus plan-owned streams, and returns when the results are in host
+ * memory. The first call allocates the plan's staging buffers (a documented exception
+ * to "run never allocates").
+ */
+sc_status_t sc_bm_run_host(sc_bm_plan_t plan, const void* h_imgs, int64_t n_images,
+                           int32_t* h_idx_out, void* h_dist_out, sc_stream_t stream);
+
+/* Plan geometry and bookkeeping. */
+sc_status_t sc_bm_plan_info(sc_bm_plan_t plan, sc_bm_info_t* info);
+
+/* Force a kernel (SC_KERNEL_*) for the cross-term/top-K step; for tests and benchmarks. */
+sc_status_t sc_bm_set_kernel(sc_bm_plan_t plan, int32_t kernel);
+
+/*
+ * Per-kernel device timing (bench.py's roofline): when enabled, every chunk enqueued by a
+ * run call records CUDA events on the run stream around its norm kernels and around its
+ * matching kernel. sc_bm_get_timing waits for the recorded events, returns the summed
+ * durations (milliseconds) and launch counts since the last call, and resets them.
+ * Enabling pre-creates the event pool (allocation); it is off by default.
+ */
+typedef struct {
+    double norm_ms, match_ms;     /* summed device time of the norm kernels / matching kernel */
+    int64_t norm_chunks, match_launches;
+} sc_bm_timing_t;
+sc_status_t sc_bm_set_timing(sc_bm_plan_t plan, int32_t enable);
+sc_status_t sc_bm_get_timing(sc_bm_plan_t plan, sc_bm_timing_t* out);
+
+/* Free the plan and its workspace (NULL is a no-op). */
+sc_status_t sc_bm_destroy(sc_bm_plan_t plan);
+
+/* Static string for a status code. */
+const char* sc_status_string(sc_status_t s);
+
+/*
+ * Test export of step a1: the norm map h_X (.) h_X of the CENTRED image
+ * (u8: x - 128; f32: x - 0.5), channels summed, built from the integral image:
+ * norm_out [(H-b+1)][(W-b+1)] int32 (u8) or float (f32). One image, device pointers.
+ */
+sc_status_t sc_bm_norm_map(sc_bm_plan_t plan, const void* img, void* norm_out, sc_stream_t stream);
+
+/*
+ * Test export of steps a2+a3 (Eq. 5 + Lemma 2) without selection: every window distance
+ * dist_all [n_refs][Wn*Wn] (slot (dy-lo)*Wn + (dx-lo)), int32 (u8) or float (f32), -1 in
+ * clipped slots. Computed by the same cross-term code as the matching kernel. One image.
+ */
+sc_status_t sc_bm_run_dense_debug(sc_bm_plan_t plan, const void* img, void* dist_all,
+                                  sc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SC_BM_H */

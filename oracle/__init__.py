@@ -46,6 +46,7 @@ def lib():
         L.sco_bm_dense.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, dp, ci]
         L.sco_norm_map.argtypes = [vp, ci, ci, ci, ci, ci, dp]
         L.sco_selfconv.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, dp]
+        L.sco_pair_dist.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
         L.sco_num_threads.restype = ci
         _lib = L
     return _lib
@@ -134,6 +135,24 @@ def selfconv(img: np.ndarray, b: int, ry: int, rx: int) -> np.ndarray:
                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     if rc != 0:
         raise ValueError("oracle.selfconv: invalid arguments")
+    return out
+
+
+def pair_dist(img: np.ndarray, b: int, ry, rx, cy, cx) -> np.ndarray:
+    """Direct distances for explicit (ref, candidate) pairs of one image [C,H,W] (float64)."""
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None]
+    C, H, W = a.shape
+    arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.int32).ravel()) for v in (ry, rx, cy, cx)]
+    n = arrs[0].size
+    out = np.empty(n, dtype=np.float64)
+    P = ctypes.POINTER(ctypes.c_int32)
+    rc = lib().sco_pair_dist(a.ctypes.data, _dtype_code(a), C, H, W, b, n,
+                             *[x.ctypes.data_as(P) for x in arrs],
+                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if rc != 0:
+        raise ValueError("oracle.pair_dist: invalid arguments")
     return out
 
 

@@ -253,6 +253,25 @@ int sco_selfconv(const void* img, int dtype, int C, int H, int W, int b, int ry,
     return 0;
 }
 
+/*
+ * Direct distances for an explicit list of (reference, candidate) pairs of one image:
+ * out[k] = ||X_{(cy,cx)} - X_{(ry,rx)}||_F^2 by direct differences (Eq. 3), channels summed.
+ * Used to check sampled GPU outputs one by one at full size.
+ */
+int sco_pair_dist(const void* img, int dtype, int C, int H, int W, int b, long long n,
+                  const int32_t* ry, const int32_t* rx, const int32_t* cy, const int32_t* cx,
+                  double* out) {
+    if (!img || !out || b < 1 || H < b || W < b) return -1;
+    for (long long k = 0; k < n; ++k) {
+        if (ry[k] < 0 || rx[k] < 0 || cy[k] < 0 || cx[k] < 0 || ry[k] > H - b || cy[k] > H - b ||
+            rx[k] > W - b || cx[k] > W - b)
+            return -1;
+        int64_t di;
+        patch_dist(img, dtype, C, H, W, b, ry[k], rx[k], cy[k], cx[k], &di, &out[k]);
+    }
+    return 0;
+}
+
 int sco_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

@@ -1,0 +1,219 @@
+"""Thin Python binding of include/sc_bm.h (argument marshalling only).
+
+Every step of the path runs in libscbm.so's CUDA kernels; torch provides device memory,
+the current stream and (in :mod:`.dist`) process groups. There is no CPU fallback: if the
+library is missing or no sm_100 device is usable, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libscbm.so")
+
+SC_DTYPE_U8, SC_DTYPE_F32 = 0, 1
+SC_KERNEL_SIMT, SC_KERNEL_TC_I8 = 0, 1
+STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_UNSUPPORTED",
+          3: "SC_ERR_OUT_OF_MEMORY", 4: "SC_ERR_CUDA", 5: "SC_ERR_WRONG_DEVICE"}
+
+EXPORTED = ["sc_bm_plan", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
+            "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
+            "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing"]
+
+
+class ScError(RuntimeError):
+    def __init__(self, fn, code):
+        super().__init__(f"{fn} failed: {STATUS.get(code, code)}")
+        self.code = code
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("n_ref_y", ctypes.c_int64), ("n_ref_x", ctypes.c_int64), ("n_refs", ctypes.c_int64),
+                ("min_candidates", ctypes.c_int64), ("max_candidates", ctypes.c_int64),
+                ("total_candidates", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+                ("frames_per_chunk", ctypes.c_int64), ("launches", ctypes.c_int64),
+                ("kernel", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Timing(ctypes.Structure):
+    _fields_ = [("norm_ms", ctypes.c_double), ("match_ms", ctypes.c_double),
+                ("norm_chunks", ctypes.c_int64), ("match_launches", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libscbm.so (built by ``python -m paper_2006_13714_b200.build``). Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2006_13714_b200.build` "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    ci = ctypes.c_int
+    L.sc_bm_plan.argtypes = [ci, ci, ci, ci, ci, ci, ci, ci, ctypes.POINTER(vp)]
+    L.sc_bm_run.argtypes = [vp, vp, vp, vp, vp]
+    L.sc_bm_run_batch.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.sc_bm_run_rows.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp]
+    L.sc_bm_run_host.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.sc_bm_plan_info.argtypes = [vp, ctypes.POINTER(Info)]
+    L.sc_bm_set_kernel.argtypes = [vp, i32]
+    L.sc_bm_destroy.argtypes = [vp]
+    L.sc_status_string.argtypes = [ci]
+    L.sc_status_string.restype = ctypes.c_char_p
+    L.sc_bm_norm_map.argtypes = [vp, vp, vp, vp]
+    L.sc_bm_run_dense_debug.argtypes = [vp, vp, vp, vp]
+    L.sc_bm_set_timing.argtypes = [vp, i32]
+    L.sc_bm_get_timing.argtypes = [vp, ctypes.POINTER(Timing)]
+    for fn in EXPORTED:
+        if fn != "sc_status_string":
+            getattr(L, fn).restype = ci
+    _lib = L
+    return L
+
+
+def _check(fn, code):
+    if code != 0:
+        raise ScError(fn, code)
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Plan:
+    """A block-matching plan (``sc_bm_plan``) bound to the current CUDA device.
+
+    dtype "u8" takes uint8 images and returns exact int32 distances; "f32" takes float32
+    images and returns float32 distances. Images are [N, C, H, W] (or [C, H, W]) torch
+    tensors on the plan's device, contiguous.
+    """
+
+    def __init__(self, H, W, C, b, stride, window, K, dtype="u8"):
+        self._lib = load_library()
+        self.H, self.W, self.C, self.b, self.s, self.Wn, self.K = H, W, C, b, stride, window, K
+        self.dtype = dtype
+        code = {"u8": SC_DTYPE_U8, "f32": SC_DTYPE_F32}[dtype]
+        h = ctypes.c_void_p()
+        _check("sc_bm_plan", self._lib.sc_bm_plan(H, W, C, b, stride, window, K, code, ctypes.byref(h)))
+        self._h = h
+        inf = self.info()
+        self.ny, self.nx, self.n_refs = inf["n_ref_y"], inf["n_ref_x"], inf["n_refs"]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.sc_bm_destroy(h)
+            self._h = None
+
+    close = __del__
+
+    def info(self) -> dict:
+        out = Info()
+        _check("sc_bm_plan_info", self._lib.sc_bm_plan_info(self._h, ctypes.byref(out)))
+        return out.as_dict()
+
+    def set_timing(self, enable: bool):
+        """Record per-kernel CUDA events on the run stream (bench roofline)."""
+        _check("sc_bm_set_timing", self._lib.sc_bm_set_timing(self._h, int(enable)))
+
+    def get_timing(self) -> dict:
+        """Summed device ms of the norm / matching kernels since the last call (syncs on them)."""
+        out = Timing()
+        _check("sc_bm_get_timing", self._lib.sc_bm_get_timing(self._h, ctypes.byref(out)))
+        return {k: getattr(out, k) for k, _ in out._fields_}
+
+    def set_kernel(self, kernel: int):
+        _check("sc_bm_set_kernel", self._lib.sc_bm_set_kernel(self._h, kernel))
+
+    # ------------------------------------------------------------------ device paths
+    def _check_img(self, imgs):
+        import torch
+        if imgs.dim() == 3:
+            imgs = imgs.unsqueeze(0)
+        want = torch.uint8 if self.dtype == "u8" else torch.float32
+        if imgs.dtype != want or not imgs.is_cuda or not imgs.is_contiguous():
+            raise ValueError(f"expected a contiguous CUDA {want} tensor [N,C,H,W]")
+        if tuple(imgs.shape[1:]) != (self.C, self.H, self.W):
+            raise ValueError(f"image shape {tuple(imgs.shape)} does not match the plan")
+        return imgs
+
+    def alloc_out(self, n_images, rows=None):
+        import torch
+        refs = self.n_refs if rows is None else (rows[1] - rows[0]) * self.nx
+        dev = torch.device("cuda", torch.cuda.current_device())
+        idx = torch.empty((n_images, refs, self.K), dtype=torch.int32, device=dev)
+        dist = torch.empty((n_images, refs, self.K),
+                           dtype=torch.int32 if self.dtype == "u8" else torch.float32, device=dev)
+        return idx, dist
+
+    def run(self, imgs, out=None, stream=None):
+        """Block matching on device tensors; returns (idx, dist) [N, n_refs, K]."""
+        imgs = self._check_img(imgs)
+        idx, dist = out if out is not None else self.alloc_out(imgs.shape[0])
+        _check("sc_bm_run_batch", self._lib.sc_bm_run_batch(
+            self._h, ctypes.c_void_p(imgs.data_ptr()), imgs.shape[0], ctypes.c_void_p(idx.data_ptr()),
+            ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
+        return idx, dist
+
+    def run_rows(self, imgs, iy_begin, iy_end, out=None, stream=None):
+        """Only reference-grid rows [iy_begin, iy_end) (row-band sharding)."""
+        imgs = self._check_img(imgs)
+        idx, dist = out if out is not None else self.alloc_out(imgs.shape[0], (iy_begin, iy_end))
+        _check("sc_bm_run_rows", self._lib.sc_bm_run_rows(
+            self._h, ctypes.c_void_p(imgs.data_ptr()), imgs.shape[0], iy_begin, iy_end,
+            ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
+        return idx, dist
+
+    def run_host(self, imgs: np.ndarray | "torch.Tensor", out=None, stream=None):
+        """Host buffers in, host buffers out (pipelined H2D / match / D2H inside the library)."""
+        import torch
+        t = imgs if isinstance(imgs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(imgs))
+        if t.dim() == 3:
+            t = t.unsqueeze(0)
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("run_host expects a contiguous host tensor/array")
+        n = t.shape[0]
+        if out is None:
+            idx = torch.empty((n, self.n_refs, self.K), dtype=torch.int32)
+            dist = torch.empty((n, self.n_refs, self.K), dtype=torch.int32 if self.dtype == "u8" else torch.float32)
+        else:
+            idx, dist = out
+        _check("sc_bm_run_host", self._lib.sc_bm_run_host(
+            self._h, ctypes.c_void_p(t.data_ptr()), n, ctypes.c_void_p(idx.data_ptr()),
+            ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
+        return idx, dist
+
+    # ------------------------------------------------------------------ test exports
+    def norm_map(self, img, stream=None):
+        import torch
+        img = self._check_img(img)[0]
+        out = torch.empty((self.H - self.b + 1, self.W - self.b + 1),
+                          dtype=torch.int32 if self.dtype == "u8" else torch.float32, device=img.device)
+        _check("sc_bm_norm_map", self._lib.sc_bm_norm_map(
+            self._h, ctypes.c_void_p(img.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def dense_debug(self, img, stream=None):
+        import torch
+        img = self._check_img(img)[0]
+        out = torch.empty((self.n_refs, self.Wn * self.Wn),
+                          dtype=torch.int32 if self.dtype == "u8" else torch.float32, device=img.device)
+        _check("sc_bm_run_dense_debug", self._lib.sc_bm_run_dense_debug(
+            self._h, ctypes.c_void_p(img.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+
+def status_string(code: int) -> str:
+    return load_library().sc_status_string(code).decode()

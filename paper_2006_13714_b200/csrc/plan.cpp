@@ -1,0 +1,346 @@
+// plan.cpp -- the C ABI of include/sc_bm.h: validation, geometry, workspace, chunked
+// norm -> match scheduling on the caller's stream, and the pipelined host-buffer path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <new>
+
+#include "sc_internal.h"
+
+using namespace scbm;
+
+namespace {
+
+constexpr int kRescoreMargin = 8;  // f32: keys re-scored beyond K
+
+sc_status_t cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return SC_OK;
+  if (e == cudaErrorMemoryAllocation) return SC_ERR_OUT_OF_MEMORY;
+  return SC_ERR_CUDA;
+}
+
+size_t elem_size(int dtype) { return dtype == SC_DTYPE_U8 ? 1 : 4; }
+
+// Clipped window extent along one axis for a reference at r (readings R1/R3).
+int64_t span(int r, int lo, int hi, int maxpos) {
+  const int a = std::max(0, r + lo), b = std::min(maxpos, r + hi);
+  return b >= a ? int64_t(b - a + 1) : 0;
+}
+
+size_t per_frame_ws(const Geometry& g, int nbands) {
+  const size_t SP = size_t((g.W + 15) / 16 * 16);
+  const size_t acc = g.dtype == SC_DTYPE_U8 ? 4 : 8;
+  return SP * g.H * acc + SP * nbands * acc + size_t(g.My) * g.Mx * 4;
+}
+
+sc_status_t check_device(const sc_bm_plan_s* p) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SC_ERR_CUDA;
+  return dev == p->device ? SC_OK : SC_ERR_WRONG_DEVICE;
+}
+
+void free_ws(sc_bm_plan_s* p) {
+  if (p->ws.sat) cudaFree(p->ws.sat);
+  if (p->ws.bandsum) cudaFree(p->ws.bandsum);
+  if (p->ws.norm) cudaFree(p->ws.norm);
+  p->ws = Workspace{};
+}
+
+void free_host(sc_bm_plan_s* p) {
+  HostStaging& h = p->host;
+  if (!h.ready) return;
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(h.d_img[i]);
+    cudaFree(h.d_idx[i]);
+    cudaFree(h.d_dist[i]);
+    cudaEventDestroy(h.ev_in[i]);
+    cudaEventDestroy(h.ev_done[i]);
+    cudaEventDestroy(h.ev_out[i]);
+  }
+  cudaStreamDestroy(h.copy_in);
+  cudaStreamDestroy(h.copy_out);
+  h = HostStaging{};
+}
+
+// Enqueue norm + match for images [0, n) of imgs, chunked so the norm workspace of a chunk
+// stays resident in L2 while its matching kernel runs.
+sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, int iy_end,
+                    int32_t* idx, void* dist, void* dense, cudaStream_t st) {
+  const Geometry& g = p->g;
+  const size_t img_bytes = size_t(g.C) * g.H * g.W * elem_size(g.dtype);
+  const size_t out_elems = size_t(iy_end - iy_begin) * g.nx * g.K;
+  for (int64_t f0 = 0; f0 < n; f0 += p->F) {
+    const int F = int(std::min<int64_t>(p->F, n - f0));
+    const void* src = static_cast<const char*>(imgs) + f0 * img_bytes;
+    cudaEvent_t* ev = nullptr;
+    Timing& tm = p->timing;
+    if (tm.enabled && size_t(tm.n_used + 1) * 3 <= tm.ev.size()) {
+      ev = &tm.ev[size_t(tm.n_used) * 3];
+      ++tm.n_used;
+      cudaEventRecord(ev[0], st);
+    }
+    cudaError_t e = launch_norm(*p, src, F, st, &p->launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (ev) cudaEventRecord(ev[1], st);
+    int32_t* io = idx ? idx + f0 * out_elems : nullptr;
+    void* dd = dist ? static_cast<char*>(dist) + f0 * out_elems * 4 : nullptr;
+    e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    if (ev) cudaEventRecord(ev[2], st);
+  }
+  return SC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sc_status_string(sc_status_t s) {
+  switch (s) {
+    case SC_OK: return "SC_OK";
+    case SC_ERR_INVALID_ARGUMENT: return "SC_ERR_INVALID_ARGUMENT";
+    case SC_ERR_UNSUPPORTED: return "SC_ERR_UNSUPPORTED";
+    case SC_ERR_OUT_OF_MEMORY: return "SC_ERR_OUT_OF_MEMORY";
+    case SC_ERR_CUDA: return "SC_ERR_CUDA";
+    case SC_ERR_WRONG_DEVICE: return "SC_ERR_WRONG_DEVICE";
+  }
+  return "SC_ERR_UNKNOWN";
+}
+
+sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K, sc_dtype_t dtype,
+                       sc_bm_plan_t* plan_out) {
+  if (!plan_out) return SC_ERR_INVALID_ARGUMENT;
+  *plan_out = nullptr;
+  if (b < 1 || b > 16 || C < 1 || C > 8 || stride < 1 || window < 1 || window > 255 || K < 1 ||
+      K > 128 || H < b || W < b || int64_t(H) * W >= (int64_t(1) << 31) ||
+      (dtype != SC_DTYPE_U8 && dtype != SC_DTYPE_F32))
+    return SC_ERR_INVALID_ARGUMENT;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return SC_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return SC_ERR_CUDA;
+  if (prop.major < 10) return SC_ERR_UNSUPPORTED;  // built for sm_100a only
+
+  sc_bm_plan_s* p = new (std::nothrow) sc_bm_plan_s();
+  if (!p) return SC_ERR_OUT_OF_MEMORY;
+  p->device = dev;
+  p->sm_count = prop.multiProcessorCount;
+  Geometry& g = p->g;
+  g.H = H; g.W = W; g.C = C; g.b = b; g.s = stride; g.Wn = window; g.K = K;
+  g.dtype = dtype;
+  g.ny = (H - b) / stride + 1;
+  g.nx = (W - b) / stride + 1;
+  g.lo = -(window / 2);
+  g.hi = window - 1 - window / 2;
+  g.My = H - b + 1;
+  g.Mx = W - b + 1;
+  g.KP = dtype == SC_DTYPE_F32 ? K + kRescoreMargin : K;
+
+  // candidate counts (separable: clipped rows x clipped cols)
+  int64_t sy = 0, sx = 0, ymin = INT64_MAX, ymax = 0, xmin = INT64_MAX, xmax = 0;
+  for (int iy = 0; iy < g.ny; ++iy) {
+    const int64_t v = span(iy * stride, g.lo, g.hi, H - b);
+    sy += v; ymin = std::min(ymin, v); ymax = std::max(ymax, v);
+  }
+  for (int ix = 0; ix < g.nx; ++ix) {
+    const int64_t v = span(ix * stride, g.lo, g.hi, W - b);
+    sx += v; xmin = std::min(xmin, v); xmax = std::max(xmax, v);
+  }
+  p->total_cand = sy * sx;
+  p->min_cand = ymin * xmin;
+  p->max_cand = ymax * xmax;
+
+  p->nbands = (H + kSatBand - 1) / kSatBand;
+  // frames per chunk: keep one chunk's SAT + norm map within ~48 MB of the 126 MB L2
+  const size_t pf = per_frame_ws(g, p->nbands);
+  p->F = int(std::max<size_t>(1, std::min<size_t>(64, (48u << 20) / std::max<size_t>(pf, 1))));
+  p->tile = choose_simt_tile(g, p->sm_count, p->F);
+
+  const size_t SP = size_t((W + 15) / 16 * 16);
+  const size_t acc = dtype == SC_DTYPE_U8 ? 4 : 8;
+  cudaError_t e = cudaMalloc(&p->ws.sat, SP * H * acc * p->F);
+  if (e == cudaSuccess) e = cudaMalloc(&p->ws.bandsum, SP * p->nbands * acc * p->F);
+  if (e == cudaSuccess) e = cudaMalloc(&p->ws.norm, size_t(g.My) * g.Mx * 4 * p->F);
+  if (e != cudaSuccess) {
+    free_ws(p);
+    delete p;
+    cudaGetLastError();
+    return cuda_status(e);
+  }
+  p->ws.bytes = per_frame_ws(g, p->nbands) * p->F;
+  *plan_out = p;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_run_rows(sc_bm_plan_t p, const void* imgs, int64_t n_images, int32_t iy_begin,
+                           int32_t iy_end, int32_t* idx_out, void* dist_out, sc_stream_t stream) {
+  if (!p || !imgs || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
+  if (iy_begin < 0 || iy_end > p->g.ny || iy_end < iy_begin) return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  if (n_images == 0 || iy_end == iy_begin) return SC_OK;
+  return enqueue(p, imgs, n_images, iy_begin, iy_end, idx_out, dist_out, nullptr,
+                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+sc_status_t sc_bm_run_batch(sc_bm_plan_t p, const void* imgs, int64_t n_images, int32_t* idx_out,
+                            void* dist_out, sc_stream_t stream) {
+  if (!p) return SC_ERR_INVALID_ARGUMENT;
+  return sc_bm_run_rows(p, imgs, n_images, 0, p->g.ny, idx_out, dist_out, stream);
+}
+
+sc_status_t sc_bm_run(sc_bm_plan_t p, const void* img, int32_t* idx_out, void* dist_out,
+                      sc_stream_t stream) {
+  return sc_bm_run_batch(p, img, 1, idx_out, dist_out, stream);
+}
+
+sc_status_t sc_bm_run_dense_debug(sc_bm_plan_t p, const void* img, void* dist_all, sc_stream_t stream) {
+  if (!p || !img || !dist_all) return SC_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(img) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  return enqueue(p, img, 1, 0, p->g.ny, nullptr, nullptr, dist_all,
+                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_stream_t stream) {
+  if (!p || !img || !norm_out) return SC_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(img) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_norm(*p, img, 1, st, &p->launches);
+  if (e != cudaSuccess) return cuda_status(e);
+  e = cudaMemcpyAsync(norm_out, p->ws.norm, size_t(p->g.My) * p->g.Mx * 4, cudaMemcpyDeviceToDevice, st);
+  return cuda_status(e);
+}
+
+sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images, int32_t* h_idx,
+                           void* h_dist, sc_stream_t stream) {
+  if (!p || !h_imgs || !h_idx || !h_dist || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  if (n_images == 0) return SC_OK;
+  const Geometry& g = p->g;
+  HostStaging& h = p->host;
+  const size_t img_bytes = size_t(g.C) * g.H * g.W * elem_size(g.dtype);
+  const size_t out_elems = size_t(g.ny) * g.nx * g.K;
+  cudaError_t e = cudaSuccess;
+  if (!h.ready) {
+    h.F = p->F;
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&h.d_img[i], img_bytes * h.F);
+      if (e == cudaSuccess) e = cudaMalloc(&h.d_idx[i], out_elems * 4 * h.F);
+      if (e == cudaSuccess) e = cudaMalloc(&h.d_dist[i], out_elems * 4 * h.F);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.ev_done[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.ev_out[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h.copy_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h.copy_out, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      h.ready = true;
+      free_host(p);
+      cudaGetLastError();
+      return cuda_status(e);
+    }
+    h.ready = true;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // double-buffered pipeline: H2D(chunk k+1) || match(chunk k) || D2H(chunk k-1)
+  int64_t k = 0;
+  for (int64_t f0 = 0; f0 < n_images; f0 += h.F, ++k) {
+    const int slot = int(k & 1);
+    const int F = int(std::min<int64_t>(h.F, n_images - f0));
+    if (k >= 2) cudaStreamWaitEvent(h.copy_in, h.ev_out[slot], 0);  // slot's D2H finished
+    e = cudaMemcpyAsync(h.d_img[slot], static_cast<const char*>(h_imgs) + f0 * img_bytes,
+                        img_bytes * F, cudaMemcpyHostToDevice, h.copy_in);
+    if (e != cudaSuccess) return cuda_status(e);
+    cudaEventRecord(h.ev_in[slot], h.copy_in);
+    cudaStreamWaitEvent(st, h.ev_in[slot], 0);
+    s = enqueue(p, h.d_img[slot], F, 0, g.ny, h.d_idx[slot], h.d_dist[slot], nullptr, st);
+    if (s != SC_OK) return s;
+    cudaEventRecord(h.ev_done[slot], st);
+    cudaStreamWaitEvent(h.copy_out, h.ev_done[slot], 0);
+    e = cudaMemcpyAsync(h_idx + f0 * out_elems, h.d_idx[slot], out_elems * 4 * F,
+                        cudaMemcpyDeviceToHost, h.copy_out);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<char*>(h_dist) + f0 * out_elems * 4, h.d_dist[slot],
+                          out_elems * 4 * F, cudaMemcpyDeviceToHost, h.copy_out);
+    if (e != cudaSuccess) return cuda_status(e);
+    cudaEventRecord(h.ev_out[slot], h.copy_out);
+  }
+  e = cudaStreamSynchronize(h.copy_out);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_status(e);
+}
+
+sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
+  if (!p || !info) return SC_ERR_INVALID_ARGUMENT;
+  std::memset(info, 0, sizeof(*info));
+  info->n_ref_y = p->g.ny;
+  info->n_ref_x = p->g.nx;
+  info->n_refs = int64_t(p->g.ny) * p->g.nx;
+  info->min_candidates = p->min_cand;
+  info->max_candidates = p->max_cand;
+  info->total_candidates = p->total_cand;
+  info->workspace_bytes = int64_t(p->ws.bytes);
+  info->frames_per_chunk = p->F;
+  info->launches = p->launches;
+  info->kernel = p->kernel;
+  info->device = p->device;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
+  if (!p) return SC_ERR_INVALID_ARGUMENT;
+  if (kernel != SC_KERNEL_SIMT) return SC_ERR_UNSUPPORTED;
+  p->kernel = kernel;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_set_timing(sc_bm_plan_t p, int32_t enable) {
+  if (!p) return SC_ERR_INVALID_ARGUMENT;
+  Timing& tm = p->timing;
+  if (enable && tm.ev.empty()) {
+    tm.ev.resize(3 * 8192);
+    for (auto& e : tm.ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return SC_ERR_CUDA;
+  }
+  tm.enabled = enable != 0;
+  tm.n_used = 0;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_get_timing(sc_bm_plan_t p, sc_bm_timing_t* out) {
+  if (!p || !out) return SC_ERR_INVALID_ARGUMENT;
+  std::memset(out, 0, sizeof(*out));
+  Timing& tm = p->timing;
+  for (int i = 0; i < tm.n_used; ++i) {
+    cudaEvent_t* ev = &tm.ev[size_t(i) * 3];
+    if (cudaEventSynchronize(ev[2]) != cudaSuccess) return SC_ERR_CUDA;
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    out->norm_ms += a;
+    out->match_ms += b;
+  }
+  out->norm_chunks = tm.n_used;
+  out->match_launches = tm.n_used;
+  tm.n_used = 0;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_destroy(sc_bm_plan_t p) {
+  if (!p) return SC_OK;
+  for (auto& e : p->timing.ev) cudaEventDestroy(e);
+  free_host(p);
+  free_ws(p);
+  delete p;
+  return SC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// sc_internal.h -- plan struct and kernel launchers shared by plan.cpp and the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/sc_bm.h"
+
+namespace scbm {
+
+struct Geometry {
+  int H, W, C, b, s, Wn, K;
+  int dtype;          // SC_DTYPE_*
+  int ny, nx;         // reference grid
+  int lo, hi;         // window offsets
+  int My, Mx;         // valid candidate positions (H-b+1, W-b+1)
+  int KP;             // keys kept per ref before output (K, or K+rescore margin for f32)
+};
+
+// Workspace for one chunk of frames.
+struct Workspace {
+  void* sat = nullptr;      // [F][H+1][W+1] uint32 (u8) or double (f32)
+  void* bandsum = nullptr;  // [F][nbands][W+1] column band totals
+  void* norm = nullptr;     // [F][My][Mx] int32 (u8) or float (f32)
+  size_t bytes = 0;
+};
+
+struct HostStaging {
+  bool ready = false;
+  int F = 0;                 // frames per chunk
+  void* d_img[2] = {nullptr, nullptr};
+  int32_t* d_idx[2] = {nullptr, nullptr};
+  void* d_dist[2] = {nullptr, nullptr};
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+};
+
+struct Timing {
+  bool enabled = false;
+  int n_used = 0;                  // event triples used since the last read
+  std::vector<cudaEvent_t> ev;     // 3 events per chunk: before norm, between, after match
+};
+
+struct TileCfg {
+  int TRY, TRX;  // reference tile (ref-grid units) per CTA
+  int VY;        // vertical candidates per lane
+  int warps;     // warps per CTA
+  size_t smem;   // dynamic shared memory bytes
+};
+
+}  // namespace scbm
+
+struct sc_bm_plan_s {
+  scbm::Geometry g;
+  int device = 0;
+  int sm_count = 148;
+  int kernel = SC_KERNEL_SIMT;
+  int F = 1;  // frames per chunk
+  int nbands = 1;
+  scbm::Workspace ws;
+  scbm::TileCfg tile;
+  scbm::HostStaging host;
+  scbm::Timing timing;
+  int64_t launches = 0;
+  int64_t min_cand = 0, max_cand = 0, total_cand = 0;
+};
+
+namespace scbm {
+
+constexpr int kSatBand = 32;  // rows per column-scan band
+
+// norm.cu: integral image of x'^2 and the 4-corner norm map for F frames.
+cudaError_t launch_norm(const sc_bm_plan_s& p, const void* imgs, int F, cudaStream_t st,
+                        int64_t* launches);
+
+// bm_simt.cu: fused cross term + distance assembly + top-K (+ f32 re-score) for F frames.
+// dense != nullptr selects the debug mode that writes every window distance instead.
+cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin,
+                           int iy_end, int32_t* idx_out, void* dist_out, void* dense,
+                           cudaStream_t st, int64_t* launches);
+TileCfg choose_simt_tile(const Geometry& g, int sm_count, int n_images);
+
+}  // namespace scbm

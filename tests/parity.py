@@ -1,0 +1,78 @@
+"""Parity rules, shared by the GPU tests and smoke().
+
+* u8 : idx and dist equal the oracle element-wise, bit-exact, order included.
+* f32: for every reference r, with D(r,c) the oracle's double distance, O_r its top-K set
+  and d_K its K-th distance:
+    1. the GPU's K indices are distinct valid candidates of r's clipped window;
+    2. |dist - D(r, idx)| <= REL * D(r, idx); the self pair has dist == 0 exactly;
+    3. each row is sorted ascending by (dist, idx);
+    4. (GPU set) symmetric-difference O_r  is a subset of {c : |D(r,c) - d_K| <= REL * d_K}.
+  REL = 1e-5 (BASELINE.json north_star).
+"""
+import numpy as np
+
+import oracle
+
+REL = 1e-5
+
+
+def check_u8(gi, gd, oi, od, where=""):
+    gi, gd, oi, od = (np.asarray(x) for x in (gi, gd, oi, od))
+    assert gi.shape == oi.shape, (gi.shape, oi.shape)
+    bad = np.argwhere((gi != oi) | (gd != od))
+    assert bad.size == 0, f"{where}: {len(bad)} mismatches, first at {bad[:3].tolist()}: " \
+        f"gpu {gi[tuple(bad[0][:-1])].tolist()} / {gd[tuple(bad[0][:-1])].tolist()} vs " \
+        f"oracle {oi[tuple(bad[0][:-1])].tolist()} / {od[tuple(bad[0][:-1])].tolist()}"
+
+
+def check_f32(img, b, s, Wn, K, gi, gd, oi, od, iy_range=None, rel=REL, where=""):
+    """img [C,H,W] float32; gi/gd/oi/od [refs, K] for reference rows iy_range of one image."""
+    C, H, W = img.shape
+    ny, nx = oracle.grid(H, W, b, s)
+    iy0, iy1 = iy_range if iy_range is not None else (0, ny)
+    gi, gd, oi, od = (np.asarray(x) for x in (gi, gd, oi, od))
+    refs = (iy1 - iy0) * nx
+    assert gi.shape == (refs, K) and oi.shape == (refs, K)
+    lo, hi = -(Wn // 2), Wn - 1 - Wn // 2
+    t = np.arange(refs)
+    ry = (iy0 + t // nx) * s
+    rx = (t % nx) * s
+    cy0, cy1 = np.maximum(0, ry + lo), np.minimum(H - b, ry + hi)
+    cx0, cx1 = np.maximum(0, rx + lo), np.minimum(W - b, rx + hi)
+    ncand = (cy1 - cy0 + 1) * (cx1 - cx0 + 1)
+    valid_slot = np.arange(K)[None, :] < np.minimum(ncand, K)[:, None]
+    # padding slots
+    assert ((gi == -1) == ~valid_slot).all(), f"{where}: padding mismatch"
+    assert np.isinf(gd[~valid_slot]).all()
+    gcy, gcx = np.where(valid_slot, gi // W, 0), np.where(valid_slot, gi % W, 0)
+    # 1. valid candidates of the window, distinct
+    inwin = (gcy >= cy0[:, None]) & (gcy <= cy1[:, None]) & (gcx >= cx0[:, None]) & (gcx <= cx1[:, None])
+    assert (inwin | ~valid_slot).all(), f"{where}: candidate outside its window"
+    srt = np.sort(np.where(valid_slot, gi, -1 - np.arange(K)[None, :]), axis=1)
+    assert (np.diff(srt, axis=1) != 0).all(), f"{where}: duplicate indices"
+    # 2. distances within rel of the oracle's direct distance; self pair exact 0
+    RY, RX = np.broadcast_to(ry[:, None], gi.shape), np.broadcast_to(rx[:, None], gi.shape)
+    D = np.zeros(gi.shape)
+    m = valid_slot
+    D[m] = oracle.pair_dist(img, b, RY[m], RX[m], gcy[m], gcx[m])
+    err = np.abs(gd.astype(np.float64) - D)
+    assert (err[m] <= rel * D[m]).all(), f"{where}: max rel err {np.max(err[m] / np.maximum(D[m], 1e-300)):.3g}"
+    is_self = m & (gcy == RY) & (gcx == RX)
+    assert (gd[is_self] == 0).all(), f"{where}: self distance not exactly 0"
+    # 3. sorted by (dist, idx)
+    d64 = gd.astype(np.float64)
+    ok_order = (d64[:, 1:] > d64[:, :-1]) | ((d64[:, 1:] == d64[:, :-1]) & (gi[:, 1:] > gi[:, :-1]))
+    ok_order |= ~valid_slot[:, 1:]
+    assert ok_order.all(), f"{where}: row not sorted by (dist, idx)"
+    # 4. set difference only within tolerance of the K-th distance
+    for r in range(refs):
+        k = int(min(ncand[r], K))
+        gs = set(gi[r, :k].tolist())
+        os_ = set(oi[r, :k].tolist())
+        if gs == os_:
+            continue
+        dK = od[r, k - 1]
+        dmap = dict(zip(oi[r, :k].tolist(), od[r, :k].tolist()))
+        dmap.update(zip(gi[r, :k].tolist(), D[r, :k].tolist()))
+        for c in gs ^ os_:
+            assert abs(dmap[c] - dK) <= rel * dK, f"{where}: ref {r} set differs beyond tolerance"

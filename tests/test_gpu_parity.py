@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs. u8 bit-exact; f32 per the tolerance rule in tests/parity.py."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2006_13714_b200 import synth
+from tests.parity import check_f32, check_u8
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _plan(cfg_or_args, dtype=None):
+    from paper_2006_13714_b200.bm import Plan
+    if isinstance(cfg_or_args, synth.BMConfig):
+        c = cfg_or_args
+        return Plan(c.H, c.W, c.C, c.b, c.s, c.Wn, c.K, c.dtype)
+    return Plan(*cfg_or_args, dtype)
+
+
+def _run(plan, x):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    idx, dist = plan.run(t)
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), dist.cpu().numpy()
+
+
+def _compare(x, b, s, Wn, K, dtype, where=""):
+    N, C, H, W = x.shape
+    p = _plan((H, W, C, b, s, Wn, K), dtype)
+    gi, gd = _run(p, x)
+    oi, od = oracle.bm(x, b, s, Wn, K)
+    if dtype == "u8":
+        check_u8(gi, gd, oi, od, where)
+    else:
+        for n in range(N):
+            check_f32(x[n], b, s, Wn, K, gi[n], gd[n], oi[n], od[n], where=f"{where} img{n}")
+
+
+# ------------------------------------------------------------------ steps a1 and a2+a3
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+@pytest.mark.parametrize("C,H,W,b", [(1, 64, 64, 8), (1, 37, 53, 7), (4, 40, 33, 8), (3, 19, 100, 1), (2, 30, 30, 16)])
+def test_norm_map(dtype, C, H, W, b):
+    rng = np.random.Generator(np.random.PCG64(H * W + C))
+    x = synth.random_image(rng, 1, C, H, W, dtype)[0]
+    p = _plan((H, W, C, b, 1, 3, 1), dtype)
+    got = p.norm_map(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    if dtype == "u8":
+        want = oracle.norm_map(x.astype(np.float64) - 128.0, b)
+        np.testing.assert_array_equal(got, want)
+    else:
+        xc = (x - np.float32(0.5)).astype(np.float32).astype(np.float64)
+        want = oracle.norm_map(xc, b)
+        np.testing.assert_allclose(got, want, rtol=2e-7, atol=0)
+
+
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+@pytest.mark.parametrize("C,H,W,b,s,Wn", [(1, 64, 64, 8, 4, 21), (1, 40, 45, 7, 1, 13), (4, 36, 41, 8, 3, 17),
+                                          (1, 20, 20, 3, 2, 30), (2, 33, 29, 12, 5, 9)])
+def test_dense_cross_term(dtype, C, H, W, b, s, Wn):
+    rng = np.random.Generator(np.random.PCG64(7 * H + W))
+    x = synth.random_image(rng, 1, C, H, W, dtype)[0]
+    p = _plan((H, W, C, b, s, Wn, 1), dtype)
+    got = p.dense_debug(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    want = oracle.bm_dense(x, b, s, Wn)
+    np.testing.assert_array_equal(got == -1, want == -1)
+    if dtype == "u8":
+        np.testing.assert_array_equal(got, want)
+    else:
+        # identity in fp32 on centred data: error relative to the norms, not to d
+        scale = b * b * C * 0.25
+        m = want >= 0
+        assert np.max(np.abs(got[m] - want[m])) <= 4e-6 * scale + 1e-5 * np.max(want[m])
+
+
+# ------------------------------------------------------------------ configs
+def test_c1_full_bitexact():
+    cfg = synth.CONFIGS["c1"]
+    x = synth.make_input(cfg)
+    p = _plan(cfg)
+    gi, gd = _run(p, x)
+    oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K)
+    check_u8(gi, gd, oi, od, "c1")
+    assert (gd[..., 0] == 0).all()
+
+
+def test_c5_full_batch_sampled():
+    """The bench launch configuration (all 64 frames in one call), sampled outputs."""
+    cfg = synth.CONFIGS["c5"]
+    x = synth.make_input(cfg)
+    p = _plan(cfg)
+    gi, gd = _run(p, x)
+    ny = p.ny
+    bands = [(0, 3), (ny // 2 - 1, ny // 2 + 1), (ny - 3, ny)]
+    for f in (0, 1, 37, 63):
+        for r0, r1 in bands:
+            oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=(f, f + 1), rows=(r0, r1))
+            sl = slice(r0 * p.nx, r1 * p.nx)
+            check_u8(gi[f:f + 1, sl], gd[f:f + 1, sl], oi, od, f"c5 frame {f} rows {r0}:{r1}")
+
+
+def test_c2_full():
+    cfg = synth.CONFIGS["c2"]
+    x = synth.make_input(cfg)
+    p = _plan(cfg)
+    gi, gd = _run(p, x)
+    oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K)
+    check_f32(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0], gd[0], oi[0], od[0], where="c2")
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_c3_c4_sampled_rows(name):
+    cfg = synth.CONFIGS[name]
+    x = synth.make_input(cfg)
+    p = _plan(cfg)
+    gi, gd = _run(p, x)
+    ny = p.ny
+    for r0, r1 in [(0, 2), (ny // 2, ny // 2 + 2), (ny - 2, ny)]:
+        oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, rows=(r0, r1))
+        sl = slice(r0 * p.nx, r1 * p.nx)
+        check_f32(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0, sl], gd[0, sl], oi[0], od[0],
+                  iy_range=(r0, r1), where=f"{name} rows {r0}:{r1}")
+
+
+# ------------------------------------------------------------------ random sweeps
+def _sweep_cases(n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = []
+    while len(out) < n:
+        b = int(rng.integers(1, 17))
+        C = int(rng.choice([1, 1, 1, 2, 3, 4, 8]))
+        H = int(rng.integers(b, b + 60))
+        W = int(rng.integers(b, b + 70))
+        s = int(rng.integers(1, 6))
+        Wn = int(rng.integers(1, 42))
+        K = int(rng.integers(1, 129))
+        pairs = ((H - b) // s + 1) * ((W - b) // s + 1) * Wn * Wn * b * b * C
+        if pairs > 3e8:
+            continue
+        out.append((C, H, W, b, s, Wn, K))
+    return out
+
+
+@pytest.mark.parametrize("case", _sweep_cases(24, 101))
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_random_sweep(case, dtype):
+    C, H, W, b, s, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 2, C, H, W, dtype)
+    _compare(x, b, s, Wn, K, dtype, where=f"{dtype} {case}")
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_constant_image_ties(dtype):
+    x = np.full((1, 1, 41, 37), 200 if dtype == "u8" else 0.75, dtype=np.uint8 if dtype == "u8" else np.float32)
+    N, C, H, W = x.shape
+    p = _plan((H, W, C, 6, 3, 15, 40), dtype)
+    gi, gd = _run(p, x)
+    oi, od = oracle.bm(x, 6, 3, 15, 40)
+    np.testing.assert_array_equal(gi, oi)  # all ties: the (distance, idx) order decides
+    assert (gd[gi >= 0] == 0).all()
+
+
+def test_periodic_tiling_duplicates_u8():
+    rng = np.random.Generator(np.random.PCG64(5))
+    motif = rng.integers(0, 256, size=(8, 8), dtype=np.uint8)
+    x = np.tile(motif, (9, 11))[None, None].copy()
+    _compare(x, 8, 4, 33, 16, "u8", where="periodic")
+
+
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+@pytest.mark.parametrize("H,W,b,s,Wn,K", [
+    (30, 31, 5, 2, 1, 3),        # Wn = 1: self only, padding
+    (12, 14, 4, 1, 41, 128),     # window covers the image; K > candidates
+    (16, 16, 16, 1, 5, 2),       # single position
+    (17, 40, 16, 3, 9, 20),      # max patch side
+    (50, 9, 3, 4, 6, 7),         # even window
+    (64, 64, 8, 64, 21, 16),     # stride larger than the image: one ref row/col
+])
+def test_edge_geometry(dtype, H, W, b, s, Wn, K):
+    rng = np.random.Generator(np.random.PCG64(H + W + b))
+    x = synth.random_image(rng, 1, 1, H, W, dtype)
+    _compare(x, b, s, Wn, K, dtype, where=f"edge {H}x{W} b{b} s{s} Wn{Wn} K{K}")
+
+
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_eight_channels(dtype):
+    rng = np.random.Generator(np.random.PCG64(88))
+    x = synth.random_image(rng, 1, 8, 30, 34, dtype)
+    _compare(x, 5, 2, 11, 9, dtype, where="C=8")
+
+
+def test_saturated_u8_extremes():
+    rng = np.random.Generator(np.random.PCG64(9))
+    x = (rng.integers(0, 2, size=(1, 1, 48, 48)) * 255).astype(np.uint8)  # max |x-128|
+    _compare(x, 16, 2, 13, 32, "u8", where="saturated")
+
+
+# ------------------------------------------------------------------ API behaviour
+def test_rows_band_matches_full():
+    cfg = synth.CONFIGS["c1"]
+    x = torch.from_numpy(synth.make_input(cfg)).cuda()
+    p = _plan(cfg)
+    fi, fd = p.run(x)
+    bi, bd = p.run_rows(x, 4, 9)
+    torch.cuda.synchronize()
+    sl = slice(4 * p.nx, 9 * p.nx)
+    assert torch.equal(bi[0], fi[0, sl]) and torch.equal(bd[0], fd[0, sl])
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_host_path_matches_device(name):
+    cfg = synth.CONFIGS[name]
+    xn = synth.make_input(cfg)
+    xn = np.concatenate([xn] * 3)  # several chunks
+    p = _plan(cfg)
+    di, dd = p.run(torch.from_numpy(xn).cuda())
+    hi, hd = p.run_host(torch.from_numpy(xn).pin_memory())
+    torch.cuda.synchronize()
+    assert torch.equal(hi, di.cpu()) and torch.equal(hd, dd.cpu())
+
+
+def test_misaligned_pointer_rejected():
+    from paper_2006_13714_b200.bm import ScError
+    p = _plan((32, 32, 1, 8, 4, 9, 4), "u8")
+    buf = torch.zeros(32 * 32 + 16, dtype=torch.uint8, device="cuda")
+    x = buf[1:1 + 32 * 32].view(1, 1, 32, 32)
+    with pytest.raises(ScError) as e:
+        p.run(x)
+    assert e.value.code == 1
+
+
+def test_launch_counter_and_info():
+    cfg = synth.CONFIGS["c5"]
+    p = _plan(cfg)
+    inf = p.info()
+    assert inf["n_refs"] == 269 * 479
+    assert inf["total_candidates"] * 64 == 8_854_426_816
+    assert inf["min_candidates"] == 289 and inf["max_candidates"] == 1089

@@ -289,3 +289,21 @@ def test_torch_conv2d_special_case():
         order = np.lexsort((ii, np.round(dd, 9)))[:K]
         np.testing.assert_array_equal(i_o[0, t], ii[order])
         np.testing.assert_allclose(d_o[0, t], dd[order], rtol=1e-9, atol=1e-9)
+
+
+def test_pair_dist_matches_dense():
+    rng = _rng(20)
+    img = rng.random((2, 21, 23))
+    b, s, Wn = 5, 3, 7
+    dense = oracle.bm_dense(img, b, s, Wn)
+    ny, nx = oracle.grid(21, 23, b, s)
+    R, Cc, V = [], [], []
+    for t in range(ny * nx):
+        ry, rx = (t // nx) * s, (t % nx) * s
+        for a in range(Wn):
+            for c in range(Wn):
+                if dense[t, a * Wn + c] >= 0:
+                    R.append((ry, rx)); Cc.append((ry + a - 3, rx + c - 3)); V.append(dense[t, a * Wn + c])
+    R, Cc = np.array(R), np.array(Cc)
+    out = oracle.pair_dist(img, b, R[:, 0], R[:, 1], Cc[:, 0], Cc[:, 1])
+    np.testing.assert_array_equal(out, np.array(V))
