@@ -1,0 +1,88 @@
+"""Multi-GPU partitioner (one process per GPU, torch.distributed for the plumbing).
+
+Block matching shards with no data-path exchange: every reference is independent given read
+access to its search window (Eq. 3 with footnote 2). Two splits:
+
+* frames: rank g of G owns a contiguous, balanced range of the batch's images (config c5);
+* row bands: rank g owns a contiguous, balanced range of reference-grid rows of one image;
+  the image is replicated (1-13 MB), each rank calls ``sc_bm_run_rows`` for its band.
+
+The only exchange the method has is collecting the result tables. ``gather_tables`` does it
+with ``all_gather_into_tensor`` (NCCL over NVLink on GPUs; gloo in the CPU tests) after
+padding every shard to the largest shard, then strips the padding.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Sequence, Tuple
+
+
+def balanced_ranges(n: int, world: int) -> List[Tuple[int, int]]:
+    """Split range(n) into `world` contiguous ranges whose sizes differ by at most one."""
+    if world < 1 or n < 0:
+        raise ValueError("balanced_ranges: world >= 1 and n >= 0 required")
+    base, extra = divmod(n, world)
+    out, start = [], 0
+    for r in range(world):
+        size = base + (1 if r < extra else 0)
+        out.append((start, start + size))
+        start += size
+    return out
+
+
+def frame_shard(n_frames: int, rank: int, world: int) -> Tuple[int, int]:
+    return balanced_ranges(n_frames, world)[rank]
+
+
+def band_shard(n_ref_rows: int, rank: int, world: int) -> Tuple[int, int]:
+    return balanced_ranges(n_ref_rows, world)[rank]
+
+
+def gather_tables(tables: Sequence, counts: Sequence[int], group=None):
+    """All-gather per-rank tables along dim 0 (uneven shards padded to the largest).
+
+    tables: tensors [count_r, ...] of this rank (same trailing shape / dtype on every rank);
+    counts: the leading size of every rank's shard. Returns full tensors [sum(counts), ...].
+    """
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    mx = max(counts)
+    out = []
+    for t in tables:
+        if t.shape[0] != counts[dist.get_rank(group)]:
+            raise ValueError("gather_tables: local shard size does not match counts")
+        pad = t
+        if t.shape[0] < mx:
+            pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            pad[: t.shape[0]] = t
+        full = torch.empty((world * mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(full, pad.contiguous(), group=group)
+        parts = [full[r * mx: r * mx + counts[r]] for r in range(world)]
+        out.append(torch.cat(parts, 0))
+    return out
+
+
+def run_frames_sharded(run: Callable, frames, rank: int, world: int, gather: bool = True, group=None):
+    """Frame-parallel BM. `run(local_frames) -> (idx, dist)` is the local plan's run (the CUDA
+    path on GPUs). `frames` is the full batch (each rank slices its range). Returns the local
+    tables, or the full gathered tables when `gather`."""
+    n = frames.shape[0]
+    a, b = frame_shard(n, rank, world)
+    idx, dist_ = run(frames[a:b])
+    if not gather or world == 1:
+        return idx, dist_
+    counts = [e - s for s, e in balanced_ranges(n, world)]
+    return tuple(gather_tables([idx, dist_], counts, group))
+
+
+def run_bands_sharded(run_rows: Callable, img, n_ref_rows: int, n_ref_x: int, rank: int, world: int,
+                      gather: bool = True, group=None):
+    """Row-band BM of one image. `run_rows(img, iy0, iy1) -> (idx, dist)` shaped [1, refs_band, K].
+    Returns local or gathered tables ([1, n_refs, K] in reference raster order)."""
+    iy0, iy1 = band_shard(n_ref_rows, rank, world)
+    idx, dist_ = run_rows(img, iy0, iy1)
+    if not gather or world == 1:
+        return idx, dist_
+    counts = [(e - s) * n_ref_x for s, e in balanced_ranges(n_ref_rows, world)]
+    gi, gd = gather_tables([idx[0], dist_[0]], counts, group)
+    return gi[None], gd[None]

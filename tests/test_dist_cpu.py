@@ -1,0 +1,85 @@
+"""Multi-process partitioner logic on CPU (gloo, world_size 2 and 3): frame sharding, row-band
+sharding and the table gather reassemble exactly the single-process result. The local compute
+is the CPU oracle here (no GPU); on GPUs it is the plan's CUDA run."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2006_13714_b200 import dist as sdist
+
+
+def test_balanced_ranges():
+    assert sdist.balanced_ranges(64, 8) == [(8 * i, 8 * i + 8) for i in range(8)]
+    r = sdist.balanced_ranges(10, 4)
+    assert r == [(0, 3), (3, 6), (6, 8), (8, 10)]
+    assert sdist.balanced_ranges(2, 4) == [(0, 1), (1, 2), (2, 2), (2, 2)]
+    for n in range(0, 40):
+        for w in range(1, 9):
+            rr = sdist.balanced_ranges(n, w)
+            assert rr[0][0] == 0 and rr[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rr, rr[1:]))
+            sizes = [e - s for s, e in rr]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mode, q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.Generator(np.random.PCG64(3))
+        b, s, Wn, K = 5, 2, 9, 7
+        if mode == "frames":
+            frames = rng.integers(0, 256, size=(5, 1, 20, 23), dtype=np.uint8)
+
+            def run(local):
+                i, d = oracle.bm(local, b, s, Wn, K)
+                return torch.from_numpy(i), torch.from_numpy(d)
+
+            gi, gd = sdist.run_frames_sharded(run, frames, rank, world)
+            wi, wd = oracle.bm(frames, b, s, Wn, K)
+        else:
+            img = rng.random((1, 2, 31, 22)).astype(np.float32)
+            ny, nx = oracle.grid(31, 22, b, s)
+
+            def run_rows(x, iy0, iy1):
+                i, d = oracle.bm(x, b, s, Wn, K, rows=(iy0, iy1))
+                return torch.from_numpy(i), torch.from_numpy(d)
+
+            gi, gd = sdist.run_bands_sharded(run_rows, img, ny, nx, rank, world)
+            wi, wd = oracle.bm(img, b, s, Wn, K)
+        ok = np.array_equal(gi.numpy(), wi) and np.array_equal(gd.numpy(), wd)
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["frames", "bands"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gather_equals_single_process(mode, world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(ok for _, ok in res), res
