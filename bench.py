@@ -253,10 +253,14 @@ def main():
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if info["kernel"] == 1:
         peak = 2.0 * peaks["bf16_tflops"]  # int8 tcgen05 = 2x the measured bf16 (guide's nominal ratio)
-        bound, unit, peak_note = "tensor", "TFLOP/s", "int8 = 2 x measured bf16 burst (MEASURED_PEAKS.json)"
+        bound, unit, peak_note = "tensor", "TOP/s", "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json x guide ratio)"
+    elif cfg.dtype == "u8":
+        # dp4a: 64 lanes/SM/clk (half rate, measured by tools/peaks.cu) x 4 MACs x 2 ops
+        peak = 148 * 64 * 4 * 2 * sm_mhz * 1e6 / 1e12
+        bound, unit, peak_note = "alu", "TOP/s", "dp4a: 148 SM x 64 lanes x 4 MAC x 2 x sm_max_mhz (DESIGN.md section 7)"
     else:
-        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # FP32/INT32 FMA lanes x 2 ops x max clock
-        bound, unit, peak_note = "alu", "TFLOP/s", "148 SM x 128 FMA lanes x 2 x sm_max_mhz (derived, DESIGN.md)"
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # FP32 FFMA lanes x 2 ops x max clock
+        bound, unit, peak_note = "alu", "TFLOP/s", "FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md section 7)"
     achieved = 2.0 * macs_launch / (match_ms / 1e3) / 1e12 if match_ms > 0 else None
     roof = {"bound": bound, "kernel": "bm_simt_kernel" if info["kernel"] == 0 else "bm_tc_i8_kernel",
             "achieved": achieved, "peak": peak, "unit": unit,

@@ -1,40 +1,30 @@
-// bm_simt.cu -- steps a0, a2, a3, a4 (+ a5 for f32) fused in one CUDA-core kernel.
+// bm_simt.cu -- steps a0, a2, a3, a4 (+ a5 for f32), a6 fused in one CUDA-core kernel.
 //
 //   a0 staging   one CTA owns a TRY x TRX tile of references; it stages the image region
-//                covering the union of their clipped windows plus the patch extent
-//                (the "window halo"), centred (u8: x-128, f32: x-0.5), and the matching
-//                tile of the norm map, in shared memory.
-//   a2 cross     C_i(j) = <X'_i, X'_j> (Self-Convolution, Eq. 5, channels
-//                summed, Eq. 12): one warp per reference; the reference patch lives in
-//                registers; each lane slides over VY vertically adjacent candidates of one
-//                column, so every image row it loads feeds up to VY patch rows
-//                (VY*b^2 FMAs per (b+VY-1)*b shared loads).
-//   a3 assembly  d' = n_c - 2 C (Lemma 2, with ||X_i||^2 deferred: it is
-//                constant per reference, so ranking by d' is ranking by d; Theorem 1's
-//                b_i = -d'/2).
-//   a4 top-K     threshold filter + warp bitonic merges on packed keys (topk.cuh).
-//   a5 re-score  f32 only: the best K+8 keys are re-scored by direct differences
+//                covering the union of their clipped windows plus the patch extent (the
+//                "window halo"), centred, in shared memory, and the matching tile of the norm
+//                map. u8: x' = x ^ 0x80 (= x - 128 as int8) stored as FOUR byte-shifted copies of
+//                packed int8 words so any 4-byte run of a row is one aligned 32-bit load
+//                (copies interleaved 8 banks apart: conflict-free across a warp); f32: x - 0.5.
+//   a2 cross     C_i(j) = <X'_i, X'_j> (Self-Convolution, Eq. 5; channels
+//                summed, Eq. 12): one warp per reference, the reference patch in registers;
+//                each lane slides over VY vertically adjacent candidates of one column, so every
+//                image row it loads feeds up to VY patch rows. u8 uses dp4a (4 int8 MACs per
+//                instruction, exact int32); f32 uses fp32 FMA.
+//   a3 assembly  d' = n_c - 2 C (Lemma 2, ||X_i||^2 deferred: constant per
+//                reference; Theorem 1's b_i = -d'/2).
+//   a4 top-K     32-bit threshold filter (ord(d') <= ord of the KP-th key: a superset, exact
+//                ties resolved in the merge) + register-resident warp merges (topk.cuh).
+//   a5 re-score  f32 only: the best KP = K+8 keys are re-scored by direct differences
 //                sum (x_r - x_c)^2 in fp32 from the uncentred input and re-sorted.
 //   a6 output    coalesced stores of K idx + K dist per reference; u8 dist = d' + n_r exact.
-//
-// u8 arithmetic is exact int32 (|C'| <= 64*128^2 = 2^20 per channel); f32 is fp32 FMA.
 #include "sc_internal.h"
 #include "topk.cuh"
 
 namespace scbm {
 namespace {
 
-template <typename In> struct Elem;
-template <> struct Elem<uint8_t> {
-  using T = int32_t;
-  __device__ static T centre(uint8_t x) { return T(x) - 128; }
-  __device__ static uint32_t ord(T v) { return ord_i32(v); }
-};
-template <> struct Elem<float> {
-  using T = float;
-  __device__ static T centre(float x) { return x - 0.5f; }
-  __device__ static uint32_t ord(T v) { return ord_f32(v); }
-};
+constexpr int kWarpKeys = 32 + 32 * 5;  // per-warp shared keys: survivor buffer + list
 
 struct SimtArgs {
   const void* imgs;   // [F][C][H][W]
@@ -42,21 +32,101 @@ struct SimtArgs {
   int32_t* idx_out;   // [F][band refs][K]
   void* dist_out;     // [F][band refs][K]
   void* dense;        // debug: [refs][Wn*Wn] (one image) or nullptr
-  int H, W, C, b, s, Wn, K, KP, MS, lo, hi, nx, My, Mx;
+  int H, W, C, b, s, Wn, K, KP, lo, hi, nx, My, Mx;
   int iy_begin, iy_end;
   int TRY, TRX, tiles_x;
-  int RWp, RHp, NWp, NHp;  // shared tile pitches / padded heights
+  int RWp, RHp;       // logical image-region pitch (elements) / padded height
+  int WP, PL;         // u8: words per row of one shifted copy, words per copy plane
+  int NWp, NHp;       // norm-tile pitch / padded height
+  int img_words;      // shared words of the image tile
 };
 
-template <int n> struct Pow2 { static constexpr int v = n; };
+template <typename In> struct Path;
 
-// BK: compile-time patch extent; EXACT: b == BK (else the reference is zero-padded to BK).
-template <typename In, int BK, int VY, bool ONE_CH>
+// -------- f32: fp32 FMA on centred floats
+template <> struct Path<float> {
+  using T = float;     // norm / accumulator type
+  template <int BK> struct Ref { float r[BK][BK]; };
+  template <int BK>
+  __device__ static void load_ref(Ref<BK>& R, const uint32_t* tile, const SimtArgs& a, int c, int ry0, int rx0) {
+    const float* t = reinterpret_cast<const float*>(tile) + size_t(c) * a.RHp * a.RWp + ry0 * a.RWp + rx0;
+#pragma unroll
+    for (int l = 0; l < BK; ++l)
+#pragma unroll
+      for (int m = 0; m < BK; ++m) R.r[l][m] = (l < a.b && m < a.b) ? t[l * a.RWp + m] : 0.f;
+  }
+  template <int BK, int VY>
+  __device__ static void cross(float (&acc)[VY], const Ref<BK>& R, const uint32_t* tile, const SimtArgs& a,
+                               int c, int y0, int x0) {
+    const float* col = reinterpret_cast<const float*>(tile) + size_t(c) * a.RHp * a.RWp + y0 * a.RWp + x0;
+#pragma unroll
+    for (int t = 0; t < BK + VY - 1; ++t) {
+      float xr[BK];
+#pragma unroll
+      for (int m = 0; m < BK; ++m) xr[m] = col[t * a.RWp + m];
+#pragma unroll
+      for (int i = 0; i < VY; ++i) {
+        const int l = t - i;
+        if (l >= 0 && l < BK) {
+#pragma unroll
+          for (int m = 0; m < BK; ++m) acc[i] = fmaf(R.r[l][m], xr[m], acc[i]);
+        }
+      }
+    }
+  }
+  __device__ static uint32_t ord(float v) { return ord_f32(v); }
+};
+
+// -------- u8: dp4a on packed centred int8 (x ^ 0x80), four byte-shifted copies
+template <> struct Path<uint8_t> {
+  using T = int32_t;
+  template <int BK> struct Ref { uint32_t r[BK][BK / 4]; };
+  __device__ static const uint32_t* plane(const uint32_t* tile, const SimtArgs& a, int c, int k) {
+    return tile + size_t(c * 4 + k) * a.PL;
+  }
+  template <int BK>
+  __device__ static void load_ref(Ref<BK>& R, const uint32_t* tile, const SimtArgs& a, int c, int ry0, int rx0) {
+    const uint32_t* t = plane(tile, a, c, rx0 & 3) + ry0 * a.WP + (rx0 >> 2);
+#pragma unroll
+    for (int l = 0; l < BK; ++l)
+#pragma unroll
+      for (int q = 0; q < BK / 4; ++q) {
+        uint32_t w = l < a.b ? t[l * a.WP + q] : 0u;
+        const int nb = a.b - 4 * q;  // valid bytes in this word
+        if (nb < 4) w = nb <= 0 ? 0u : (w & ((1u << (8 * nb)) - 1u));
+        R.r[l][q] = w;
+      }
+  }
+  template <int BK, int VY>
+  __device__ static void cross(int32_t (&acc)[VY], const Ref<BK>& R, const uint32_t* tile, const SimtArgs& a,
+                               int c, int y0, int x0) {
+    const uint32_t* col = plane(tile, a, c, x0 & 3) + y0 * a.WP + (x0 >> 2);
+#pragma unroll
+    for (int t = 0; t < BK + VY - 1; ++t) {
+      uint32_t xw[BK / 4];
+#pragma unroll
+      for (int q = 0; q < BK / 4; ++q) xw[q] = col[t * a.WP + q];
+#pragma unroll
+      for (int i = 0; i < VY; ++i) {
+        const int l = t - i;
+        if (l >= 0 && l < BK) {
+#pragma unroll
+          for (int q = 0; q < BK / 4; ++q)
+            acc[i] = __dp4a(int(R.r[l][q]), int(xw[q]), acc[i]);
+        }
+      }
+    }
+  }
+  __device__ static uint32_t ord(int32_t v) { return ord_i32(v); }
+};
+
+template <typename In, int BK, int VY, int NJ, bool ONE_CH>
 __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_band, int iy, int ix,
-                                            const typename Elem<In>::T* __restrict__ tile,
-                                            const typename Elem<In>::T* __restrict__ ntile,
-                                            uint64_t* arr, int Y0, int X0, int lane) {
-  using T = typename Elem<In>::T;
+                                            const uint32_t* __restrict__ tile,
+                                            const typename Path<In>::T* __restrict__ ntile,
+                                            uint64_t* __restrict__ buf, int Y0, int X0, int lane) {
+  using P = Path<In>;
+  using T = typename P::T;
   const int s = a.s, b = a.b;
   const int ry = iy * s, rx = ix * s;
   const int cy0 = max(0, ry + a.lo), cy1 = min(a.H - b, ry + a.hi);
@@ -64,33 +134,23 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
   const int ncols = cx1 - cx0 + 1, nrows = cy1 - cy0 + 1;
   const int nby = (nrows + VY - 1) / VY;
   const int nitems = nby * ncols;
-  const int plane = a.RHp * a.RWp;
   const T nr = ntile[(ry - Y0) * a.NWp + (rx - X0)];
 
-  for (int i = lane; i < a.MS; i += 32) arr[i] = kKeyInf;
+  uint64_t* lst = buf + 32;  // 32*NJ sorted keys (shared)
+  for (int j = lane; j < 32 * NJ; j += 32) lst[j] = kKeyInf;
   __syncwarp();
-  uint64_t thr = kKeyInf;
+  uint32_t thr = 0xffffffffu;  // ord(d') of the KP-th key (inclusive superset filter)
   int cnt = 0;
 
-  T refv[BK][BK];
-  auto load_ref = [&](int c) {
-    const T* rp = tile + c * plane + (ry - Y0) * a.RWp + (rx - X0);
-#pragma unroll
-    for (int l = 0; l < BK; ++l)
-#pragma unroll
-      for (int m = 0; m < BK; ++m) refv[l][m] = (l < b && m < b) ? rp[l * a.RWp + m] : T(0);
-  };
-  if (ONE_CH) load_ref(0);
+  typename P::template Ref<BK> R;
+  if (ONE_CH) P::template load_ref<BK>(R, tile, a, 0, ry - Y0, rx - X0);
 
-  int32_t* dense_i = nullptr;
   T* dense_row = nullptr;
   if (a.dense) {
-    const size_t ref_g = size_t(ref_band);
-    dense_row = static_cast<T*>(a.dense) + ref_g * a.Wn * a.Wn;
+    dense_row = static_cast<T*>(a.dense) + size_t(ref_band) * a.Wn * a.Wn;
     for (int i = lane; i < a.Wn * a.Wn; i += 32) dense_row[i] = T(-1);
     __syncwarp();
   }
-  (void)dense_i;
 
   for (int base = 0; base < nitems; base += 32) {
     const int item = base + lane;
@@ -103,22 +163,8 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
     for (int i = 0; i < VY; ++i) acc[i] = T(0);
     const int nch = ONE_CH ? 1 : a.C;
     for (int c = 0; c < nch; ++c) {
-      if (!ONE_CH) load_ref(c);
-      const T* col = tile + c * plane + (cy - Y0) * a.RWp + (cx - X0);
-#pragma unroll
-      for (int t = 0; t < BK + VY - 1; ++t) {
-        T xr[BK];
-#pragma unroll
-        for (int m = 0; m < BK; ++m) xr[m] = col[t * a.RWp + m];
-#pragma unroll
-        for (int i = 0; i < VY; ++i) {
-          const int l = t - i;
-          if (l >= 0 && l < BK) {
-#pragma unroll
-            for (int m = 0; m < BK; ++m) acc[i] += refv[l][m] * xr[m];
-          }
-        }
-      }
+      if (!ONE_CH) P::template load_ref<BK>(R, tile, a, c, ry - Y0, rx - X0);
+      P::template cross<BK, VY>(acc, R, tile, a, c, cy - Y0, cx - X0);
     }
 #pragma unroll
     for (int i = 0; i < VY; ++i) {
@@ -130,42 +176,49 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
         if (ok) dense_row[(cyi - ry - a.lo) * a.Wn + (cx - rx - a.lo)] = dp + nr;
         continue;
       }
-      const uint64_t key = (uint64_t(Elem<In>::ord(dp)) << 32) | uint32_t(cyi * a.W + cx);
-      const bool pass = ok && key < thr;
+      const uint32_t u = P::ord(dp);
+      const bool pass = ok && u <= thr;
       const unsigned msk = __ballot_sync(0xffffffffu, pass);
-      if (pass) arr[a.KP + cnt + __popc(msk & ((1u << lane) - 1u))] = key;
-      cnt += __popc(msk);
-      if (cnt >= 32) {
+      if (msk) {
+        const int n = __popc(msk);
+        if (cnt + n > 32) {  // flush the buffer first
+          thr = smem_list_merge<NJ>(lst, buf, cnt, a.KP, lane);
+          cnt = 0;
+        }
+        if (pass) buf[cnt + __popc(msk & ((1u << lane) - 1u))] = (uint64_t(u) << 32) | uint32_t(cyi * a.W + cx);
+        cnt += n;
         __syncwarp();
-        thr = warp_topk_merge(arr, a.KP, a.MS, lane);
-        cnt = 0;
       }
     }
   }
   if (a.dense) return;
-  __syncwarp();
-  if (cnt > 0) warp_topk_merge(arr, a.KP, a.MS, lane);
+  if (cnt > 0) smem_list_merge<NJ>(lst, buf, cnt, a.KP, lane);
 
   const size_t out_base = (size_t(f) * ((a.iy_end - a.iy_begin) * a.nx) + ref_band) * a.K;
   if constexpr (sizeof(In) == 1) {
     int32_t* dist = static_cast<int32_t*>(a.dist_out);
-    for (int k = lane; k < a.K; k += 32) {
-      const uint64_t key = arr[k];
-      if (key == kKeyInf) {
-        a.idx_out[out_base + k] = -1;
-        dist[out_base + k] = 0x7fffffff;
-      } else {
-        a.idx_out[out_base + k] = int32_t(uint32_t(key));
-        dist[out_base + k] = unord_i32(uint32_t(key >> 32)) + nr;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int k = lane + 32 * j;
+      if (k < a.K) {
+        const uint64_t key = lst[k];
+        const bool none = key == kKeyInf;
+        a.idx_out[out_base + k] = none ? -1 : int32_t(uint32_t(key));
+        dist[out_base + k] = none ? 0x7fffffff : unord_i32(uint32_t(key >> 32)) + nr;
       }
     }
   } else {
     // a5: re-score the best KP keys by direct differences from the uncentred input.
     const float* img = static_cast<const float*>(a.imgs) + size_t(f) * a.C * a.H * a.W;
     const size_t pl = size_t(a.H) * a.W;
-    for (int k = lane; k < a.KP; k += 32) {
-      const uint64_t key = arr[k];
-      if (key == kKeyInf) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int k = lane + 32 * j;
+      const uint64_t key = lst[k];
+      if (k >= a.KP || key == kKeyInf) {
+        lst[k] = kKeyInf;
+        continue;
+      }
       const uint32_t idx = uint32_t(key);
       const int cyk = int(idx) / a.W, cxk = int(idx) - cyk * a.W;
       float d = 0.f;
@@ -179,33 +232,28 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
             d = fmaf(df, df, d);
           }
       }
-      arr[k] = (uint64_t(__float_as_uint(d)) << 32) | idx;  // d >= +0: bits are monotone
+      lst[k] = (uint64_t(__float_as_uint(d)) << 32) | idx;  // d >= +0: bits are monotone
     }
     __syncwarp();
-    int n2 = 32;
-    while (n2 < a.KP) n2 <<= 1;
-    for (int i = a.KP + lane; i < n2; i += 32) arr[i] = kKeyInf;
-    __syncwarp();
-    warp_bitonic_sort(arr, n2, lane);
+    smem_list_sort<NJ>(lst, lane);
     float* dist = static_cast<float*>(a.dist_out);
-    for (int k = lane; k < a.K; k += 32) {
-      const uint64_t key = arr[k];
-      if (key == kKeyInf) {
-        a.idx_out[out_base + k] = -1;
-        dist[out_base + k] = __int_as_float(0x7f800000);
-      } else {
-        a.idx_out[out_base + k] = int32_t(uint32_t(key));
-        dist[out_base + k] = __uint_as_float(uint32_t(key >> 32));
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int k = lane + 32 * j;
+      if (k < a.K) {
+        const uint64_t key = lst[k];
+        const bool none = key == kKeyInf;
+        a.idx_out[out_base + k] = none ? -1 : int32_t(uint32_t(key));
+        dist[out_base + k] = none ? __int_as_float(0x7f800000) : __uint_as_float(uint32_t(key >> 32));
       }
     }
   }
-  __syncwarp();
 }
 
-template <typename In, int BK, int VY, bool ONE_CH>
+template <typename In, int BK, int VY, int NJ, bool ONE_CH>
 __global__ void __launch_bounds__(256) bm_simt_kernel(SimtArgs a) {
-  using T = typename Elem<In>::T;
-  extern __shared__ __align__(16) unsigned char smem[];
+  using T = typename Path<In>::T;
+  extern __shared__ __align__(16) uint32_t smem_u32[];
   const int f = blockIdx.y;
   const int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
   const int iy_first = a.iy_begin + ty * a.TRY;
@@ -221,19 +269,40 @@ __global__ void __launch_bounds__(256) bm_simt_kernel(SimtArgs a) {
   const int NY1 = min(a.H - b, iy_last * s + a.hi), NX1 = min(a.W - b, ix_last * s + a.hi);
   const int NH = NY1 - Y0 + 1, NW = NX1 - X0 + 1;
 
-  T* tile = reinterpret_cast<T*>(smem);
-  T* ntile = tile + size_t(a.C) * a.RHp * a.RWp;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(ntile + size_t(a.NHp) * a.NWp + 2);
-  keys = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(keys) + 15) & ~uintptr_t(15));
+  uint32_t* tile = smem_u32;
+  T* ntile = reinterpret_cast<T*>(smem_u32 + a.img_words);
+  uint64_t* bufs = reinterpret_cast<uint64_t*>(smem_u32 + a.img_words + ((a.NHp * a.NWp + 1) & ~1));
 
-  const In* img = static_cast<const In*>(a.imgs) + size_t(f) * a.C * a.H * a.W;
-  for (int c = 0; c < a.C; ++c) {
-    const In* src = img + size_t(c) * a.H * a.W;
-    T* dst = tile + size_t(c) * a.RHp * a.RWp;
-    for (int yy = threadIdx.x / 32; yy < a.RHp; yy += blockDim.x / 32)
-      for (int xx = threadIdx.x & 31; xx < a.RWp; xx += 32)
-        dst[yy * a.RWp + xx] =
-            (yy < RH && xx < RW) ? Elem<In>::centre(src[size_t(Y0 + yy) * a.W + X0 + xx]) : T(0);
+  const size_t plane_px = size_t(a.H) * a.W;
+  if constexpr (sizeof(In) == 1) {
+    const uint8_t* img = static_cast<const uint8_t*>(a.imgs) + size_t(f) * a.C * plane_px;
+    const int total = a.C * 4 * a.PL;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int pk = e / a.PL, r = e - pk * a.PL;
+      const int c = pk >> 2, k = pk & 3;
+      const int yy = r / a.WP, w = r - yy * a.WP;
+      uint32_t word = 0;
+      if (yy < RH) {
+        const uint8_t* row = img + size_t(c) * plane_px + size_t(Y0 + yy) * a.W + X0;
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const int xx = 4 * w + k + e2;
+          const uint32_t v = xx < RW ? uint32_t(row[xx] ^ 0x80u) : 0u;
+          word |= v << (8 * e2);
+        }
+      }
+      tile[e] = word;
+    }
+  } else {
+    const float* img = static_cast<const float*>(a.imgs) + size_t(f) * a.C * plane_px;
+    float* ft = reinterpret_cast<float*>(tile);
+    for (int c = 0; c < a.C; ++c) {
+      const float* src = img + size_t(c) * plane_px;
+      float* dst = ft + size_t(c) * a.RHp * a.RWp;
+      for (int yy = threadIdx.x / 32; yy < a.RHp; yy += blockDim.x / 32)
+        for (int xx = threadIdx.x & 31; xx < a.RWp; xx += 32)
+          dst[yy * a.RWp + xx] = (yy < RH && xx < RW) ? src[size_t(Y0 + yy) * a.W + X0 + xx] - 0.5f : 0.f;
+    }
   }
   const T* nsrc = static_cast<const T*>(a.norm) + size_t(f) * a.My * a.Mx;
   for (int yy = threadIdx.x / 32; yy < a.NHp; yy += blockDim.x / 32)
@@ -242,57 +311,85 @@ __global__ void __launch_bounds__(256) bm_simt_kernel(SimtArgs a) {
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  uint64_t* arr = keys + warp * a.MS;
+  uint64_t* buf = bufs + warp * kWarpKeys;
   const int ty_n = iy_last - iy_first + 1, tx_n = ix_last - ix_first + 1;
   for (int r = warp; r < ty_n * tx_n; r += nwarps) {
     const int iy = iy_first + r / tx_n, ix = ix_first + r % tx_n;
     const int ref_band = (iy - a.iy_begin) * a.nx + ix;
-    process_ref<In, BK, VY, ONE_CH>(a, f, ref_band, iy, ix, tile, ntile, arr, Y0, X0, lane);
+    process_ref<In, BK, VY, NJ, ONE_CH>(a, f, ref_band, iy, ix, tile, ntile, buf, Y0, X0, lane);
   }
 }
 
-template <typename In, int BK, int VY>
+template <typename In, int BK, int VY, int NJ>
 cudaError_t launch_t(const SimtArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + a.TRY - 1) / a.TRY;
   dim3 grid(a.tiles_x * tiles_y, F);
   if (a.C == 1) {
-    auto k = bm_simt_kernel<In, BK, VY, true>;
+    auto k = bm_simt_kernel<In, BK, VY, NJ, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k<<<grid, 256, smem, st>>>(a);
   } else {
-    auto k = bm_simt_kernel<In, BK, VY, false>;
+    auto k = bm_simt_kernel<In, BK, VY, NJ, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k<<<grid, 256, smem, st>>>(a);
   }
   return cudaGetLastError();
 }
 
-template <typename In>
-cudaError_t dispatch_b(const SimtArgs& a, int F, size_t smem, cudaStream_t st, int VY) {
-  // exact instantiations for the configs' patch sides, zero-padded generic ones otherwise
-  if (a.b == 8) return launch_t<In, 8, 8>(a, F, smem, st);
-  if (a.b == 7) return launch_t<In, 7, 8>(a, F, smem, st);
-  if (a.b <= 4) return launch_t<In, 4, 8>(a, F, smem, st);
-  if (a.b <= 8) return launch_t<In, 8, 8>(a, F, smem, st);
-  return launch_t<In, 16, 4>(a, F, smem, st);
+int nj_for(int KP) { return KP <= 32 ? 1 : KP <= 64 ? 2 : KP <= 96 ? 3 : 5; }
+
+template <typename In, int BK, int VY, bool SPEC>
+cudaError_t dispatch_nj(const SimtArgs& a, int F, size_t smem, cudaStream_t st) {
+  const int nj = nj_for(a.KP);
+  if constexpr (SPEC) {
+    if (nj == 1) return launch_t<In, BK, VY, 1>(a, F, smem, st);
+    if (nj == 2) return launch_t<In, BK, VY, 2>(a, F, smem, st);
+    if (nj == 3) return launch_t<In, BK, VY, 3>(a, F, smem, st);
+  }
+  return launch_t<In, BK, VY, 5>(a, F, smem, st);
 }
 
-int bk_for(int b) { return b == 7 ? 7 : b <= 4 ? 4 : b <= 8 ? 8 : 16; }
+// Compile-time patch extent: exact for the configs' sides, zero-padded generic otherwise.
+int bk_for(int b, bool u8) {
+  if (u8) return b <= 4 ? 4 : b <= 8 ? 8 : 16;
+  return b == 7 ? 7 : b <= 4 ? 4 : b <= 8 ? 8 : 16;
+}
 int vy_for(int b) { return b <= 8 ? 8 : 4; }
 
-size_t smem_bytes(const Geometry& g, int TRY, int TRX, int* RWp, int* RHp, int* NWp, int* NHp,
-                  int* MS) {
-  const int BK = bk_for(g.b), VY = vy_for(g.b);
+template <typename In>
+cudaError_t dispatch_b(const SimtArgs& a, int F, size_t smem, cudaStream_t st) {
+  constexpr bool u8 = sizeof(In) == 1;
+  const int bk = bk_for(a.b, u8);
+  if (bk == 8 && a.b == 8) return dispatch_nj<In, 8, 8, true>(a, F, smem, st);
+  if (bk == 8) return dispatch_nj<In, 8, 8, false>(a, F, smem, st);
+  if constexpr (!u8) {
+    if (bk == 7) return dispatch_nj<In, 7, 8, true>(a, F, smem, st);
+  }
+  if (bk == 4) return dispatch_nj<In, 4, 8, false>(a, F, smem, st);
+  return dispatch_nj<In, 16, 4, false>(a, F, smem, st);
+}
+
+size_t smem_bytes(const Geometry& g, int TRY, int TRX, SimtArgs* a) {
+  const bool u8 = g.dtype == SC_DTYPE_U8;
+  const int BK = bk_for(g.b, u8), VY = vy_for(g.b);
   const int pad = BK - g.b;
-  *RWp = (TRX - 1) * g.s + g.Wn + g.b - 1 + pad;
-  *RHp = (TRY - 1) * g.s + g.Wn + g.b - 1 + pad + VY - 1;
-  *NWp = (TRX - 1) * g.s + g.Wn;
-  *NHp = (TRY - 1) * g.s + g.Wn + VY - 1;
-  int ms = 64;
-  while (ms < g.KP + 64) ms <<= 1;
-  *MS = ms;
-  size_t bytes = size_t(g.C) * (*RHp) * (*RWp) * 4 + size_t(*NHp) * (*NWp) * 4 + 8 + 16;
-  bytes += size_t(8) * ms * 8;  // 8 warps
+  a->RWp = (TRX - 1) * g.s + g.Wn + g.b - 1 + pad;
+  a->RHp = (TRY - 1) * g.s + g.Wn + g.b - 1 + pad + VY - 1;
+  if (u8) {
+    a->WP = (a->RWp + 3) / 4 + 1;
+    int pl = a->RHp * a->WP;
+    pl += ((8 - pl % 32) + 32) % 32;  // plane size == 8 (mod 32) words: copies 8 banks apart
+    a->PL = pl;
+    a->img_words = g.C * 4 * pl;
+  } else {
+    a->WP = a->PL = 0;
+    a->img_words = g.C * a->RHp * a->RWp;
+  }
+  a->img_words = (a->img_words + 3) & ~3;
+  a->NWp = (TRX - 1) * g.s + g.Wn;
+  a->NHp = (TRY - 1) * g.s + g.Wn + VY - 1;
+  size_t bytes = size_t(a->img_words) * 4 + size_t((a->NHp * a->NWp + 1) & ~1) * 4;
+  bytes += size_t(8) * kWarpKeys * 8;  // 8 warps x (32 survivors + 32*NJ list)
   return bytes;
 }
 
@@ -303,11 +400,11 @@ TileCfg choose_simt_tile(const Geometry& g, int sm_count, int n_images) {
   t.warps = 8;
   t.VY = vy_for(g.b);
   int best_try = 1, best_trx = 1;
-  // largest square-ish tile that fits ~100 KB and still gives >= 4 waves of 2 CTAs/SM
+  // largest square-ish tile that fits ~100 KB and still gives >= 8 CTAs per SM
   const int cands[][2] = {{8, 8}, {4, 8}, {4, 4}, {2, 4}, {2, 2}, {1, 2}, {1, 1}};
   for (auto& c : cands) {
-    int a, bb, cc, d, ms;
-    const size_t sm = smem_bytes(g, c[0], c[1], &a, &bb, &cc, &d, &ms);
+    SimtArgs a{};
+    const size_t sm = smem_bytes(g, c[0], c[1], &a);
     const long long tiles = (long long)((g.ny + c[0] - 1) / c[0]) * ((g.nx + c[1] - 1) / c[1]) * n_images;
     best_try = c[0];
     best_trx = c[1];
@@ -315,8 +412,8 @@ TileCfg choose_simt_tile(const Geometry& g, int sm_count, int n_images) {
   }
   t.TRY = best_try;
   t.TRX = best_trx;
-  int a, bb, cc, d, ms;
-  t.smem = smem_bytes(g, t.TRY, t.TRX, &a, &bb, &cc, &d, &ms);
+  SimtArgs a{};
+  t.smem = smem_bytes(g, t.TRY, t.TRX, &a);
   return t;
 }
 
@@ -335,10 +432,10 @@ cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int i
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.TRY = p.tile.TRY; a.TRX = p.tile.TRX;
   a.tiles_x = (g.nx + a.TRX - 1) / a.TRX;
-  const size_t smem = smem_bytes(g, a.TRY, a.TRX, &a.RWp, &a.RHp, &a.NWp, &a.NHp, &a.MS);
+  const size_t smem = smem_bytes(g, a.TRY, a.TRX, &a);
   if (launches) *launches += 1;
-  if (g.dtype == SC_DTYPE_U8) return dispatch_b<uint8_t>(a, F, smem, st, p.tile.VY);
-  return dispatch_b<float>(a, F, smem, st, p.tile.VY);
+  if (g.dtype == SC_DTYPE_U8) return dispatch_b<uint8_t>(a, F, smem, st);
+  return dispatch_b<float>(a, F, smem, st);
 }
 
 }  // namespace scbm
