@@ -173,6 +173,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL all-gather of the tables")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc"],
+                    help="force the matching kernel (default: the plan's choice)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -203,6 +205,8 @@ def main():
     del x_all
     x = torch.from_numpy(x_host).cuda()
     plan = Plan(cfg.H, cfg.W, cfg.C, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype)
+    if args.kernel != "auto":
+        plan.set_kernel({"simt": 0, "tc": 1, "warp": 2}[args.kernel])
     info = plan.info()
     idx, dst = plan.alloc_out(nloc)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -262,7 +266,8 @@ def main():
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # FP32 FFMA lanes x 2 ops x max clock
         bound, unit, peak_note = "alu", "TFLOP/s", "FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md section 7)"
     achieved = 2.0 * macs_launch / (match_ms / 1e3) / 1e12 if match_ms > 0 else None
-    roof = {"bound": bound, "kernel": "bm_simt_kernel" if info["kernel"] == 0 else "bm_tc_i8_kernel",
+    kname = {0: "bm_lanes_kernel", 1: "bm_tc_i8_kernel", 2: "bm_simt_kernel"}[info["kernel"]]
+    roof = {"bound": bound, "kernel": kname,
             "achieved": achieved, "peak": peak, "unit": unit,
             "frac": (achieved / peak) if achieved else None, "traffic": None,
             "peak_source": peak_note, "kernel_ms_per_step": match_ms, "norm_ms_per_step": norm_ms,

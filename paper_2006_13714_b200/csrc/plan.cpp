@@ -86,7 +86,10 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
     if (ev) cudaEventRecord(ev[1], st);
     int32_t* io = idx ? idx + f0 * out_elems : nullptr;
     void* dd = dist ? static_cast<char*>(dist) + f0 * out_elems * 4 : nullptr;
-    e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
+    if (p->kernel == SC_KERNEL_SIMT_WARP)
+      e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
+    else
+      e = launch_bm_lanes(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
     if (e != cudaSuccess) return cuda_status(e);
     if (ev) cudaEventRecord(ev[2], st);
   }
@@ -157,6 +160,13 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   const size_t pf = per_frame_ws(g, p->nbands);
   p->F = int(std::max<size_t>(1, std::min<size_t>(64, (48u << 20) / std::max<size_t>(pf, 1))));
   p->tile = choose_simt_tile(g, p->sm_count, p->F);
+  p->lanes_nwy = lanes_warps_for(g, p->sm_count, p->F);
+  // Default matcher: lanes = references where its 32-reference-wide CTA keeps >= 4 warps per
+  // CTA in shared memory (u8 frames such as c5); the one-warp-per-reference kernel otherwise
+  // (f32 / multi-channel / large K / narrow images, where it measured faster: DESIGN.md s7).
+  const bool lanes_ok = dtype == SC_DTYPE_U8 && g.nx >= 64 && p->lanes_nwy >= 4 &&
+                        lanes_smem_bytes(g, p->lanes_nwy) <= 227 * 1024;
+  p->kernel = lanes_ok ? SC_KERNEL_SIMT : SC_KERNEL_SIMT_WARP;
 
   const size_t SP = size_t((W + 15) / 16 * 16);
   const size_t acc = dtype == SC_DTYPE_U8 ? 4 : 8;
@@ -297,7 +307,8 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
 
 sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
-  if (kernel != SC_KERNEL_SIMT) return SC_ERR_UNSUPPORTED;
+  if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
+  if (kernel != SC_KERNEL_SIMT && kernel != SC_KERNEL_SIMT_WARP) return SC_ERR_UNSUPPORTED;
   p->kernel = kernel;
   return SC_OK;
 }

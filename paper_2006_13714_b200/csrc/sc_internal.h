@@ -60,6 +60,7 @@ struct sc_bm_plan_s {
   int nbands = 1;
   scbm::Workspace ws;
   scbm::TileCfg tile;
+  int lanes_nwy = 4;  // reference rows (warps) per CTA of the lanes = references kernel
   scbm::HostStaging host;
   scbm::Timing timing;
   int64_t launches = 0;
@@ -80,5 +81,12 @@ cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int i
                            int iy_end, int32_t* idx_out, void* dist_out, void* dense,
                            cudaStream_t st, int64_t* launches);
 TileCfg choose_simt_tile(const Geometry& g, int sm_count, int n_images);
+
+// bm_lanes.cu: the lanes = references matcher (SC_KERNEL_SIMT).
+cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin,
+                            int iy_end, int32_t* idx_out, void* dist_out, void* dense,
+                            cudaStream_t st, int64_t* launches);
+int lanes_warps_for(const Geometry& g, int sm_count, int n_images);
+size_t lanes_smem_bytes(const Geometry& g, int nwy);
 
 }  // namespace scbm

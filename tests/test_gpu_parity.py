@@ -26,9 +26,11 @@ def _run(plan, x):
     return idx.cpu().numpy(), dist.cpu().numpy()
 
 
-def _compare(x, b, s, Wn, K, dtype, where=""):
+def _compare(x, b, s, Wn, K, dtype, where="", kernel=None):
     N, C, H, W = x.shape
     p = _plan((H, W, C, b, s, Wn, K), dtype)
+    if kernel is not None:
+        p.set_kernel(kernel)
     gi, gd = _run(p, x)
     oi, od = oracle.bm(x, b, s, Wn, K)
     if dtype == "u8":
@@ -149,6 +151,25 @@ def test_random_sweep(case, dtype):
     rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
     x = synth.random_image(rng, 2, C, H, W, dtype)
     _compare(x, b, s, Wn, K, dtype, where=f"{dtype} {case}")
+
+
+@pytest.mark.parametrize("case", _sweep_cases(10, 202))
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_random_sweep_warp_kernel(case, dtype):
+    """The one-warp-per-reference SIMT kernel (SC_KERNEL_SIMT_WARP) on its own sweep."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_SIMT_WARP
+    C, H, W, b, s, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 2, C, H, W, dtype)
+    _compare(x, b, s, Wn, K, dtype, where=f"warp {dtype} {case}", kernel=SC_KERNEL_SIMT_WARP)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_configs_warp_kernel(name):
+    from paper_2006_13714_b200.bm import SC_KERNEL_SIMT_WARP
+    cfg = synth.CONFIGS[name]
+    x = synth.make_input(cfg)
+    _compare(x, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype, where=f"warp {name}", kernel=SC_KERNEL_SIMT_WARP)
 
 
 # ------------------------------------------------------------------ edge cases
