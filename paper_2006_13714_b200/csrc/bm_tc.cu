@@ -1,0 +1,353 @@
+// bm_tc.cu -- the tensor-core matcher (SC_KERNEL_TC_I8): uint8 images, b = 8, C = 1.
+//
+// a2 (the Self-Convolution cross term, Eq. 5) runs on the 5th-generation
+// tensor cores as an int8 GEMM  D[ref][cand] = sum_k A[ref][k] * B[cand][k]  (k = 8*l + m over
+// the 8x8 patch, centred x' = x - 128 as signed int8, exact int32 accumulation in TMEM):
+//
+//   * A (M = 128 references of an 8 x 16 reference block) is K-major in shared memory: one
+//     64-byte centred patch per reference in canonical 8-row x 16-byte core matrices.
+//   * B (N = 128 candidates: an 8-row x 16-column block of candidate top-left positions) is
+//     MN-major straight out of a "shift-expanded" copy of the image region E[y][c][m][t] =
+//     x'(y, X0 + 16c + t + m): K-group l of candidate row i is image row y0 + i + l, so ONE
+//     descriptor (LBO = SBO = row pitch) addresses the whole 8 x 16 candidate block -- no
+//     im2col materialisation, 8 bytes of E per image byte.
+//   * each tile is two tcgen05.mma.cta_group::1.kind::i8 (K = 32 each) into a 128 x 128 int32
+//     TMEM accumulator, double-buffered (256 TMEM columns) so the MMA of tile t+1 overlaps the
+//     epilogue of tile t; one elected thread of the MMA warp issues them and commits to an
+//     mbarrier.
+//
+// Epilogue (4 warps, TMEM lane quarter q = references 32q..32q+31 = a 4 x 8 sub-block):
+// tcgen05.ld 16 columns (one candidate row of the tile), d' = n_c - 2C (Lemma 2),
+// one compare per pair against the reference's heap root into a bitmask; rows where some lane
+// passed go through the window check and the survivor queue / per-reference heaps of refq.cuh
+// (a4). Tiles outside a warp's window union are skipped. a6 as in bm_lanes.cu (exact int32).
+#include "refq.cuh"
+#include "sc_internal.h"
+#include "sm100.cuh"
+#include "topk.cuh"
+
+namespace scbm {
+namespace {
+
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = (kEpiWarps + 1) * 32;
+constexpr int kRBY = 8, kRBX = 16;   // reference block (M = 128)
+constexpr int kTR = 8, kTC = 16;     // candidate tile: 8 rows x 16 columns (N = 128)
+constexpr int kBig = 0x3fffffff;     // norm of positions that are not candidates
+constexpr uint32_t kIdesc = sm100::idesc_i8(128, 128, /*a_mn=*/false, /*b_mn=*/true);
+
+struct TcArgs {
+  const uint8_t* imgs;
+  const int32_t* norm;
+  int32_t* idx_out;
+  int32_t* dist_out;
+  int H, W, s, Wn, K, KP, lo, hi, nx, My, Mx, iy_begin, iy_end, tiles_x;
+  int NCmax, NTImax;
+  uint32_t off_A, off_E, off_N, off_heap, off_q;  // shared byte offsets
+  int heap_pitch;
+};
+
+__device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
+// k-th index of a centre-out enumeration of [0, n)
+__device__ __forceinline__ int co_index(int k, int n) {
+  const int c = (n - 1) >> 1;
+  int idx = c + centre_out(k);
+  // for even n the enumeration c, c+1, c-1, ... stays in range for k < n
+  return idx;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int f = blockIdx.y;
+  const int by = blockIdx.x / a.tiles_x, bx = blockIdx.x - by * a.tiles_x;
+  const int iy_first = a.iy_begin + by * kRBY;
+  const int iy_last = min(a.iy_end, iy_first + kRBY) - 1;
+  const int ix_first = bx * kRBX;
+  const int ix_last = min(a.nx, ix_first + kRBX) - 1;
+  const int s = a.s, H = a.H, W = a.W, b = 8;
+  const int cyA = max(0, iy_first * s + a.lo), cyB = min(H - b, iy_last * s + a.hi);
+  const int cxA = max(0, ix_first * s + a.lo), cxB = min(W - b, ix_last * s + a.hi);
+  const int X0 = cxA & ~15;
+  const int NC = (cxB - X0) / kTC + 1;           // candidate column chunks
+  const int NTI = (cyB - cyA) / kTR + 1;         // candidate row blocks
+  const int RH = NTI * kTR + 7;                  // image rows of E
+  const uint32_t RP = uint32_t(NC) * 128u;       // E row pitch (bytes)
+  const int NWc = NC * kTC;                      // norm-tile columns
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const uint32_t sbase = smem_addr(smem);
+  const uint32_t bar_full = sbase, bar_empty = sbase + 16;  // 2 + 2 mbarriers
+  const uint32_t tmem_slot = sbase + 32;
+  const uint32_t sA = sbase + a.off_A, sE = sbase + a.off_E;
+  int32_t* ntile = reinterpret_cast<int32_t*>(smem + a.off_N);
+  uint64_t* heaps = reinterpret_cast<uint64_t*>(smem + a.off_heap);
+
+  if (warp == kEpiWarps) {
+    sm100::tmem_alloc(tmem_slot, 256);
+    sm100::tmem_relinquish();
+  }
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(bar_full, 1);
+    sm100::mbar_init(bar_full + 8, 1);
+    sm100::mbar_init(bar_empty, kEpiWarps);
+    sm100::mbar_init(bar_empty + 8, kEpiWarps);
+    sm100::fence_barrier_init();
+  }
+
+  // ---- a0 staging: A (reference patches), E (shift-expanded image), norm tile, heaps
+  const uint8_t* img = a.imgs + size_t(f) * H * W;
+  for (int e = threadIdx.x; e < 128 * 4; e += kThreads) {
+    const int m = e >> 2, kc = e & 3;
+    const int w = m >> 5, L = m & 31;
+    const int iy = iy_first + 4 * (w >> 1) + (L >> 3), ix = ix_first + 8 * (w & 1) + (L & 7);
+    uint32_t v[4] = {0, 0, 0, 0};
+    if (iy <= iy_last && ix <= ix_last) {
+      const uint8_t* p = img + size_t(iy * s + 2 * kc) * W + ix * s;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          uint32_t wd = 0;
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2) wd |= uint32_t(p[h * W + 4 * q + e2]) << (8 * e2);
+          v[2 * h + q] = wd ^ 0x80808080u;
+        }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(smem + a.off_A + (m >> 3) * 512 + kc * 128 + (m & 7) * 16);
+    *dst = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  for (int e = threadIdx.x; e < RH * NC; e += kThreads) {
+    const int yr = e / NC, c = e - yr * NC;
+    const int y = cyA + yr;
+    uint32_t w[8];
+    const int x0 = X0 + 16 * c;
+    const uint8_t* rowp = img + size_t(y) * W + x0;
+    if (y < H && x0 + 32 <= W && (reinterpret_cast<uintptr_t>(rowp) & 15) == 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(rowp);
+      const uint4 q0 = src[0], q1 = src[1];
+      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w; w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] ^= 0x80808080u;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t wd = 0;
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          const int x = x0 + 4 * i + e2;
+          const uint32_t v = (y < H && x < W) ? uint32_t(img[size_t(y) * W + x] ^ 0x80u) : 0u;
+          wd |= v << (8 * e2);
+        }
+        w[i] = wd;
+      }
+    }
+    uint8_t* row = smem + a.off_E + size_t(yr) * RP + c * 128;
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+      const int q = mm >> 2, sh = 8 * (mm & 3);
+      uint4 o;
+      o.x = __funnelshift_r(w[q + 0], w[q + 1], sh);
+      o.y = __funnelshift_r(w[q + 1], w[q + 2], sh);
+      o.z = __funnelshift_r(w[q + 2], w[q + 3], sh);
+      o.w = __funnelshift_r(w[q + 3], w[q + 4], sh);
+      *reinterpret_cast<uint4*>(row + mm * 16) = o;
+    }
+  }
+  const int32_t* nsrc = a.norm + size_t(f) * a.My * a.Mx;
+  for (int e = threadIdx.x; e < NTI * kTR * NWc; e += kThreads) {
+    const int r = e / NWc, j = e - r * NWc;
+    const int cy = cyA + r, cx = X0 + j;
+    ntile[e] = (cy <= H - b && cx <= W - b) ? nsrc[size_t(cy) * a.Mx + cx] : kBig;
+  }
+  for (int e = threadIdx.x; e < 128 * a.heap_pitch; e += kThreads) heaps[e] = kKeyInf;
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + 32);
+  const int ntiles = NTI * NC;
+
+  if (warp == kEpiWarps) {
+    // ---------------- MMA issuer (one elected thread)
+    if (lane == 0) {
+      for (int t = 0; t < ntiles; ++t) {
+        const int tr = co_index(t / NC, NTI), tc = co_index(t % NC, NC);
+        const int buf = t & 1;
+        if (t >= 2) sm100::mbar_wait(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1));
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const uint64_t ad = sm100::smem_desc(sA + 256u * j, 128u, 512u);
+          const uint64_t bd = sm100::smem_desc(sE + uint32_t(kTR * tr + 4 * j) * RP + uint32_t(tc) * 128u, RP, RP);
+          sm100::mma_i8(tmem + 128u * buf, ad, bd, kIdesc, j);
+        }
+        sm100::mma_commit(bar_full + 8 * buf);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps
+    const int wy = warp >> 1, wx = warp & 1;
+    const int iy = iy_first + 4 * wy + (lane >> 3), ix = ix_first + 8 * wx + (lane & 7);
+    const bool valid = iy <= iy_last && ix <= ix_last;
+    const int ry = iy * s, rx = ix * s;
+    const int wiy0 = iy_first + 4 * wy, wiy1 = min(iy_last, wiy0 + 3);
+    const int wix0 = ix_first + 8 * wx, wix1 = min(ix_last, wix0 + 7);
+    const bool wvalid = wiy0 <= iy_last && wix0 <= ix_last;
+    const int wy_lo = wiy0 * s + a.lo, wy_hi = wiy1 * s + a.hi;  // candidate rows of this warp
+    const int wx_lo = wix0 * s + a.lo, wx_hi = wix1 * s + a.hi;
+    const int ref_local = warp * 32 + lane;
+    uint64_t* qk = heaps + size_t(128) * a.heap_pitch + warp * 64;
+    RefHeaps hp{smem_addr(heaps), a.heap_pitch, a.KP, heap_depth(a.KP)};
+    WarpQueue q{smem_addr(qk), smem_addr(reinterpret_cast<int32_t*>(heaps + size_t(128) * a.heap_pitch +
+                                                                     kEpiWarps * 64) + warp * 64)};
+    const uint32_t myheap = hp.heap(ref_local);
+    int32_t thr = 0x7fffffff;  // d' threshold (root of this reference's heap)
+    int qcnt = 0;
+    const uint32_t tq = tmem + (uint32_t(32 * warp) << 16);
+
+    for (int t = 0; t < ntiles; ++t) {
+      const int tr = co_index(t / NC, NTI), tc = co_index(t % NC, NC);
+      const int buf = t & 1;
+      sm100::mbar_wait(bar_full + 8 * buf, uint32_t((t >> 1) & 1));
+      sm100::tc_fence_after();
+      const int cx0 = X0 + kTC * tc;
+      const bool xrel = wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo;
+      if (xrel) {
+#pragma unroll 1
+        for (int i = 0; i < kTR; ++i) {
+          const int cy = cyA + kTR * tr + i;
+          if (cy < wy_lo || cy > wy_hi || cy > cyB) continue;  // warp-uniform
+          uint32_t c[16];
+          sm100::tmem_ld16(tq + 128u * buf + 16u * i, c);
+          const int4* nrow = reinterpret_cast<const int4*>(ntile + (kTR * tr + i) * NWc + kTC * tc);
+          int nc[16];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int4 x = nrow[v];
+            nc[4 * v] = x.x; nc[4 * v + 1] = x.y; nc[4 * v + 2] = x.z; nc[4 * v + 3] = x.w;
+          }
+          sm100::tmem_wait_ld();
+          int dp[16];
+          unsigned bits = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            dp[j] = nc[j] - 2 * int(c[j]);
+            bits |= (dp[j] <= thr ? 1u : 0u) << j;
+          }
+          // window of this lane's reference (rows and columns)
+          const bool yok = valid && cy - ry >= a.lo && cy - ry <= a.hi;
+          const int jlo = max(0, rx + a.lo - cx0), jhi = min(15, min(rx + a.hi, W - b) - cx0);
+          const unsigned cols = (yok && jhi >= jlo) ? (((2u << jhi) - 1u) & ~((1u << jlo) - 1u)) : 0u;
+          bits &= cols;
+          const unsigned any = __reduce_or_sync(0xffffffffu, bits);
+          if (any) {
+            bool refresh = false;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (!(any & (1u << j))) continue;
+              const bool pb = (bits >> j) & 1u;
+              const uint64_t key = (uint64_t(ord_i32(dp[j])) << 32) | uint32_t(cy * W + cx0 + j);
+              const bool fill = pb && thr == 0x7fffffff;
+              if (fill) {
+                heap_push_cold(myheap, a.KP, hp.depth, key);
+                thr = unord_i32(hp.thr_hi(ref_local));
+              }
+              const bool pass = pb && !fill && dp[j] <= thr;
+              refresh |= queue_push(q, hp, qcnt, pass, key, ref_local, lane);
+            }
+            if (refresh) thr = unord_i32(hp.thr_hi(ref_local));
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(bar_empty + 8 * buf);
+    }
+    while (qcnt > 0) qcnt = queue_drain(q, hp, qcnt, lane);
+    heap_sort(myheap, a.KP, hp.depth);
+    __syncwarp();
+    // ---- a6: outputs, one reference at a time across the warp
+    const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
+    const int32_t nr = valid ? nsrc[size_t(ry) * a.Mx + rx] : 0;
+    for (int r = 0; r < 32; ++r) {
+      const int riy = iy_first + 4 * wy + (r >> 3), rix = ix_first + 8 * wx + (r & 7);
+      const int32_t nr_r = __shfl_sync(0xffffffffu, nr, r);
+      if (riy > iy_last || rix > ix_last) continue;  // warp-uniform
+      const uint64_t* Lh = heaps + size_t(warp * 32 + r) * a.heap_pitch;
+      const size_t o = (size_t(f) * band_refs + size_t(riy - a.iy_begin) * a.nx + rix) * a.K;
+      for (int k = lane; k < a.K; k += 32) {
+        const uint64_t key = Lh[k];
+        const bool none = key == kKeyInf;
+        a.idx_out[o + k] = none ? -1 : int32_t(uint32_t(key));
+        a.dist_out[o + k] = none ? 0x7fffffff : unord_i32(uint32_t(key >> 32)) + nr_r;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == kEpiWarps) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, 256);
+  }
+}
+
+struct TcLayout {
+  int NCmax, NTImax, heap_pitch;
+  uint32_t off_A, off_E, off_N, off_heap, off_q, bytes;
+};
+
+TcLayout tc_layout(const Geometry& g) {
+  TcLayout L{};
+  const int span_x = (kRBX - 1) * g.s + g.Wn;  // candidate columns of a full block
+  const int span_y = (kRBY - 1) * g.s + g.Wn;
+  L.NCmax = (span_x + 15) / kTC + 1;
+  L.NTImax = (span_y + kTR - 1) / kTR;
+  L.heap_pitch = g.KP | 1;
+  uint32_t off = 1024;  // barriers + TMEM slot
+  L.off_A = off;
+  off += 128 * 64;
+  L.off_E = off;
+  off += uint32_t(L.NTImax * kTR + 7) * L.NCmax * 128;
+  L.off_N = off;
+  off += uint32_t(L.NTImax * kTR) * L.NCmax * kTC * 4;
+  off = (off + 15) & ~15u;
+  L.off_heap = off;
+  off += uint32_t(128 * L.heap_pitch) * 8;
+  L.off_q = off;
+  off += kEpiWarps * 64 * (8 + 4);
+  L.bytes = off;
+  return L;
+}
+
+}  // namespace
+
+bool tc_supported(const Geometry& g) {
+  if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.C != 1 || g.KP > 64 || g.Wn > 64) return false;
+  return tc_layout(g).bytes <= 227 * 1024;
+}
+
+cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                         int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
+  const Geometry& g = p.g;
+  const TcLayout L = tc_layout(g);
+  TcArgs a{};
+  a.imgs = static_cast<const uint8_t*>(imgs);
+  a.norm = static_cast<const int32_t*>(p.ws.norm);
+  a.idx_out = idx_out;
+  a.dist_out = static_cast<int32_t*>(dist_out);
+  a.H = g.H; a.W = g.W; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
+  a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mx;
+  a.iy_begin = iy_begin; a.iy_end = iy_end;
+  a.tiles_x = (g.nx + kRBX - 1) / kRBX;
+  a.NCmax = L.NCmax; a.NTImax = L.NTImax;
+  a.off_A = L.off_A; a.off_E = L.off_E; a.off_N = L.off_N; a.off_heap = L.off_heap; a.off_q = L.off_q;
+  a.heap_pitch = L.heap_pitch;
+  const int tiles_y = (iy_end - iy_begin + kRBY - 1) / kRBY;
+  cudaFuncSetAttribute(bm_tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.bytes));
+  bm_tc_i8_kernel<<<dim3(a.tiles_x * tiles_y, F), kThreads, L.bytes, st>>>(a);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace scbm

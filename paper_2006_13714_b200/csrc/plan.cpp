@@ -86,7 +86,9 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
     if (ev) cudaEventRecord(ev[1], st);
     int32_t* io = idx ? idx + f0 * out_elems : nullptr;
     void* dd = dist ? static_cast<char*>(dist) + f0 * out_elems * 4 : nullptr;
-    if (p->kernel == SC_KERNEL_SIMT_WARP)
+    if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
+      e = launch_bm_tc(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
+    else if (p->kernel == SC_KERNEL_SIMT_WARP)
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
     else
       e = launch_bm_lanes(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
@@ -308,7 +310,9 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
 sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
   if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
-  if (kernel != SC_KERNEL_SIMT && kernel != SC_KERNEL_SIMT_WARP) return SC_ERR_UNSUPPORTED;
+  if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;
+  if (kernel != SC_KERNEL_SIMT && kernel != SC_KERNEL_SIMT_WARP && kernel != SC_KERNEL_TC_I8)
+    return SC_ERR_UNSUPPORTED;
   p->kernel = kernel;
   return SC_OK;
 }

@@ -100,7 +100,7 @@ struct WarpQueue {
 
 // Insert the first min(cnt, 32) queued entries; returns the new count (the undrained tail is
 // moved to the front).
-__device__ __noinline__ int queue_drain(WarpQueue q, RefHeaps hp, int cnt, int lane) {
+static __device__ __noinline__ int queue_drain(WarpQueue q, RefHeaps hp, int cnt, int lane) {
   const int n = cnt < 32 ? cnt : 32;
   const bool has = lane < n;
   const uint64_t k = has ? lds64(q.key + 8u * lane) : 0ull;
@@ -158,7 +158,7 @@ __host__ __device__ inline int heap_depth(int KP) {
 
 namespace scbm {
 // Out-of-line heap push for rarely taken paths (keeps one copy of the sift code per kernel).
-__device__ __noinline__ void heap_push_cold(uint32_t h, int KP, int depth, uint64_t x) {
+static __device__ __noinline__ void heap_push_cold(uint32_t h, int KP, int depth, uint64_t x) {
   heap_push(h, KP, depth, x);
 }
 }  // namespace scbm

@@ -87,6 +87,11 @@ cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int 
                             int iy_end, int32_t* idx_out, void* dist_out, void* dense,
                             cudaStream_t st, int64_t* launches);
 int lanes_warps_for(const Geometry& g, int sm_count, int n_images);
+
+// bm_tc.cu: the tcgen05 kind::i8 matcher (SC_KERNEL_TC_I8; u8, b = 8, C = 1).
+bool tc_supported(const Geometry& g);
+cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                         int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
 size_t lanes_smem_bytes(const Geometry& g, int nwy);
 
 }  // namespace scbm

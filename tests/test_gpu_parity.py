@@ -260,3 +260,62 @@ def test_launch_counter_and_info():
     assert inf["n_refs"] == 269 * 479
     assert inf["total_candidates"] * 64 == 8_854_426_816
     assert inf["min_candidates"] == 289 and inf["max_candidates"] == 1089
+
+
+# ------------------------------------------------------------------ tensor-core kernel
+def _tc_cases(n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = []
+    while len(out) < n:
+        H = int(rng.integers(8, 90))
+        W = int(rng.integers(8, 130))
+        s = int(rng.integers(1, 6))
+        Wn = int(rng.integers(1, 50))
+        K = int(rng.integers(1, 65))
+        out.append((H, W, s, Wn, K))
+    return out
+
+
+def _tc_compare(x, s, Wn, K, where):
+    from paper_2006_13714_b200.bm import SC_KERNEL_TC_I8
+    _compare(x, 8, s, Wn, K, "u8", where=where, kernel=SC_KERNEL_TC_I8)
+
+
+@pytest.mark.parametrize("case", _tc_cases(20, 303))
+def test_tc_random_sweep(case):
+    H, W, s, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 2, 1, H, W, "u8")
+    _tc_compare(x, s, Wn, K, f"tc {case}")
+
+
+def test_tc_c1_full():
+    cfg = synth.CONFIGS["c1"]
+    _tc_compare(synth.make_input(cfg), cfg.s, cfg.Wn, cfg.K, "tc c1")
+
+
+def test_tc_c5_sampled():
+    from paper_2006_13714_b200.bm import SC_KERNEL_TC_I8
+    cfg = synth.CONFIGS["c5"]
+    x = synth.make_input(cfg, n_frames=4)
+    p = _plan((cfg.H, cfg.W, 1, 8, cfg.s, cfg.Wn, cfg.K), "u8")
+    p.set_kernel(SC_KERNEL_TC_I8)
+    gi, gd = _run(p, x)
+    ny = p.ny
+    for f in (0, 3):
+        for r0, r1 in [(0, 3), (ny // 2, ny // 2 + 2), (ny - 3, ny)]:
+            oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=(f, f + 1), rows=(r0, r1))
+            sl = slice(r0 * p.nx, r1 * p.nx)
+            check_u8(gi[f:f + 1, sl], gd[f:f + 1, sl], oi, od, f"tc c5 frame {f} rows {r0}:{r1}")
+
+
+@pytest.mark.parametrize("kind", ["constant", "periodic", "saturated"])
+def test_tc_ties_and_extremes(kind):
+    rng = np.random.Generator(np.random.PCG64(11))
+    if kind == "constant":
+        x = np.full((1, 1, 50, 70), 93, dtype=np.uint8)
+    elif kind == "periodic":
+        x = np.tile(rng.integers(0, 256, size=(8, 8), dtype=np.uint8), (7, 9))[None, None].copy()
+    else:
+        x = (rng.integers(0, 2, size=(1, 1, 48, 64)) * 255).astype(np.uint8)
+    _tc_compare(x, 3, 21, 40, f"tc {kind}")
