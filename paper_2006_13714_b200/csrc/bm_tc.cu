@@ -21,6 +21,9 @@
 // one compare per pair against the reference's heap root into a bitmask; rows where some lane
 // passed go through the window check and the survivor queue / per-reference heaps of refq.cuh
 // (a4). Tiles outside a warp's window union are skipped. a6 as in bm_lanes.cu (exact int32).
+#include <cstdio>
+#include <cstdlib>
+
 #include "refq.cuh"
 #include "sc_internal.h"
 #include "sm100.cuh"
@@ -29,7 +32,7 @@
 namespace scbm {
 namespace {
 
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarps + 1) * 32;
 constexpr int kRBY = 8, kRBX = 16;   // reference block (M = 128)
 constexpr int kTR = 8, kTC = 16;     // candidate tile: 8 rows x 16 columns (N = 128)
@@ -45,7 +48,12 @@ struct TcArgs {
   int NCmax, NTImax;
   uint32_t off_A, off_E, off_N, off_heap, off_q;  // shared byte offsets
   int heap_pitch;
+  int dbg;  // SCBM_TC_DEBUG: bit0 skip epilogue work, bit1 skip MMA (timing experiments only)
 };
+
+__device__ unsigned long long g_tc_stats[8];  // debug counters (SCBM_TC_DEBUG & 4)
+__device__ unsigned long long g_tc_clk[8];    // debug cycle accumulators (SCBM_TC_DEBUG & 8)
+#define TCLK(i, t0) do { if (a.dbg & 8) { const long long _t = clock64(); if (lane == 0) atomicAdd(&g_tc_clk[i], (unsigned long long)(_t - (t0))); (t0) = _t; } } while (0)
 
 __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
 // k-th index of a centre-out enumeration of [0, n)
@@ -58,6 +66,7 @@ __device__ __forceinline__ int co_index(int k, int n) {
 
 __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  long long t0 = clock64();
   const int f = blockIdx.y;
   const int by = blockIdx.x / a.tiles_x, bx = blockIdx.x - by * a.tiles_x;
   const int iy_first = a.iy_begin + by * kRBY;
@@ -159,22 +168,52 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
     const int cy = cyA + r, cx = X0 + j;
     ntile[e] = (cy <= H - b && cx <= W - b) ? nsrc[size_t(cy) * a.Mx + cx] : kBig;
   }
-  for (int e = threadIdx.x; e < 128 * a.heap_pitch; e += kThreads) heaps[e] = kKeyInf;
+  for (int e = threadIdx.x; e < 2 * 128 * a.heap_pitch; e += kThreads) heaps[e] = kKeyInf;
+  for (int e = threadIdx.x; e < 2 * 128; e += kThreads)  // published thresholds: +inf until set
+    reinterpret_cast<uint64_t*>(smem + a.off_q)[e] = kKeyInf;
+  // Tile order: by L1 gap to the rectangle of the block's own reference positions, so every
+  // reference meets its spatial neighbourhood (including itself) first and its top-K threshold
+  // tightens early (fewer survivors); ties by index.
+  int16_t* order = reinterpret_cast<int16_t*>(smem + 64);
+  {
+    const int ry0 = iy_first * s, ry1 = iy_last * s, rx0 = ix_first * s, rx1 = ix_last * s;
+    auto dist_of = [&](int t) {
+      const int tr = t / NC, tc = t - (t / NC) * NC;
+      const int y0 = cyA + kTR * tr, y1 = y0 + kTR - 1, x0 = X0 + kTC * tc, x1 = x0 + kTC - 1;
+      const int gy = max(0, max(ry0 - y1, y0 - ry1)), gx = max(0, max(rx0 - x1, x0 - rx1));
+      return gy + gx;
+    };
+    const int nt = NTI * NC;
+    for (int t = threadIdx.x; t < nt; t += kThreads) {
+      const int dt = dist_of(t);
+      int rank = 0;
+      for (int u = 0; u < nt; ++u) {
+        const int du = dist_of(u);
+        rank += (du < dt || (du == dt && u < t)) ? 1 : 0;
+      }
+      order[rank] = int16_t(t);
+    }
+  }
   sm100::fence_proxy_async_smem();
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + 32);
   const int ntiles = NTI * NC;
+  const int lane_ = threadIdx.x & 31;
+  { const int lane = lane_; TCLK(0, t0); }
 
   if (warp == kEpiWarps) {
     // ---------------- MMA issuer (one elected thread)
     if (lane == 0) {
       for (int t = 0; t < ntiles; ++t) {
-        const int tr = co_index(t / NC, NTI), tc = co_index(t % NC, NC);
+        const int ot = order[t];
+        const int tr = ot / NC, tc = ot - tr * NC;
         const int buf = t & 1;
         if (t >= 2) sm100::mbar_wait(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1));
+        TCLK(5, t0);
         sm100::tc_fence_after();
+        if (a.dbg & 2) { sm100::mbar_arrive(bar_full + 8 * buf); continue; }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const uint64_t ad = sm100::smem_desc(sA + 256u * j, 128u, 512u);
@@ -186,8 +225,14 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue warps
-    const int wy = warp >> 1, wx = warp & 1;
+    // ---------------- epilogue warps: e = warp; lane quarter q = e % 4 (TMEM lanes 32q..32q+31
+    // = references 32q..32q+31, a 4 x 8 sub-block); half hh = e / 4 takes tile rows 4hh..4hh+3.
+    // Each lane keeps the best 16 keys of ITS reference over ITS half in registers (branch-free
+    // insertion network, no memory latency, no divergence). The filter threshold is
+    // min(own 16th, partner's published 16th): each list holds KP keys of the reference, so the
+    // KP-th best of their union is <= either (a valid upper bound).
+    const int q = warp & 3, hh = warp >> 2;
+    const int wy = q >> 1, wx = q & 1;
     const int iy = iy_first + 4 * wy + (lane >> 3), ix = ix_first + 8 * wx + (lane & 7);
     const bool valid = iy <= iy_last && ix <= ix_last;
     const int ry = iy * s, rx = ix * s;
@@ -196,28 +241,39 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
     const bool wvalid = wiy0 <= iy_last && wix0 <= ix_last;
     const int wy_lo = wiy0 * s + a.lo, wy_hi = wiy1 * s + a.hi;  // candidate rows of this warp
     const int wx_lo = wix0 * s + a.lo, wx_hi = wix1 * s + a.hi;
-    const int ref_local = warp * 32 + lane;
-    uint64_t* qk = heaps + size_t(128) * a.heap_pitch + warp * 64;
-    RefHeaps hp{smem_addr(heaps), a.heap_pitch, a.KP, heap_depth(a.KP)};
-    WarpQueue q{smem_addr(qk), smem_addr(reinterpret_cast<int32_t*>(heaps + size_t(128) * a.heap_pitch +
-                                                                     kEpiWarps * 64) + warp * 64)};
-    const uint32_t myheap = hp.heap(ref_local);
-    int32_t thr = 0x7fffffff;  // d' threshold (root of this reference's heap)
-    int qcnt = 0;
-    const uint32_t tq = tmem + (uint32_t(32 * warp) << 16);
+    const int ref_local = q * 32 + lane;
+    uint64_t* pub = reinterpret_cast<uint64_t*>(smem + a.off_q);  // [2][128] published KP-th keys
+    uint64_t r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = kKeyInf;
+    const int kp1 = a.KP - 1;
+#define KTH_OF(r_) ({ uint64_t _v = (r_)[15]; _Pragma("unroll") for (int _i = 0; _i < 15; ++_i) if (_i == kp1) _v = (r_)[_i]; _v; })
+    uint64_t other = kKeyInf;
+    int32_t thr = 0x7fffffff;  // d' threshold
+    const uint32_t tq = tmem + (uint32_t(32 * q) << 16);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + a.off_q + kEpiWarps * 64 * 12) + warp * 32 * 16;
 
     for (int t = 0; t < ntiles; ++t) {
-      const int tr = co_index(t / NC, NTI), tc = co_index(t % NC, NC);
+      const int ot = order[t];
+      const int tr = ot / NC, tc = ot - tr * NC;
       const int buf = t & 1;
+      TCLK(2, t0);
       sm100::mbar_wait(bar_full + 8 * buf, uint32_t((t >> 1) & 1));
       sm100::tc_fence_after();
+      TCLK(1, t0);
       const int cx0 = X0 + kTC * tc;
-      const bool xrel = wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo;
+      const bool xrel = !(a.dbg & 1) && wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo;
       if (xrel) {
+        // exchange thresholds with the partner half once per tile (stale reads are conservative)
+        const uint64_t mine = KTH_OF(r);
+        pub[hh * 128 + ref_local] = mine;
+        other = pub[(1 - hh) * 128 + ref_local];
+        thr = unord_i32(uint32_t((mine < other ? mine : other) >> 32));
 #pragma unroll 1
-        for (int i = 0; i < kTR; ++i) {
+        for (int i = 4 * hh; i < 4 * hh + 4; ++i) {
           const int cy = cyA + kTR * tr + i;
           if (cy < wy_lo || cy > wy_hi || cy > cyB) continue;  // warp-uniform
+          if ((a.dbg & 4) && lane == 0) atomicAdd(&g_tc_stats[0], 1ull);
           uint32_t c[16];
           sm100::tmem_ld16(tq + 128u * buf + 16u * i, c);
           const int4* nrow = reinterpret_cast<const int4*>(ntile + (kTR * tr + i) * NWc + kTC * tc);
@@ -240,23 +296,33 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
           const int jlo = max(0, rx + a.lo - cx0), jhi = min(15, min(rx + a.hi, W - b) - cx0);
           const unsigned cols = (yok && jhi >= jlo) ? (((2u << jhi) - 1u) & ~((1u << jlo) - 1u)) : 0u;
           bits &= cols;
-          const unsigned any = __reduce_or_sync(0xffffffffu, bits);
-          if (any) {
-            bool refresh = false;
+          if (a.dbg & 4) {
+            const int tot = __reduce_add_sync(0xffffffffu, __popc(bits));
+            if (lane == 0) { atomicAdd(&g_tc_stats[1], tot ? 1ull : 0ull); atomicAdd(&g_tc_stats[2], (unsigned long long)tot); }
+          }
+          TCLK(2, t0);
+          if (__any_sync(0xffffffffu, bits != 0)) {
+            // slow path: stage the 16 ordered distances, then insert one survivor per lane per
+            // round into the register list
+            uint32_t* sc = scratch + lane;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              if (!(any & (1u << j))) continue;
-              const bool pb = (bits >> j) & 1u;
-              const uint64_t key = (uint64_t(ord_i32(dp[j])) << 32) | uint32_t(cy * W + cx0 + j);
-              const bool fill = pb && thr == 0x7fffffff;
-              if (fill) {
-                heap_push_cold(myheap, a.KP, hp.depth, key);
-                thr = unord_i32(hp.thr_hi(ref_local));
+            for (int j = 0; j < 16; ++j) sc[32 * j] = ord_i32(dp[j]);
+            const uint32_t idx0 = uint32_t(cy * W + cx0);
+            while (__any_sync(0xffffffffu, bits != 0)) {
+              const int j = bits ? __ffs(bits) - 1 : 0;
+              const uint64_t x = bits ? ((uint64_t(sc[32 * j]) << 32) | (idx0 + j)) : kKeyInf;
+              bits &= bits - 1;
+#pragma unroll
+              for (int k = 15; k > 0; --k) {
+                const uint64_t m = x < r[k] ? x : r[k];
+                r[k] = r[k - 1] > m ? r[k - 1] : m;
               }
-              const bool pass = pb && !fill && dp[j] <= thr;
-              refresh |= queue_push(q, hp, qcnt, pass, key, ref_local, lane);
+              r[0] = x < r[0] ? x : r[0];
             }
-            if (refresh) thr = unord_i32(hp.thr_hi(ref_local));
+            const uint64_t mn = KTH_OF(r);
+            thr = unord_i32(uint32_t((mn < other ? mn : other) >> 32));
+            __syncwarp();
+            TCLK(3, t0);
           }
         }
       }
@@ -264,26 +330,43 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(bar_empty + 8 * buf);
     }
-    while (qcnt > 0) qcnt = queue_drain(q, hp, qcnt, lane);
-    heap_sort(myheap, a.KP, hp.depth);
-    __syncwarp();
-    // ---- a6: outputs, one reference at a time across the warp
+    TCLK(2, t0);
+    // publish this half's list, merge the partner's into half 0's, output split by halves
+    uint64_t* lists = heaps;  // [2][128][heap_pitch]
+#pragma unroll
+    for (int i = 0; i < 16; ++i) lists[(size_t(hh) * 128 + ref_local) * a.heap_pitch + i] = r[i];
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32));
+    if (hh == 0) {
+      for (int i = 0; i < 16; ++i) {
+        const uint64_t x = lists[(size_t(128) + ref_local) * a.heap_pitch + i];
+#pragma unroll
+        for (int k = 15; k > 0; --k) {
+          const uint64_t m = x < r[k] ? x : r[k];
+          r[k] = r[k - 1] > m ? r[k - 1] : m;
+        }
+        r[0] = x < r[0] ? x : r[0];
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) lists[size_t(ref_local) * a.heap_pitch + i] = r[i];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32));
+    // ---- a6: outputs; the two warps of a quarter split its 32 references
     const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
     const int32_t nr = valid ? nsrc[size_t(ry) * a.Mx + rx] : 0;
-    for (int r = 0; r < 32; ++r) {
-      const int riy = iy_first + 4 * wy + (r >> 3), rix = ix_first + 8 * wx + (r & 7);
-      const int32_t nr_r = __shfl_sync(0xffffffffu, nr, r);
+    for (int rr = 16 * hh; rr < 16 * hh + 16; ++rr) {
+      const int riy = iy_first + 4 * wy + (rr >> 3), rix = ix_first + 8 * wx + (rr & 7);
+      const int32_t nr_r = __shfl_sync(0xffffffffu, nr, rr);
       if (riy > iy_last || rix > ix_last) continue;  // warp-uniform
-      const uint64_t* Lh = heaps + size_t(warp * 32 + r) * a.heap_pitch;
       const size_t o = (size_t(f) * band_refs + size_t(riy - a.iy_begin) * a.nx + rix) * a.K;
       for (int k = lane; k < a.K; k += 32) {
-        const uint64_t key = Lh[k];
+        const uint64_t key = lists[size_t(q * 32 + rr) * a.heap_pitch + k];
         const bool none = key == kKeyInf;
         a.idx_out[o + k] = none ? -1 : int32_t(uint32_t(key));
         a.dist_out[o + k] = none ? 0x7fffffff : unord_i32(uint32_t(key >> 32)) + nr_r;
       }
     }
   }
+  { const int lane = lane_; if (warp < kEpiWarps) TCLK(4, t0); }
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == kEpiWarps) {
@@ -303,7 +386,7 @@ TcLayout tc_layout(const Geometry& g) {
   const int span_y = (kRBY - 1) * g.s + g.Wn;
   L.NCmax = (span_x + 15) / kTC + 1;
   L.NTImax = (span_y + kTR - 1) / kTR;
-  L.heap_pitch = g.KP | 1;
+  L.heap_pitch = 17;  // 16 register-list keys per reference, odd pitch
   uint32_t off = 1024;  // barriers + TMEM slot
   L.off_A = off;
   off += 128 * 64;
@@ -313,9 +396,10 @@ TcLayout tc_layout(const Geometry& g) {
   off += uint32_t(L.NTImax * kTR) * L.NCmax * kTC * 4;
   off = (off + 15) & ~15u;
   L.off_heap = off;
-  off += uint32_t(128 * L.heap_pitch) * 8;
+  off += uint32_t(2 * 128 * L.heap_pitch) * 8;  // two partial heaps per reference
   L.off_q = off;
   off += kEpiWarps * 64 * (8 + 4);
+  off += kEpiWarps * 32 * 16 * 4;  // per-warp slow-path scratch (16 ordered distances per lane)
   L.bytes = off;
   return L;
 }
@@ -323,7 +407,7 @@ TcLayout tc_layout(const Geometry& g) {
 }  // namespace
 
 bool tc_supported(const Geometry& g) {
-  if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.C != 1 || g.KP > 64 || g.Wn > 64) return false;
+  if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.C != 1 || g.KP > 16 || g.Wn > 64) return false;
   return tc_layout(g).bytes <= 227 * 1024;
 }
 
@@ -343,9 +427,24 @@ cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
   a.NCmax = L.NCmax; a.NTImax = L.NTImax;
   a.off_A = L.off_A; a.off_E = L.off_E; a.off_N = L.off_N; a.off_heap = L.off_heap; a.off_q = L.off_q;
   a.heap_pitch = L.heap_pitch;
+  {
+    const char* e = getenv("SCBM_TC_DEBUG");
+    a.dbg = e ? atoi(e) : 0;
+  }
   const int tiles_y = (iy_end - iy_begin + kRBY - 1) / kRBY;
   cudaFuncSetAttribute(bm_tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.bytes));
   bm_tc_i8_kernel<<<dim3(a.tiles_x * tiles_y, F), kThreads, L.bytes, st>>>(a);
+  if (a.dbg & 12) {
+    unsigned long long h[8];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_tc_stats, sizeof(h));
+    unsigned long long c[8];
+    cudaMemcpyFromSymbol(c, g_tc_clk, sizeof(c));
+    fprintf(stderr, "tc clk (warp-cycles): staging %llu wait_full %llu fast %llu slow %llu tail %llu mma_wait_empty %llu\n",
+            c[0], c[1], c[2], c[3], c[4], c[5]);
+    fprintf(stderr, "tc stats: rows %llu rows_with_surv %llu survivors %llu warmup_survivors %llu\n", h[0], h[1],
+            h[2], h[3]);
+  }
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

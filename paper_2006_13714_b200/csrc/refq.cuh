@@ -53,17 +53,17 @@ struct RefHeaps {
 __device__ __forceinline__ void heap_push(uint32_t h, int KP, int depth, uint64_t x) {
   if (x >= lds64(h)) return;
   int pos = 0;
-  bool done = false;
+#pragma unroll 1
   for (int lvl = 0; lvl < depth; ++lvl) {
-    const int c = 2 * pos + 1;
-    const uint64_t a = (!done && c < KP) ? lds64(h + 8u * c) : 0ull;
-    const uint64_t b = (!done && c + 1 < KP) ? lds64(h + 8u * (c + 1)) : 0ull;
-    const bool right = b > a;
-    const uint64_t big = right ? b : a;
-    const bool move = !done && big > x;
-    if (move) sts64(h + 8u * pos, big);
-    pos = move ? c + (right ? 1 : 0) : pos;
-    done = done || !move;
+    int c = 2 * pos + 1;
+    if (c >= KP) break;
+    const uint64_t l = lds64(h + 8u * c);
+    const uint64_t r = (c + 1 < KP) ? lds64(h + 8u * (c + 1)) : 0ull;
+    const bool right = r > l;
+    const uint64_t big = right ? r : l;
+    if (big <= x) break;
+    sts64(h + 8u * pos, big);
+    pos = c + (right ? 1 : 0);
   }
   sts64(h + 8u * pos, x);
 }

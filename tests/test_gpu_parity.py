@@ -271,7 +271,7 @@ def _tc_cases(n, seed):
         W = int(rng.integers(8, 130))
         s = int(rng.integers(1, 6))
         Wn = int(rng.integers(1, 50))
-        K = int(rng.integers(1, 65))
+        K = int(rng.integers(1, 17))  # the TC kernel keeps a 16-key register list per reference
         out.append((H, W, s, Wn, K))
     return out
 
@@ -318,4 +318,14 @@ def test_tc_ties_and_extremes(kind):
         x = np.tile(rng.integers(0, 256, size=(8, 8), dtype=np.uint8), (7, 9))[None, None].copy()
     else:
         x = (rng.integers(0, 2, size=(1, 1, 48, 64)) * 255).astype(np.uint8)
-    _tc_compare(x, 3, 21, 40, f"tc {kind}")
+    _tc_compare(x, 3, 21, 16, f"tc {kind}")
+
+
+def test_tc_rejects_unsupported():
+    from paper_2006_13714_b200.bm import SC_KERNEL_TC_I8, ScError
+    for args, dt in [((64, 64, 1, 8, 4, 21, 32), "u8"), ((64, 64, 1, 7, 4, 21, 16), "u8"),
+                     ((64, 64, 2, 8, 4, 21, 16), "u8"), ((64, 64, 1, 8, 4, 21, 16), "f32")]:
+        p = _plan(args, dt)
+        with pytest.raises(ScError) as e:
+            p.set_kernel(SC_KERNEL_TC_I8)
+        assert e.value.code == 2
