@@ -108,12 +108,12 @@ def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1)):
         xs = [min(cfg.W - cfg.b, ix * cfg.s + hi) - max(0, ix * cfg.s + lo) + 1 for ix in range(nx)]
         return sum(ys) * sum(xs)
 
-    # calibrate on one middle row, then size the sample to ~target_s seconds
-    mid = ny // 2
+    # calibrate on one row, then size the sample (starting at the top rows) to ~target_s seconds
+    mid = 0
     t0 = time.perf_counter()
-    oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(mid, mid + 1))
+    oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(ny // 2, ny // 2 + 1))
     dt = max(time.perf_counter() - t0, 1e-3)
-    rows = int(max(1, min(ny - mid, target_s / dt)))
+    rows = int(max(1, min(ny, target_s / dt)))
     t0 = time.perf_counter()
     oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(mid, mid + rows))
     dt = time.perf_counter() - t0
@@ -266,10 +266,19 @@ def main():
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # FP32 FFMA lanes x 2 ops x max clock
         bound, unit, peak_note = "alu", "TFLOP/s", "FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md section 7)"
     achieved = 2.0 * macs_launch / (match_ms / 1e3) / 1e12 if match_ms > 0 else None
+    traffic, traffic_src = None, None
     kname = {0: "bm_lanes_kernel", 1: "bm_tc_i8_kernel", 2: "bm_simt_kernel"}[info["kernel"]]
+    prof = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{kname.replace('_kernel', '')}_{cfg.name}_metrics.json")
+    if os.path.exists(prof):
+        m = json.load(open(prof))
+        mb = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+        traffic = sum(float(m[k]["value"]) * mb.get(m[k]["unit"], 1.0) for k in
+                      ("dram__bytes_read.sum", "dram__bytes_write.sum")) * 1e6
+        traffic_src = (f"{os.path.relpath(prof, ROOT)}: dram read+write bytes of one launch "
+                       f"({info['frames_per_chunk']} frames), ncu --set full")
     roof = {"bound": bound, "kernel": kname,
             "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peak_note, "kernel_ms_per_step": match_ms, "norm_ms_per_step": norm_ms,
             "kernel_share_of_step": match_ms / ms if ms > 0 else None,
             "algorithmic_ops_per_launch": 2.0 * macs_launch}
