@@ -16,6 +16,7 @@
 // Arithmetic is identical to bm_simt.cu: u8 exact int32, f32 fp32 FMA + fp32 re-score.
 #include "sc_internal.h"
 #include "refq.cuh"
+#include "regtopk.cuh"
 #include "topk.cuh"
 
 namespace scbm {
@@ -35,6 +36,10 @@ struct LanesArgs {
   int NP, NPs, NQ, NHp;  // norm tile: phase planes (x mod NP, NP = 1 << NPs), words per plane row, height
   int PADT;           // zero rows above both tiles
   int img_words, norm_words, list_pitch;
+  int rb;             // R32 path: window-relative index bits of the 32-bit keys
+  uint32_t dsat;      // R32 path: distance saturation value
+  int* fix_count;     // R32 path: references needing the exact fix-up (count + list)
+  int* fix_list;
 };
 
 template <typename In> struct LPath;
@@ -119,7 +124,9 @@ template <> struct LPath<uint8_t> {
 // Offset k of a centre-out enumeration of [lo, hi]: 0, 1, -1, 2, -2, ... (skips outside values).
 __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
 
-template <typename In, int BK, int VY, bool ONE_CH>
+// KR == 0: shared heaps + survivor queue (refq.cuh); KR in {16, 32}: per-lane 32-bit register
+// top-KR (regtopk.cuh, u8 only) with the exact fix-up for saturated / short references.
+template <typename In, int BK, int VY, bool ONE_CH, int KR>
 __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
   using P = LPath<In>;
   using T = typename P::T;
@@ -212,6 +219,15 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
   const int nplane = a.NHp * a.NQ, npm = a.NP - 1;
   auto nidx = [&](int yl, int xl) { return (xl & npm) * nplane + yl * a.NQ + (xl >> a.NPs); };
   const T nr = ntile[nidx(ry_l, rx_l)];
+  constexpr bool R32 = KR > 0;
+  RegTopK32<(KR > 0 ? KR : 1)> rt;
+  const Key32 key32{a.rb, a.dsat};
+  int thr_dp = 0;  // R32: largest d' that may still pass (d' = d - ||X_i||^2)
+  if constexpr (R32) {
+    rt.init();
+    thr_dp = int(a.dsat) - int(nr);
+  }
+  uint32_t* r32scratch = reinterpret_cast<uint32_t*>(qkeys) + warp * 32 * 16;  // VY <= 16 values per lane
 
   typename P::template Ref<BK> R;
   if (ONE_CH) P::template load_ref<BK>(R, tile, a, 0, ry_l, rx_l);
@@ -255,8 +271,37 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
         }
         continue;
       }
-      // fast path: one compare per candidate into a per-lane bitmask of passing rows
+      // rows inside the (warp-uniform) vertical window, columns inside this lane's window
+      const int i_lo = max(0, cy0 - cyb), i_hi = min(VY - 1, cy1 - cyb);
+      const unsigned rows = (i_hi >= i_lo) ? (((2u << i_hi) - 1u) & ~((1u << i_lo) - 1u)) : 0u;
       const T* nb = ntile + nidx(ny_l, cxl);
+      if constexpr (R32) {
+        // fast path: d' <= thr_dp into a bitmask; survivors inserted into the register list
+        int dpv[VY];
+        unsigned bits = 0;
+#pragma unroll
+        for (int i = 0; i < VY; ++i) {
+          dpv[i] = int(nb[i * a.NQ]) - 2 * int(acc[i]);
+          bits |= (dpv[i] <= thr_dp ? 1u : 0u) << i;
+        }
+        bits &= xok ? rows : 0u;
+        if (__any_sync(0xffffffffu, bits != 0)) {
+          uint32_t* sc = r32scratch + lane;
+#pragma unroll
+          for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(dpv[i] + int(nr));
+          const int rel0 = (dyb - a.lo) * a.Wn + (dx - a.lo);
+          while (__any_sync(0xffffffffu, bits != 0)) {
+            const int i = bits ? __ffs(bits) - 1 : 0;
+            const uint32_t x = bits ? key32.make(int(sc[32 * i]), rel0 + i * a.Wn) : 0xffffffffu;
+            bits &= bits - 1;
+            rt.insert(x);
+          }
+          thr_dp = key32.thr(rt.at(a.KP - 1)) - int(nr);
+          __syncwarp();
+        }
+        continue;
+      }
+      // fast path: one compare per candidate into a per-lane bitmask of passing rows
       uint32_t u[VY];
       unsigned bits = 0;
 #pragma unroll
@@ -264,9 +309,6 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
         u[i] = P::ord(nb[i * a.NQ] - T(2) * acc[i]);
         bits |= (u[i] <= thr ? 1u : 0u) << i;
       }
-      // rows inside the (warp-uniform) vertical window, columns inside this lane's window
-      const int i_lo = max(0, cy0 - cyb), i_hi = min(VY - 1, cy1 - cyb);
-      const unsigned rows = (i_hi >= i_lo) ? (((2u << i_hi) - 1u) & ~((1u << i_lo) - 1u)) : 0u;
       bits &= xok ? rows : 0u;
       const unsigned any = __reduce_or_sync(0xffffffffu, bits);
       if (any) {
@@ -289,6 +331,32 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
         if (refresh) thr = hp.thr_hi(ref_local);
       }
     }
+  }
+  if constexpr (R32) {
+    if (a.dense) return;
+    // a6 from registers; references whose K-th key is saturated / unfilled go to the fix-up
+    const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
+    if (lane_ok) {
+      const size_t ref_band = size_t(iy - a.iy_begin) * a.nx + ix;
+      if (!key32.exact(rt.at(a.KP - 1))) {
+        const int pos = atomicAdd(a.fix_count, 1);
+        a.fix_list[pos] = int(size_t(f) * band_refs + ref_band);
+      } else {
+        const size_t o = (size_t(f) * band_refs + ref_band) * a.K;
+        int32_t* dist = static_cast<int32_t*>(a.dist_out);
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          if (k < a.K) {
+            const uint32_t kk = rt.r[k];
+            const int rel = key32.rel(kk);
+            const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+            a.idx_out[o + k] = (ry + dyy + a.lo) * a.W + rx + dxx + a.lo;
+            dist[o + k] = key32.dist(kk);
+          }
+        }
+      }
+    }
+    return;
   }
   if (a.dense) return;
   while (qcnt > 0) qcnt = queue_drain(q, hp, qcnt, lane);
@@ -398,20 +466,20 @@ size_t lanes_smem(const Geometry& g, int NWY, int VY, LanesArgs* a) {
   a->list_pitch = g.KP | 1;
   size_t bytes = size_t(a->img_words + a->norm_words) * 4;
   bytes += size_t(NWY) * 32 * a->list_pitch * 8;  // reference lists
-  bytes += size_t(NWY) * 64 * (8 + 4);           // survivor queues
+  bytes += size_t(NWY) * 32 * 16 * 4;           // survivor queues (64 x 12 B) / R32 scratch (32 x 16 x 4 B)
   return bytes;
 }
 
-template <typename In, int BK, int VY>
+template <typename In, int BK, int VY, int KR>
 cudaError_t launch_t(const LanesArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + a.NWY - 1) / a.NWY;
   dim3 grid(a.tiles_x * tiles_y, F);
   if (a.C == 1) {
-    auto k = bm_lanes_kernel<In, BK, VY, true>;
+    auto k = bm_lanes_kernel<In, BK, VY, true, KR>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k<<<grid, 32 * a.NWY, smem, st>>>(a);
   } else {
-    auto k = bm_lanes_kernel<In, BK, VY, false>;
+    auto k = bm_lanes_kernel<In, BK, VY, false, KR>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k<<<grid, 32 * a.NWY, smem, st>>>(a);
   }
@@ -419,20 +487,29 @@ cudaError_t launch_t(const LanesArgs& a, int F, size_t smem, cudaStream_t st) {
 }
 
 template <typename In>
-cudaError_t dispatch(const LanesArgs& a, int F, size_t smem, cudaStream_t st, int bk, int vy) {
+cudaError_t dispatch(const LanesArgs& a, int F, size_t smem, cudaStream_t st, int bk, int vy, int kr) {
   if constexpr (sizeof(In) == 1) {
-    if (bk == 8 && vy == 11) return launch_t<In, 8, 11>(a, F, smem, st);
-    if (bk == 8 && vy == 7) return launch_t<In, 8, 7>(a, F, smem, st);
-    if (bk == 8) return launch_t<In, 8, 8>(a, F, smem, st);
-    if (bk == 4) return launch_t<In, 4, 8>(a, F, smem, st);
-    return launch_t<In, 16, 4>(a, F, smem, st);
+    if (bk == 8 && kr == 16) {
+      if (vy == 11) return launch_t<In, 8, 11, 16>(a, F, smem, st);
+      if (vy == 7) return launch_t<In, 8, 7, 16>(a, F, smem, st);
+      return launch_t<In, 8, 8, 16>(a, F, smem, st);
+    }
+    if (bk == 8 && kr == 32) {
+      if (vy == 11) return launch_t<In, 8, 11, 32>(a, F, smem, st);
+      return launch_t<In, 8, 8, 32>(a, F, smem, st);
+    }
+    if (bk == 8 && vy == 11) return launch_t<In, 8, 11, 0>(a, F, smem, st);
+    if (bk == 8 && vy == 7) return launch_t<In, 8, 7, 0>(a, F, smem, st);
+    if (bk == 8) return launch_t<In, 8, 8, 0>(a, F, smem, st);
+    if (bk == 4) return launch_t<In, 4, 8, 0>(a, F, smem, st);
+    return launch_t<In, 16, 4, 0>(a, F, smem, st);
   } else {
-    if (bk == 8 && vy == 13) return launch_t<In, 8, 13>(a, F, smem, st);
-    if (bk == 8 && vy == 7) return launch_t<In, 8, 7>(a, F, smem, st);
-    if (bk == 8) return launch_t<In, 8, 8>(a, F, smem, st);
-    if (bk == 7) return launch_t<In, 7, 8>(a, F, smem, st);
-    if (bk == 4) return launch_t<In, 4, 8>(a, F, smem, st);
-    return launch_t<In, 16, 4>(a, F, smem, st);
+    if (bk == 8 && vy == 13) return launch_t<In, 8, 13, 0>(a, F, smem, st);
+    if (bk == 8 && vy == 7) return launch_t<In, 8, 7, 0>(a, F, smem, st);
+    if (bk == 8) return launch_t<In, 8, 8, 0>(a, F, smem, st);
+    if (bk == 7) return launch_t<In, 7, 8, 0>(a, F, smem, st);
+    if (bk == 4) return launch_t<In, 4, 8, 0>(a, F, smem, st);
+    return launch_t<In, 16, 4, 0>(a, F, smem, st);
   }
 }
 
@@ -455,6 +532,14 @@ size_t lanes_smem_bytes(const Geometry& g, int nwy) {
   return lanes_smem(g, nwy, vy_for(g), &a);
 }
 
+// Register 32-bit top-K eligibility (u8, exact patch side 8, K <= 32, Wn^2 <= 2^11 so that the
+// distance field keeps >= 21 bits).
+int lanes_r32_slots(const Geometry& g) {
+  if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.KP > 32) return 0;
+  if (key32_rel_bits(g.Wn) > 11) return 0;
+  return g.KP <= 16 ? 16 : 32;
+}
+
 cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                             int32_t* idx_out, void* dist_out, void* dense, cudaStream_t st,
                             int64_t* launches) {
@@ -472,10 +557,23 @@ cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int 
   a.tiles_x = (g.nx + 31) / 32;
   const int vy = vy_for(g);
   const size_t smem = lanes_smem(g, a.NWY, vy, &a);
+  const int kr = dense ? 0 : lanes_r32_slots(g);
+  a.rb = key32_rel_bits(g.Wn);
+  a.dsat = (a.rb >= 32) ? 0u : uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
+  a.fix_count = p.ws.fix_count;
+  a.fix_list = p.ws.fix_list;
   if (launches) *launches += 1;
   const int bk = bk_for(g.b, g.dtype == SC_DTYPE_U8);
-  if (g.dtype == SC_DTYPE_U8) return dispatch<uint8_t>(a, F, smem, st, bk, vy);
-  return dispatch<float>(a, F, smem, st, bk, vy);
+  cudaError_t e;
+  if (kr > 0) {
+    e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
+  if (g.dtype == SC_DTYPE_U8) e = dispatch<uint8_t>(a, F, smem, st, bk, vy, kr);
+  else e = dispatch<float>(a, F, smem, st, bk, vy, kr);
+  if (e != cudaSuccess || kr == 0) return e;
+  if (launches) *launches += 1;
+  return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
 }
 
 }  // namespace scbm

@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "refq.cuh"
+#include "regtopk.cuh"
 #include "sc_internal.h"
 #include "sm100.cuh"
 #include "topk.cuh"
@@ -48,6 +49,10 @@ struct TcArgs {
   int NCmax, NTImax;
   uint32_t off_A, off_E, off_N, off_heap, off_q;  // shared byte offsets
   int heap_pitch;
+  int rb;          // 32-bit keys: window-relative index bits
+  uint32_t dsat;   // 32-bit keys: distance saturation value
+  int* fix_count;  // exact fix-up list (fixup.cu)
+  int* fix_list;
   int dbg;  // SCBM_TC_DEBUG: bit0 skip epilogue work, bit1 skip MMA (timing experiments only)
 };
 
@@ -242,14 +247,14 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
     const int wy_lo = wiy0 * s + a.lo, wy_hi = wiy1 * s + a.hi;  // candidate rows of this warp
     const int wx_lo = wix0 * s + a.lo, wx_hi = wix1 * s + a.hi;
     const int ref_local = q * 32 + lane;
-    uint64_t* pub = reinterpret_cast<uint64_t*>(smem + a.off_q);  // [2][128] published KP-th keys
-    uint64_t r[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) r[i] = kKeyInf;
+    uint32_t* pub = reinterpret_cast<uint32_t*>(smem + a.off_q);  // [2][128] published K-th keys
+    RegTopK32<16> rt;
+    rt.init();
+    const Key32 key32{a.rb, a.dsat};
     const int kp1 = a.KP - 1;
-#define KTH_OF(r_) ({ uint64_t _v = (r_)[15]; _Pragma("unroll") for (int _i = 0; _i < 15; ++_i) if (_i == kp1) _v = (r_)[_i]; _v; })
-    uint64_t other = kKeyInf;
-    int32_t thr = 0x7fffffff;  // d' threshold
+    const int32_t nr = valid ? ntile[(ry - cyA) * NWc + (rx - X0)] : 0;  // ||X_i||^2 (centred)
+    uint32_t other = 0xffffffffu;
+    int32_t thr = 0x7fffffff;  // d' threshold (d' = d - ||X_i||^2)
     const uint32_t tq = tmem + (uint32_t(32 * q) << 16);
     uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + a.off_q + kEpiWarps * 64 * 12) + warp * 32 * 16;
 
@@ -265,10 +270,10 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
       const bool xrel = !(a.dbg & 1) && wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo;
       if (xrel) {
         // exchange thresholds with the partner half once per tile (stale reads are conservative)
-        const uint64_t mine = KTH_OF(r);
+        const uint32_t mine = rt.at(kp1);
         pub[hh * 128 + ref_local] = mine;
         other = pub[(1 - hh) * 128 + ref_local];
-        thr = unord_i32(uint32_t((mine < other ? mine : other) >> 32));
+        thr = key32.thr(min(mine, other)) - nr;
 #pragma unroll 1
         for (int i = 4 * hh; i < 4 * hh + 4; ++i) {
           const int cy = cyA + kTR * tr + i;
@@ -302,25 +307,19 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
           }
           TCLK(2, t0);
           if (__any_sync(0xffffffffu, bits != 0)) {
-            // slow path: stage the 16 ordered distances, then insert one survivor per lane per
-            // round into the register list
+            // slow path: stage the 16 distances, then insert one survivor per lane per round
+            // into the 32-bit register list
             uint32_t* sc = scratch + lane;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sc[32 * j] = ord_i32(dp[j]);
-            const uint32_t idx0 = uint32_t(cy * W + cx0);
+            for (int j = 0; j < 16; ++j) sc[32 * j] = uint32_t(dp[j] + nr);
+            const int rel0 = (cy - ry - a.lo) * a.Wn + (cx0 - rx - a.lo);
             while (__any_sync(0xffffffffu, bits != 0)) {
               const int j = bits ? __ffs(bits) - 1 : 0;
-              const uint64_t x = bits ? ((uint64_t(sc[32 * j]) << 32) | (idx0 + j)) : kKeyInf;
+              const uint32_t x = bits ? key32.make(int(sc[32 * j]), rel0 + j) : 0xffffffffu;
               bits &= bits - 1;
-#pragma unroll
-              for (int k = 15; k > 0; --k) {
-                const uint64_t m = x < r[k] ? x : r[k];
-                r[k] = r[k - 1] > m ? r[k - 1] : m;
-              }
-              r[0] = x < r[0] ? x : r[0];
+              rt.insert(x);
             }
-            const uint64_t mn = KTH_OF(r);
-            thr = unord_i32(uint32_t((mn < other ? mn : other) >> 32));
+            thr = key32.thr(min(rt.at(kp1), other)) - nr;
             __syncwarp();
             TCLK(3, t0);
           }
@@ -331,38 +330,34 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
       if (lane == 0) sm100::mbar_arrive(bar_empty + 8 * buf);
     }
     TCLK(2, t0);
-    // publish this half's list, merge the partner's into half 0's, output split by halves
-    uint64_t* lists = heaps;  // [2][128][heap_pitch]
+    // merge the partner half's list into half 0's, then output (or flag for the exact fix-up)
+    uint32_t* lists = reinterpret_cast<uint32_t*>(heaps);  // [128][17] half-1 lists
+    if (hh == 1) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) lists[(size_t(hh) * 128 + ref_local) * a.heap_pitch + i] = r[i];
-    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32));
-    if (hh == 0) {
-      for (int i = 0; i < 16; ++i) {
-        const uint64_t x = lists[(size_t(128) + ref_local) * a.heap_pitch + i];
-#pragma unroll
-        for (int k = 15; k > 0; --k) {
-          const uint64_t m = x < r[k] ? x : r[k];
-          r[k] = r[k - 1] > m ? r[k - 1] : m;
-        }
-        r[0] = x < r[0] ? x : r[0];
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) lists[size_t(ref_local) * a.heap_pitch + i] = r[i];
+      for (int i = 0; i < 16; ++i) lists[ref_local * 17 + i] = rt.r[i];
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32));
-    // ---- a6: outputs; the two warps of a quarter split its 32 references
-    const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
-    const int32_t nr = valid ? nsrc[size_t(ry) * a.Mx + rx] : 0;
-    for (int rr = 16 * hh; rr < 16 * hh + 16; ++rr) {
-      const int riy = iy_first + 4 * wy + (rr >> 3), rix = ix_first + 8 * wx + (rr & 7);
-      const int32_t nr_r = __shfl_sync(0xffffffffu, nr, rr);
-      if (riy > iy_last || rix > ix_last) continue;  // warp-uniform
-      const size_t o = (size_t(f) * band_refs + size_t(riy - a.iy_begin) * a.nx + rix) * a.K;
-      for (int k = lane; k < a.K; k += 32) {
-        const uint64_t key = lists[size_t(q * 32 + rr) * a.heap_pitch + k];
-        const bool none = key == kKeyInf;
-        a.idx_out[o + k] = none ? -1 : int32_t(uint32_t(key));
-        a.dist_out[o + k] = none ? 0x7fffffff : unord_i32(uint32_t(key >> 32)) + nr_r;
+    if (hh == 0) {
+      for (int i = 0; i < 16; ++i) rt.insert(lists[ref_local * 17 + i]);
+      if (valid) {
+        const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
+        const size_t ref_band = size_t(iy - a.iy_begin) * a.nx + ix;
+        if (!key32.exact(rt.at(kp1))) {
+          const int pos = atomicAdd(a.fix_count, 1);
+          a.fix_list[pos] = int(size_t(f) * band_refs + ref_band);
+        } else {
+          const size_t o = (size_t(f) * band_refs + ref_band) * a.K;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            if (k < a.K) {
+              const uint32_t kk = rt.r[k];
+              const int rel = key32.rel(kk);
+              const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+              a.idx_out[o + k] = (ry + dyy + a.lo) * W + rx + dxx + a.lo;
+              a.dist_out[o + k] = key32.dist(kk);
+            }
+          }
+        }
       }
     }
   }
@@ -407,7 +402,7 @@ TcLayout tc_layout(const Geometry& g) {
 }  // namespace
 
 bool tc_supported(const Geometry& g) {
-  if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.C != 1 || g.KP > 16 || g.Wn > 64) return false;
+  if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.C != 1 || g.KP > 16 || g.Wn > 45) return false;
   return tc_layout(g).bytes <= 227 * 1024;
 }
 
@@ -427,12 +422,18 @@ cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
   a.NCmax = L.NCmax; a.NTImax = L.NTImax;
   a.off_A = L.off_A; a.off_E = L.off_E; a.off_N = L.off_N; a.off_heap = L.off_heap; a.off_q = L.off_q;
   a.heap_pitch = L.heap_pitch;
+  a.rb = key32_rel_bits(g.Wn);
+  a.dsat = uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
+  a.fix_count = p.ws.fix_count;
+  a.fix_list = p.ws.fix_list;
   {
     const char* e = getenv("SCBM_TC_DEBUG");
     a.dbg = e ? atoi(e) : 0;
   }
   const int tiles_y = (iy_end - iy_begin + kRBY - 1) / kRBY;
   cudaFuncSetAttribute(bm_tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.bytes));
+  cudaError_t e0 = cudaMemsetAsync(a.fix_count, 0, sizeof(int), st);
+  if (e0 != cudaSuccess) return e0;
   bm_tc_i8_kernel<<<dim3(a.tiles_x * tiles_y, F), kThreads, L.bytes, st>>>(a);
   if (a.dbg & 12) {
     unsigned long long h[8];
@@ -445,8 +446,10 @@ cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
     fprintf(stderr, "tc stats: rows %llu rows_with_surv %llu survivors %llu warmup_survivors %llu\n", h[0], h[1],
             h[2], h[3]);
   }
-  if (launches) *launches += 1;
-  return cudaGetLastError();
+  if (launches) *launches += 2;
+  cudaError_t e1 = cudaGetLastError();
+  if (e1 != cudaSuccess) return e1;
+  return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
 }
 
 }  // namespace scbm

@@ -45,6 +45,8 @@ void free_ws(sc_bm_plan_s* p) {
   if (p->ws.sat) cudaFree(p->ws.sat);
   if (p->ws.bandsum) cudaFree(p->ws.bandsum);
   if (p->ws.norm) cudaFree(p->ws.norm);
+  if (p->ws.fix_count) cudaFree(p->ws.fix_count);
+  if (p->ws.fix_list) cudaFree(p->ws.fix_list);
   p->ws = Workspace{};
 }
 
@@ -175,6 +177,9 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   cudaError_t e = cudaMalloc(&p->ws.sat, SP * H * acc * p->F);
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.bandsum, SP * p->nbands * acc * p->F);
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.norm, size_t(g.My) * g.Mx * 4 * p->F);
+  if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_count, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_list, size_t(g.ny) * g.nx * sizeof(int) * p->F);
+  if (e == cudaSuccess) e = cudaMemset(p->ws.fix_count, 0, sizeof(int));
   if (e != cudaSuccess) {
     free_ws(p);
     delete p;

@@ -23,6 +23,8 @@ struct Workspace {
   void* sat = nullptr;      // [F][H+1][W+1] uint32 (u8) or double (f32)
   void* bandsum = nullptr;  // [F][nbands][W+1] column band totals
   void* norm = nullptr;     // [F][My][Mx] int32 (u8) or float (f32)
+  int* fix_count = nullptr; // exact fix-up: number of flagged references of the current chunk
+  int* fix_list = nullptr;  // [F * n_refs] flagged (frame * band_refs + band ref) indices
   size_t bytes = 0;
 };
 
@@ -87,6 +89,12 @@ cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int 
                             int iy_end, int32_t* idx_out, void* dist_out, void* dense,
                             cudaStream_t st, int64_t* launches);
 int lanes_warps_for(const Geometry& g, int sm_count, int n_images);
+int lanes_r32_slots(const Geometry& g);
+
+// fixup.cu: exact top-K (64-bit keys, direct differences) for references flagged by the
+// 32-bit register top-K paths (saturated distance field or fewer than K candidates).
+cudaError_t launch_fixup(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                         int32_t* idx_out, void* dist_out, cudaStream_t st);
 
 // bm_tc.cu: the tcgen05 kind::i8 matcher (SC_KERNEL_TC_I8; u8, b = 8, C = 1).
 bool tc_supported(const Geometry& g);

@@ -270,7 +270,7 @@ def _tc_cases(n, seed):
         H = int(rng.integers(8, 90))
         W = int(rng.integers(8, 130))
         s = int(rng.integers(1, 6))
-        Wn = int(rng.integers(1, 50))
+        Wn = int(rng.integers(1, 46))  # TC: Wn^2 <= 2048 (32-bit keys keep >= 21 distance bits)
         K = int(rng.integers(1, 17))  # the TC kernel keeps a 16-key register list per reference
         out.append((H, W, s, Wn, K))
     return out
@@ -329,3 +329,19 @@ def test_tc_rejects_unsupported():
         with pytest.raises(ScError) as e:
             p.set_kernel(SC_KERNEL_TC_I8)
         assert e.value.code == 2
+
+
+# ------------------------------------------------------------------ 32-bit register top-K + fix-up
+@pytest.mark.parametrize("kind,Wn,K", [("saturated", 35, 16), ("short", 3, 16), ("short", 5, 30),
+                                        ("random", 33, 16), ("random", 41, 32), ("constant", 33, 16)])
+def test_r32_keys_and_fixup(kind, Wn, K):
+    """u8, b=8: the default kernel keeps 32-bit keys (distance field saturating at 2^21-1 for
+    Wn >= 33) and recomputes saturated / short references exactly (fixup.cu)."""
+    rng = np.random.Generator(np.random.PCG64(31))
+    if kind == "saturated":
+        x = (rng.integers(0, 2, size=(2, 1, 72, 200)) * 255).astype(np.uint8)
+    elif kind == "constant":
+        x = np.full((1, 1, 60, 150), 17, dtype=np.uint8)
+    else:
+        x = rng.integers(0, 256, size=(2, 1, 70, 260), dtype=np.uint8)
+    _compare(x, 8, 4, Wn, K, "u8", where=f"r32 {kind} Wn{Wn} K{K}")
