@@ -551,7 +551,7 @@ cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int 
   a.dist_out = dist_out;
   a.dense = dense;
   a.H = g.H; a.W = g.W; a.C = g.C; a.b = g.b; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
-  a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mx;
+  a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.NWY = p.lanes_nwy;
   a.tiles_x = (g.nx + 31) / 32;

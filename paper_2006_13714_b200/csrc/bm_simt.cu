@@ -428,7 +428,7 @@ cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int i
   a.dist_out = dist_out;
   a.dense = dense;
   a.H = g.H; a.W = g.W; a.C = g.C; a.b = g.b; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
-  a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mx;
+  a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.TRY = p.tile.TRY; a.TRX = p.tile.TRX;
   a.tiles_x = (g.nx + a.TRX - 1) / a.TRX;

@@ -69,7 +69,7 @@ __device__ __forceinline__ int co_index(int k, int n) {
   return idx;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) bm_tc_i8_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   long long t0 = clock64();
   const int f = blockIdx.y;
@@ -92,8 +92,8 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
   const uint32_t sbase = smem_addr(smem);
   const uint32_t bar_full = sbase, bar_empty = sbase + 16;  // 2 + 2 mbarriers
   const uint32_t tmem_slot = sbase + 32;
+  const uint32_t bar_nc = sbase + 40;  // 2 mbarriers: norm values of the tile staged (count 32)
   const uint32_t sA = sbase + a.off_A, sE = sbase + a.off_E;
-  int32_t* ntile = reinterpret_cast<int32_t*>(smem + a.off_N);
   uint64_t* heaps = reinterpret_cast<uint64_t*>(smem + a.off_heap);
 
   if (warp == kEpiWarps) {
@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
     sm100::mbar_init(bar_full + 8, 1);
     sm100::mbar_init(bar_empty, kEpiWarps);
     sm100::mbar_init(bar_empty + 8, kEpiWarps);
+    sm100::mbar_init(bar_nc, 32);
+    sm100::mbar_init(bar_nc + 8, 32);
     sm100::fence_barrier_init();
   }
 
@@ -167,13 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
       *reinterpret_cast<uint4*>(row + mm * 16) = o;
     }
   }
-  const int32_t* nsrc = a.norm + size_t(f) * a.My * a.Mx;
-  for (int e = threadIdx.x; e < NTI * kTR * NWc; e += kThreads) {
-    const int r = e / NWc, j = e - r * NWc;
-    const int cy = cyA + r, cx = X0 + j;
-    ntile[e] = (cy <= H - b && cx <= W - b) ? nsrc[size_t(cy) * a.Mx + cx] : kBig;
-  }
-  for (int e = threadIdx.x; e < 2 * 128 * a.heap_pitch; e += kThreads) heaps[e] = kKeyInf;
+  const int32_t* nsrc = a.norm + size_t(f) * a.My * a.Mx;  // a.Mx = padded norm pitch
+
   for (int e = threadIdx.x; e < 2 * 128; e += kThreads)  // published thresholds: +inf until set
     reinterpret_cast<uint64_t*>(smem + a.off_q)[e] = kKeyInf;
   // Tile order: by L1 gap to the rectangle of the block's own reference positions, so every
@@ -209,24 +206,39 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
   { const int lane = lane_; TCLK(0, t0); }
 
   if (warp == kEpiWarps) {
-    // ---------------- MMA issuer (one elected thread)
-    if (lane == 0) {
-      for (int t = 0; t < ntiles; ++t) {
-        const int ot = order[t];
-        const int tr = ot / NC, tc = ot - tr * NC;
-        const int buf = t & 1;
-        if (t >= 2) sm100::mbar_wait(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1));
+    // ---------------- MMA issuer (one elected thread) + norm producer (all 32 lanes):
+    // before tile t's MMA the warp stages the tile's 8 x 16 candidate norms into ring slot t & 1
+    // (16-byte loads from the L2-resident norm map) and arrives on bar_nc[slot].
+    int32_t* ncring = reinterpret_cast<int32_t*>(smem + a.off_N);  // [2][8][16]
+    for (int t = 0; t < ntiles; ++t) {
+      const int ot = order[t];
+      const int tr = ot / NC, tc = ot - tr * NC;
+      const int buf = t & 1;
+      if (t >= 2) sm100::mbar_wait(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1));
+      {
+        const int rr = lane >> 2, cq = lane & 3;
+        const int cy = min(cyA + kTR * tr + rr, H - b);
+        const int4 v = __ldg(reinterpret_cast<const int4*>(nsrc + size_t(cy) * a.Mx + X0 + kTC * tc) + cq);
+        reinterpret_cast<int4*>(ncring + (buf * kTR + rr) * kTC)[cq] = v;
+        sm100::mbar_arrive(bar_nc + 8 * buf);
+      }
+      if (lane == 0) {
         TCLK(5, t0);
         sm100::tc_fence_after();
-        if (a.dbg & 2) { sm100::mbar_arrive(bar_full + 8 * buf); continue; }
+        if (a.dbg & 2) {
+          sm100::mbar_arrive(bar_full + 8 * buf);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint64_t ad = sm100::smem_desc(sA + 256u * j, 128u, 512u);
-          const uint64_t bd = sm100::smem_desc(sE + uint32_t(kTR * tr + 4 * j) * RP + uint32_t(tc) * 128u, RP, RP);
-          sm100::mma_i8(tmem + 128u * buf, ad, bd, kIdesc, j);
+          for (int j = 0; j < 2; ++j) {
+            const uint64_t ad = sm100::smem_desc(sA + 256u * j, 128u, 512u);
+            const uint64_t bd =
+                sm100::smem_desc(sE + uint32_t(kTR * tr + 4 * j) * RP + uint32_t(tc) * 128u, RP, RP);
+            sm100::mma_i8(tmem + 128u * buf, ad, bd, kIdesc, j);
+          }
+          sm100::mma_commit(bar_full + 8 * buf);
         }
-        sm100::mma_commit(bar_full + 8 * buf);
       }
+      __syncwarp();
     }
     __syncwarp();
   } else {
@@ -252,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
     rt.init();
     const Key32 key32{a.rb, a.dsat};
     const int kp1 = a.KP - 1;
-    const int32_t nr = valid ? ntile[(ry - cyA) * NWc + (rx - X0)] : 0;  // ||X_i||^2 (centred)
+    const int32_t nr = valid ? __ldg(nsrc + size_t(ry) * a.Mx + rx) : 0;  // ||X_i||^2 (centred)
     uint32_t other = 0xffffffffu;
     int32_t thr = 0x7fffffff;  // d' threshold (d' = d - ||X_i||^2)
     const uint32_t tq = tmem + (uint32_t(32 * q) << 16);
@@ -264,9 +276,11 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
       const int buf = t & 1;
       TCLK(2, t0);
       sm100::mbar_wait(bar_full + 8 * buf, uint32_t((t >> 1) & 1));
+      sm100::mbar_wait(bar_nc + 8 * buf, uint32_t((t >> 1) & 1));
       sm100::tc_fence_after();
       TCLK(1, t0);
       const int cx0 = X0 + kTC * tc;
+      const int4* ncr = reinterpret_cast<const int4*>(smem + a.off_N) + buf * kTR * 4;
       const bool xrel = !(a.dbg & 1) && wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo;
       if (xrel) {
         // exchange thresholds with the partner half once per tile (stale reads are conservative)
@@ -275,53 +289,61 @@ __global__ void __launch_bounds__(kThreads, 1) bm_tc_i8_kernel(TcArgs a) {
         other = pub[(1 - hh) * 128 + ref_local];
         thr = key32.thr(min(mine, other)) - nr;
 #pragma unroll 1
-        for (int i = 4 * hh; i < 4 * hh + 4; ++i) {
-          const int cy = cyA + kTR * tr + i;
-          if (cy < wy_lo || cy > wy_hi || cy > cyB) continue;  // warp-uniform
-          if ((a.dbg & 4) && lane == 0) atomicAdd(&g_tc_stats[0], 1ull);
-          uint32_t c[16];
-          sm100::tmem_ld16(tq + 128u * buf + 16u * i, c);
-          const int4* nrow = reinterpret_cast<const int4*>(ntile + (kTR * tr + i) * NWc + kTC * tc);
-          int nc[16];
+        for (int i2 = 4 * hh; i2 < 4 * hh + 4; i2 += 2) {
+          const int cyp = cyA + kTR * tr + i2;
+          const bool r0 = !(cyp < wy_lo || cyp > wy_hi || cyp > cyB);
+          const bool r1 = !(cyp + 1 < wy_lo || cyp + 1 > wy_hi || cyp + 1 > cyB);
+          if (!r0 && !r1) continue;  // warp-uniform
+          uint32_t c2[32];
+          sm100::tmem_ld32(tq + 128u * buf + 16u * i2, c2);
+          int4 nq[8];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int4 x = nrow[v];
-            nc[4 * v] = x.x; nc[4 * v + 1] = x.y; nc[4 * v + 2] = x.z; nc[4 * v + 3] = x.w;
-          }
+          for (int v = 0; v < 8; ++v) nq[v] = ncr[i2 * 4 + v];
           sm100::tmem_wait_ld();
-          int dp[16];
-          unsigned bits = 0;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            dp[j] = nc[j] - 2 * int(c[j]);
-            bits |= (dp[j] <= thr ? 1u : 0u) << j;
-          }
-          // window of this lane's reference (rows and columns)
-          const bool yok = valid && cy - ry >= a.lo && cy - ry <= a.hi;
-          const int jlo = max(0, rx + a.lo - cx0), jhi = min(15, min(rx + a.hi, W - b) - cx0);
-          const unsigned cols = (yok && jhi >= jlo) ? (((2u << jhi) - 1u) & ~((1u << jlo) - 1u)) : 0u;
-          bits &= cols;
-          if (a.dbg & 4) {
-            const int tot = __reduce_add_sync(0xffffffffu, __popc(bits));
-            if (lane == 0) { atomicAdd(&g_tc_stats[1], tot ? 1ull : 0ull); atomicAdd(&g_tc_stats[2], (unsigned long long)tot); }
-          }
-          TCLK(2, t0);
-          if (__any_sync(0xffffffffu, bits != 0)) {
-            // slow path: stage the 16 distances, then insert one survivor per lane per round
-            // into the 32-bit register list
-            uint32_t* sc = scratch + lane;
+          for (int h = 0; h < 2; ++h) {
+            if (!(h ? r1 : r0)) continue;
+            const int cy = cyp + h;
+            if ((a.dbg & 4) && lane == 0) atomicAdd(&g_tc_stats[0], 1ull);
+            int dp[16];
+            unsigned bits = 0;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sc[32 * j] = uint32_t(dp[j] + nr);
-            const int rel0 = (cy - ry - a.lo) * a.Wn + (cx0 - rx - a.lo);
-            while (__any_sync(0xffffffffu, bits != 0)) {
-              const int j = bits ? __ffs(bits) - 1 : 0;
-              const uint32_t x = bits ? key32.make(int(sc[32 * j]), rel0 + j) : 0xffffffffu;
-              bits &= bits - 1;
-              rt.insert(x);
+            for (int v = 0; v < 4; ++v) {
+              const int4 x = nq[4 * h + v];
+              dp[4 * v + 0] = x.x - 2 * int(c2[16 * h + 4 * v + 0]);
+              dp[4 * v + 1] = x.y - 2 * int(c2[16 * h + 4 * v + 1]);
+              dp[4 * v + 2] = x.z - 2 * int(c2[16 * h + 4 * v + 2]);
+              dp[4 * v + 3] = x.w - 2 * int(c2[16 * h + 4 * v + 3]);
             }
-            thr = key32.thr(min(rt.at(kp1), other)) - nr;
-            __syncwarp();
-            TCLK(3, t0);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) bits |= (dp[j] <= thr ? 1u : 0u) << j;
+            // window of this lane's reference (rows and columns)
+            const bool yok = valid && cy - ry >= a.lo && cy - ry <= a.hi;
+            const int jlo = max(0, rx + a.lo - cx0), jhi = min(15, min(rx + a.hi, W - b) - cx0);
+            const unsigned cols = (yok && jhi >= jlo) ? (((2u << jhi) - 1u) & ~((1u << jlo) - 1u)) : 0u;
+            bits &= cols;
+            if (a.dbg & 4) {
+              const int tot = __reduce_add_sync(0xffffffffu, __popc(bits));
+              if (lane == 0) { atomicAdd(&g_tc_stats[1], tot ? 1ull : 0ull); atomicAdd(&g_tc_stats[2], (unsigned long long)tot); }
+            }
+            TCLK(2, t0);
+            if (__any_sync(0xffffffffu, bits != 0)) {
+              // slow path: stage the 16 distances, then insert one survivor per lane per round
+              // into the 32-bit register list
+              uint32_t* sc = scratch + lane;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) sc[32 * j] = uint32_t(dp[j] + nr);
+              const int rel0 = (cy - ry - a.lo) * a.Wn + (cx0 - rx - a.lo);
+              while (__any_sync(0xffffffffu, bits != 0)) {
+                const int j = bits ? __ffs(bits) - 1 : 0;
+                const uint32_t x = bits ? key32.make(int(sc[32 * j]), rel0 + j) : 0xffffffffu;
+                bits &= bits - 1;
+                rt.insert(x);
+              }
+              thr = key32.thr(min(rt.at(kp1), other)) - nr;
+              __syncwarp();
+              TCLK(3, t0);
+            }
           }
         }
       }
@@ -387,11 +409,11 @@ TcLayout tc_layout(const Geometry& g) {
   off += 128 * 64;
   L.off_E = off;
   off += uint32_t(L.NTImax * kTR + 7) * L.NCmax * 128;
-  L.off_N = off;
-  off += uint32_t(L.NTImax * kTR) * L.NCmax * kTC * 4;
-  off = (off + 15) & ~15u;
+  L.off_N = off;  // 2-slot ring of the current tiles' candidate norms [2][8][16] int32
+  off += 2 * kTR * kTC * 4;
   L.off_heap = off;
-  off += uint32_t(2 * 128 * L.heap_pitch) * 8;  // two partial heaps per reference
+  off += uint32_t(128 * L.heap_pitch) * 4;  // half-1 32-bit lists for the final merge
+  off = (off + 15) & ~15u;
   L.off_q = off;
   off += kEpiWarps * 64 * (8 + 4);
   off += kEpiWarps * 32 * 16 * 4;  // per-warp slow-path scratch (16 ordered distances per lane)
@@ -416,7 +438,7 @@ cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
   a.idx_out = idx_out;
   a.dist_out = static_cast<int32_t*>(dist_out);
   a.H = g.H; a.W = g.W; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
-  a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mx;
+  a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.tiles_x = (g.nx + kRBX - 1) / kRBX;
   a.NCmax = L.NCmax; a.NTImax = L.NTImax;

@@ -135,7 +135,7 @@ __device__ __forceinline__ Acc sat_at(const Acc* __restrict__ buf, int SP, int y
 
 template <typename In>
 __global__ void norm_box(const typename NormTraits<In>::Acc* __restrict__ buf, int H, int W, int SP,
-                         int b, typename NormTraits<In>::Out* __restrict__ norm) {
+                         int b, int Mxp, typename NormTraits<In>::Out* __restrict__ norm) {
   using Acc = typename NormTraits<In>::Acc;
   using Out = typename NormTraits<In>::Out;
   const int My = H - b + 1, Mx = W - b + 1;
@@ -146,7 +146,7 @@ __global__ void norm_box(const typename NormTraits<In>::Acc* __restrict__ buf, i
   const Acc* S = buf + size_t(f) * H * SP;
   Acc v = sat_at(S, SP, y + b, x + b) - sat_at(S, SP, y, x + b) - sat_at(S, SP, y + b, x) +
           sat_at(S, SP, y, x);
-  norm[(size_t(f) * My + y) * Mx + x] = Out(v);
+  norm[(size_t(f) * My + y) * Mxp + x] = Out(v);
 }
 
 template <typename In>
@@ -163,7 +163,7 @@ cudaError_t launch_norm_t(const sc_bm_plan_s& p, const In* imgs, int F, cudaStre
   dim3 cg((g.W + 127) / 128, nb, F);
   sat_bands<Acc><<<cg, 128, 0, st>>>(buf, g.H, g.W, SP, nb, tot);
   sat_cols<Acc><<<cg, 128, 0, st>>>(buf, g.H, g.W, SP, nb, tot);
-  norm_box<In><<<dim3((g.Mx + 127) / 128, g.My, F), 128, 0, st>>>(buf, g.H, g.W, SP, g.b,
+  norm_box<In><<<dim3((g.Mx + 127) / 128, g.My, F), 128, 0, st>>>(buf, g.H, g.W, SP, g.b, g.Mxp,
                                                                   static_cast<Out*>(p.ws.norm));
   if (launches) *launches += 4;
   return cudaGetLastError();

@@ -32,7 +32,7 @@ int64_t span(int r, int lo, int hi, int maxpos) {
 size_t per_frame_ws(const Geometry& g, int nbands) {
   const size_t SP = size_t((g.W + 15) / 16 * 16);
   const size_t acc = g.dtype == SC_DTYPE_U8 ? 4 : 8;
-  return SP * g.H * acc + SP * nbands * acc + size_t(g.My) * g.Mx * 4;
+  return SP * g.H * acc + SP * nbands * acc + size_t(g.My) * g.Mxp * 4;
 }
 
 sc_status_t check_device(const sc_bm_plan_s* p) {
@@ -143,6 +143,7 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   g.hi = window - 1 - window / 2;
   g.My = H - b + 1;
   g.Mx = W - b + 1;
+  g.Mxp = (g.Mx + 3) & ~3;
   g.KP = dtype == SC_DTYPE_F32 ? K + kRescoreMargin : K;
 
   // candidate counts (separable: clipped rows x clipped cols)
@@ -176,7 +177,7 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   const size_t acc = dtype == SC_DTYPE_U8 ? 4 : 8;
   cudaError_t e = cudaMalloc(&p->ws.sat, SP * H * acc * p->F);
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.bandsum, SP * p->nbands * acc * p->F);
-  if (e == cudaSuccess) e = cudaMalloc(&p->ws.norm, size_t(g.My) * g.Mx * 4 * p->F);
+  if (e == cudaSuccess) e = cudaMalloc(&p->ws.norm, (size_t(g.My) * g.Mxp * p->F + 64) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_count, sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_list, size_t(g.ny) * g.nx * sizeof(int) * p->F);
   if (e == cudaSuccess) e = cudaMemset(p->ws.fix_count, 0, sizeof(int));
@@ -231,7 +232,8 @@ sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_s
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = launch_norm(*p, img, 1, st, &p->launches);
   if (e != cudaSuccess) return cuda_status(e);
-  e = cudaMemcpyAsync(norm_out, p->ws.norm, size_t(p->g.My) * p->g.Mx * 4, cudaMemcpyDeviceToDevice, st);
+  e = cudaMemcpy2DAsync(norm_out, size_t(p->g.Mx) * 4, p->ws.norm, size_t(p->g.Mxp) * 4, size_t(p->g.Mx) * 4,
+                        p->g.My, cudaMemcpyDeviceToDevice, st);
   return cuda_status(e);
 }
 

@@ -15,6 +15,7 @@ struct Geometry {
   int ny, nx;         // reference grid
   int lo, hi;         // window offsets
   int My, Mx;         // valid candidate positions (H-b+1, W-b+1)
+  int Mxp;            // norm-map row pitch (Mx rounded up to 4 ints: 16-byte aligned rows)
   int KP;             // keys kept per ref before output (K, or K+rescore margin for f32)
 };
 
