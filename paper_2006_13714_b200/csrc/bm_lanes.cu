@@ -156,21 +156,36 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
   const size_t plane_px = size_t(a.H) * a.W;
   const int PADT = a.PADT;  // zero rows above the region (blocks may start above the image)
   if constexpr (sizeof(In) == 1) {
+    // packed centred bytes, 4 words (16 B) per thread-iteration: one 16-byte global load when the
+    // row segment is 16-byte aligned and in range (c5: X0 = 128 tx - 16), else byte loads
     const uint8_t* img = static_cast<const uint8_t*>(a.imgs) + size_t(f) * a.C * plane_px;
-    const int total = a.C * a.PL;
+    const int WQ = (a.WP + 3) >> 2;  // 16-byte groups per row
+    const int total = a.C * a.RHp * WQ;
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int c = e / a.PL, r = e - c * a.PL;
-      const int yy = r / a.WP - PADT, w = r - (r / a.WP) * a.WP;
-      uint32_t word = 0;
+      const int c = e / (a.RHp * WQ), r = e - c * (a.RHp * WQ);
+      const int y2 = r / WQ, g4 = r - y2 * WQ;
+      const int yy = y2 - PADT;
+      uint32_t wv[4] = {0u, 0u, 0u, 0u};
       if (yy >= 0 && yy < RH) {
         const uint8_t* row = img + size_t(c) * plane_px + size_t(Y0 + yy) * a.W + X0;
+        const int xb = 16 * g4;
+        if (xb + 16 <= RW && (reinterpret_cast<uintptr_t>(row + xb) & 15) == 0) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + xb));
+          wv[0] = v.x ^ 0x80808080u; wv[1] = v.y ^ 0x80808080u; wv[2] = v.z ^ 0x80808080u; wv[3] = v.w ^ 0x80808080u;
+        } else {
 #pragma unroll
-        for (int e2 = 0; e2 < 4; ++e2) {
-          const int xx = 4 * w + e2;
-          word |= (xx < RW ? uint32_t(row[xx] ^ 0x80u) : 0u) << (8 * e2);
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              const int xx = xb + 4 * q + e2;
+              wv[q] |= (xx < RW ? uint32_t(row[xx] ^ 0x80u) : 0u) << (8 * e2);
+            }
         }
       }
-      tile[e] = word;
+      uint32_t* dst = tile + size_t(c) * a.PL + y2 * a.WP + 4 * g4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * g4 + q < a.WP) dst[q] = wv[q];
     }
   } else {
     const float* img = static_cast<const float*>(a.imgs) + size_t(f) * a.C * plane_px;
