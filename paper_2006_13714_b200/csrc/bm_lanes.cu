@@ -127,7 +127,7 @@ __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 
 // KR == 0: shared heaps + survivor queue (refq.cuh); KR in {16, 32}: per-lane 32-bit register
 // top-KR (regtopk.cuh, u8 only) with the exact fix-up for saturated / short references.
 template <typename In, int BK, int VY, bool ONE_CH, int KR>
-__global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
+__global__ void __launch_bounds__(256, KR > 0 ? 3 : 1) bm_lanes_kernel(LanesArgs a) {
   using P = LPath<In>;
   using T = typename P::T;
   extern __shared__ __align__(16) uint32_t smem_u32[];
@@ -201,9 +201,10 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
       }
     }
   }
-  {
+  const T* nsrc_g = static_cast<const T*>(a.norm) + size_t(f) * a.My * a.Mx;  // a.Mx = padded pitch
+  if (KR == 0) {
     // norm tile in NP phase planes: element (y, x) at plane x % NP, word x / NP
-    const T* nsrc = static_cast<const T*>(a.norm) + size_t(f) * a.My * a.Mx;
+    const T* nsrc = nsrc_g;
     const int per_plane = a.NHp * a.NQ;
     for (int e = threadIdx.x; e < a.NP * per_plane; e += blockDim.x) {
       const int ph = e / per_plane, r = e - ph * per_plane;
@@ -233,8 +234,8 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
   const int ry_l = ry - Y0 + PADT, rx_l = rx - X0;  // tile coordinates (rows include PADT)
   const int nplane = a.NHp * a.NQ, npm = a.NP - 1;
   auto nidx = [&](int yl, int xl) { return (xl & npm) * nplane + yl * a.NQ + (xl >> a.NPs); };
-  const T nr = ntile[nidx(ry_l, rx_l)];
   constexpr bool R32 = KR > 0;
+  const T nr = R32 ? __ldg(nsrc_g + size_t(ry) * a.Mx + rx) : ntile[nidx(ry_l, rx_l)];
   RegTopK32<(KR > 0 ? KR : 1)> rt;
   const Key32 key32{a.rb, a.dsat};
   int thr_dp = 0;  // R32: largest d' that may still pass (d' = d - ||X_i||^2)
@@ -289,14 +290,16 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
       // rows inside the (warp-uniform) vertical window, columns inside this lane's window
       const int i_lo = max(0, cy0 - cyb), i_hi = min(VY - 1, cy1 - cyb);
       const unsigned rows = (i_hi >= i_lo) ? (((2u << i_hi) - 1u) & ~((1u << i_lo) - 1u)) : 0u;
-      const T* nb = ntile + nidx(ny_l, cxl);
       if constexpr (R32) {
-        // fast path: d' <= thr_dp into a bitmask; survivors inserted into the register list
+        // fast path: d' <= thr_dp into a bitmask; survivors inserted into the register list.
+        // Candidate norms come straight from the L1/L2-resident norm map (no shared tile).
+        const T* nbg = nsrc_g + size_t(min(max(cyb, 0), a.H - b)) * a.Mx + (cxl + X0);
         int dpv[VY];
         unsigned bits = 0;
 #pragma unroll
         for (int i = 0; i < VY; ++i) {
-          dpv[i] = int(nb[i * a.NQ]) - 2 * int(acc[i]);
+          const int cyi = min(max(cyb + i, 0), a.H - b);
+          dpv[i] = int(__ldg(nsrc_g + size_t(cyi) * a.Mx + (cxl + X0))) - 2 * int(acc[i]);
           bits |= (dpv[i] <= thr_dp ? 1u : 0u) << i;
         }
         bits &= xok ? rows : 0u;
@@ -316,6 +319,7 @@ __global__ void __launch_bounds__(256) bm_lanes_kernel(LanesArgs a) {
         }
         continue;
       }
+      const T* nb = ntile + nidx(ny_l, cxl);
       // fast path: one compare per candidate into a per-lane bitmask of passing rows
       uint32_t u[VY];
       unsigned bits = 0;
@@ -456,6 +460,10 @@ int vy_for(const Geometry& g) {
   return 8;
 }
 
+}  // namespace
+int lanes_r32_slots(const Geometry& g);
+namespace {
+
 size_t lanes_smem(const Geometry& g, int NWY, int VY, LanesArgs* a) {
   const bool u8 = g.dtype == SC_DTYPE_U8;
   const int BK = bk_for(g.b, u8);
@@ -477,8 +485,8 @@ size_t lanes_smem(const Geometry& g, int NWY, int VY, LanesArgs* a) {
   const int NW = 31 * g.s + g.Wn;
   a->NQ = (NW + a->NP - 1) / a->NP + 1;
   a->NHp = (NWY - 1) * g.s + g.Wn + 2 * (VY - 1);
-  a->norm_words = (a->NP * a->NHp * a->NQ + 3) & ~3;
-  a->list_pitch = g.KP | 1;
+  a->norm_words = lanes_r32_slots(g) > 0 ? 0 : ((a->NP * a->NHp * a->NQ + 3) & ~3);
+  a->list_pitch = lanes_r32_slots(g) > 0 ? 0 : (g.KP | 1);  // the register top-K path needs no heaps
   size_t bytes = size_t(a->img_words + a->norm_words) * 4;
   bytes += size_t(NWY) * 32 * a->list_pitch * 8;  // reference lists
   bytes += size_t(NWY) * 32 * 16 * 4;           // survivor queues (64 x 12 B) / R32 scratch (32 x 16 x 4 B)
