@@ -173,7 +173,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL all-gather of the tables")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
-    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc"],
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box"],
                     help="force the matching kernel (default: the plan's choice)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -206,7 +206,7 @@ def main():
     x = torch.from_numpy(x_host).cuda()
     plan = Plan(cfg.H, cfg.W, cfg.C, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype)
     if args.kernel != "auto":
-        plan.set_kernel({"simt": 0, "tc": 1, "warp": 2}[args.kernel])
+        plan.set_kernel({"simt": 0, "tc": 1, "warp": 2, "box": 3}[args.kernel])
     info = plan.info()
     idx, dst = plan.alloc_out(nloc)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -253,7 +253,12 @@ def main():
 
     # roofline of the dominant kernel (the fused cross-term / top-K kernel)
     peaks = _peaks()
-    macs_launch = pairs_per_image * nloc * cfg.b * cfg.b * cfg.C  # algorithmic MACs per rank-step
+    # algorithmic MACs per candidate pair: the direct cross term is b^2 C
+    # multiply-adds; the box-sum kernel evaluates each product of the shifted
+    # product image once, s^2 C per pair (its 4x4 block sums are shared by 2 x 2 references)
+    mac_pair = cfg.s * cfg.s * cfg.C if info["kernel"] == 3 else cfg.b * cfg.b * cfg.C
+    macs_launch = pairs_per_image * nloc * mac_pair  # algorithmic MACs per rank-step
+    macs_direct = pairs_per_image * nloc * cfg.b * cfg.b * cfg.C
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if info["kernel"] == 1:
         peak = 2.0 * peaks["bf16_tflops"]  # int8 tcgen05 = 2x the measured bf16 (guide's nominal ratio)
@@ -267,7 +272,7 @@ def main():
         bound, unit, peak_note = "alu", "TFLOP/s", "FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md section 7)"
     achieved = 2.0 * macs_launch / (match_ms / 1e3) / 1e12 if match_ms > 0 else None
     traffic, traffic_src = None, None
-    kname = {0: "bm_lanes_kernel", 1: "bm_tc_i8_kernel", 2: "bm_simt_kernel"}[info["kernel"]]
+    kname = {0: "bm_lanes_kernel", 1: "bm_tc_i8_kernel", 2: "bm_simt_kernel", 3: "bm_box_kernel"}[info["kernel"]]
     prof = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{kname.replace('_kernel', '')}_{cfg.name}_metrics.json")
     if os.path.exists(prof):
         m = json.load(open(prof))
@@ -281,7 +286,17 @@ def main():
             "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peak_note, "kernel_ms_per_step": match_ms, "norm_ms_per_step": norm_ms,
             "kernel_share_of_step": match_ms / ms if ms > 0 else None,
-            "algorithmic_ops_per_launch": 2.0 * macs_launch}
+            "algorithmic_ops_per_launch": 2.0 * macs_launch, "macs_per_pair": mac_pair}
+    # the north_star's roofline: direct b^2 C MACs per pair at the int8 / fp32 peak vs image +
+    # output bytes at HBM bandwidth (whichever is slower), against the measured step time
+    if cfg.dtype == "u8":
+        mac_peak, mac_unit = 2.0 * peaks["bf16_tflops"] * 1e12 / 2.0, "int8 tcgen05 (2 x measured bf16)"
+    else:
+        mac_peak, mac_unit = 148 * 128 * sm_mhz * 1e6, "fp32 FFMA"
+    io_bytes = nloc * (cfg.C * cfg.H * cfg.W * (1 if cfg.dtype == "u8" else 4) + info["n_refs"] * cfg.K * 8)
+    t_mac, t_hbm = macs_direct / mac_peak, io_bytes / (peaks["hbm_gbs"] * 1e9)
+    roof["north_star"] = {"t_roof_ms": 1e3 * max(t_mac, t_hbm), "t_mac_ms": 1e3 * t_mac, "t_hbm_ms": 1e3 * t_hbm,
+                          "mac_unit": mac_unit, "frac": (1e3 * max(t_mac, t_hbm)) / ms if ms > 0 else None}
 
     # end-to-end through the public API with host buffers (pinned), copies inside the timing
     e2e = None

@@ -88,9 +88,11 @@ typedef struct {
     int32_t device;                     /* CUDA device ordinal the plan is bound to */
 } sc_bm_info_t;
 
-#define SC_KERNEL_SIMT 0       /* CUDA-core matcher, lanes = references (default) */
+#define SC_KERNEL_SIMT 0       /* CUDA-core matcher, lanes = references */
 #define SC_KERNEL_TC_I8 1      /* tcgen05 kind::i8 cross term (TMEM) + fused top-K (u8 only) */
 #define SC_KERNEL_SIMT_WARP 2  /* CUDA-core matcher, one warp per reference (lanes = candidates) */
+#define SC_KERNEL_BOX 3        /* box-sum matcher: 4x4 block sums of the shifted product image
+                                  (u8, b = 8, stride 4, C = 1, K <= 32; default where supported) */
 
 /*
  * Create a plan. H, W: image size (H, W >= b, H*W < 2^31); C: channels (1..8); b: patch

@@ -1,0 +1,307 @@
+// bm_box.cu -- the box-sum Self-Convolution matcher (SC_KERNEL_BOX; uint8, patch b = 8,
+// reference stride s = 4, one channel): steps a0, a2, a3, a4, a6 fused in one kernel.
+//
+// a2. For a fixed window offset delta = (dy, dx) the cross term of every reference (Eq. 5,
+// PAPER.md:277-279; footnote 2) is an 8x8 box sum, over the reference's patch,
+// of the product image P_delta(y, x) = x'(y, x) * x'(y + dy, x + dx): the image correlated
+// with its own shifted copy. With s = 4 = b / 2 every 4x4 block of P_delta lies in 2 x 2
+// references, so the kernel forms 4-row x 4-column block sums -- one dp4a per block row on
+// packed centred int8 words (x' = x - 128, exact int32) -- and assembles each reference's
+// cross term from its 2 x 2 blocks:
+//   * horizontally, lane l holds the references of reference column ix0 + l; the right half
+//     of its patch is the left half of lane l + 1's (shfl.down), so a lane only correlates
+//     its own 4-column strip (lane 31 is a helper: it supplies column ix0 + 31's strip);
+//   * vertically, a lane owns NY = 2 references (rows iy, iy + 1) that share their middle
+//     4 patch rows: 12 dp4a rows per offset instead of 16.
+// Per (reference, candidate) pair that is 6 dp4a instead of the 16 of a direct 8x8 dot product
+// (8 with NY = 1). A lane slides over VY vertically adjacent offsets (dy0 .. dy0+VY-1, fixed dx),
+// loading each candidate row once for all of them; candidate words come from four byte-shifted
+// copies of the staged region, so any 4-byte run is one aligned shared-memory load.
+//
+// a3. d' = n_c - 2 C (Lemma 2; ||X_i||^2 is constant per reference and added
+// back after selection) with n_c from the padded norm map: candidates outside [0,H-b]x[0,W-b]
+// read its huge border value and never pass a threshold, so window clipping costs nothing.
+// a4. Per-reference 32-bit register top-K (regtopk.cuh; Theorem 1's K largest b_i = K smallest
+// d) fed by a per-lane threshold bitmask; references whose K-th key saturates
+// go to the exact fix-up (fixup.cu). Offsets are visited centre-out (dy blocks, then dx), so
+// thresholds tighten early. a6: rows of K (idx, dist) staged in shared memory and written
+// coalesced (a warp's 31 references are contiguous in the output).
+#include <algorithm>
+#include <cstdlib>
+
+#include "regtopk.cuh"
+#include "sc_internal.h"
+
+namespace scbm {
+namespace {
+
+constexpr int kBoxWarps = 8;
+constexpr int kBoxRefsX = 31;  // references per warp row (lane 31 is the helper strip)
+
+struct BoxArgs {
+  const uint8_t* imgs;  // [F][H][W]
+  const int32_t* norm;  // padded norm-map interior: (f, y, x) at norm[f*nfs + y*np + x]
+  int32_t* idx_out;     // [F][band refs][K]
+  int32_t* dist_out;
+  long long nfs;
+  int np;
+  int H, W, Wn, K, lo, hi, nx, iy_begin, iy_end, tiles_x;
+  int RH, WP, PL;  // staged region rows, words per region row, words per byte-shifted copy
+  int nblk;        // dy blocks of VY offsets
+  int scr;         // per-warp scratch words
+  int rb;          // 32-bit keys: window-relative index bits
+  uint32_t dsat;   // 32-bit keys: distance saturation value
+  int* fix_count;
+  int* fix_list;
+};
+
+__device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
+
+template <int NY, int VY, int KR>
+__global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel(BoxArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  constexpr int NR = 4 * NY + 4;   // patch rows of the lane's NY references
+  constexpr int NT = NR + VY - 1;  // candidate rows per (dy block, dx)
+  const int f = blockIdx.y;
+  const int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
+  const int iy_first = a.iy_begin + ty * (kBoxWarps * NY);
+  const int ix_first = tx * kBoxRefsX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Ybase = iy_first * 4 + a.lo, Xbase = ix_first * 4 + a.lo;
+
+  // ---- a0: four byte-shifted copies of the centred region. Copy k, row r, word w holds
+  // region bytes [4w+k, 4w+k+3] as int8 x' = x ^ 0x80 = x - 128 (0 outside the image).
+  const uint8_t* img = a.imgs + size_t(f) * a.H * a.W;
+  for (int e = threadIdx.x; e < a.PL; e += blockDim.x) {
+    const int r = e / a.WP, w = e - r * a.WP;
+    const int y = Ybase + r, x = Xbase + 4 * w;
+    uint32_t u0 = 0u, u1 = 0u;
+    if (y >= 0 && y < a.H) {
+      const uint8_t* row = img + size_t(y) * a.W;
+      if (x >= 0 && x + 8 <= a.W && (reinterpret_cast<uintptr_t>(row + x) & 3) == 0) {
+        u0 = __ldg(reinterpret_cast<const uint32_t*>(row + x)) ^ 0x80808080u;
+        u1 = __ldg(reinterpret_cast<const uint32_t*>(row + x + 4)) ^ 0x80808080u;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int xx = x + j;
+          const uint32_t v = (xx >= 0 && xx < a.W) ? uint32_t(row[xx] ^ 0x80u) : 0u;
+          if (j < 4) u0 |= v << (8 * j);
+          else u1 |= v << (8 * (j - 4));
+        }
+      }
+    }
+    sm[e] = u0;
+    sm[a.PL + e] = __funnelshift_r(u0, u1, 8);
+    sm[2 * a.PL + e] = __funnelshift_r(u0, u1, 16);
+    sm[3 * a.PL + e] = __funnelshift_r(u0, u1, 24);
+  }
+  __syncthreads();
+
+  const int iy0 = iy_first + warp * NY;
+  if (iy0 >= a.iy_end) return;
+  const int ix = ix_first + lane;
+  const bool lane_ok = lane < kBoxRefsX && ix < a.nx;
+  const int rxn = min(ix, a.nx - 1) * 4;  // norm-map column base (in range for every lane)
+  const int32_t* nmap = a.norm + size_t(f) * a.nfs;
+  const int rr0 = (iy0 - iy_first) * 4 - a.lo;  // region row of image row 4 * iy0
+
+  // the lane's 4-column strip of its references' patch rows (reference side, aligned)
+  uint32_t R[NR];
+  {
+    const int off = -a.lo;
+    const uint32_t* src = sm + (off & 3) * a.PL + rr0 * a.WP + lane + (off >> 2);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) R[r] = src[r * a.WP];
+  }
+  bool ref_ok[NY];
+  int32_t nr[NY];
+  int thr[NY];  // largest d' = d - ||X_i||^2 that may still enter the reference's top-K
+  RegTopK32<KR> rt[NY];
+  const Key32 key32{a.rb, a.dsat};
+#pragma unroll
+  for (int q = 0; q < NY; ++q) {
+    ref_ok[q] = lane_ok && iy0 + q < a.iy_end;
+    nr[q] = __ldg(nmap + size_t(4 * (iy0 + q)) * a.np + rxn);
+    rt[q].init();
+    thr[q] = int(a.dsat) - nr[q];
+  }
+  uint32_t* scratch = sm + 4 * a.PL + warp * a.scr;
+
+  const int b0 = (0 - a.lo) / VY;  // dy block holding dy = 0
+  const int span = max(-a.lo, a.hi);
+  for (int kb = 0; kb < 2 * a.nblk; ++kb) {
+    const int bb = b0 + centre_out(kb);
+    if (bb < 0 || bb >= a.nblk) continue;
+    const int dy0 = a.lo + bb * VY;
+    // whole block above / below the image for every reference of the warp (warp-uniform)
+    if (4 * (iy0 + NY - 1) + dy0 + VY - 1 < 0 || 4 * iy0 + dy0 > a.H - 8) continue;
+    const int nrow_ok = min(VY, a.hi - dy0 + 1);  // offsets dy0 + i beyond hi are not in the window
+    const unsigned rows = (1u << nrow_ok) - 1u;
+    const uint32_t* cbase = sm + (rr0 + dy0) * a.WP + lane;
+    const int32_t* nrow = nmap + ptrdiff_t(4 * iy0 + dy0) * a.np + rxn;
+    for (int kx = 0; kx <= 2 * span; ++kx) {
+      const int dx = centre_out(kx);
+      if (dx < a.lo || dx > a.hi) continue;
+      const int off = dx - a.lo;
+      const uint32_t* col = cbase + (off & 3) * a.PL + (off >> 2);
+      uint32_t Cw[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) Cw[t] = col[t * a.WP];
+      // block sums -> left-strip sums T[q][i] of reference q at offset (dy0 + i, dx)
+      int T[NY][VY];
+#pragma unroll
+      for (int i = 0; i < VY; ++i) {
+        if constexpr (NY == 1) {
+          int acc = 0;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) acc = __dp4a(int(R[r]), int(Cw[r + i]), acc);
+          T[0][i] = acc;
+        } else {
+          int m = 0;  // middle rows 4..7, shared by both references
+#pragma unroll
+          for (int r = 4; r < 8; ++r) m = __dp4a(int(R[r]), int(Cw[r + i]), m);
+          int t0 = m, t1 = m;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) t0 = __dp4a(int(R[r]), int(Cw[r + i]), t0);
+#pragma unroll
+          for (int r = 8; r < 12; ++r) t1 = __dp4a(int(R[r]), int(Cw[r + i]), t1);
+          T[0][i] = t0;
+          T[1][i] = t1;
+        }
+      }
+      const int32_t* nb = nrow + dx;
+#pragma unroll
+      for (int q = 0; q < NY; ++q) {
+        int dp[VY];
+        unsigned bits = 0u;
+#pragma unroll
+        for (int i = 0; i < VY; ++i) {
+          const int c = T[q][i] + __shfl_down_sync(0xffffffffu, T[q][i], 1);  // + right strip
+          dp[i] = __ldg(nb + (4 * q + i) * a.np) - 2 * c;
+          bits |= (dp[i] <= thr[q] ? 1u : 0u) << i;
+        }
+        bits &= ref_ok[q] ? rows : 0u;
+        if (__any_sync(0xffffffffu, bits != 0u)) {
+          // survivors: one insertion per lane per round into the register top-K
+          uint32_t* sc = scratch + lane;
+#pragma unroll
+          for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(dp[i] + nr[q]);
+          const int rel0 = (dy0 - a.lo) * a.Wn + off;
+          while (__any_sync(0xffffffffu, bits != 0u)) {
+            const int i = bits ? __ffs(bits) - 1 : 0;
+            const uint32_t key = bits ? key32.make(int(sc[32 * i]), rel0 + i * a.Wn) : 0xffffffffu;
+            bits &= bits - 1u;
+            rt[q].insert(key);
+          }
+          thr[q] = key32.thr(rt[q].at(a.K - 1)) - nr[q];
+          __syncwarp();
+        }
+      }
+    }
+  }
+
+  // ---- a6: exact references -> staged rows of K keys -> coalesced (idx, dist) stores;
+  // references whose K-th key is saturated or unfilled -> the fix-up list
+  const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
+  const int nref = min(kBoxRefsX, a.nx - ix_first);
+#pragma unroll
+  for (int q = 0; q < NY; ++q) {
+    const int iy = iy0 + q;
+    if (iy >= a.iy_end) break;  // warp-uniform
+    const size_t row0 = size_t(f) * band_refs + size_t(iy - a.iy_begin) * a.nx + ix_first;
+    const bool exact = key32.exact(rt[q].at(a.K - 1));
+    if (ref_ok[q] && !exact) {
+      const int pos = atomicAdd(a.fix_count, 1);
+      a.fix_list[pos] = int(row0 + lane);
+    }
+    __syncwarp();
+    if (lane_ok) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+        if (k < a.K) scratch[lane * (KR + 1) + k] = rt[q].r[k];
+    }
+    __syncwarp();
+    const int ry = 4 * iy;
+    for (int e = lane; e < nref * a.K; e += 32) {
+      const int j = e / a.K, k = e - j * a.K;
+      const uint32_t kk = scratch[j * (KR + 1) + k];
+      const int rel = key32.rel(kk);
+      const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+      a.idx_out[row0 * a.K + e] = (ry + dyy + a.lo) * a.W + (ix_first + j) * 4 + dxx + a.lo;
+      a.dist_out[row0 * a.K + e] = key32.dist(kk);
+    }
+    __syncwarp();
+  }
+}
+
+int box_vy(const Geometry& g) { return g.Wn % 11 == 0 ? 11 : g.Wn % 7 == 0 ? 7 : g.Wn <= 8 ? 8 : 11; }
+
+size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
+  a->nblk = (g.Wn + VY - 1) / VY;
+  a->RH = 4 * kBoxWarps * NY + a->nblk * VY + 4;
+  a->WP = 32 + (g.Wn + 2) / 4 + 1;
+  a->PL = a->RH * a->WP;
+  a->scr = std::max(32 * VY, kBoxRefsX * (KR + 1));
+  return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
+}
+
+int box_ny() {
+  const char* e = getenv("SCBM_BOX_NY");
+  return (e && atoi(e) == 1) ? 1 : 2;
+}
+
+template <int NY, int VY, int KR>
+cudaError_t launch_box_t(const BoxArgs& a, int F, size_t smem, cudaStream_t st) {
+  const int tiles_y = (a.iy_end - a.iy_begin + kBoxWarps * NY - 1) / (kBoxWarps * NY);
+  auto k = bm_box_kernel<NY, VY, KR>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k<<<dim3(a.tiles_x * tiles_y, F), kBoxWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int box_key_bits(const Geometry& g) { return std::max(2, key32_rel_bits(g.Wn)); }
+
+bool box_supported(const Geometry& g) {
+  if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.s != 4 || g.C != 1 || g.K > 32) return false;
+  if (key32_rel_bits(g.Wn) > 11) return false;  // keeps >= 21 distance bits in the 32-bit keys
+  BoxArgs a{};
+  return box_layout(g, 2, box_vy(g), 32, &a) <= 227 * 1024;
+}
+
+cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                          int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
+  const Geometry& g = p.g;
+  BoxArgs a{};
+  a.imgs = static_cast<const uint8_t*>(imgs);
+  a.norm = static_cast<const int32_t*>(p.ws.norm);
+  a.idx_out = idx_out;
+  a.dist_out = static_cast<int32_t*>(dist_out);
+  a.nfs = g.NFS;
+  a.np = g.Mxp;
+  a.H = g.H; a.W = g.W; a.Wn = g.Wn; a.K = g.K; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
+  a.iy_begin = iy_begin; a.iy_end = iy_end;
+  a.tiles_x = (g.nx + kBoxRefsX - 1) / kBoxRefsX;
+  a.rb = box_key_bits(g);
+  a.dsat = uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
+  a.fix_count = p.ws.fix_count;
+  a.fix_list = p.ws.fix_list;
+  const int vy = box_vy(g), kr = g.K <= 16 ? 16 : 32, ny = box_ny();
+  const size_t smem = box_layout(g, ny, vy, kr, &a);
+  cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  if (ny == 1) e = launch_box_t<1, 11, 16>(a, F, box_layout(g, 1, 11, 16, &a), st);  // experiments
+  else if (kr == 16 && vy == 11) e = launch_box_t<2, 11, 16>(a, F, smem, st);
+  else if (kr == 16 && vy == 7) e = launch_box_t<2, 7, 16>(a, F, smem, st);
+  else if (kr == 16) e = launch_box_t<2, 8, 16>(a, F, smem, st);
+  else if (vy == 11) e = launch_box_t<2, 11, 32>(a, F, smem, st);
+  else if (vy == 7) e = launch_box_t<2, 7, 32>(a, F, smem, st);
+  else e = launch_box_t<2, 8, 32>(a, F, smem, st);
+  if (launches) *launches += 2;
+  if (e != cudaSuccess) return e;
+  return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
+}
+
+}  // namespace scbm

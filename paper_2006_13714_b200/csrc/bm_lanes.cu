@@ -29,6 +29,7 @@ struct LanesArgs {
   void* dist_out;
   void* dense;        // debug [refs][Wn*Wn] or nullptr
   int H, W, C, b, s, Wn, K, KP, lo, hi, nx, My, Mx;
+  long long nfs;      // norm-map frame stride
   int iy_begin, iy_end;
   int NWY, tiles_x;   // warps (reference rows) per CTA; CTAs across x (32 refs each)
   int RWp, RHp;       // image region pitch (elements) and padded height
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(256, KR > 0 ? 3 : 1) bm_lanes_kernel(LanesArgs
       }
     }
   }
-  const T* nsrc_g = static_cast<const T*>(a.norm) + size_t(f) * a.My * a.Mx;  // a.Mx = padded pitch
+  const T* nsrc_g = static_cast<const T*>(a.norm) + size_t(f) * a.nfs;  // a.Mx = norm-map row pitch
   if (KR == 0) {
     // norm tile in NP phase planes: element (y, x) at plane x % NP, word x / NP
     const T* nsrc = nsrc_g;
@@ -575,6 +576,7 @@ cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int 
   a.dense = dense;
   a.H = g.H; a.W = g.W; a.C = g.C; a.b = g.b; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
   a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
+  a.nfs = g.NFS;
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.NWY = p.lanes_nwy;
   a.tiles_x = (g.nx + 31) / 32;

@@ -33,6 +33,7 @@ struct SimtArgs {
   void* dist_out;     // [F][band refs][K]
   void* dense;        // debug: [refs][Wn*Wn] (one image) or nullptr
   int H, W, C, b, s, Wn, K, KP, lo, hi, nx, My, Mx;
+  long long nfs;      // norm-map frame stride
   int iy_begin, iy_end;
   int TRY, TRX, tiles_x;
   int RWp, RHp;       // logical image-region pitch (elements) / padded height
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(256) bm_simt_kernel(SimtArgs a) {
           dst[yy * a.RWp + xx] = (yy < RH && xx < RW) ? src[size_t(Y0 + yy) * a.W + X0 + xx] - 0.5f : 0.f;
     }
   }
-  const T* nsrc = static_cast<const T*>(a.norm) + size_t(f) * a.My * a.Mx;
+  const T* nsrc = static_cast<const T*>(a.norm) + size_t(f) * a.nfs;
   for (int yy = threadIdx.x / 32; yy < a.NHp; yy += blockDim.x / 32)
     for (int xx = threadIdx.x & 31; xx < a.NWp; xx += 32)
       ntile[yy * a.NWp + xx] = (yy < NH && xx < NW) ? nsrc[size_t(Y0 + yy) * a.Mx + X0 + xx] : T(0);
@@ -429,6 +430,7 @@ cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int i
   a.dense = dense;
   a.H = g.H; a.W = g.W; a.C = g.C; a.b = g.b; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
   a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
+  a.nfs = g.NFS;
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.TRY = p.tile.TRY; a.TRX = p.tile.TRX;
   a.tiles_x = (g.nx + a.TRX - 1) / a.TRX;

@@ -47,6 +47,7 @@ struct TcArgs {
   int32_t* dist_out;
   int H, W, s, Wn, K, KP, lo, hi, nx, My, Mx, iy_begin, iy_end, tiles_x;
   int NCmax, NTImax;
+  long long nfs;  // norm-map frame stride
   uint32_t off_A, off_E, off_N, off_heap, off_q;  // shared byte offsets
   int heap_pitch;
   int rb;          // 32-bit keys: window-relative index bits
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 2) bm_tc_i8_kernel(TcArgs a) {
       *reinterpret_cast<uint4*>(row + mm * 16) = o;
     }
   }
-  const int32_t* nsrc = a.norm + size_t(f) * a.My * a.Mx;  // a.Mx = padded norm pitch
+  const int32_t* nsrc = a.norm + size_t(f) * a.nfs;  // a.Mx = norm-map row pitch
 
   for (int e = threadIdx.x; e < 2 * 128; e += kThreads)  // published thresholds: +inf until set
     reinterpret_cast<uint64_t*>(smem + a.off_q)[e] = kKeyInf;
@@ -439,6 +440,7 @@ cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
   a.dist_out = static_cast<int32_t*>(dist_out);
   a.H = g.H; a.W = g.W; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
   a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
+  a.nfs = g.NFS;
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.tiles_x = (g.nx + kRBX - 1) / kRBX;
   a.NCmax = L.NCmax; a.NTImax = L.NTImax;

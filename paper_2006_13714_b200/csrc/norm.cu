@@ -10,7 +10,16 @@
 //      wraps.
 // f32: fp64 SAT (an fp32 SAT loses 1e-3 relative distance accuracy at full size).
 //
-// Kernels (per chunk of F frames, all coalesced):
+// u8 frames use ONE kernel instead (norm_direct_u8): the same box sums formed directly by a
+// separable box filter (vertical b-sums, then horizontal b-sums) of x'^2 staged in shared
+// memory -- exact int32, bit-identical to the integral-image values, and 1 pass over the
+// image instead of 4 passes over a 4-byte/pixel SAT (c5: 2.05 -> ~0.15 ms per 64 frames).
+//
+// The map is written into the interior of a padded buffer (NPAD rows / columns of a huge
+// value on every side, set once at plan creation) so that the box-sum matcher can read
+// norms of out-of-image candidates without clamping: they never pass a threshold.
+//
+// f32 kernels (per chunk of F frames, all coalesced):
 //   sat_rows     one warp per image row; 16-byte vector loads, register prefix per lane,
 //                warp shuffle scan across lanes, vector stores.
 //   sat_bands    column totals of 32-row bands (thread per column).
@@ -135,7 +144,7 @@ __device__ __forceinline__ Acc sat_at(const Acc* __restrict__ buf, int SP, int y
 
 template <typename In>
 __global__ void norm_box(const typename NormTraits<In>::Acc* __restrict__ buf, int H, int W, int SP,
-                         int b, int Mxp, typename NormTraits<In>::Out* __restrict__ norm) {
+                         int b, int Mxp, long long nfs, typename NormTraits<In>::Out* __restrict__ norm) {
   using Acc = typename NormTraits<In>::Acc;
   using Out = typename NormTraits<In>::Out;
   const int My = H - b + 1, Mx = W - b + 1;
@@ -146,7 +155,47 @@ __global__ void norm_box(const typename NormTraits<In>::Acc* __restrict__ buf, i
   const Acc* S = buf + size_t(f) * H * SP;
   Acc v = sat_at(S, SP, y + b, x + b) - sat_at(S, SP, y, x + b) - sat_at(S, SP, y + b, x) +
           sat_at(S, SP, y, x);
-  norm[(size_t(f) * My + y) * Mxp + x] = Out(v);
+  norm[size_t(f) * nfs + size_t(y) * Mxp + x] = Out(v);
+}
+
+// u8: direct separable box sums of x'^2 (exact int32; identical to the integral-image values).
+// One CTA per 32-row x 128-column output tile: the squared centred tile (+ b-1 halo) summed
+// over channels goes to shared memory, then vertical b-sums, then horizontal b-sums.
+constexpr int kNdRows = 32, kNdCols = 128;
+__global__ void __launch_bounds__(256) norm_direct_u8(const uint8_t* __restrict__ imgs, int C, int H, int W,
+                                                      int b, int Mxp, long long nfs, int32_t* __restrict__ norm) {
+  __shared__ int sq[kNdRows + 15][kNdCols + 16];
+  __shared__ int vs[kNdRows][kNdCols + 16];
+  const int My = H - b + 1, Mx = W - b + 1;
+  const int y0 = blockIdx.y * kNdRows, x0 = blockIdx.x * kNdCols, f = blockIdx.z;
+  const int rows = min(kNdRows, My - y0) + b - 1, cols = min(kNdCols, Mx - x0) + b - 1;
+  const size_t plane = size_t(H) * W;
+  const uint8_t* img = imgs + size_t(f) * C * plane;
+  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    const int r = e / cols, c = e - r * cols;
+    int v = 0;
+    for (int ch = 0; ch < C; ++ch) {
+      const int t = int(img[ch * plane + size_t(y0 + r) * W + x0 + c]) - 128;
+      v += t * t;
+    }
+    sq[r][c] = v;
+  }
+  __syncthreads();
+  const int orows = rows - b + 1;
+  for (int e = threadIdx.x; e < orows * cols; e += blockDim.x) {
+    const int r = e / cols, c = e - r * cols;
+    int v = 0;
+    for (int l = 0; l < b; ++l) v += sq[r + l][c];
+    vs[r][c] = v;
+  }
+  __syncthreads();
+  const int ocols = cols - b + 1;
+  for (int e = threadIdx.x; e < orows * ocols; e += blockDim.x) {
+    const int r = e / ocols, c = e - r * ocols;
+    int v = 0;
+    for (int m = 0; m < b; ++m) v += vs[r][c + m];
+    norm[size_t(f) * nfs + size_t(y0 + r) * Mxp + x0 + c] = v;
+  }
 }
 
 template <typename In>
@@ -155,6 +204,12 @@ cudaError_t launch_norm_t(const sc_bm_plan_s& p, const In* imgs, int F, cudaStre
   using Acc = typename NormTraits<In>::Acc;
   using Out = typename NormTraits<In>::Out;
   const Geometry& g = p.g;
+  if constexpr (sizeof(In) == 1) {
+    norm_direct_u8<<<dim3((g.Mx + kNdCols - 1) / kNdCols, (g.My + kNdRows - 1) / kNdRows, F), 256, 0, st>>>(
+        imgs, g.C, g.H, g.W, g.b, g.Mxp, g.NFS, static_cast<int32_t*>(p.ws.norm));
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   const int SP = (g.W + 15) / 16 * 16;
   Acc* buf = static_cast<Acc*>(p.ws.sat);
   Acc* tot = static_cast<Acc*>(p.ws.bandsum);
@@ -163,7 +218,7 @@ cudaError_t launch_norm_t(const sc_bm_plan_s& p, const In* imgs, int F, cudaStre
   dim3 cg((g.W + 127) / 128, nb, F);
   sat_bands<Acc><<<cg, 128, 0, st>>>(buf, g.H, g.W, SP, nb, tot);
   sat_cols<Acc><<<cg, 128, 0, st>>>(buf, g.H, g.W, SP, nb, tot);
-  norm_box<In><<<dim3((g.Mx + 127) / 128, g.My, F), 128, 0, st>>>(buf, g.H, g.W, SP, g.b, g.Mxp,
+  norm_box<In><<<dim3((g.Mx + 127) / 128, g.My, F), 128, 0, st>>>(buf, g.H, g.W, SP, g.b, g.Mxp, g.NFS,
                                                                   static_cast<Out*>(p.ws.norm));
   if (launches) *launches += 4;
   return cudaGetLastError();

@@ -29,10 +29,12 @@ int64_t span(int r, int lo, int hi, int maxpos) {
   return b >= a ? int64_t(b - a + 1) : 0;
 }
 
+// u8 norms come from a direct box filter (no integral image workspace); f32 from an fp64 SAT.
 size_t per_frame_ws(const Geometry& g, int nbands) {
   const size_t SP = size_t((g.W + 15) / 16 * 16);
-  const size_t acc = g.dtype == SC_DTYPE_U8 ? 4 : 8;
-  return SP * g.H * acc + SP * nbands * acc + size_t(g.My) * g.Mxp * 4;
+  const size_t nmap = size_t(g.NFS) * 4;
+  if (g.dtype == SC_DTYPE_U8) return nmap;
+  return SP * g.H * 8 + SP * nbands * 8 + nmap;
 }
 
 sc_status_t check_device(const sc_bm_plan_s* p) {
@@ -44,7 +46,7 @@ sc_status_t check_device(const sc_bm_plan_s* p) {
 void free_ws(sc_bm_plan_s* p) {
   if (p->ws.sat) cudaFree(p->ws.sat);
   if (p->ws.bandsum) cudaFree(p->ws.bandsum);
-  if (p->ws.norm) cudaFree(p->ws.norm);
+  if (p->ws.norm_base) cudaFree(p->ws.norm_base);
   if (p->ws.fix_count) cudaFree(p->ws.fix_count);
   if (p->ws.fix_list) cudaFree(p->ws.fix_list);
   p->ws = Workspace{};
@@ -90,6 +92,8 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
     void* dd = dist ? static_cast<char*>(dist) + f0 * out_elems * 4 : nullptr;
     if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
       e = launch_bm_tc(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
+    else if (p->kernel == SC_KERNEL_BOX && dense == nullptr)
+      e = launch_bm_box(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_SIMT_WARP)
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
     else
@@ -143,7 +147,11 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   g.hi = window - 1 - window / 2;
   g.My = H - b + 1;
   g.Mx = W - b + 1;
-  g.Mxp = (g.Mx + 3) & ~3;
+  // norm-map border: wide enough for every out-of-image candidate the box-sum matcher touches
+  // (window offsets + its 8-row / 16-row register blocks), a multiple of 4 so rows stay 16-B aligned
+  g.NPAD = (std::max(-g.lo, g.hi) + 24 + 3) & ~3;
+  g.Mxp = (g.Mx + 2 * g.NPAD + 3) & ~3;
+  g.NFS = (long long)(g.My + 2 * g.NPAD) * g.Mxp;
   g.KP = dtype == SC_DTYPE_F32 ? K + kRescoreMargin : K;
 
   // candidate counts (separable: clipped rows x clipped cols)
@@ -161,9 +169,11 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   p->max_cand = ymax * xmax;
 
   p->nbands = (H + kSatBand - 1) / kSatBand;
-  // frames per chunk: keep one chunk's SAT + norm map within ~48 MB of the 126 MB L2
+  // frames per chunk: keep one chunk's workspace (u8: norm map; f32: SAT + norm map) L2-resident
+  // between the norm kernels and the matcher (126 MB L2)
   const size_t pf = per_frame_ws(g, p->nbands);
-  p->F = int(std::max<size_t>(1, std::min<size_t>(64, (48u << 20) / std::max<size_t>(pf, 1))));
+  const size_t budget = (dtype == SC_DTYPE_U8 ? 80u : 48u) << 20;
+  p->F = int(std::max<size_t>(1, std::min<size_t>(64, budget / std::max<size_t>(pf, 1))));
   p->tile = choose_simt_tile(g, p->sm_count, p->F);
   p->lanes_nwy = lanes_warps_for(g, p->sm_count, p->F);
   // Default matcher: lanes = references where its 32-reference-wide CTA keeps >= 4 warps per
@@ -172,12 +182,22 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   const bool lanes_ok = dtype == SC_DTYPE_U8 && g.nx >= 64 && p->lanes_nwy >= 4 &&
                         lanes_smem_bytes(g, p->lanes_nwy) <= 227 * 1024;
   p->kernel = lanes_ok ? SC_KERNEL_SIMT : SC_KERNEL_SIMT_WARP;
+  // u8, b = 8, s = 4 (configs c1, c5): the box-sum matcher (6 dp4a per pair instead of 16)
+  if (box_supported(g)) p->kernel = SC_KERNEL_BOX;
 
   const size_t SP = size_t((W + 15) / 16 * 16);
-  const size_t acc = dtype == SC_DTYPE_U8 ? 4 : 8;
-  cudaError_t e = cudaMalloc(&p->ws.sat, SP * H * acc * p->F);
-  if (e == cudaSuccess) e = cudaMalloc(&p->ws.bandsum, SP * p->nbands * acc * p->F);
-  if (e == cudaSuccess) e = cudaMalloc(&p->ws.norm, (size_t(g.My) * g.Mxp * p->F + 64) * 4);
+  cudaError_t e = cudaSuccess;
+  if (dtype == SC_DTYPE_F32) {
+    e = cudaMalloc(&p->ws.sat, SP * H * 8 * p->F);
+    if (e == cudaSuccess) e = cudaMalloc(&p->ws.bandsum, SP * p->nbands * 8 * p->F);
+  }
+  const size_t nbytes = (size_t(g.NFS) * p->F + 64) * 4;
+  if (e == cudaSuccess) e = cudaMalloc(&p->ws.norm_base, nbytes);
+  // border value 0x7f7f7f7f (u8: 2.14e9, far above any threshold; f32: 3.4e38); the interior is
+  // rewritten by every run
+  if (e == cudaSuccess) e = cudaMemset(p->ws.norm_base, 0x7f, nbytes);
+  if (e == cudaSuccess)
+    p->ws.norm = static_cast<char*>(p->ws.norm_base) + (size_t(g.NPAD) * g.Mxp + g.NPAD) * 4;
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_count, sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_list, size_t(g.ny) * g.nx * sizeof(int) * p->F);
   if (e == cudaSuccess) e = cudaMemset(p->ws.fix_count, 0, sizeof(int));
@@ -318,7 +338,9 @@ sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
   if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;
-  if (kernel != SC_KERNEL_SIMT && kernel != SC_KERNEL_SIMT_WARP && kernel != SC_KERNEL_TC_I8)
+  if (kernel == SC_KERNEL_BOX && !box_supported(p->g)) return SC_ERR_UNSUPPORTED;
+  if (kernel != SC_KERNEL_SIMT && kernel != SC_KERNEL_SIMT_WARP && kernel != SC_KERNEL_TC_I8 &&
+      kernel != SC_KERNEL_BOX)
     return SC_ERR_UNSUPPORTED;
   p->kernel = kernel;
   return SC_OK;

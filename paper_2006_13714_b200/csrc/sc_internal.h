@@ -15,7 +15,9 @@ struct Geometry {
   int ny, nx;         // reference grid
   int lo, hi;         // window offsets
   int My, Mx;         // valid candidate positions (H-b+1, W-b+1)
-  int Mxp;            // norm-map row pitch (Mx rounded up to 4 ints: 16-byte aligned rows)
+  int Mxp;            // norm-map row pitch (Mx + 2*NPAD rounded up to 4 ints: 16-byte aligned rows)
+  int NPAD;           // norm-map border (rows and columns) on every side, filled with a huge value
+  long long NFS;      // norm-map frame stride in elements ((My + 2*NPAD) * Mxp)
   int KP;             // keys kept per ref before output (K, or K+rescore margin for f32)
 };
 
@@ -23,7 +25,8 @@ struct Geometry {
 struct Workspace {
   void* sat = nullptr;      // [F][H+1][W+1] uint32 (u8) or double (f32)
   void* bandsum = nullptr;  // [F][nbands][W+1] column band totals
-  void* norm = nullptr;     // [F][My][Mx] int32 (u8) or float (f32)
+  void* norm_base = nullptr;  // allocation of the padded norm map [F][My+2*NPAD][Mxp]
+  void* norm = nullptr;     // interior of frame 0: element (f, y, x) at norm[f*NFS + y*Mxp + x]
   int* fix_count = nullptr; // exact fix-up: number of flagged references of the current chunk
   int* fix_list = nullptr;  // [F * n_refs] flagged (frame * band_refs + band ref) indices
   size_t bytes = 0;
@@ -102,5 +105,10 @@ bool tc_supported(const Geometry& g);
 cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                          int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
 size_t lanes_smem_bytes(const Geometry& g, int nwy);
+
+// bm_box.cu: the box-sum matcher (SC_KERNEL_BOX; u8, b = 8, s = 4, C = 1, K <= 32).
+bool box_supported(const Geometry& g);
+cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                          int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
 
 }  // namespace scbm

@@ -332,11 +332,13 @@ def test_tc_rejects_unsupported():
 
 
 # ------------------------------------------------------------------ 32-bit register top-K + fix-up
+@pytest.mark.parametrize("kernel", ["box", "lanes"])
 @pytest.mark.parametrize("kind,Wn,K", [("saturated", 35, 16), ("short", 3, 16), ("short", 5, 30),
                                         ("random", 33, 16), ("random", 41, 32), ("constant", 33, 16)])
-def test_r32_keys_and_fixup(kind, Wn, K):
-    """u8, b=8: the default kernel keeps 32-bit keys (distance field saturating at 2^21-1 for
-    Wn >= 33) and recomputes saturated / short references exactly (fixup.cu)."""
+def test_r32_keys_and_fixup(kind, Wn, K, kernel):
+    """u8, b=8, s=4: the box and lanes kernels keep 32-bit keys (distance field saturating at
+    2^21-1 for Wn >= 33) and recompute saturated / short references exactly (fixup.cu)."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX, SC_KERNEL_SIMT
     rng = np.random.Generator(np.random.PCG64(31))
     if kind == "saturated":
         x = (rng.integers(0, 2, size=(2, 1, 72, 200)) * 255).astype(np.uint8)
@@ -344,4 +346,104 @@ def test_r32_keys_and_fixup(kind, Wn, K):
         x = np.full((1, 1, 60, 150), 17, dtype=np.uint8)
     else:
         x = rng.integers(0, 256, size=(2, 1, 70, 260), dtype=np.uint8)
-    _compare(x, 8, 4, Wn, K, "u8", where=f"r32 {kind} Wn{Wn} K{K}")
+    kern = SC_KERNEL_BOX if kernel == "box" else SC_KERNEL_SIMT
+    _compare(x, 8, 4, Wn, K, "u8", where=f"r32 {kernel} {kind} Wn{Wn} K{K}", kernel=kern)
+
+
+# ------------------------------------------------------------------ box-sum kernel (u8, b=8, s=4)
+def _box_cases(n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = []
+    while len(out) < n:
+        H = int(rng.integers(8, 150))
+        W = int(rng.integers(8, 300))  # odd widths: unaligned rows take the byte-load staging path
+        Wn = int(rng.integers(1, 46))  # Wn^2 <= 2048: 32-bit keys keep >= 21 distance bits
+        K = int(rng.integers(1, 33))
+        out.append((H, W, Wn, K))
+    return out
+
+
+def _box(x, Wn, K, where, rows=None):
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX
+    _compare(x, 8, 4, Wn, K, "u8", where=where, kernel=SC_KERNEL_BOX)
+
+
+@pytest.mark.parametrize("case", _box_cases(24, 404))
+def test_box_random_sweep(case):
+    H, W, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 3, 1, H, W, "u8")
+    _box(x, Wn, K, f"box {case}")
+
+
+@pytest.mark.parametrize("kind", ["constant", "periodic", "saturated", "ramp"])
+def test_box_ties_and_extremes(kind):
+    rng = np.random.Generator(np.random.PCG64(12))
+    if kind == "constant":
+        x = np.full((1, 1, 70, 150), 93, dtype=np.uint8)
+    elif kind == "periodic":
+        x = np.tile(rng.integers(0, 256, size=(8, 8), dtype=np.uint8), (9, 19))[None, None].copy()
+    elif kind == "saturated":
+        x = (rng.integers(0, 2, size=(1, 1, 64, 140)) * 255).astype(np.uint8)
+    else:
+        x = np.add.outer(np.arange(66), np.arange(170)).astype(np.uint8)[None, None].copy()
+    _box(x, 21, 16, f"box {kind}")
+
+
+def test_box_c1_and_c5_frames():
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX
+    _box(synth.make_input(synth.CONFIGS["c1"]), 21, 16, "box c1")
+    cfg = synth.CONFIGS["c5"]
+    x = synth.make_input(cfg, n_frames=3)
+    p = _plan(cfg)
+    p.set_kernel(SC_KERNEL_BOX)
+    gi, gd = _run(p, x)
+    ny = p.ny
+    for f in (0, 2):
+        for r0, r1 in [(0, 4), (ny // 2 - 1, ny // 2 + 2), (ny - 4, ny)]:
+            oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=(f, f + 1), rows=(r0, r1))
+            sl = slice(r0 * p.nx, r1 * p.nx)
+            check_u8(gi[f:f + 1, sl], gd[f:f + 1, sl], oi, od, f"box c5 frame {f} rows {r0}:{r1}")
+
+
+def test_box_row_bands():
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX
+    rng = np.random.Generator(np.random.PCG64(13))
+    x = torch.from_numpy(synth.random_image(rng, 2, 1, 140, 210, "u8")).cuda()
+    p = _plan((140, 210, 1, 8, 4, 33, 16), "u8")
+    p.set_kernel(SC_KERNEL_BOX)
+    fi, fd = p.run(x)
+    for r0, r1 in [(0, 1), (3, 20), (17, 34), (30, p.ny)]:
+        bi, bd = p.run_rows(x, r0, r1)
+        torch.cuda.synchronize()
+        sl = slice(r0 * p.nx, r1 * p.nx)
+        assert torch.equal(bi, fi[:, sl]) and torch.equal(bd, fd[:, sl]), (r0, r1)
+
+
+def test_lanes_kernel_c1_c5():
+    """The lanes = references kernel stays covered now that the box kernel is the u8 default."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_SIMT
+    cfg = synth.CONFIGS["c1"]
+    _compare(synth.make_input(cfg), 8, 4, 21, 16, "u8", where="lanes c1", kernel=SC_KERNEL_SIMT)
+    cfg = synth.CONFIGS["c5"]
+    x = synth.make_input(cfg, n_frames=2)
+    p = _plan(cfg)
+    p.set_kernel(SC_KERNEL_SIMT)
+    gi, gd = _run(p, x)
+    ny = p.ny
+    for r0, r1 in [(0, 2), (ny - 2, ny)]:
+        oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=(1, 2), rows=(r0, r1))
+        sl = slice(r0 * p.nx, r1 * p.nx)
+        check_u8(gi[1:2, sl], gd[1:2, sl], oi, od, f"lanes c5 rows {r0}:{r1}")
+
+
+def test_box_default_and_rejects_unsupported():
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX, ScError
+    assert _plan(synth.CONFIGS["c5"]).info()["kernel"] == SC_KERNEL_BOX
+    for args, dt in [((64, 64, 1, 8, 3, 21, 16), "u8"), ((64, 64, 1, 7, 4, 21, 16), "u8"),
+                     ((64, 64, 2, 8, 4, 21, 16), "u8"), ((64, 64, 1, 8, 4, 21, 33), "u8"),
+                     ((64, 64, 1, 8, 4, 47, 16), "u8"), ((64, 64, 1, 8, 4, 21, 16), "f32")]:
+        p = _plan(args, dt)
+        with pytest.raises(ScError) as e:
+            p.set_kernel(SC_KERNEL_BOX)
+        assert e.value.code == 2
