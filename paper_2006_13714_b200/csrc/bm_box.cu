@@ -18,9 +18,12 @@
 // loading each candidate row once for all of them; candidate words come from four byte-shifted
 // copies of the staged region, so any 4-byte run is one aligned shared-memory load.
 //
+// a1 in registers. The candidate norm h_X(.)h_X is the same kind of box sum of
+// x'^2: a dp4a chain over the lane's candidate rows, P[t] = sum_{u<t} |row u|^2, gives each
+// offset's strip norm as P[t+8] - P[t] (no norm map, no norm pass; exact int32).
 // a3. d' = n_c - 2 C (Lemma 2; ||X_i||^2 is constant per reference and added
-// back after selection) with n_c from the padded norm map: candidates outside [0,H-b]x[0,W-b]
-// read its huge border value and never pass a threshold, so window clipping costs nothing.
+// back after selection) = E_l + E_{l+1} with E = strip norm - 2 strip cross term, so one shfl
+// per pair. Window clipping: warp-uniform row masks and a per-lane column predicate.
 // a4. Per-reference 32-bit register top-K (regtopk.cuh; Theorem 1's K largest b_i = K smallest
 // d) fed by a per-lane threshold bitmask; references whose K-th key saturates
 // go to the exact fix-up (fixup.cu). Offsets are visited centre-out (dy blocks, then dx), so
@@ -40,11 +43,8 @@ constexpr int kBoxRefsX = 31;  // references per warp row (lane 31 is the helper
 
 struct BoxArgs {
   const uint8_t* imgs;  // [F][H][W]
-  const int32_t* norm;  // padded norm-map interior: (f, y, x) at norm[f*nfs + y*np + x]
   int32_t* idx_out;     // [F][band refs][K]
   int32_t* dist_out;
-  long long nfs;
-  int np;
   int H, W, Wn, K, lo, hi, nx, iy_begin, iy_end, tiles_x;
   int RH, WP, PL;  // staged region rows, words per region row, words per byte-shifted copy
   int nblk;        // dy blocks of VY offsets
@@ -102,8 +102,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
   if (iy0 >= a.iy_end) return;
   const int ix = ix_first + lane;
   const bool lane_ok = lane < kBoxRefsX && ix < a.nx;
-  const int rxn = min(ix, a.nx - 1) * 4;  // norm-map column base (in range for every lane)
-  const int32_t* nmap = a.norm + size_t(f) * a.nfs;
+  const int rx = ix * 4;
   const int rr0 = (iy0 - iy_first) * 4 - a.lo;  // region row of image row 4 * iy0
 
   // the lane's 4-column strip of its references' patch rows (reference side, aligned)
@@ -115,14 +114,17 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
     for (int r = 0; r < NR; ++r) R[r] = src[r * a.WP];
   }
   bool ref_ok[NY];
-  int32_t nr[NY];
-  int thr[NY];  // largest d' = d - ||X_i||^2 that may still enter the reference's top-K
+  int32_t nr[NY];  // ||X_i||^2 of the centred reference (left strip + lane l+1's right strip)
+  int thr[NY];     // largest d' = d - ||X_i||^2 that may still enter the reference's top-K
   RegTopK32<KR> rt[NY];
   const Key32 key32{a.rb, a.dsat};
 #pragma unroll
   for (int q = 0; q < NY; ++q) {
+    int n = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) n = __dp4a(int(R[4 * q + r]), int(R[4 * q + r]), n);
+    nr[q] = n + __shfl_down_sync(0xffffffffu, n, 1);
     ref_ok[q] = lane_ok && iy0 + q < a.iy_end;
-    nr[q] = __ldg(nmap + size_t(4 * (iy0 + q)) * a.np + rxn);
     rt[q].init();
     thr[q] = int(a.dsat) - nr[q];
   }
@@ -134,12 +136,18 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
     const int bb = b0 + centre_out(kb);
     if (bb < 0 || bb >= a.nblk) continue;
     const int dy0 = a.lo + bb * VY;
-    // whole block above / below the image for every reference of the warp (warp-uniform)
-    if (4 * (iy0 + NY - 1) + dy0 + VY - 1 < 0 || 4 * iy0 + dy0 > a.H - 8) continue;
-    const int nrow_ok = min(VY, a.hi - dy0 + 1);  // offsets dy0 + i beyond hi are not in the window
-    const unsigned rows = (1u << nrow_ok) - 1u;
+    // offsets dy0 + i inside the window (dy <= hi) whose candidate row lies in [0, H-b]
+    unsigned rows[NY];
+    bool any_row = false;
+#pragma unroll
+    for (int q = 0; q < NY; ++q) {
+      const int cy0 = 4 * (iy0 + q) + dy0;  // candidate row of offset i = 0
+      const int ilo = max(0, -cy0), ihi = min(min(VY - 1, a.hi - dy0), a.H - 8 - cy0);
+      rows[q] = ihi >= ilo ? (((2u << ihi) - 1u) & ~((1u << ilo) - 1u)) : 0u;
+      any_row |= rows[q] != 0u;
+    }
+    if (!any_row) continue;  // warp-uniform
     const uint32_t* cbase = sm + (rr0 + dy0) * a.WP + lane;
-    const int32_t* nrow = nmap + ptrdiff_t(4 * iy0 + dy0) * a.np + rxn;
     for (int kx = 0; kx <= 2 * span; ++kx) {
       const int dx = centre_out(kx);
       if (dx < a.lo || dx > a.hi) continue;
@@ -148,15 +156,21 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
       uint32_t Cw[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t) Cw[t] = col[t * a.WP];
-      // block sums -> left-strip sums T[q][i] of reference q at offset (dy0 + i, dx)
-      int T[NY][VY];
+      // a1 in registers: P[t] = sum_{u < t} |candidate strip row u|^2 (a dp4a prefix chain),
+      // so the strip norm of offset i of reference q is P[4q+i+8] - P[4q+i]
+      int P[NT + 1];
+      P[0] = 0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) P[t + 1] = __dp4a(int(Cw[t]), int(Cw[t]), P[t]);
+      // a2: block sums -> left-strip cross terms U[q][i] of reference q at offset (dy0 + i, dx)
+      int U[NY][VY];
 #pragma unroll
       for (int i = 0; i < VY; ++i) {
         if constexpr (NY == 1) {
           int acc = 0;
 #pragma unroll
           for (int r = 0; r < 8; ++r) acc = __dp4a(int(R[r]), int(Cw[r + i]), acc);
-          T[0][i] = acc;
+          U[0][i] = acc;
         } else {
           int m = 0;  // middle rows 4..7, shared by both references
 #pragma unroll
@@ -166,24 +180,25 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
           for (int r = 0; r < 4; ++r) t0 = __dp4a(int(R[r]), int(Cw[r + i]), t0);
 #pragma unroll
           for (int r = 8; r < 12; ++r) t1 = __dp4a(int(R[r]), int(Cw[r + i]), t1);
-          T[0][i] = t0;
-          T[1][i] = t1;
+          U[0][i] = t0;
+          U[1][i] = t1;
         }
       }
-      const int32_t* nb = nrow + dx;
+      const bool colok = unsigned(rx + dx) <= unsigned(a.W - 8);  // candidate column in [0, W-b]
 #pragma unroll
       for (int q = 0; q < NY; ++q) {
+        // a3: d' = n_c - 2 C = E_l + E_{l+1}, E = strip norm - 2 * strip cross term
         int dp[VY];
         unsigned bits = 0u;
 #pragma unroll
         for (int i = 0; i < VY; ++i) {
-          const int c = T[q][i] + __shfl_down_sync(0xffffffffu, T[q][i], 1);  // + right strip
-          dp[i] = __ldg(nb + (4 * q + i) * a.np) - 2 * c;
+          const int e = P[4 * q + i + 8] - P[4 * q + i] - 2 * U[q][i];
+          dp[i] = e + __shfl_down_sync(0xffffffffu, e, 1);
           bits |= (dp[i] <= thr[q] ? 1u : 0u) << i;
         }
-        bits &= ref_ok[q] ? rows : 0u;
+        bits &= (ref_ok[q] && colok) ? rows[q] : 0u;
         if (__any_sync(0xffffffffu, bits != 0u)) {
-          // survivors: one insertion per lane per round into the register top-K
+          // a4 survivors: one insertion per lane per round into the register top-K
           uint32_t* sc = scratch + lane;
 #pragma unroll
           for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(dp[i] + nr[q]);
@@ -194,7 +209,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
             bits &= bits - 1u;
             rt[q].insert(key);
           }
-          thr[q] = key32.thr(rt[q].at(a.K - 1)) - nr[q];
+          thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
           __syncwarp();
         }
       }
@@ -276,11 +291,8 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   const Geometry& g = p.g;
   BoxArgs a{};
   a.imgs = static_cast<const uint8_t*>(imgs);
-  a.norm = static_cast<const int32_t*>(p.ws.norm);
   a.idx_out = idx_out;
   a.dist_out = static_cast<int32_t*>(dist_out);
-  a.nfs = g.NFS;
-  a.np = g.Mxp;
   a.H = g.H; a.W = g.W; a.Wn = g.Wn; a.K = g.K; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.tiles_x = (g.nx + kBoxRefsX - 1) / kBoxRefsX;

@@ -75,8 +75,9 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
   const Geometry& g = p->g;
   const size_t img_bytes = size_t(g.C) * g.H * g.W * elem_size(g.dtype);
   const size_t out_elems = size_t(iy_end - iy_begin) * g.nx * g.K;
-  for (int64_t f0 = 0; f0 < n; f0 += p->F) {
-    const int F = int(std::min<int64_t>(p->F, n - f0));
+  const int chunk = (p->kernel == SC_KERNEL_BOX && dense == nullptr) ? p->FB : p->F;
+  for (int64_t f0 = 0; f0 < n; f0 += chunk) {
+    const int F = int(std::min<int64_t>(chunk, n - f0));
     const void* src = static_cast<const char*>(imgs) + f0 * img_bytes;
     cudaEvent_t* ev = nullptr;
     Timing& tm = p->timing;
@@ -85,7 +86,9 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
       ++tm.n_used;
       cudaEventRecord(ev[0], st);
     }
-    cudaError_t e = launch_norm(*p, src, F, st, &p->launches);
+    // the box-sum matcher forms the norms in registers; every other matcher reads the norm map
+    const bool box = p->kernel == SC_KERNEL_BOX && dense == nullptr;
+    cudaError_t e = box ? cudaSuccess : launch_norm(*p, src, F, st, &p->launches);
     if (e != cudaSuccess) return cuda_status(e);
     if (ev) cudaEventRecord(ev[1], st);
     int32_t* io = idx ? idx + f0 * out_elems : nullptr;
@@ -199,7 +202,8 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   if (e == cudaSuccess)
     p->ws.norm = static_cast<char*>(p->ws.norm_base) + (size_t(g.NPAD) * g.Mxp + g.NPAD) * 4;
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_count, sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_list, size_t(g.ny) * g.nx * sizeof(int) * p->F);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&p->ws.fix_list, size_t(g.ny) * g.nx * sizeof(int) * std::max(p->F, p->FB));
   if (e == cudaSuccess) e = cudaMemset(p->ws.fix_count, 0, sizeof(int));
   if (e != cudaSuccess) {
     free_ws(p);
