@@ -185,6 +185,10 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
         }
       }
       const bool colok = unsigned(rx + dx) <= unsigned(a.W - 8);  // candidate column in [0, W-b]
+      // strip norms of the 4(NY-1) + VY distinct candidate rows: D[j] = P[j + 8] - P[j]
+      int D[4 * (NY - 1) + VY];
+#pragma unroll
+      for (int j = 0; j < 4 * (NY - 1) + VY; ++j) D[j] = P[j + 8] - P[j];
 #pragma unroll
       for (int q = 0; q < NY; ++q) {
         // a3: d' = n_c - 2 C = E_l + E_{l+1}, E = strip norm - 2 * strip cross term
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
         unsigned bits = 0u;
 #pragma unroll
         for (int i = 0; i < VY; ++i) {
-          const int e = P[4 * q + i + 8] - P[4 * q + i] - 2 * U[q][i];
+          const int e = D[4 * q + i] - 2 * U[q][i];
           dp[i] = e + __shfl_down_sync(0xffffffffu, e, 1);
           bits |= (dp[i] <= thr[q] ? 1u : 0u) << i;
         }
@@ -261,11 +265,6 @@ size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
   return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
 }
 
-int box_ny() {
-  const char* e = getenv("SCBM_BOX_NY");
-  return (e && atoi(e) == 1) ? 1 : 2;
-}
-
 template <int NY, int VY, int KR>
 cudaError_t launch_box_t(const BoxArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + kBoxWarps * NY - 1) / (kBoxWarps * NY);
@@ -300,12 +299,11 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   a.dsat = uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
   a.fix_count = p.ws.fix_count;
   a.fix_list = p.ws.fix_list;
-  const int vy = box_vy(g), kr = g.K <= 16 ? 16 : 32, ny = box_ny();
-  const size_t smem = box_layout(g, ny, vy, kr, &a);
+  const int vy = box_vy(g), kr = g.K <= 16 ? 16 : 32;
+  const size_t smem = box_layout(g, 2, vy, kr, &a);
   cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  if (ny == 1) e = launch_box_t<1, 11, 16>(a, F, box_layout(g, 1, 11, 16, &a), st);  // experiments
-  else if (kr == 16 && vy == 11) e = launch_box_t<2, 11, 16>(a, F, smem, st);
+  if (kr == 16 && vy == 11) e = launch_box_t<2, 11, 16>(a, F, smem, st);
   else if (kr == 16 && vy == 7) e = launch_box_t<2, 7, 16>(a, F, smem, st);
   else if (kr == 16) e = launch_box_t<2, 8, 16>(a, F, smem, st);
   else if (vy == 11) e = launch_box_t<2, 11, 32>(a, F, smem, st);

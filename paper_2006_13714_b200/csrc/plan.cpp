@@ -185,8 +185,11 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   const bool lanes_ok = dtype == SC_DTYPE_U8 && g.nx >= 64 && p->lanes_nwy >= 4 &&
                         lanes_smem_bytes(g, p->lanes_nwy) <= 227 * 1024;
   p->kernel = lanes_ok ? SC_KERNEL_SIMT : SC_KERNEL_SIMT_WARP;
-  // u8, b = 8, s = 4 (configs c1, c5): the box-sum matcher (6 dp4a per pair instead of 16)
-  if (box_supported(g)) p->kernel = SC_KERNEL_BOX;
+  // u8, b = 8, s = 4 (config c5): the box-sum matcher (7 dp4a per pair instead of 16 + norm pass).
+  // Its CTA covers 16 x 31 references; on small images (c1: 15 x 15 references = 1 CTA) the
+  // one-warp-per-reference kernel spreads the work over more SMs and measured faster.
+  const int64_t box_ctas = int64_t((g.ny + 15) / 16) * ((g.nx + 30) / 31);
+  if (box_supported(g) && box_ctas >= 16) p->kernel = SC_KERNEL_BOX;
 
   const size_t SP = size_t((W + 15) / 16 * 16);
   cudaError_t e = cudaSuccess;
@@ -331,7 +334,7 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
   info->max_candidates = p->max_cand;
   info->total_candidates = p->total_cand;
   info->workspace_bytes = int64_t(p->ws.bytes);
-  info->frames_per_chunk = p->F;
+  info->frames_per_chunk = p->kernel == SC_KERNEL_BOX ? p->FB : p->F;
   info->launches = p->launches;
   info->kernel = p->kernel;
   info->device = p->device;

@@ -6,4 +6,4 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
 timeout 300 $B > gpurun_out/plain_launch.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "launches=$?" >> gpurun_out/deliv_status.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"bm_lanes" -s 2 -c 1 -o gpurun_out/prof_default $B > gpurun_out/ncu_full.log 2>&1; echo "ncufull=$?" >> gpurun_out/deliv_status.txt
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"bm_box" -s 2 -c 1 -o gpurun_out/prof_default $B > gpurun_out/ncu_full.log 2>&1; echo "ncufull=$?" >> gpurun_out/deliv_status.txt
