@@ -192,25 +192,28 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
 #pragma unroll
       for (int q = 0; q < NY; ++q) {
         // a3: d' = n_c - 2 C = E_l + E_{l+1}, E = strip norm - 2 * strip cross term
-        int dp[VY];
-        unsigned bits = 0u;
+        // slack t = thr - d' (>= 0: the candidate may enter the top-K); fail bits = sign bits
+        int t[VY];
+        unsigned fails = 0u;
 #pragma unroll
-        for (int i = 0; i < VY; ++i) {
+        for (int i = VY - 1; i >= 0; --i) {
           const int e = D[4 * q + i] - 2 * U[q][i];
-          dp[i] = e + __shfl_down_sync(0xffffffffu, e, 1);
-          bits |= (dp[i] <= thr[q] ? 1u : 0u) << i;
+          t[i] = thr[q] - e - __shfl_down_sync(0xffffffffu, e, 1);
+          fails = (fails << 1) + (uint32_t(t[i]) >> 31);
         }
-        bits &= (ref_ok[q] && colok) ? rows[q] : 0u;
+        unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);
         if (__any_sync(0xffffffffu, bits != 0u)) {
           // a4 survivors: one insertion per lane per round into the register top-K
           uint32_t* sc = scratch + lane;
+          const int dthr = thr[q] + nr[q];  // d = d' + ||X_i||^2 = dthr - t (exact, >= 0)
 #pragma unroll
-          for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(dp[i] + nr[q]);
+          for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(dthr - t[i]);
           const int rel0 = (dy0 - a.lo) * a.Wn + off;
           while (__any_sync(0xffffffffu, bits != 0u)) {
-            const int i = bits ? __ffs(bits) - 1 : 0;
-            const uint32_t key = bits ? key32.make(int(sc[32 * i]), rel0 + i * a.Wn) : 0xffffffffu;
-            bits &= bits - 1u;
+            const int i = 31 - __clz(bits | 1u);  // any survivor (insertion order is irrelevant)
+            const uint32_t d = sc[32 * i];        // safe address for every lane
+            const uint32_t key = bits ? (min(d, a.dsat) << a.rb) | uint32_t(rel0 + i * a.Wn) : 0xffffffffu;
+            bits &= ~(1u << i);
             rt[q].insert(key);
           }
           thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
