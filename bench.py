@@ -173,7 +173,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL all-gather of the tables")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
-    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box"],
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf"],
                     help="force the matching kernel (default: the plan's choice)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -206,7 +206,7 @@ def main():
     x = torch.from_numpy(x_host).cuda()
     plan = Plan(cfg.H, cfg.W, cfg.C, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype)
     if args.kernel != "auto":
-        plan.set_kernel({"simt": 0, "tc": 1, "warp": 2, "box": 3}[args.kernel])
+        plan.set_kernel({"simt": 0, "tc": 1, "warp": 2, "box": 3, "boxf": 4}[args.kernel])
     info = plan.info()
     idx, dst = plan.alloc_out(nloc)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -256,7 +256,8 @@ def main():
     # algorithmic MACs per candidate pair: the direct cross term is b^2 C
     # multiply-adds; the box-sum kernel evaluates each product of the shifted
     # product image once, s^2 C per pair (its 4x4 block sums are shared by 2 x 2 references)
-    mac_pair = cfg.s * cfg.s * cfg.C if info["kernel"] == 3 else cfg.b * cfg.b * cfg.C
+    # (c5); the float box kernel correlates one s-column strip per reference and offset, b s C
+    mac_pair = {3: cfg.s * cfg.s * cfg.C, 4: cfg.b * cfg.s * cfg.C}.get(info["kernel"], cfg.b * cfg.b * cfg.C)
     macs_launch = pairs_per_image * nloc * mac_pair  # algorithmic MACs per rank-step
     macs_direct = pairs_per_image * nloc * cfg.b * cfg.b * cfg.C
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -272,7 +273,8 @@ def main():
         bound, unit, peak_note = "alu", "TFLOP/s", "FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md section 7)"
     achieved = 2.0 * macs_launch / (match_ms / 1e3) / 1e12 if match_ms > 0 else None
     traffic, traffic_src = None, None
-    kname = {0: "bm_lanes_kernel", 1: "bm_tc_i8_kernel", 2: "bm_simt_kernel", 3: "bm_box_kernel"}[info["kernel"]]
+    kname = {0: "bm_lanes_kernel", 1: "bm_tc_i8_kernel", 2: "bm_simt_kernel", 3: "bm_box_kernel",
+             4: "bm_boxf_kernel"}[info["kernel"]]
     prof = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{kname.replace('_kernel', '')}_{cfg.name}_metrics.json")
     if os.path.exists(prof):
         m = json.load(open(prof))

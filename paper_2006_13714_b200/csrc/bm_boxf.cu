@@ -1,0 +1,328 @@
+// bm_boxf.cu -- the float box-sum Self-Convolution matcher (SC_KERNEL_BOXF): f32 images, one
+// channel, reference stride s <= patch side b (instantiated for (s, b) = (3, 8), (1, 7), (4, 8),
+// (2, 8)): steps a0-a6 fused in one kernel.
+//
+// The same regrouping as the u8 box kernel (bm_box.cu): for one window offset delta the cross
+// term of every reference (Eq. 5) is a box sum of the product image
+// P_delta(y, x) = x'(y, x) x'(y + dy, x + dx), so references that overlap share work:
+//   * lane l holds reference column ix0 + l and correlates only its own s-column strip of the
+//     patch rows; a reference's patch is NS = ceil(b / s) consecutive strips (the last one
+//     WL = b - (NS-1) s columns wide), i.e. lanes l .. l+NS-1: NS-1 shuffles per pair (a
+//     doubling tree for s = 1). Lanes 33-NS .. 31 are helper strips.
+//   * the candidate norm (a1) uses the same strips: running sums of the squared
+//     candidate rows, so d' = n_c - 2 C (Lemma 2) is assembled per strip,
+//     E = strip norm - 2 strip cross term, and summed over the NS strips.
+//   * a lane slides over VY vertically adjacent offsets, loading each candidate row once.
+// For c2 (s = 3, b = 8) that is 24 FMAs + 24 square FMAs per (reference, candidate row) group
+// of 8 offsets, i.e. ~27 FMAs per pair instead of 64; for c3 (s = 1, b = 7) ~8 instead of 49.
+//
+// a4: per-lane register top-KP of 32-bit keys (regtopk.cuh): key = (float bits of d >> (rb-1))
+// << rb | (rel + 1); d >= 0 so the float bits are monotone, and the 21 (20) kept bits give
+// a relative resolution of 2^-13 (2^-12). The first KR - KP slots hold a 0 sentinel (real keys
+// are >= 1), so the KP-th key always sits in the last register. The filter is a superset
+// (threshold = the largest distance of the KP-th key's quantum), and a5 re-scores the KP keys
+// of every reference exactly by direct differences in fp32 from the input and keeps the best
+// K (BASELINE.json north_star tolerance): a true top-K candidate can only
+// be lost if more than KP - K = 8 others lie within one quantum (~1e-4 relative) of it.
+#include <algorithm>
+
+#include "regtopk.cuh"
+#include "sc_internal.h"
+#include "topk.cuh"
+
+namespace scbm {
+namespace {
+
+constexpr int kFWarps = 8;
+
+struct BoxfArgs {
+  const float* imgs;  // [F][1][H][W]
+  int32_t* idx_out;   // [F][band refs][K]
+  float* dist_out;
+  int H, W, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
+  int RH, RWp, PL;  // staged region rows, row pitch (floats), floats per plane
+  int nblk;         // dy blocks of VY offsets
+  int scr;          // per-warp scratch words
+  int rb;           // window-relative index bits of the 32-bit keys
+};
+
+__device__ __forceinline__ int centre_out_f(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
+
+// sum over the reference's strips: full strips of lanes l .. l+NS-2, partial strip of lane l+NS-1
+template <int NS, int WL, int S>
+__device__ __forceinline__ float hcombine(float ef, float ep) {
+  if constexpr (NS == 1) {
+    return ep;
+  } else if constexpr (NS == 7 && WL == S) {  // s = 1, b = 7: doubling tree, 4 shuffles
+    const float s2 = ef + __shfl_down_sync(0xffffffffu, ef, 1);
+    const float s4 = s2 + __shfl_down_sync(0xffffffffu, s2, 2);
+    const float s6 = s4 + __shfl_down_sync(0xffffffffu, s2, 4);
+    return s6 + __shfl_down_sync(0xffffffffu, ef, 6);
+  } else {
+    float acc = ef;
+#pragma unroll
+    for (int j = 1; j < NS - 1; ++j) acc += __shfl_down_sync(0xffffffffu, ef, j);
+    return acc + __shfl_down_sync(0xffffffffu, ep, NS - 1);
+  }
+}
+
+template <int S, int BK, int VY, int KR>
+__global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
+  constexpr int NS = (BK + S - 1) / S;   // strips per patch
+  constexpr int WL = BK - (NS - 1) * S;  // width of the last strip
+  constexpr int RX = 33 - NS;            // references per warp (lanes RX..31: helper strips)
+  constexpr int NT = BK + VY - 1;        // candidate rows per (dy block, dx)
+  extern __shared__ __align__(16) float smf[];
+  const int f = blockIdx.y;
+  const int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
+  const int iy_first = a.iy_begin + ty * kFWarps;
+  const int ix_first = tx * RX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Ybase = iy_first * S + a.lo, Xbase = ix_first * S + a.lo;
+
+  // ---- a0: the centred region x' = x - 0.5 (0 outside the image)
+  const float* img = a.imgs + size_t(f) * a.H * a.W;
+  for (int e = threadIdx.x; e < a.PL; e += blockDim.x) {
+    const int r = e / a.RWp, x = e - r * a.RWp;
+    const int yy = Ybase + r, xx = Xbase + x;
+    smf[e] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) ? __ldg(img + size_t(yy) * a.W + xx) - 0.5f : 0.f;
+  }
+  __syncthreads();
+
+  const int iy0 = iy_first + warp;
+  if (iy0 >= a.iy_end) return;
+  const int ix = ix_first + lane;
+  const bool lane_ok = lane < RX && ix < a.nx;
+  const int rx = ix * S, ry = iy0 * S;
+  const int rr0 = (iy0 - iy_first) * S - a.lo;  // region row of image row ry
+  const int rc0 = lane * S - a.lo;              // region column of the lane's strip
+  float R[BK][S];
+#pragma unroll
+  for (int r = 0; r < BK; ++r)
+#pragma unroll
+    for (int m = 0; m < S; ++m) R[r][m] = smf[(rr0 + r) * a.RWp + rc0 + m];
+  float nr;  // ||X_i||^2 of the centred reference
+  {
+    float nf = 0.f, np = 0.f;
+#pragma unroll
+    for (int r = 0; r < BK; ++r)
+#pragma unroll
+      for (int m = 0; m < S; ++m) {
+        if (m < WL) np = fmaf(R[r][m], R[r][m], np);
+        nf = fmaf(R[r][m], R[r][m], nf);
+      }
+    nr = hcombine<NS, WL, S>(nf, np);
+  }
+  RegTopK32<KR> rt;
+#pragma unroll
+  for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;  // 0 sentinels
+  const int rb = a.rb;
+  float thr = __int_as_float(0x7f800000);  // +inf: largest d' that may still enter the top-KP
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smf + a.PL) + warp * a.scr;
+
+  const int b0 = (0 - a.lo) / VY;
+  const int span = max(-a.lo, a.hi);
+  for (int kb = 0; kb < 2 * a.nblk; ++kb) {
+    const int bb = b0 + centre_out_f(kb);
+    if (bb < 0 || bb >= a.nblk) continue;
+    const int dy0 = a.lo + bb * VY;
+    const int cy0 = ry + dy0;  // candidate row of offset i = 0
+    const int ilo = max(0, -cy0), ihi = min(min(VY - 1, a.hi - dy0), a.H - BK - cy0);
+    if (ihi < ilo) continue;  // warp-uniform
+    const unsigned rows = ((2u << ihi) - 1u) & ~((1u << ilo) - 1u);
+    const float* cbase = smf + (rr0 + dy0) * a.RWp + rc0;
+    for (int kx = 0; kx <= 2 * span; ++kx) {
+      const int dx = centre_out_f(kx);
+      if (dx < a.lo || dx > a.hi) continue;
+      const float* col = cbase + dx;
+      // cross terms of the full / partial strip, and running squared-row sums for the norms
+      float Tp[VY], Tr[VY];
+#pragma unroll
+      for (int i = 0; i < VY; ++i) Tp[i] = Tr[i] = 0.f;
+      float Qp[NT + 1], Qr[NT + 1];
+      Qp[0] = Qr[0] = 0.f;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        float cv[S];
+#pragma unroll
+        for (int m = 0; m < S; ++m) cv[m] = col[t * a.RWp + m];
+        float qp = Qp[t], qr = Qr[t];
+#pragma unroll
+        for (int m = 0; m < S; ++m) {
+          if (m < WL) qp = fmaf(cv[m], cv[m], qp);
+          else qr = fmaf(cv[m], cv[m], qr);
+        }
+        Qp[t + 1] = qp;
+        Qr[t + 1] = qr;
+#pragma unroll
+        for (int i = 0; i < VY; ++i) {
+          const int r = t - i;
+          if (r >= 0 && r < BK) {
+#pragma unroll
+            for (int m = 0; m < S; ++m) {
+              if (m < WL) Tp[i] = fmaf(R[r][m], cv[m], Tp[i]);
+              else Tr[i] = fmaf(R[r][m], cv[m], Tr[i]);
+            }
+          }
+        }
+      }
+      const bool colok = unsigned(rx + dx) <= unsigned(a.W - BK);
+      float dpv[VY];
+      unsigned fails = 0u;
+#pragma unroll
+      for (int i = VY - 1; i >= 0; --i) {
+        const float np = Qp[i + BK] - Qp[i], nrest = Qr[i + BK] - Qr[i];
+        const float ep = fmaf(-2.f, Tp[i], np);
+        const float ef = ep + fmaf(-2.f, Tr[i], nrest);
+        dpv[i] = hcombine<NS, WL, S>(ef, ep);  // d' = n_c - 2 C
+        // slack thr - d' >= 0 (or +inf): the candidate may enter the top-KP
+        fails = (fails << 1) + (__float_as_uint(thr - dpv[i]) >> 31);
+      }
+      unsigned bits = ~fails & ((lane_ok && colok) ? rows : 0u);
+      if (__any_sync(0xffffffffu, bits != 0u)) {
+        uint32_t* sc = scratch + lane;
+#pragma unroll
+        for (int i = 0; i < VY; ++i) sc[32 * i] = __float_as_uint(fmaxf(dpv[i] + nr, 0.f));
+        const int rel1 = (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
+        while (__any_sync(0xffffffffu, bits != 0u)) {
+          const int i = 31 - __clz(bits | 1u);
+          const uint32_t q = sc[32 * i] >> (rb - 1);
+          const uint32_t key = bits ? (q << rb) | uint32_t(rel1 + i * a.Wn) : 0xffffffffu;
+          bits &= ~(1u << i);
+          rt.insert(key);
+        }
+        const uint32_t kth = rt.r[KR - 1];
+        if (kth != 0xffffffffu) {
+          // largest distance whose key can still tie the KP-th key, plus a rounding margin
+          const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
+          thr = fmaf(dmax, 1.0f + 1e-6f, -nr) + 1e-30f;
+        }
+        __syncwarp();
+      }
+    }
+  }
+
+  // ---- a5 + a6: stage each reference's KP keys, then per reference (warp-cooperative) re-score
+  // them by direct differences from the input, sort the (distance, idx) keys and write K.
+  if (lane_ok) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k) scratch[lane * (KR + 1) + k] = rt.r[k];
+  }
+  __syncwarp();
+  const int nref = min(RX, a.nx - ix_first);
+  const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
+  const size_t row0 = size_t(f) * band_refs + size_t(iy0 - a.iy_begin) * a.nx + ix_first;
+  constexpr int NJ = (KR + 31) / 32;
+  for (int j = 0; j < nref; ++j) {
+    const int rxj = (ix_first + j) * S;
+    WarpTopK<NJ> top;
+    top.init();
+#pragma unroll
+    for (int sl = 0; sl < NJ; ++sl) {
+      const int k = sl * 32 + lane;
+      uint64_t key = kKeyInf;
+      const uint32_t kk = k < KR ? scratch[j * (KR + 1) + k] : 0xffffffffu;
+      if (kk != 0u && kk != 0xffffffffu) {
+        const int rel = int(kk & ((1u << rb) - 1u)) - 1;
+        const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+        const int cy = ry + dyy + a.lo, cx = rxj + dxx + a.lo;
+        const float* pr = img + size_t(ry) * a.W + rxj;
+        const float* pc = img + size_t(cy) * a.W + cx;
+        float d = 0.f;
+        for (int l = 0; l < BK; ++l)
+#pragma unroll
+          for (int m = 0; m < BK; ++m) {
+            const float df = __ldg(pr + l * a.W + m) - __ldg(pc + l * a.W + m);
+            d = fmaf(df, df, d);
+          }
+        key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * a.W + cx);
+      }
+      top.merge(key, lane);
+    }
+#pragma unroll
+    for (int sl = 0; sl < NJ; ++sl) {
+      const int k = sl * 32 + lane;
+      if (k < a.K) {
+        const uint64_t key = top.v[sl];
+        const bool none = key == kKeyInf;
+        a.idx_out[(row0 + j) * a.K + k] = none ? -1 : int32_t(uint32_t(key));
+        a.dist_out[(row0 + j) * a.K + k] = none ? __int_as_float(0x7f800000) : __uint_as_float(uint32_t(key >> 32));
+      }
+    }
+  }
+}
+
+constexpr int kFVY = 8;
+
+size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) {
+  const int ns = (g.b + g.s - 1) / g.s, rx = 33 - ns;
+  a->nblk = (g.Wn + kFVY - 1) / kFVY;
+  a->RH = (kFWarps - 1) * g.s + a->nblk * kFVY + g.b;
+  a->RWp = 32 * g.s + g.Wn - 1 + 1;
+  a->PL = a->RH * a->RWp;
+  a->scr = std::max(32 * kFVY, rx * (KR + 1));
+  return size_t(a->PL + kFWarps * a->scr) * 4;
+}
+
+// key bits of the window-relative index + 1 (values 1 .. Wn^2; 0 is the sentinel)
+int boxf_rel_bits(int Wn) {
+  int rb = 1;
+  while ((1 << rb) <= Wn * Wn) ++rb;
+  return rb;
+}
+
+int boxf_kr(const Geometry& g) { return g.KP <= 32 ? 32 : g.KP <= 48 ? 48 : g.KP <= 80 ? 80 : 0; }
+
+template <int S, int BK, int KR>
+cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st) {
+  const int tiles_y = (a.iy_end - a.iy_begin + kFWarps - 1) / kFWarps;
+  auto k = bm_boxf_kernel<S, BK, kFVY, KR>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k<<<dim3(a.tiles_x * tiles_y, F), kFWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool boxf_supported(const Geometry& g) {
+  if (g.dtype != SC_DTYPE_F32 || g.C != 1) return false;
+  const bool shape = (g.s == 3 && g.b == 8) || (g.s == 1 && g.b == 7) || (g.s == 4 && g.b == 8) ||
+                     (g.s == 2 && g.b == 8);
+  if (!shape) return false;
+  const int kr = boxf_kr(g);
+  if (kr == 0) return false;
+  if (boxf_rel_bits(g.Wn) > 12) return false;  // keeps >= 20 distance bits in the 32-bit keys
+  BoxfArgs a{};
+  return boxf_layout(g, kr, &a) <= 113 * 1024;  // 2 CTAs per SM
+}
+
+cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
+  const Geometry& g = p.g;
+  BoxfArgs a{};
+  a.imgs = static_cast<const float*>(imgs);
+  a.idx_out = idx_out;
+  a.dist_out = static_cast<float*>(dist_out);
+  a.H = g.H; a.W = g.W; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
+  a.iy_begin = iy_begin; a.iy_end = iy_end;
+  const int ns = (g.b + g.s - 1) / g.s;
+  a.tiles_x = (g.nx + (33 - ns) - 1) / (33 - ns);
+  a.rb = boxf_rel_bits(g.Wn);
+  const int kr = boxf_kr(g);  // the layout and the instantiation use the same list size
+  const size_t smem = boxf_layout(g, kr, &a);
+  if (launches) *launches += 1;
+#define SCBM_BOXF_CASE(S_, B_)                                                    \
+  if (g.s == S_ && g.b == B_) {                                                   \
+    if (kr == 32) return launch_boxf_t<S_, B_, 32>(a, F, smem, st);               \
+    if (kr == 48) return launch_boxf_t<S_, B_, 48>(a, F, smem, st);               \
+    return launch_boxf_t<S_, B_, 80>(a, F, smem, st);                             \
+  }
+  SCBM_BOXF_CASE(3, 8)
+  SCBM_BOXF_CASE(1, 7)
+  SCBM_BOXF_CASE(4, 8)
+  SCBM_BOXF_CASE(2, 8)
+#undef SCBM_BOXF_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace scbm

@@ -75,7 +75,7 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
   const Geometry& g = p->g;
   const size_t img_bytes = size_t(g.C) * g.H * g.W * elem_size(g.dtype);
   const size_t out_elems = size_t(iy_end - iy_begin) * g.nx * g.K;
-  const int chunk = (p->kernel == SC_KERNEL_BOX && dense == nullptr) ? p->FB : p->F;
+  const int chunk = ((p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr) ? p->FB : p->F;
   for (int64_t f0 = 0; f0 < n; f0 += chunk) {
     const int F = int(std::min<int64_t>(chunk, n - f0));
     const void* src = static_cast<const char*>(imgs) + f0 * img_bytes;
@@ -87,7 +87,7 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
       cudaEventRecord(ev[0], st);
     }
     // the box-sum matcher forms the norms in registers; every other matcher reads the norm map
-    const bool box = p->kernel == SC_KERNEL_BOX && dense == nullptr;
+    const bool box = (p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr;
     cudaError_t e = box ? cudaSuccess : launch_norm(*p, src, F, st, &p->launches);
     if (e != cudaSuccess) return cuda_status(e);
     if (ev) cudaEventRecord(ev[1], st);
@@ -97,6 +97,8 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
       e = launch_bm_tc(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_BOX && dense == nullptr)
       e = launch_bm_box(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
+    else if (p->kernel == SC_KERNEL_BOXF && dense == nullptr)
+      e = launch_bm_boxf(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_SIMT_WARP)
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
     else
@@ -190,6 +192,9 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   // one-warp-per-reference kernel spreads the work over more SMs and measured faster.
   const int64_t box_ctas = int64_t((g.ny + 15) / 16) * ((g.nx + 30) / 31);
   if (box_supported(g) && box_ctas >= 16) p->kernel = SC_KERNEL_BOX;
+  // f32, one channel, (s, b) in {(3,8), (1,7), (4,8), (2,8)}, K + 8 <= 80 (c2, c3): the float
+  // box-sum matcher
+  if (boxf_supported(g)) p->kernel = SC_KERNEL_BOXF;
 
   const size_t SP = size_t((W + 15) / 16 * 16);
   cudaError_t e = cudaSuccess;
@@ -334,7 +339,7 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
   info->max_candidates = p->max_cand;
   info->total_candidates = p->total_cand;
   info->workspace_bytes = int64_t(p->ws.bytes);
-  info->frames_per_chunk = p->kernel == SC_KERNEL_BOX ? p->FB : p->F;
+  info->frames_per_chunk = (p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) ? p->FB : p->F;
   info->launches = p->launches;
   info->kernel = p->kernel;
   info->device = p->device;
@@ -346,8 +351,9 @@ sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_BOX && !box_supported(p->g)) return SC_ERR_UNSUPPORTED;
+  if (kernel == SC_KERNEL_BOXF && !boxf_supported(p->g)) return SC_ERR_UNSUPPORTED;
   if (kernel != SC_KERNEL_SIMT && kernel != SC_KERNEL_SIMT_WARP && kernel != SC_KERNEL_TC_I8 &&
-      kernel != SC_KERNEL_BOX)
+      kernel != SC_KERNEL_BOX && kernel != SC_KERNEL_BOXF)
     return SC_ERR_UNSUPPORTED;
   p->kernel = kernel;
   return SC_OK;

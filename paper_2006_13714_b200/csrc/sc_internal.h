@@ -112,4 +112,9 @@ bool box_supported(const Geometry& g);
 cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
 
+// bm_boxf.cu: the float box-sum matcher (SC_KERNEL_BOXF; f32, C = 1, (s, b) in a small set).
+bool boxf_supported(const Geometry& g);
+cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
+
 }  // namespace scbm

@@ -447,3 +447,89 @@ def test_box_default_and_rejects_unsupported():
         with pytest.raises(ScError) as e:
             p.set_kernel(SC_KERNEL_BOX)
         assert e.value.code == 2
+
+
+# ------------------------------------------------------------------ float box-sum kernel
+def _boxf_fits(s, b, Wn, K):
+    """Mirror of boxf_supported's shared-memory / key-width rule (bm_boxf.cu)."""
+    ns = -(-b // s)
+    kr = 32 if K + 8 <= 32 else 48 if K + 8 <= 48 else 80 if K + 8 <= 80 else 0
+    rb = max(1, (Wn * Wn).bit_length())
+    if kr == 0 or rb > 12:
+        return False
+    nblk = -(-Wn // 8)
+    pl = (7 * s + nblk * 8 + b) * (32 * s + Wn)
+    scr = max(256, (33 - ns) * (kr + 1))
+    return (pl + 8 * scr) * 4 <= 113 * 1024
+
+
+def _boxf_cases(n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shapes = [(3, 8), (1, 7), (4, 8), (2, 8)]
+    out = []
+    while len(out) < n:
+        s, b = shapes[len(out) % len(shapes)]
+        H = int(rng.integers(b, 110))
+        W = int(rng.integers(b, 160))
+        Wn = int(rng.integers(1, 64))
+        K = int(rng.integers(1, 73))
+        if ((H - b) // s + 1) * ((W - b) // s + 1) * Wn * Wn > 4e7 or not _boxf_fits(s, b, Wn, K):
+            continue
+        out.append((s, b, H, W, Wn, K))
+    return out
+
+
+def _boxf(x, b, s, Wn, K, where):
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOXF
+    _compare(x, b, s, Wn, K, "f32", where=where, kernel=SC_KERNEL_BOXF)
+
+
+@pytest.mark.parametrize("case", _boxf_cases(24, 505))
+def test_boxf_random_sweep(case):
+    s, b, H, W, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 2, 1, H, W, "f32")
+    _boxf(x, b, s, Wn, K, f"boxf {case}")
+
+
+@pytest.mark.parametrize("kind", ["constant", "periodic", "binary", "smooth"])
+@pytest.mark.parametrize("s,b", [(3, 8), (1, 7)])
+def test_boxf_ties_and_extremes(kind, s, b):
+    rng = np.random.Generator(np.random.PCG64(14))
+    if kind == "constant":
+        x = np.full((1, 1, 60, 90), 0.3, dtype=np.float32)
+    elif kind == "periodic":
+        x = np.tile(rng.random((8, 8), dtype=np.float32), (8, 12))[None, None].copy()
+    elif kind == "binary":
+        x = rng.integers(0, 2, size=(1, 1, 60, 90)).astype(np.float32)
+    else:
+        yy, xx = np.mgrid[0:64, 0:96]
+        x = (0.5 + 0.4 * np.sin(yy / 7.0) * np.cos(xx / 9.0)).astype(np.float32)[None, None].copy()
+    _boxf(x, b, s, 21, 30, f"boxf {kind} s{s} b{b}")
+
+
+def test_boxf_default_and_rejects_unsupported():
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOXF, ScError
+    for name in ("c2", "c3"):
+        assert _plan(synth.CONFIGS[name]).info()["kernel"] == SC_KERNEL_BOXF
+    for args, dt in [((64, 64, 1, 8, 5, 21, 16), "f32"), ((64, 64, 2, 8, 3, 21, 16), "f32"),
+                     ((64, 64, 1, 8, 3, 21, 80), "f32"), ((64, 64, 1, 8, 3, 21, 16), "u8")]:
+        p = _plan(args, dt)
+        with pytest.raises(ScError) as e:
+            p.set_kernel(SC_KERNEL_BOXF)
+        assert e.value.code == 2
+
+
+def test_c3_warp_kernel_sampled_rows():
+    """The warp kernel stays covered on c3 now that the float box kernel is its default."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_SIMT_WARP
+    cfg = synth.CONFIGS["c3"]
+    x = synth.make_input(cfg)
+    p = _plan(cfg)
+    p.set_kernel(SC_KERNEL_SIMT_WARP)
+    gi, gd = _run(p, x)
+    for r0, r1 in [(0, 2), (p.ny - 2, p.ny)]:
+        oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, rows=(r0, r1))
+        sl = slice(r0 * p.nx, r1 * p.nx)
+        check_f32(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0, sl], gd[0, sl], oi[0], od[0],
+                  iy_range=(r0, r1), where=f"warp c3 rows {r0}:{r1}")
