@@ -1,6 +1,6 @@
-// bm_boxf.cu -- the float box-sum Self-Convolution matcher (SC_KERNEL_BOXF): f32 images, one
-// channel, reference stride s <= patch side b (instantiated for (s, b) = (3, 8), (1, 7), (4, 8),
-// (2, 8)): steps a0-a6 fused in one kernel.
+// bm_boxf.cu -- the float box-sum Self-Convolution matcher (SC_KERNEL_BOXF): f32 images, any
+// channel count (channels summed, Eq. 12), reference stride s <= patch side b (instantiated for
+// (s, b) = (3, 8), (1, 7), (4, 8), (2, 8)): steps a0-a6 fused in one kernel.
 //
 // The same regrouping as the u8 box kernel (bm_box.cu): for one window offset delta the cross
 // term of every reference (Eq. 5) is a box sum of the product image
@@ -36,11 +36,11 @@ namespace {
 constexpr int kFWarps = 8;
 
 struct BoxfArgs {
-  const float* imgs;  // [F][1][H][W]
+  const float* imgs;  // [F][C][H][W]
   int32_t* idx_out;   // [F][band refs][K]
   float* dist_out;
-  int H, W, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
-  int RH, RWp, PL;  // staged region rows, row pitch (floats), floats per plane
+  int H, W, C, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
+  int RH, RWp, PL;  // staged region rows, row pitch (floats), floats per channel plane
   int nblk;         // dy blocks of VY offsets
   int scr;          // per-warp scratch words
   int rb;           // window-relative index bits of the 32-bit keys
@@ -66,7 +66,7 @@ __device__ __forceinline__ float hcombine(float ef, float ep) {
   }
 }
 
-template <int S, int BK, int VY, int KR>
+template <int S, int BK, int VY, int KR, bool C1>
 __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   constexpr int NS = (BK + S - 1) / S;   // strips per patch
   constexpr int WL = BK - (NS - 1) * S;  // width of the last strip
@@ -80,12 +80,16 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Ybase = iy_first * S + a.lo, Xbase = ix_first * S + a.lo;
 
-  // ---- a0: the centred region x' = x - 0.5 (0 outside the image)
-  const float* img = a.imgs + size_t(f) * a.H * a.W;
-  for (int e = threadIdx.x; e < a.PL; e += blockDim.x) {
-    const int r = e / a.RWp, x = e - r * a.RWp;
+  // ---- a0: the centred region x' = x - 0.5 of every channel (0 outside the image)
+  const int nch = C1 ? 1 : a.C;
+  const size_t plane = size_t(a.H) * a.W;
+  const float* img = a.imgs + size_t(f) * nch * plane;
+  for (int e = threadIdx.x; e < nch * a.PL; e += blockDim.x) {
+    const int c = e / a.PL, e2 = e - c * a.PL;
+    const int r = e2 / a.RWp, x = e2 - r * a.RWp;
     const int yy = Ybase + r, xx = Xbase + x;
-    smf[e] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) ? __ldg(img + size_t(yy) * a.W + xx) - 0.5f : 0.f;
+    smf[e] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) ? __ldg(img + c * plane + size_t(yy) * a.W + xx) - 0.5f
+                                                           : 0.f;
   }
   __syncthreads();
 
@@ -96,29 +100,35 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const int rx = ix * S, ry = iy0 * S;
   const int rr0 = (iy0 - iy_first) * S - a.lo;  // region row of image row ry
   const int rc0 = lane * S - a.lo;              // region column of the lane's strip
-  float R[BK][S];
-#pragma unroll
-  for (int r = 0; r < BK; ++r)
-#pragma unroll
-    for (int m = 0; m < S; ++m) R[r][m] = smf[(rr0 + r) * a.RWp + rc0 + m];
-  float nr;  // ||X_i||^2 of the centred reference
-  {
-    float nf = 0.f, np = 0.f;
+  float R[BK][S];  // the lane's strip of the reference patch (one channel at a time if C > 1)
+  auto load_ref = [&](int c) {
 #pragma unroll
     for (int r = 0; r < BK; ++r)
 #pragma unroll
-      for (int m = 0; m < S; ++m) {
-        if (m < WL) np = fmaf(R[r][m], R[r][m], np);
-        nf = fmaf(R[r][m], R[r][m], nf);
-      }
+      for (int m = 0; m < S; ++m) R[r][m] = smf[c * a.PL + (rr0 + r) * a.RWp + rc0 + m];
+  };
+  float nr;  // ||X_i||^2 of the centred reference, channels summed (Eq. 12)
+  {
+    float nf = 0.f, np = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      load_ref(c);
+#pragma unroll
+      for (int r = 0; r < BK; ++r)
+#pragma unroll
+        for (int m = 0; m < S; ++m) {
+          if (m < WL) np = fmaf(R[r][m], R[r][m], np);
+          nf = fmaf(R[r][m], R[r][m], nf);
+        }
+    }
     nr = hcombine<NS, WL, S>(nf, np);
+    if (C1) load_ref(0);
   }
   RegTopK32<KR> rt;
 #pragma unroll
   for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;  // 0 sentinels
   const int rb = a.rb;
   float thr = __int_as_float(0x7f800000);  // +inf: largest d' that may still enter the top-KP
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(smf + a.PL) + warp * a.scr;
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smf + nch * a.PL) + warp * a.scr;
 
   const int b0 = (0 - a.lo) / VY;
   const int span = max(-a.lo, a.hi);
@@ -140,31 +150,41 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
 #pragma unroll
       for (int i = 0; i < VY; ++i) Tp[i] = Tr[i] = 0.f;
       float Qp[NT + 1], Qr[NT + 1];
-      Qp[0] = Qr[0] = 0.f;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        float cv[S];
+      for (int t = 0; t <= NT; ++t) Qp[t] = Qr[t] = 0.f;
+      for (int c = 0; c < nch; ++c) {
+        if (!C1) load_ref(c);
+        const float* colc = col + c * a.PL;
 #pragma unroll
-        for (int m = 0; m < S; ++m) cv[m] = col[t * a.RWp + m];
-        float qp = Qp[t], qr = Qr[t];
+        for (int t = 0; t < NT; ++t) {
+          float cv[S];
 #pragma unroll
-        for (int m = 0; m < S; ++m) {
-          if (m < WL) qp = fmaf(cv[m], cv[m], qp);
-          else qr = fmaf(cv[m], cv[m], qr);
-        }
-        Qp[t + 1] = qp;
-        Qr[t + 1] = qr;
+          for (int m = 0; m < S; ++m) cv[m] = colc[t * a.RWp + m];
+          float qp = Qp[t + 1], qr = Qr[t + 1];  // squared row sums (prefix taken below)
 #pragma unroll
-        for (int i = 0; i < VY; ++i) {
-          const int r = t - i;
-          if (r >= 0 && r < BK) {
+          for (int m = 0; m < S; ++m) {
+            if (m < WL) qp = fmaf(cv[m], cv[m], qp);
+            else qr = fmaf(cv[m], cv[m], qr);
+          }
+          Qp[t + 1] = qp;
+          Qr[t + 1] = qr;
 #pragma unroll
-            for (int m = 0; m < S; ++m) {
-              if (m < WL) Tp[i] = fmaf(R[r][m], cv[m], Tp[i]);
-              else Tr[i] = fmaf(R[r][m], cv[m], Tr[i]);
+          for (int i = 0; i < VY; ++i) {
+            const int r = t - i;
+            if (r >= 0 && r < BK) {
+#pragma unroll
+              for (int m = 0; m < S; ++m) {
+                if (m < WL) Tp[i] = fmaf(R[r][m], cv[m], Tp[i]);
+                else Tr[i] = fmaf(R[r][m], cv[m], Tr[i]);
+              }
             }
           }
         }
+      }
+#pragma unroll
+      for (int t = 1; t <= NT; ++t) {  // prefix sums over the candidate rows
+        Qp[t] += Qp[t - 1];
+        Qr[t] += Qr[t - 1];
       }
       const bool colok = unsigned(rx + dx) <= unsigned(a.W - BK);
       float dpv[VY];
@@ -226,15 +246,17 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
         const int rel = int(kk & ((1u << rb) - 1u)) - 1;
         const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
         const int cy = ry + dyy + a.lo, cx = rxj + dxx + a.lo;
-        const float* pr = img + size_t(ry) * a.W + rxj;
-        const float* pc = img + size_t(cy) * a.W + cx;
         float d = 0.f;
-        for (int l = 0; l < BK; ++l)
+        for (int c = 0; c < nch; ++c) {
+          const float* pr = img + c * plane + size_t(ry) * a.W + rxj;
+          const float* pc = img + c * plane + size_t(cy) * a.W + cx;
+          for (int l = 0; l < BK; ++l)
 #pragma unroll
-          for (int m = 0; m < BK; ++m) {
-            const float df = __ldg(pr + l * a.W + m) - __ldg(pc + l * a.W + m);
-            d = fmaf(df, df, d);
-          }
+            for (int m = 0; m < BK; ++m) {
+              const float df = __ldg(pr + l * a.W + m) - __ldg(pc + l * a.W + m);
+              d = fmaf(df, df, d);
+            }
+        }
         key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * a.W + cx);
       }
       top.merge(key, lane);
@@ -261,7 +283,7 @@ size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) {
   a->RWp = 32 * g.s + g.Wn - 1 + 1;
   a->PL = a->RH * a->RWp;
   a->scr = std::max(32 * kFVY, rx * (KR + 1));
-  return size_t(a->PL + kFWarps * a->scr) * 4;
+  return size_t(g.C * a->PL + kFWarps * a->scr) * 4;
 }
 
 // key bits of the window-relative index + 1 (values 1 .. Wn^2; 0 is the sentinel)
@@ -276,7 +298,7 @@ int boxf_kr(const Geometry& g) { return g.KP <= 32 ? 32 : g.KP <= 48 ? 48 : g.KP
 template <int S, int BK, int KR>
 cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + kFWarps - 1) / kFWarps;
-  auto k = bm_boxf_kernel<S, BK, kFVY, KR>;
+  auto k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true> : bm_boxf_kernel<S, BK, kFVY, KR, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<dim3(a.tiles_x * tiles_y, F), kFWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
@@ -285,7 +307,7 @@ cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st
 }  // namespace
 
 bool boxf_supported(const Geometry& g) {
-  if (g.dtype != SC_DTYPE_F32 || g.C != 1) return false;
+  if (g.dtype != SC_DTYPE_F32) return false;
   const bool shape = (g.s == 3 && g.b == 8) || (g.s == 1 && g.b == 7) || (g.s == 4 && g.b == 8) ||
                      (g.s == 2 && g.b == 8);
   if (!shape) return false;
@@ -293,7 +315,8 @@ bool boxf_supported(const Geometry& g) {
   if (kr == 0) return false;
   if (boxf_rel_bits(g.Wn) > 12) return false;  // keeps >= 20 distance bits in the 32-bit keys
   BoxfArgs a{};
-  return boxf_layout(g, kr, &a) <= 113 * 1024;  // 2 CTAs per SM
+  // one channel: 2 CTAs per SM; several channels (c4): the staged planes may take the whole SM
+  return boxf_layout(g, kr, &a) <= (g.C == 1 ? 113 : 227) * 1024;
 }
 
 cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
@@ -303,7 +326,7 @@ cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int i
   a.imgs = static_cast<const float*>(imgs);
   a.idx_out = idx_out;
   a.dist_out = static_cast<float*>(dist_out);
-  a.H = g.H; a.W = g.W; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
+  a.H = g.H; a.W = g.W; a.C = g.C; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   const int ns = (g.b + g.s - 1) / g.s;
   a.tiles_x = (g.nx + (33 - ns) - 1) / (33 - ns);

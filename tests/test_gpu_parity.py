@@ -450,7 +450,7 @@ def test_box_default_and_rejects_unsupported():
 
 
 # ------------------------------------------------------------------ float box-sum kernel
-def _boxf_fits(s, b, Wn, K):
+def _boxf_fits(s, b, Wn, K, C=1):
     """Mirror of boxf_supported's shared-memory / key-width rule (bm_boxf.cu)."""
     ns = -(-b // s)
     kr = 32 if K + 8 <= 32 else 48 if K + 8 <= 48 else 80 if K + 8 <= 80 else 0
@@ -460,7 +460,7 @@ def _boxf_fits(s, b, Wn, K):
     nblk = -(-Wn // 8)
     pl = (7 * s + nblk * 8 + b) * (32 * s + Wn)
     scr = max(256, (33 - ns) * (kr + 1))
-    return (pl + 8 * scr) * 4 <= 113 * 1024
+    return (C * pl + 8 * scr) * 4 <= (113 if C == 1 else 227) * 1024
 
 
 def _boxf_cases(n, seed):
@@ -473,9 +473,10 @@ def _boxf_cases(n, seed):
         W = int(rng.integers(b, 160))
         Wn = int(rng.integers(1, 64))
         K = int(rng.integers(1, 73))
-        if ((H - b) // s + 1) * ((W - b) // s + 1) * Wn * Wn > 4e7 or not _boxf_fits(s, b, Wn, K):
+        C = int(rng.choice([1, 1, 2, 4]))
+        if ((H - b) // s + 1) * ((W - b) // s + 1) * Wn * Wn * C > 4e7 or not _boxf_fits(s, b, Wn, K, C):
             continue
-        out.append((s, b, H, W, Wn, K))
+        out.append((s, b, C, H, W, Wn, K))
     return out
 
 
@@ -486,9 +487,9 @@ def _boxf(x, b, s, Wn, K, where):
 
 @pytest.mark.parametrize("case", _boxf_cases(24, 505))
 def test_boxf_random_sweep(case):
-    s, b, H, W, Wn, K = case
+    s, b, C, H, W, Wn, K = case
     rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
-    x = synth.random_image(rng, 2, 1, H, W, "f32")
+    x = synth.random_image(rng, 2, C, H, W, "f32")
     _boxf(x, b, s, Wn, K, f"boxf {case}")
 
 
@@ -510,9 +511,9 @@ def test_boxf_ties_and_extremes(kind, s, b):
 
 def test_boxf_default_and_rejects_unsupported():
     from paper_2006_13714_b200.bm import SC_KERNEL_BOXF, ScError
-    for name in ("c2", "c3"):
+    for name in ("c2", "c3", "c4"):
         assert _plan(synth.CONFIGS[name]).info()["kernel"] == SC_KERNEL_BOXF
-    for args, dt in [((64, 64, 1, 8, 5, 21, 16), "f32"), ((64, 64, 2, 8, 3, 21, 16), "f32"),
+    for args, dt in [((64, 64, 1, 8, 5, 21, 16), "f32"), ((64, 64, 8, 8, 3, 41, 32), "f32"),
                      ((64, 64, 1, 8, 3, 21, 80), "f32"), ((64, 64, 1, 8, 3, 21, 16), "u8")]:
         p = _plan(args, dt)
         with pytest.raises(ScError) as e:
@@ -520,10 +521,11 @@ def test_boxf_default_and_rejects_unsupported():
         assert e.value.code == 2
 
 
-def test_c3_warp_kernel_sampled_rows():
-    """The warp kernel stays covered on c3 now that the float box kernel is its default."""
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_warp_kernel_sampled_rows(name):
+    """The warp kernel stays covered on c3/c4 now that the float box kernel is their default."""
     from paper_2006_13714_b200.bm import SC_KERNEL_SIMT_WARP
-    cfg = synth.CONFIGS["c3"]
+    cfg = synth.CONFIGS[name]
     x = synth.make_input(cfg)
     p = _plan(cfg)
     p.set_kernel(SC_KERNEL_SIMT_WARP)
@@ -532,4 +534,4 @@ def test_c3_warp_kernel_sampled_rows():
         oi, od = oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, rows=(r0, r1))
         sl = slice(r0 * p.nx, r1 * p.nx)
         check_f32(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0, sl], gd[0, sl], oi[0], od[0],
-                  iy_range=(r0, r1), where=f"warp c3 rows {r0}:{r1}")
+                  iy_range=(r0, r1), where=f"warp {name} rows {r0}:{r1}")
