@@ -42,7 +42,8 @@ struct BoxfArgs {
   int H, W, C, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
   int RH, RWp, PL;  // staged region rows, row pitch (floats), floats per channel plane
   int nblk;         // dy blocks of VY offsets
-  int scr;          // per-warp scratch words
+  int scr;          // per-warp scratch words (survivor staging [+ output staging | + heaps])
+  int hp;           // heap pitch (words per reference) when the top-KP lives in shared heaps
   int rb;           // window-relative index bits of the 32-bit keys
 };
 
@@ -123,9 +124,22 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     nr = hcombine<NS, WL, S>(nf, np);
     if (C1) load_ref(0);
   }
-  RegTopK32<KR> rt;
+  // a4 state. KR <= 48: a sorted register list (0 sentinels in the first KR - KP slots, so the
+  // KP-th key is r[KR-1]). KR = 80: a per-reference binary max-heap of KP keys in shared memory
+  // (1-indexed, root = the KP-th key): an insertion is a ~7-level sift-down instead of a
+  // 160-instruction register network.
+  constexpr bool HEAP = KR > 48;
+  RegTopK32<HEAP ? 1 : KR> rt;
+  if constexpr (!HEAP) {
 #pragma unroll
-  for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;  // 0 sentinels
+    for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
+  }
+  // (helper lanes RX..31 never insert; they alias lane RX-1's heap for the root reads)
+  uint32_t* heap = reinterpret_cast<uint32_t*>(smf + nch * a.PL) + warp * a.scr + 32 * VY + min(lane, RX - 1) * a.hp;
+  if constexpr (HEAP) {
+    if (lane < RX)
+      for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
+  }
   const int rb = a.rb;
   float thr = __int_as_float(0x7f800000);  // +inf: largest d' that may still enter the top-KP
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smf + nch * a.PL) + warp * a.scr;
@@ -209,9 +223,25 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
           const uint32_t q = sc[32 * i] >> (rb - 1);
           const uint32_t key = bits ? (q << rb) | uint32_t(rel1 + i * a.Wn) : 0xffffffffu;
           bits &= ~(1u << i);
-          rt.insert(key);
+          if constexpr (HEAP) {
+            if (key < heap[1]) {  // replace the root, sift down (children of i: 2i, 2i+1)
+              int h = 1;
+              for (int c = 2; c <= a.KP; c = 2 * h) {
+                const uint32_t v0 = heap[c];
+                const uint32_t v1 = c + 1 <= a.KP ? heap[c + 1] : 0u;
+                const int cb = v1 > v0 ? c + 1 : c;
+                const uint32_t big = max(v0, v1);
+                if (big <= key) break;
+                heap[h] = big;
+                h = cb;
+              }
+              heap[h] = key;
+            }
+          } else {
+            rt.insert(key);
+          }
         }
-        const uint32_t kth = rt.r[KR - 1];
+        const uint32_t kth = HEAP ? heap[1] : rt.r[KR - 1];
         if (kth != 0xffffffffu) {
           // largest distance whose key can still tie the KP-th key, plus a rounding margin
           const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
@@ -222,11 +252,14 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     }
   }
 
-  // ---- a5 + a6: stage each reference's KP keys, then per reference (warp-cooperative) re-score
-  // them by direct differences from the input, sort the (distance, idx) keys and write K.
-  if (lane_ok) {
+  // ---- a5 + a6: stage each reference's KP keys (register lists; the heaps already are in shared
+  // memory), then per reference (warp-cooperative) re-score them by direct differences from the
+  // input, sort the (distance, idx) keys and write K.
+  if constexpr (!HEAP) {
+    if (lane_ok) {
 #pragma unroll
-    for (int k = 0; k < KR; ++k) scratch[lane * (KR + 1) + k] = rt.r[k];
+      for (int k = 0; k < KR; ++k) scratch[lane * (KR + 1) + k] = rt.r[k];
+    }
   }
   __syncwarp();
   const int nref = min(RX, a.nx - ix_first);
@@ -241,7 +274,9 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     for (int sl = 0; sl < NJ; ++sl) {
       const int k = sl * 32 + lane;
       uint64_t key = kKeyInf;
-      const uint32_t kk = k < KR ? scratch[j * (KR + 1) + k] : 0xffffffffu;
+      uint32_t kk;
+      if constexpr (HEAP) kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
+      else kk = k < KR ? scratch[j * (KR + 1) + k] : 0xffffffffu;
       if (kk != 0u && kk != 0xffffffffu) {
         const int rel = int(kk & ((1u << rb) - 1u)) - 1;
         const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
@@ -282,7 +317,8 @@ size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) {
   a->RH = (kFWarps - 1) * g.s + a->nblk * kFVY + g.b;
   a->RWp = 32 * g.s + g.Wn - 1 + 1;
   a->PL = a->RH * a->RWp;
-  a->scr = std::max(32 * kFVY, rx * (KR + 1));
+  a->hp = (g.KP + 1) | 1;  // heap pitch: 1-indexed heap, odd pitch
+  a->scr = KR > 48 ? 32 * kFVY + rx * a->hp : std::max(32 * kFVY, rx * (KR + 1));
   return size_t(g.C * a->PL + kFWarps * a->scr) * 4;
 }
 
