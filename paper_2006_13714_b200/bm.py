@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscbm.so")
+LIB_PATH = os.environ.get("SCBM_LIB") or os.path.join(_HERE, "libscbm.so")  # SCBM_LIB: tuning builds
 
 SC_DTYPE_U8, SC_DTYPE_F32 = 0, 1
 SC_KERNEL_SIMT, SC_KERNEL_TC_I8, SC_KERNEL_SIMT_WARP, SC_KERNEL_BOX, SC_KERNEL_BOXF = 0, 1, 2, 3, 4

@@ -57,8 +57,15 @@ struct BoxArgs {
 
 __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
 
+#ifndef SCBM_BOX_SHFL_OUT
+#define SCBM_BOX_SHFL_OUT 0  // 1: write the output rows through shuffles (no staging scratch)
+#endif
+#ifndef SCBM_BOX_MINB
+#define SCBM_BOX_MINB 2  // CTAs per SM the register allocation targets (tuning builds override)
+#endif
+
 template <int NY, int VY, int KR>
-__global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel(BoxArgs a) {
+__global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) bm_box_kernel(BoxArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
   constexpr int NR = 4 * NY + 4;   // patch rows of the lane's NY references
   constexpr int NT = NR + VY - 1;  // candidate rows per (dy block, dx)
@@ -237,6 +244,26 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
       const int pos = atomicAdd(a.fix_count, 1);
       a.fix_list[pos] = int(row0 + lane);
     }
+    const int ry = 4 * iy;
+#if SCBM_BOX_SHFL_OUT
+    // transpose through shuffles: output element e = j K + k is lane j's k-th key
+    for (int e0 = 0; e0 < nref * a.K; e0 += 32) {
+      const int e = e0 + lane;
+      const int j = min(e / a.K, 31), k = e - (e / a.K) * a.K;
+      uint32_t kk = 0u;
+#pragma unroll
+      for (int kq = 0; kq < KR; ++kq) {
+        const uint32_t v = __shfl_sync(0xffffffffu, rt[q].r[kq], j);
+        if (kq == k) kk = v;
+      }
+      if (e < nref * a.K) {
+        const int rel = key32.rel(kk);
+        const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+        a.idx_out[row0 * a.K + e] = (ry + dyy + a.lo) * a.W + (ix_first + j) * 4 + dxx + a.lo;
+        a.dist_out[row0 * a.K + e] = key32.dist(kk);
+      }
+    }
+#else
     __syncwarp();
     if (lane_ok) {
 #pragma unroll
@@ -244,7 +271,6 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
         if (k < a.K) scratch[lane * (KR + 1) + k] = rt[q].r[k];
     }
     __syncwarp();
-    const int ry = 4 * iy;
     for (int e = lane; e < nref * a.K; e += 32) {
       const int j = e / a.K, k = e - j * a.K;
       const uint32_t kk = scratch[j * (KR + 1) + k];
@@ -254,6 +280,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : 2) bm_box_kernel
       a.dist_out[row0 * a.K + e] = key32.dist(kk);
     }
     __syncwarp();
+#endif
   }
 }
 
@@ -261,10 +288,10 @@ int box_vy(const Geometry& g) { return g.Wn % 11 == 0 ? 11 : g.Wn % 7 == 0 ? 7 :
 
 size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
   a->nblk = (g.Wn + VY - 1) / VY;
-  a->RH = 4 * kBoxWarps * NY + a->nblk * VY + 4;
-  a->WP = 32 + (g.Wn + 2) / 4 + 1;
+  a->RH = 4 * kBoxWarps * NY + a->nblk * VY + 3;  // deepest candidate row read + 1
+  a->WP = 32 + (g.Wn - 1) / 4;                    // lane 31's last candidate word + 1
   a->PL = a->RH * a->WP;
-  a->scr = std::max(32 * VY, kBoxRefsX * (KR + 1));
+  a->scr = SCBM_BOX_SHFL_OUT ? 32 * VY : std::max(32 * VY, kBoxRefsX * (KR + 1));
   return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
 }
 
