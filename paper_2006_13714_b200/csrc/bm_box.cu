@@ -155,6 +155,33 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     }
     if (!any_row) continue;  // warp-uniform
     const uint32_t* cbase = sm + (rr0 + dy0) * a.WP + lane;
+    // a4 survivors of two consecutive offset groups are inserted together (fewer, fuller rounds:
+    // a round lasts as long as the busiest lane); the bits of group h sit at h*VY .. h*VY+VY-1
+    // and its distances in scratch rows q*2VY + h*VY + i
+    unsigned pend[NY];
+#pragma unroll
+    for (int q = 0; q < NY; ++q) pend[q] = 0u;
+    int half = 0, rel0p = 0;
+    auto flush = [&](int rel0c) {
+#pragma unroll
+      for (int q = 0; q < NY; ++q) {
+        unsigned bits = pend[q];
+        if (__any_sync(0xffffffffu, bits != 0u)) {
+          const uint32_t* sc = scratch + q * (64 * VY) + lane;
+          while (__any_sync(0xffffffffu, bits != 0u)) {
+            const int i = 31 - __clz(bits | 1u);  // any survivor (insertion order is irrelevant)
+            const uint32_t d = sc[32 * i];        // safe address for every lane
+            const int rel = i < VY ? rel0p + i * a.Wn : rel0c + (i - VY) * a.Wn;
+            const uint32_t key = bits ? (min(d, a.dsat) << a.rb) | uint32_t(rel) : 0xffffffffu;
+            bits &= ~(1u << i);
+            rt[q].insert(key);
+          }
+          thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
+          __syncwarp();
+        }
+        pend[q] = 0u;
+      }
+    };
     for (int kx = 0; kx <= 2 * span; ++kx) {
       const int dx = centre_out(kx);
       if (dx < a.lo || dx > a.hi) continue;
@@ -208,26 +235,25 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           t[i] = thr[q] - e - __shfl_down_sync(0xffffffffu, e, 1);
           fails = (fails << 1) + (uint32_t(t[i]) >> 31);
         }
-        unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);
+        const unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);
         if (__any_sync(0xffffffffu, bits != 0u)) {
-          // a4 survivors: one insertion per lane per round into the register top-K
-          uint32_t* sc = scratch + lane;
+          uint32_t* sc = scratch + q * (64 * VY) + half * (32 * VY) + lane;
           const int dthr = thr[q] + nr[q];  // d = d' + ||X_i||^2 = dthr - t (exact, >= 0)
 #pragma unroll
           for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(dthr - t[i]);
-          const int rel0 = (dy0 - a.lo) * a.Wn + off;
-          while (__any_sync(0xffffffffu, bits != 0u)) {
-            const int i = 31 - __clz(bits | 1u);  // any survivor (insertion order is irrelevant)
-            const uint32_t d = sc[32 * i];        // safe address for every lane
-            const uint32_t key = bits ? (min(d, a.dsat) << a.rb) | uint32_t(rel0 + i * a.Wn) : 0xffffffffu;
-            bits &= ~(1u << i);
-            rt[q].insert(key);
-          }
-          thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
-          __syncwarp();
+          pend[q] |= bits << (half * VY);
         }
       }
+      const int rel0 = (dy0 - a.lo) * a.Wn + off;
+      if (half == 0) {
+        rel0p = rel0;
+        half = 1;
+      } else {
+        flush(rel0);
+        half = 0;
+      }
     }
+    if (half == 1) flush(0);  // a lone last group (its bits are in the first half)
   }
 
   // ---- a6: exact references -> staged rows of K keys -> coalesced (idx, dist) stores;
@@ -291,7 +317,7 @@ size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
   a->RH = 4 * kBoxWarps * NY + a->nblk * VY + 3;  // deepest candidate row read + 1
   a->WP = 32 + (g.Wn - 1) / 4;                    // lane 31's last candidate word + 1
   a->PL = a->RH * a->WP;
-  a->scr = SCBM_BOX_SHFL_OUT ? 32 * VY : std::max(32 * VY, kBoxRefsX * (KR + 1));
+  a->scr = std::max(64 * VY * NY, SCBM_BOX_SHFL_OUT ? 0 : kBoxRefsX * (KR + 1));
   return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
 }
 

@@ -210,6 +210,8 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   if (e == cudaSuccess)
     p->ws.norm = static_cast<char*>(p->ws.norm_base) + (size_t(g.NPAD) * g.Mxp + g.NPAD) * 4;
   if (e == cudaSuccess) e = cudaMalloc(&p->ws.fix_count, sizeof(int));
+  // box matchers: up to 64 frames per launch, the fix-up list capped at 16 M entries
+  p->FB = int(std::max<int64_t>(1, std::min<int64_t>(64, (int64_t(16) << 20) / (int64_t(g.ny) * g.nx))));
   if (e == cudaSuccess)
     e = cudaMalloc(&p->ws.fix_list, size_t(g.ny) * g.nx * sizeof(int) * std::max(p->F, p->FB));
   if (e == cudaSuccess) e = cudaMemset(p->ws.fix_count, 0, sizeof(int));

@@ -63,7 +63,7 @@ struct sc_bm_plan_s {
   int sm_count = 148;
   int kernel = SC_KERNEL_SIMT;
   int F = 1;  // frames per chunk (norm-map matchers: the chunk's norm workspace stays in L2)
-  int FB = 16;  // frames per launch of the box-sum matcher (no workspace; big grids, few tails)
+  int FB = 64;  // frames per launch of the box-sum matchers (no workspace: one big grid, one tail)
   int nbands = 1;
   scbm::Workspace ws;
   scbm::TileCfg tile;
