@@ -162,6 +162,52 @@ def _config_obj(cfg, args):
             "l2": "flushed between timed steps (256 MiB write); working set > L2"}
 
 
+def bench_group(args, cfg, plan, x, idx, ws, rank, local, dist):
+    """Patch grouping Y_i of the run's idx table: gathered bytes/s vs HBM."""
+    import torch
+    info = plan.info()
+    n = x.shape[0]
+    Y = torch.empty((n, info["n_refs"], cfg.K, cfg.C, cfg.b, cfg.b), dtype=x.dtype, device=x.device)
+    for _ in range(args.warmup):
+        plan.group(x, idx, out=Y)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = plan.info()["launches"]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            starts[k].record(stream)
+            plan.group(x, idx, out=Y)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    ms = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    out_bytes = Y.numel() * Y.element_size()
+    in_bytes = x.numel() * x.element_size() + idx.numel() * 4
+    alg = out_bytes + in_bytes  # algorithmic bytes: every group byte written once, inputs read once
+    peaks = _peaks()
+    gbs = alg / (ms / 1e3) / 1e9
+    if rank == 0:
+        line = {"metric": "patch-group bytes/sec", "op": "group", "value": alg * ws / (ms / 1e3), "unit": "B/s",
+                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+                "data": "synthetic", "config": _config_obj(cfg, args),
+                "groups_per_s": n * ws * info["n_refs"] / (ms / 1e3),
+                "roofline": {"bound": "hbm", "kernel": "group_kernel", "achieved": gbs, "peak": peaks["hbm_gbs"],
+                             "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"], "traffic": None,
+                             "algorithmic_bytes_per_launch": alg},
+                "gpu_launches": int(plan.info()["launches"] - launches0), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -173,6 +219,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL all-gather of the tables")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--op", default="bm", choices=["bm", "group"],
+                    help="bm: the block-matching hot path (default); group: patch grouping Y_i of its output")
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf"],
                     help="force the matching kernel (default: the plan's choice)")
     args = ap.parse_args()
@@ -215,6 +263,8 @@ def main():
     for _ in range(args.warmup):
         plan.run(x, out=(idx, dst))
     torch.cuda.synchronize()
+    if args.op == "group":
+        return bench_group(args, cfg, plan, x, idx, ws, rank, local, dist)
 
     plan.set_timing(True)
     plan.get_timing()

@@ -132,6 +132,20 @@ sc_status_t sc_bm_run_rows(sc_bm_plan_t plan, const void* imgs, int64_t n_images
 sc_status_t sc_bm_run_host(sc_bm_plan_t plan, const void* h_imgs, int64_t n_images,
                            int32_t* h_idx_out, void* h_dist_out, sc_stream_t stream);
 
+/*
+ * Patch grouping (the step after block matching): Y_i = [y_{S_i(1)}, ..., y_{S_i(K)}]
+ * (footnote PAPER.md:548). For every reference i of the n_images images and
+ * each of its K matches (idx: the idx_out of a run on the same images, [n][n_refs][K] int32),
+ * copy the matched b x b x C patch of imgs into
+ *     groups_out [n_images][n_refs][K][C][b][b]   (input dtype, uncentred; column k of Y_i is
+ *                                                 the channel-major vectorisation of patch k)
+ * idx = -1 (fewer than K candidates) gives a zero column. Device pointers: imgs and groups_out
+ * 16-byte aligned, idx 4-byte aligned; idx entries must be valid indices from a run of this plan
+ * (not checked on the device). Asynchronous on `stream`, never allocates.
+ */
+sc_status_t sc_bm_group(sc_bm_plan_t plan, const void* imgs, int64_t n_images, const int32_t* idx,
+                        void* groups_out, sc_stream_t stream);
+
 /* Plan geometry and bookkeeping. */
 sc_status_t sc_bm_plan_info(sc_bm_plan_t plan, sc_bm_info_t* info);
 

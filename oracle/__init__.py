@@ -156,5 +156,29 @@ def pair_dist(img: np.ndarray, b: int, ry, rx, cy, cx) -> np.ndarray:
     return out
 
 
+def group(img: np.ndarray, idx: np.ndarray, b: int) -> np.ndarray:
+    """Patch groups Y_i = [y_S(1), ..., y_S(K)] (footnote PAPER.md:548).
+
+    img [N, C, H, W], idx [N, refs, K] (pixel-raster index of each match's top-left, -1 = none)
+    -> [N, refs, K, C, b, b] in img's dtype: column k of Y_i is the full-depth b x b x C patch at
+    idx (channel-major vectorisation, reading R13); -1 gives a zero column. Plain
+    loops over the definition (use on small or sampled tables).
+    """
+    a = np.asarray(img)
+    if a.ndim == 3:
+        a = a[None]
+    N, C, H, W = a.shape
+    out = np.zeros(tuple(idx.shape) + (C, b, b), dtype=a.dtype)
+    for n in range(idx.shape[0]):
+        for r in range(idx.shape[1]):
+            for k in range(idx.shape[2]):
+                j = int(idx[n, r, k])
+                if j < 0:
+                    continue
+                cy, cx = divmod(j, W)
+                out[n, r, k] = a[n, :, cy:cy + b, cx:cx + b]
+    return out
+
+
 def num_threads() -> int:
     return int(lib().sco_num_threads())

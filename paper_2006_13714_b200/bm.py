@@ -21,7 +21,7 @@ STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_UNSUPPORTED",
 
 EXPORTED = ["sc_bm_plan", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
-            "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing"]
+            "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group"]
 
 
 class ScError(RuntimeError):
@@ -74,6 +74,7 @@ def load_library():
     L.sc_bm_run_dense_debug.argtypes = [vp, vp, vp, vp]
     L.sc_bm_set_timing.argtypes = [vp, i32]
     L.sc_bm_get_timing.argtypes = [vp, ctypes.POINTER(Timing)]
+    L.sc_bm_group.argtypes = [vp, vp, i64, vp, vp, vp]
     for fn in EXPORTED:
         if fn != "sc_status_string":
             getattr(L, fn).restype = ci
@@ -194,6 +195,21 @@ class Plan:
             self._h, ctypes.c_void_p(t.data_ptr()), n, ctypes.c_void_p(idx.data_ptr()),
             ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
         return idx, dist
+
+    def group(self, imgs, idx, out=None, stream=None):
+        """Patch groups Y_i of a run's idx table: [N, n_refs, K, C, b, b] (input dtype)."""
+        import torch
+        imgs = self._check_img(imgs)
+        n = imgs.shape[0]
+        if idx.dtype != torch.int32 or not idx.is_cuda or not idx.is_contiguous() or \
+                tuple(idx.shape) != (n, self.n_refs, self.K):
+            raise ValueError("idx must be the contiguous CUDA int32 [N, n_refs, K] table of a run")
+        if out is None:
+            out = torch.empty((n, self.n_refs, self.K, self.C, self.b, self.b), dtype=imgs.dtype, device=imgs.device)
+        _check("sc_bm_group", self._lib.sc_bm_group(
+            self._h, ctypes.c_void_p(imgs.data_ptr()), n, ctypes.c_void_p(idx.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
 
     # ------------------------------------------------------------------ test exports
     def norm_map(self, img, stream=None):

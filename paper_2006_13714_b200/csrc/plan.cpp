@@ -331,6 +331,19 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
   return cuda_status(e);
 }
 
+sc_status_t sc_bm_group(sc_bm_plan_t p, const void* imgs, int64_t n_images, const int32_t* idx,
+                        void* groups_out, sc_stream_t stream) {
+  if (!p || !imgs || !idx || !groups_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0 || (reinterpret_cast<uintptr_t>(groups_out) & 15) != 0 ||
+      (reinterpret_cast<uintptr_t>(idx) & 3) != 0)
+    return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  if (n_images == 0) return SC_OK;
+  return cuda_status(launch_group(*p, imgs, n_images, idx, groups_out, reinterpret_cast<cudaStream_t>(stream),
+                                  &p->launches));
+}
+
 sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
   if (!p || !info) return SC_ERR_INVALID_ARGUMENT;
   std::memset(info, 0, sizeof(*info));

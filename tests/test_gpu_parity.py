@@ -536,3 +536,41 @@ def test_warp_kernel_sampled_rows(name):
         sl = slice(r0 * p.nx, r1 * p.nx)
         check_f32(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0, sl], gd[0, sl], oi[0], od[0],
                   iy_range=(r0, r1), where=f"warp {name} rows {r0}:{r1}")
+
+
+# ------------------------------------------------------------------ patch grouping Y_i
+@pytest.mark.parametrize("dtype,C,H,W,b,s,Wn,K", [("u8", 1, 64, 64, 8, 4, 21, 16), ("f32", 2, 37, 45, 7, 2, 11, 9),
+                                                   ("u8", 3, 30, 41, 5, 3, 9, 12), ("f32", 1, 40, 40, 8, 3, 39, 30)])
+def test_group_matches_oracle(dtype, C, H, W, b, s, Wn, K):
+    rng = np.random.Generator(np.random.PCG64(H * W + K))
+    x = synth.random_image(rng, 2, C, H, W, dtype)
+    p = _plan((H, W, C, b, s, Wn, K), dtype)
+    t = torch.from_numpy(x).cuda()
+    idx, _ = p.run(t)
+    if Wn * Wn < K:  # exercise the -1 padding path explicitly
+        assert (idx == -1).any()
+    Y = p.group(t, idx)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(Y.cpu().numpy(), oracle.group(x, idx.cpu().numpy(), b))
+
+
+def test_group_padding_and_c5_sample():
+    # K > window candidates: -1 entries -> zero columns
+    rng = np.random.Generator(np.random.PCG64(3))
+    x = synth.random_image(rng, 1, 1, 20, 24, "u8")
+    p = _plan((20, 24, 1, 4, 2, 3, 12), "u8")
+    t = torch.from_numpy(x).cuda()
+    idx, _ = p.run(t)
+    assert (idx == -1).any()
+    np.testing.assert_array_equal(p.group(t, idx).cpu().numpy(), oracle.group(x, idx.cpu().numpy(), 4))
+    # c5 (bench configuration, 64 frames in one call): sampled references of frames 0 and 63
+    cfg = synth.CONFIGS["c5"]
+    xs = synth.make_input(cfg)
+    p = _plan(cfg)
+    t = torch.from_numpy(xs).cuda()
+    idx, _ = p.run(t)
+    Y = p.group(t, idx)
+    sel = np.random.Generator(np.random.PCG64(5)).choice(p.n_refs, 300, replace=False)
+    for f in (0, 63):
+        ii = idx[f:f + 1, sel].cpu().numpy()
+        np.testing.assert_array_equal(Y[f:f + 1, sel].cpu().numpy(), oracle.group(xs[f:f + 1], ii, cfg.b))

@@ -16,6 +16,7 @@ import numpy as np
 import pytest
 
 import oracle
+from paper_2006_13714_b200 import synth
 from tests.bm_numpy import bm_np
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "worked_3x3.json")
@@ -307,3 +308,35 @@ def test_pair_dist_matches_dense():
     R, Cc = np.array(R), np.array(Cc)
     out = oracle.pair_dist(img, b, R[:, 0], R[:, 1], Cc[:, 0], Cc[:, 1])
     np.testing.assert_array_equal(out, np.array(V))
+
+
+# ---------------------------------------------------------------- patch grouping Y_i
+def test_group_worked_example():
+    """Y_i of the hand-worked 3x3 example: K = 3 matches of ref (0,0) are positions (0,0), (0,1),
+    (1,0) (tests/golden/worked_3x3.json), so the group's columns are those 2x2 patches."""
+    g = json.load(open(GOLD))
+    img = np.array(g["image"], dtype=np.uint8)
+    idx, _ = oracle.bm(img, 2, 2, 3, 3)
+    Y = oracle.group(img[None, None], idx, 2)
+    assert Y.shape == (1, 1, 3, 1, 2, 2)
+    np.testing.assert_array_equal(Y[0, 0, :, 0], [[[1, 2], [4, 5]], [[2, 3], [5, 6]], [[4, 5], [7, 8]]])
+    Y5 = oracle.group(img[None, None], oracle.bm(img, 2, 2, 3, 5)[0], 2)  # 4 candidates: last column 0
+    assert (Y5[0, 0, 4] == 0).all() and (Y5[0, 0, 3, 0] == [[5, 6], [8, 9]]).all()
+
+
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_group_column_norms_and_self_first(dtype):
+    """column j's squared norm = the norm map at S(j); on data without exact
+    duplicates the first column is the reference patch itself (footnote PAPER.md:548)."""
+    rng = _rng(77)
+    x = synth.random_image(rng, 1, 2, 26, 31, dtype)
+    b, s, Wn, K = 5, 3, 9, 6
+    idx, _ = oracle.bm(x, b, s, Wn, K)
+    Y = oracle.group(x, idx, b).astype(np.float64)
+    nm = oracle.norm_map(x[0], b)
+    W = x.shape[3]
+    np.testing.assert_allclose((Y ** 2).sum(axis=(3, 4, 5)), nm[idx // W, idx % W], rtol=1e-12)
+    ny, nx = oracle.grid(26, 31, b, s)
+    for r in range(ny * nx):
+        ry, rx = (r // nx) * s, (r % nx) * s
+        np.testing.assert_array_equal(Y[0, r, 0], x[0, :, ry:ry + b, rx:rx + b])
