@@ -159,6 +159,7 @@ def _config_obj(cfg, args):
     return {"workload": cfg.name, "images": cfg.N, "channels": cfg.C, "H": cfg.H, "W": cfg.W,
             "input_dtype": "u8" if cfg.dtype == "u8" else "f32", "patch": cfg.b, "stride": cfg.s,
             "window": cfg.Wn, "K": cfg.K, "sharding": "frames" if cfg.N > 1 else "replicas",
+            "similarity": getattr(args, "metric", "l2"),
             "l2": "flushed between timed steps (256 MiB write); working set > L2"}
 
 
@@ -219,6 +220,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL all-gather of the tables")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--metric", default="l2", choices=["l2", "ncc"],
+                    help="l2: Euclidean BM, Eq. 3 (the headline); ncc: normalised cross-correlation, Eq. 4")
     ap.add_argument("--op", default="bm", choices=["bm", "group"],
                     help="bm: the block-matching hot path (default); group: patch grouping Y_i of its output")
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf"],
@@ -252,7 +255,7 @@ def main():
     x_host = np.ascontiguousarray(x_all[f0:f0 + nloc])
     del x_all
     x = torch.from_numpy(x_host).cuda()
-    plan = Plan(cfg.H, cfg.W, cfg.C, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype)
+    plan = Plan(cfg.H, cfg.W, cfg.C, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype, metric=args.metric)
     if args.kernel != "auto":
         plan.set_kernel({"simt": 0, "tc": 1, "warp": 2, "box": 3, "boxf": 4}[args.kernel])
     info = plan.info()
@@ -356,7 +359,7 @@ def main():
         xh = torch.from_numpy(x_host).pin_memory()
         hi = torch.empty((nloc, info["n_refs"], cfg.K), dtype=torch.int32).pin_memory()
         hd = torch.empty((nloc, info["n_refs"], cfg.K),
-                         dtype=torch.int32 if cfg.dtype == "u8" else torch.float32).pin_memory()
+                         dtype=torch.int32 if (cfg.dtype == "u8" and args.metric == "l2") else torch.float32).pin_memory()
         plan.run_host(xh, out=(hi, hd))
         e_steps = max(3, min(args.steps, 5))
         if dist:
@@ -401,7 +404,7 @@ def main():
                 "ref_patches_per_s": refs_step / (ms / 1e3), "candidate_pairs_per_step": pairs_step,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "gather": gather,
-                "kernel": info["kernel"], "frames_per_chunk": info["frames_per_chunk"]}
+                "kernel": info["kernel"], "frames_per_chunk": info["frames_per_chunk"], "metric_kind": args.metric}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -65,6 +65,12 @@ typedef struct CUstream_st* sc_stream_t; /* == cudaStream_t; NULL = legacy defau
 
 typedef enum { SC_DTYPE_U8 = 0, SC_DTYPE_F32 = 1 } sc_dtype_t;
 
+/* Similarity metric: SC_METRIC_L2 = squared Euclidean distance (Eq. 3, the default);
+ * SC_METRIC_NCC = normalised cross-correlation (Eq. 4, Lemma 1) on
+ * the raw values: the K LARGEST NCC = C_i(j) / (||X_i|| ||X_j||) per window, NCC := 0 when a
+ * norm is 0; dist_out holds d_NCC = -NCC as float32 for both dtypes; uint8 orderings are exact. */
+typedef enum { SC_METRIC_L2 = 0, SC_METRIC_NCC = 1 } sc_metric_t;
+
 typedef enum {
     SC_OK = 0,
     SC_ERR_INVALID_ARGUMENT = 1, /* null pointer, misaligned pointer, parameter out of range */
@@ -103,6 +109,11 @@ typedef struct {
  */
 sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K,
                        sc_dtype_t dtype, sc_bm_plan_t* plan_out);
+
+/* Same with an explicit metric. SC_METRIC_NCC runs on the float box-sum kernel: it needs
+ * (stride, b) in {(3,8), (1,7), (4,8), (2,8)} and K <= 24 (else SC_ERR_UNSUPPORTED). */
+sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, int K,
+                          sc_dtype_t dtype, sc_metric_t metric, sc_bm_plan_t* plan_out);
 
 /* One image [C][H][W] -> idx_out / dist_out [n_refs][K]. Device pointers; img 16-B aligned. */
 sc_status_t sc_bm_run(sc_bm_plan_t plan, const void* img, int32_t* idx_out, void* dist_out,

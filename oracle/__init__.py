@@ -48,6 +48,7 @@ def lib():
         L.sco_selfconv.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, dp]
         L.sco_pair_dist.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
         L.sco_num_threads.restype = ci
+        L.sco_ncc_rows.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, dp, ci]
         _lib = L
     return _lib
 
@@ -92,6 +93,31 @@ def bm(img: np.ndarray, b: int, s: int, Wn: int, K: int, *, images=None, rows=No
                            dist.ctypes.data, nthreads)
     if rc != 0:
         raise ValueError("oracle.bm: invalid arguments")
+    return idx, dist
+
+
+def ncc(img: np.ndarray, b: int, s: int, Wn: int, K: int, *, images=None, rows=None,
+        nthreads: int = 0):
+    """NCC block matching (Eq. 4): the K largest normalised cross-correlations
+    of raw values per reference window. Returns (idx int32, dist float64 = d_NCC = -NCC)
+    [n, refs, K]; exact integer ordering for uint8 input (see oracle.c sco_ncc_rows)."""
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None, None]
+    elif a.ndim == 3:
+        a = a[None]
+    N, C, H, W = a.shape
+    ny, nx = grid(H, W, b, s)
+    i0, i1 = images if images is not None else (0, N)
+    r0, r1 = rows if rows is not None else (0, ny)
+    n, refs = i1 - i0, (r1 - r0) * nx
+    idx = np.empty((n, refs, K), dtype=np.int32)
+    dist = np.empty((n, refs, K), dtype=np.float64)
+    rc = lib().sco_ncc_rows(a.ctypes.data, _dtype_code(a), C, H, W, b, s, Wn, K, i0, i1, r0, r1,
+                            idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                            dist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), nthreads)
+    if rc != 0:
+        raise ValueError("oracle.ncc: invalid arguments")
     return idx, dist
 
 

@@ -272,6 +272,121 @@ int sco_pair_dist(const void* img, int dtype, int C, int H, int W, int b, long l
     return 0;
 }
 
+/*
+ * NCC block matching (the "next" row): Eq. 4,
+ *   S_i = argmin_{|S| <= K} sum_{j in S} d_NCC(X_j, X_i),
+ *   d_NCC(X_j, X_i) = - vec(X_j)^T vec(X_i) / (||X_j||_F ||X_i||_F)
+ * on the RAW (uncentred, "non-negative natural image") values, channels summed jointly, over
+ * the same clipped window, i.e. the K LARGEST normalised cross-correlations. Readings
+ * (R14-R16): NCC := 0 when ||X_j|| ||X_i|| = 0; ties by (d_NCC, idx).
+ * Ordering is EXACT for uint8 input: NCC_a > NCC_b is decided on integers, comparing
+ * C_a |C_a| n_b with C_b |C_b| n_a in 128-bit arithmetic (n = squared norms); double for
+ * float input. dist_out = d_NCC = -NCC (double), idx -1 / +inf for missing candidates.
+ */
+typedef struct {
+    int64_t c, n;  /* exact cross term / candidate squared norm (u8) */
+    double f;      /* NCC (float input, and the reported value) */
+    int32_t idx;
+} sco_nkey;
+
+static int cmp_ncc_int(const void* a, const void* b) {
+    const sco_nkey* x = (const sco_nkey*)a;
+    const sco_nkey* y = (const sco_nkey*)b;
+    /* larger NCC first: sign(c) c^2 / n, cross-multiplied (n > 0 here: zero norms map to c=0, n=1) */
+    const __int128 lx = (__int128)(x->c < 0 ? -x->c : x->c) * x->c * y->n;
+    const __int128 ly = (__int128)(y->c < 0 ? -y->c : y->c) * y->c * x->n;
+    if (lx != ly) return lx > ly ? -1 : 1;
+    return (x->idx > y->idx) - (x->idx < y->idx);
+}
+
+static int cmp_ncc_dbl(const void* a, const void* b) {
+    const sco_nkey* x = (const sco_nkey*)a;
+    const sco_nkey* y = (const sco_nkey*)b;
+    if (x->f != y->f) return x->f > y->f ? -1 : 1;
+    return (x->idx > y->idx) - (x->idx < y->idx);
+}
+
+int sco_ncc_rows(const void* imgs, int dtype, int C, int H, int W, int b, int s, int Wn, int K,
+                 int img_begin, int img_end, int iy_begin, int iy_end,
+                 int32_t* idx_out, double* dist_out, int nthreads) {
+    if (!imgs || !idx_out || !dist_out || b < 1 || s < 1 || Wn < 1 || K < 1 || C < 1 ||
+        H < b || W < b || img_end < img_begin)
+        return -1;
+    const int ny = grid_n(H, b, s), nx = grid_n(W, b, s);
+    if (iy_begin < 0 || iy_end > ny || iy_end < iy_begin) return -1;
+    const int lo = -(Wn / 2), hi = Wn - 1 - Wn / 2;
+    const long long refs_per_img = (long long)(iy_end - iy_begin) * nx;
+    const long long total = refs_per_img * (img_end - img_begin);
+    const size_t img_elems = (size_t)C * H * W;
+    const size_t esz = dtype == SCO_U8 ? 1 : dtype == SCO_F32 ? 4 : 8;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel
+    {
+        sco_nkey* keys = (sco_nkey*)malloc(sizeof(sco_nkey) * (size_t)Wn * (size_t)Wn);
+#pragma omp for schedule(dynamic, 16)
+        for (long long t = 0; t < total; ++t) {
+            const int n = img_begin + (int)(t / refs_per_img);
+            const long long j = t % refs_per_img;
+            const int ry = (iy_begin + (int)(j / nx)) * s, rx = (int)(j % nx) * s;
+            const void* img = (const char*)imgs + (size_t)n * img_elems * esz;
+            const int cy0 = ry + lo < 0 ? 0 : ry + lo, cy1 = ry + hi > H - b ? H - b : ry + hi;
+            const int cx0 = rx + lo < 0 ? 0 : rx + lo, cx1 = rx + hi > W - b ? W - b : rx + hi;
+            /* reference squared norm */
+            int64_t nri = 0;
+            double nrd = 0.0;
+            for (int c = 0; c < C; ++c)
+                for (int l = 0; l < b; ++l)
+                    for (int m = 0; m < b; ++m) {
+                        const double v = px(img, dtype, (size_t)c * H * W + (size_t)(ry + l) * W + rx + m);
+                        nrd += v * v;
+                        nri += (int64_t)v * (int64_t)v;
+                    }
+            int cnt = 0;
+            for (int cy = cy0; cy <= cy1; ++cy)
+                for (int cx = cx0; cx <= cx1; ++cx) {
+                    int64_t ci = 0, nci = 0;
+                    double cd = 0.0, ncd = 0.0;
+                    for (int c = 0; c < C; ++c)
+                        for (int l = 0; l < b; ++l)
+                            for (int m = 0; m < b; ++m) {
+                                const size_t base = (size_t)c * H * W;
+                                const double vr = px(img, dtype, base + (size_t)(ry + l) * W + rx + m);
+                                const double vc = px(img, dtype, base + (size_t)(cy + l) * W + cx + m);
+                                cd += vr * vc;
+                                ncd += vc * vc;
+                                if (dtype == SCO_U8) {
+                                    ci += (int64_t)vr * (int64_t)vc;
+                                    nci += (int64_t)vc * (int64_t)vc;
+                                }
+                            }
+                    sco_nkey* k = &keys[cnt++];
+                    k->idx = cy * W + cx;
+                    const double den = sqrt(nrd * ncd);
+                    k->f = den > 0.0 ? cd / den : 0.0;
+                    if (nri == 0 || nci == 0) {  /* NCC := 0 */
+                        k->c = 0;
+                        k->n = 1;
+                    } else {
+                        k->c = ci;
+                        k->n = nci;
+                    }
+                }
+            qsort(keys, (size_t)cnt, sizeof(sco_nkey), dtype == SCO_U8 ? cmp_ncc_int : cmp_ncc_dbl);
+            const long long o = t * K;
+            for (int k = 0; k < K; ++k) {
+                idx_out[o + k] = k < cnt ? keys[k].idx : -1;
+                dist_out[o + k] = k < cnt ? -keys[k].f : INFINITY;
+            }
+        }
+        free(keys);
+    }
+    return 0;
+}
+
 int sco_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

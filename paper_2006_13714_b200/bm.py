@@ -19,7 +19,8 @@ SC_KERNEL_SIMT, SC_KERNEL_TC_I8, SC_KERNEL_SIMT_WARP, SC_KERNEL_BOX, SC_KERNEL_B
 STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_UNSUPPORTED",
           3: "SC_ERR_OUT_OF_MEMORY", 4: "SC_ERR_CUDA", 5: "SC_ERR_WRONG_DEVICE"}
 
-EXPORTED = ["sc_bm_plan", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
+SC_METRIC_L2, SC_METRIC_NCC = 0, 1
+EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
             "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group"]
 
@@ -61,6 +62,7 @@ def load_library():
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     ci = ctypes.c_int
     L.sc_bm_plan.argtypes = [ci, ci, ci, ci, ci, ci, ci, ci, ctypes.POINTER(vp)]
+    L.sc_bm_plan_ex.argtypes = [ci, ci, ci, ci, ci, ci, ci, ci, ci, ctypes.POINTER(vp)]
     L.sc_bm_run.argtypes = [vp, vp, vp, vp, vp]
     L.sc_bm_run_batch.argtypes = [vp, vp, i64, vp, vp, vp]
     L.sc_bm_run_rows.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp]
@@ -101,13 +103,14 @@ class Plan:
     tensors on the plan's device, contiguous.
     """
 
-    def __init__(self, H, W, C, b, stride, window, K, dtype="u8"):
+    def __init__(self, H, W, C, b, stride, window, K, dtype="u8", metric="l2"):
         self._lib = load_library()
         self.H, self.W, self.C, self.b, self.s, self.Wn, self.K = H, W, C, b, stride, window, K
-        self.dtype = dtype
+        self.dtype, self.metric = dtype, metric
         code = {"u8": SC_DTYPE_U8, "f32": SC_DTYPE_F32}[dtype]
+        mcode = {"l2": SC_METRIC_L2, "ncc": SC_METRIC_NCC}[metric]
         h = ctypes.c_void_p()
-        _check("sc_bm_plan", self._lib.sc_bm_plan(H, W, C, b, stride, window, K, code, ctypes.byref(h)))
+        _check("sc_bm_plan_ex", self._lib.sc_bm_plan_ex(H, W, C, b, stride, window, K, code, mcode, ctypes.byref(h)))
         self._h = h
         inf = self.info()
         self.ny, self.nx, self.n_refs = inf["n_ref_y"], inf["n_ref_x"], inf["n_refs"]
@@ -138,6 +141,10 @@ class Plan:
     def set_kernel(self, kernel: int):
         _check("sc_bm_set_kernel", self._lib.sc_bm_set_kernel(self._h, kernel))
 
+    def _dist_dtype(self):
+        import torch
+        return torch.int32 if (self.dtype == "u8" and self.metric == "l2") else torch.float32
+
     # ------------------------------------------------------------------ device paths
     def _check_img(self, imgs):
         import torch
@@ -155,8 +162,7 @@ class Plan:
         refs = self.n_refs if rows is None else (rows[1] - rows[0]) * self.nx
         dev = torch.device("cuda", torch.cuda.current_device())
         idx = torch.empty((n_images, refs, self.K), dtype=torch.int32, device=dev)
-        dist = torch.empty((n_images, refs, self.K),
-                           dtype=torch.int32 if self.dtype == "u8" else torch.float32, device=dev)
+        dist = torch.empty((n_images, refs, self.K), dtype=self._dist_dtype(), device=dev)
         return idx, dist
 
     def run(self, imgs, out=None, stream=None):
@@ -188,7 +194,7 @@ class Plan:
         n = t.shape[0]
         if out is None:
             idx = torch.empty((n, self.n_refs, self.K), dtype=torch.int32)
-            dist = torch.empty((n, self.n_refs, self.K), dtype=torch.int32 if self.dtype == "u8" else torch.float32)
+            dist = torch.empty((n, self.n_refs, self.K), dtype=self._dist_dtype())
         else:
             idx, dist = out
         _check("sc_bm_run_host", self._lib.sc_bm_run_host(

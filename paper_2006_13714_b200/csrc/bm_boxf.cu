@@ -36,9 +36,9 @@ namespace {
 constexpr int kFWarps = 8;
 
 struct BoxfArgs {
-  const float* imgs;  // [F][C][H][W]
+  const void* imgs;   // [F][C][H][W] float (or uint8 for the NCC metric)
   int32_t* idx_out;   // [F][band refs][K]
-  float* dist_out;
+  float* dist_out;    // L2: d; NCC: d_NCC = -NCC
   int H, W, C, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
   int RH, RWp, PL;  // staged region rows, row pitch (floats), floats per channel plane
   int nblk;         // dy blocks of VY offsets
@@ -67,7 +67,51 @@ __device__ __forceinline__ float hcombine(float ef, float ep) {
   }
 }
 
-template <int S, int BK, int VY, int KR, bool C1>
+// One candidate of the NCC re-rank (a5 for the NCC metric): exact integer cross term / squared
+// norm for uint8 input (compared by cross-multiplication in 128 bits), double NCC for float.
+struct NccItem {
+  long long c, n;  // uint8: C, ||X_c||^2 (NCC := 0 for zero norms: c = 0, n = 1)
+  double f;        // NCC value (float input: the comparison key)
+  int idx;         // -1: empty slot (sorts last)
+};
+template <bool EXACT>
+__device__ __forceinline__ bool ncc_better(const NccItem& x, const NccItem& y) {
+  if (x.idx < 0 || y.idx < 0) return y.idx < 0 && x.idx >= 0;
+  if constexpr (EXACT) {
+    const __int128 lx = (__int128)(x.c < 0 ? -x.c : x.c) * x.c * y.n;
+    const __int128 ly = (__int128)(y.c < 0 ? -y.c : y.c) * y.c * x.n;
+    if (lx != ly) return lx > ly;
+  } else {
+    if (x.f != y.f) return x.f > y.f;
+  }
+  return x.idx < y.idx;
+}
+__device__ __forceinline__ NccItem shfl_item(const NccItem& v, int src_lane_xor) {
+  NccItem o;
+  o.c = __shfl_xor_sync(0xffffffffu, v.c, src_lane_xor);
+  o.n = __shfl_xor_sync(0xffffffffu, v.n, src_lane_xor);
+  o.f = __shfl_xor_sync(0xffffffffu, v.f, src_lane_xor);
+  o.idx = __shfl_xor_sync(0xffffffffu, v.idx, src_lane_xor);
+  return o;
+}
+// warp bitonic sort, best first, one item per lane
+template <bool EXACT>
+__device__ NccItem warp_sort_ncc(NccItem x, int lane) {
+#pragma unroll 1
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const NccItem p = shfl_item(x, j);
+      const bool lower = (lane & j) == 0, up = (lane & k) == 0;
+      const bool p_better = ncc_better<EXACT>(p, x);
+      // ascending (best first) when up: the lower lane keeps the better item
+      if ((lower == up) ? p_better : !p_better && ncc_better<EXACT>(x, p)) x = p;
+    }
+  }
+  return x;
+}
+
+template <int S, int BK, int VY, int KR, bool C1, bool NCC, typename TIN>
 __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   constexpr int NS = (BK + S - 1) / S;   // strips per patch
   constexpr int WL = BK - (NS - 1) * S;  // width of the last strip
@@ -81,16 +125,18 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Ybase = iy_first * S + a.lo, Xbase = ix_first * S + a.lo;
 
-  // ---- a0: the centred region x' = x - 0.5 of every channel (0 outside the image)
+  // ---- a0: the staged region of every channel (0 outside the image): L2 centres x' = x - 0.5
+  // (halves the identity's cancellation); NCC keeps the raw values (not shift-invariant, Eq. 4)
   const int nch = C1 ? 1 : a.C;
   const size_t plane = size_t(a.H) * a.W;
-  const float* img = a.imgs + size_t(f) * nch * plane;
+  const TIN* img = static_cast<const TIN*>(a.imgs) + size_t(f) * nch * plane;
+  const float shift = NCC ? 0.f : 0.5f;
   for (int e = threadIdx.x; e < nch * a.PL; e += blockDim.x) {
     const int c = e / a.PL, e2 = e - c * a.PL;
     const int r = e2 / a.RWp, x = e2 - r * a.RWp;
     const int yy = Ybase + r, xx = Xbase + x;
-    smf[e] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W) ? __ldg(img + c * plane + size_t(yy) * a.W + xx) - 0.5f
-                                                           : 0.f;
+    smf[e] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
+                 ? float(__ldg(img + c * plane + size_t(yy) * a.W + xx)) - shift : 0.f;
   }
   __syncthreads();
 
@@ -124,6 +170,10 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     nr = hcombine<NS, WL, S>(nf, np);
     if (C1) load_ref(0);
   }
+  // NCC: the filter score of a candidate is sqrt(n_r) - C / sqrt(n_c) >= 0 (Cauchy-Schwarz; smaller
+  // = larger NCC, NCC := 0 for zero norms); keys quantise it like a distance (no n_r offset)
+  const float nrs = NCC ? sqrtf(nr) : 0.f;
+  const float nadd = NCC ? 0.f : nr;
   // a4 state. KR <= 48: a sorted register list (0 sentinels in the first KR - KP slots, so the
   // KP-th key is r[KR-1]). KR = 80: a per-reference binary max-heap of KP keys in shared memory
   // (1-indexed, root = the KP-th key): an insertion is a ~7-level sift-down instead of a
@@ -206,9 +256,15 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
 #pragma unroll
       for (int i = VY - 1; i >= 0; --i) {
         const float np = Qp[i + BK] - Qp[i], nrest = Qr[i + BK] - Qr[i];
-        const float ep = fmaf(-2.f, Tp[i], np);
-        const float ef = ep + fmaf(-2.f, Tr[i], nrest);
-        dpv[i] = hcombine<NS, WL, S>(ef, ep);  // d' = n_c - 2 C
+        if constexpr (NCC) {
+          const float cc = hcombine<NS, WL, S>(Tp[i] + Tr[i], Tp[i]);  // C (Eq. 5)
+          const float nc = hcombine<NS, WL, S>(np + nrest, np);       // ||X_c||^2
+          dpv[i] = nrs - (nc > 0.f ? cc * rsqrtf(nc) : 0.f);
+        } else {
+          const float ep = fmaf(-2.f, Tp[i], np);
+          const float ef = ep + fmaf(-2.f, Tr[i], nrest);
+          dpv[i] = hcombine<NS, WL, S>(ef, ep);  // d' = n_c - 2 C
+        }
         // slack thr - d' >= 0 (or +inf): the candidate may enter the top-KP
         fails = (fails << 1) + (__float_as_uint(thr - dpv[i]) >> 31);
       }
@@ -216,7 +272,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
       if (__any_sync(0xffffffffu, bits != 0u)) {
         uint32_t* sc = scratch + lane;
 #pragma unroll
-        for (int i = 0; i < VY; ++i) sc[32 * i] = __float_as_uint(fmaxf(dpv[i] + nr, 0.f));
+        for (int i = 0; i < VY; ++i) sc[32 * i] = __float_as_uint(fmaxf(dpv[i] + nadd, 0.f));
         const int rel1 = (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
         while (__any_sync(0xffffffffu, bits != 0u)) {
           const int i = 31 - __clz(bits | 1u);
@@ -245,7 +301,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
         if (kth != 0xffffffffu) {
           // largest distance whose key can still tie the KP-th key, plus a rounding margin
           const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
-          thr = fmaf(dmax, 1.0f + 1e-6f, -nr) + 1e-30f;
+          thr = fmaf(dmax, 1.0f + (NCC ? 1e-5f : 1e-6f), -nadd) + 1e-30f;
         }
         __syncwarp();
       }
@@ -266,6 +322,64 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
   const size_t row0 = size_t(f) * band_refs + size_t(iy0 - a.iy_begin) * a.nx + ix_first;
   constexpr int NJ = (KR + 31) / 32;
+  if constexpr (NCC) {
+    // a5 (NCC): exact cross terms / norms of the KP (<= 32) kept candidates, warp bitonic sort
+    // (exact 128-bit comparisons for uint8), write K (idx, d_NCC = -NCC)
+    constexpr bool EXACT = sizeof(TIN) == 1;
+    for (int j = 0; j < nref; ++j) {
+      const int rxj = (ix_first + j) * S;
+      const uint32_t kk = lane < KR ? scratch[j * (KR + 1) + lane] : 0xffffffffu;
+      NccItem it;
+      it.c = 0; it.n = 1; it.f = 0.0; it.idx = -1;
+      double nrd = 0.0, cd = 0.0, ncd = 0.0;
+      long long nri = 0, ci = 0, nci = 0;
+      int cy = 0, cx = 0;
+      const bool have = kk != 0u && kk != 0xffffffffu;
+      if (have) {
+        const int rel = int(kk & ((1u << rb) - 1u)) - 1;
+        const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+        cy = ry + dyy + a.lo;
+        cx = rxj + dxx + a.lo;
+      }
+      for (int c = 0; c < nch; ++c) {
+        const TIN* pr = img + c * plane + size_t(ry) * a.W + rxj;
+        const TIN* pc = img + c * plane + size_t(cy) * a.W + cx;
+        for (int l = 0; l < BK; ++l)
+#pragma unroll
+          for (int m = 0; m < BK; ++m) {
+            const TIN vr = __ldg(pr + l * a.W + m), vc = have ? __ldg(pc + l * a.W + m) : TIN(0);
+            if constexpr (EXACT) {
+              nri += int(vr) * int(vr);
+              ci += int(vr) * int(vc);
+              nci += int(vc) * int(vc);
+            } else {
+              nrd = fma(double(vr), double(vr), nrd);
+              cd = fma(double(vr), double(vc), cd);
+              ncd = fma(double(vc), double(vc), ncd);
+            }
+          }
+      }
+      if (have) {
+        it.idx = cy * a.W + cx;
+        if constexpr (EXACT) {
+          const bool zero = nri == 0 || nci == 0;
+          it.c = zero ? 0 : ci;
+          it.n = zero ? 1 : nci;
+          it.f = zero ? 0.0 : double(ci) / sqrt(double(nri) * double(nci));
+        } else {
+          const double den = sqrt(nrd * ncd);
+          // ordered by the reported float32 value, ties by idx (rows sorted by (dist, idx))
+          it.f = double(float(den > 0.0 ? cd / den : 0.0));
+        }
+      }
+      it = warp_sort_ncc<EXACT>(it, lane);
+      if (lane < a.K) {
+        a.idx_out[(row0 + j) * a.K + lane] = it.idx;
+        a.dist_out[(row0 + j) * a.K + lane] = it.idx < 0 ? __int_as_float(0x7f800000) : float(-it.f);
+      }
+    }
+    return;
+  } else {
   for (int j = 0; j < nref; ++j) {
     const int rxj = (ix_first + j) * S;
     WarpTopK<NJ> top;
@@ -307,6 +421,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
       }
     }
   }
+  }
 }
 
 constexpr int kFVY = 8;
@@ -331,10 +446,10 @@ int boxf_rel_bits(int Wn) {
 
 int boxf_kr(const Geometry& g) { return g.KP <= 32 ? 32 : g.KP <= 48 ? 48 : g.KP <= 80 ? 80 : 0; }
 
-template <int S, int BK, int KR>
+template <int S, int BK, int KR, bool NCC = false, typename TIN = float>
 cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + kFWarps - 1) / kFWarps;
-  auto k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true> : bm_boxf_kernel<S, BK, kFVY, KR, false>;
+  auto k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN> : bm_boxf_kernel<S, BK, kFVY, KR, false, NCC, TIN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<dim3(a.tiles_x * tiles_y, F), kFWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
@@ -343,7 +458,9 @@ cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st
 }  // namespace
 
 bool boxf_supported(const Geometry& g) {
-  if (g.dtype != SC_DTYPE_F32) return false;
+  // L2: float images (uint8 L2 has the dp4a box kernel); NCC: both dtypes, K + 8 <= 32
+  if (g.metric == SC_METRIC_L2 && g.dtype != SC_DTYPE_F32) return false;
+  if (g.metric == SC_METRIC_NCC && g.KP > 32) return false;
   const bool shape = (g.s == 3 && g.b == 8) || (g.s == 1 && g.b == 7) || (g.s == 4 && g.b == 8) ||
                      (g.s == 2 && g.b == 8);
   if (!shape) return false;
@@ -359,7 +476,7 @@ cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int i
                            int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
   const Geometry& g = p.g;
   BoxfArgs a{};
-  a.imgs = static_cast<const float*>(imgs);
+  a.imgs = imgs;
   a.idx_out = idx_out;
   a.dist_out = static_cast<float*>(dist_out);
   a.H = g.H; a.W = g.W; a.C = g.C; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
@@ -370,6 +487,18 @@ cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int i
   const int kr = boxf_kr(g);  // the layout and the instantiation use the same list size
   const size_t smem = boxf_layout(g, kr, &a);
   if (launches) *launches += 1;
+  if (g.metric == SC_METRIC_NCC) {  // KP <= 32: register lists, exact re-rank
+#define SCBM_NCC_CASE(S_, B_)                                                                          \
+  if (g.s == S_ && g.b == B_)                                                                          \
+    return g.dtype == SC_DTYPE_U8 ? launch_boxf_t<S_, B_, 32, true, uint8_t>(a, F, smem, st)           \
+                                  : launch_boxf_t<S_, B_, 32, true, float>(a, F, smem, st);
+    SCBM_NCC_CASE(3, 8)
+    SCBM_NCC_CASE(1, 7)
+    SCBM_NCC_CASE(4, 8)
+    SCBM_NCC_CASE(2, 8)
+#undef SCBM_NCC_CASE
+    return cudaErrorInvalidValue;
+  }
 #define SCBM_BOXF_CASE(S_, B_)                                                    \
   if (g.s == S_ && g.b == B_) {                                                   \
     if (kr == 32) return launch_boxf_t<S_, B_, 32>(a, F, smem, st);               \

@@ -127,11 +127,16 @@ const char* sc_status_string(sc_status_t s) {
 
 sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K, sc_dtype_t dtype,
                        sc_bm_plan_t* plan_out) {
+  return sc_bm_plan_ex(H, W, C, b, stride, window, K, dtype, SC_METRIC_L2, plan_out);
+}
+
+sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, int K, sc_dtype_t dtype,
+                          sc_metric_t metric, sc_bm_plan_t* plan_out) {
   if (!plan_out) return SC_ERR_INVALID_ARGUMENT;
   *plan_out = nullptr;
   if (b < 1 || b > 16 || C < 1 || C > 8 || stride < 1 || window < 1 || window > 255 || K < 1 ||
       K > 128 || H < b || W < b || int64_t(H) * W >= (int64_t(1) << 31) ||
-      (dtype != SC_DTYPE_U8 && dtype != SC_DTYPE_F32))
+      (dtype != SC_DTYPE_U8 && dtype != SC_DTYPE_F32) || (metric != SC_METRIC_L2 && metric != SC_METRIC_NCC))
     return SC_ERR_INVALID_ARGUMENT;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return SC_ERR_CUDA;
@@ -157,7 +162,12 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   g.NPAD = (std::max(-g.lo, g.hi) + 24 + 3) & ~3;
   g.Mxp = (g.Mx + 2 * g.NPAD + 3) & ~3;
   g.NFS = (long long)(g.My + 2 * g.NPAD) * g.Mxp;
-  g.KP = dtype == SC_DTYPE_F32 ? K + kRescoreMargin : K;
+  g.metric = metric;
+  g.KP = (dtype == SC_DTYPE_F32 || metric == SC_METRIC_NCC) ? K + kRescoreMargin : K;
+  if (metric == SC_METRIC_NCC && !boxf_supported(g)) {  // NCC runs on the float box kernel only
+    delete p;
+    return SC_ERR_UNSUPPORTED;
+  }
 
   // candidate counts (separable: clipped rows x clipped cols)
   int64_t sy = 0, sx = 0, ymin = INT64_MAX, ymax = 0, xmin = INT64_MAX, xmax = 0;
@@ -195,6 +205,7 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
   // f32, one channel, (s, b) in {(3,8), (1,7), (4,8), (2,8)}, K + 8 <= 80 (c2, c3): the float
   // box-sum matcher
   if (boxf_supported(g)) p->kernel = SC_KERNEL_BOXF;
+  if (metric == SC_METRIC_NCC) p->kernel = SC_KERNEL_BOXF;
 
   const size_t SP = size_t((W + 15) / 16 * 16);
   cudaError_t e = cudaSuccess;
@@ -251,6 +262,7 @@ sc_status_t sc_bm_run(sc_bm_plan_t p, const void* img, int32_t* idx_out, void* d
 
 sc_status_t sc_bm_run_dense_debug(sc_bm_plan_t p, const void* img, void* dist_all, sc_stream_t stream) {
   if (!p || !img || !dist_all) return SC_ERR_INVALID_ARGUMENT;
+  if (p->g.metric != SC_METRIC_L2) return SC_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(img) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
   sc_status_t s = check_device(p);
   if (s != SC_OK) return s;
@@ -363,6 +375,7 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
 
 sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
+  if (p->g.metric == SC_METRIC_NCC && kernel != SC_KERNEL_BOXF) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_BOX && !box_supported(p->g)) return SC_ERR_UNSUPPORTED;

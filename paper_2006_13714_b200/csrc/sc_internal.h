@@ -18,7 +18,8 @@ struct Geometry {
   int Mxp;            // norm-map row pitch (Mx + 2*NPAD rounded up to 4 ints: 16-byte aligned rows)
   int NPAD;           // norm-map border (rows and columns) on every side, filled with a huge value
   long long NFS;      // norm-map frame stride in elements ((My + 2*NPAD) * Mxp)
-  int KP;             // keys kept per ref before output (K, or K+rescore margin for f32)
+  int KP;             // keys kept per ref before output (K, or K+rescore margin for f32 / NCC)
+  int metric;         // SC_METRIC_L2 (Eq. 3) or SC_METRIC_NCC (Eq. 4)
 };
 
 // Workspace for one chunk of frames.

@@ -47,3 +47,44 @@ def bm_np(img: np.ndarray, b: int, s: int, Wn: int, K: int):
             dist_out[r, :len(order)] = d[order]
             r += 1
     return idx_out, dist_out
+
+
+def ncc_np(img: np.ndarray, b: int, s: int, Wn: int, K: int):
+    """Independent NCC brute force (Eq. 4): sliding-window patches, all-position cross terms and
+    norms, window mask, then an EXACT ordering -- Python Fractions of sign(C) C^2 / n_c for integer
+    input (n_r is common to a reference), float64 NCC otherwise -- ties by pixel index.
+    Returns idx [refs, K] int64 and d_NCC = -NCC [refs, K] float64."""
+    from fractions import Fraction
+    if img.ndim == 2:
+        img = img[None]
+    integer = np.issubdtype(img.dtype, np.integer)
+    x = img.astype(np.int64 if integer else np.float64)
+    C, H, W = x.shape
+    P = all_patches(x, b)
+    My, Mx = P.shape[:2]
+    lo, hi = -(Wn // 2), Wn - 1 - Wn // 2
+    ys, xs = np.arange(0, H - b + 1, s), np.arange(0, W - b + 1, s)
+    idx_out = np.full((len(ys) * len(xs), K), -1, dtype=np.int64)
+    d_out = np.full((len(ys) * len(xs), K), np.inf)
+    r = 0
+    for ry in ys:
+        for rx in xs:
+            pr = P[ry, rx]
+            nr = (pr * pr).sum()
+            cands = []
+            for cy in range(max(0, ry + lo), min(My - 1, ry + hi) + 1):
+                for cx in range(max(0, rx + lo), min(Mx - 1, rx + hi) + 1):
+                    pc = P[cy, cx]
+                    c, nc = (pr * pc).sum(), (pc * pc).sum()
+                    f = float(c) / np.sqrt(float(nr) * float(nc)) if nr * nc > 0 else 0.0
+                    if integer:
+                        key = Fraction(int(c) * abs(int(c)), int(nc)) if nr * nc > 0 else Fraction(0)
+                    else:
+                        key = f
+                    cands.append((-key, cy * W + cx, f))
+            cands.sort()
+            for k, (_, i, f) in enumerate(cands[:K]):
+                idx_out[r, k] = i
+                d_out[r, k] = -f
+            r += 1
+    return idx_out, d_out

@@ -76,3 +76,57 @@ def check_f32(img, b, s, Wn, K, gi, gd, oi, od, iy_range=None, rel=REL, where=""
         dmap.update(zip(gi[r, :k].tolist(), D[r, :k].tolist()))
         for c in gs ^ os_:
             assert abs(dmap[c] - dK) <= rel * dK, f"{where}: ref {r} set differs beyond tolerance"
+
+
+NCC_ATOL = 1e-5  # d_NCC = -NCC lies in [-1, 1]: absolute tolerance
+
+
+def pair_ncc(img, b, ry, rx, cy, cx):
+    """-NCC of explicit (reference, candidate) pairs of one image [C,H,W], float64 (Eq. 4)."""
+    x = np.asarray(img, dtype=np.float64)
+    out = np.empty(len(ry))
+    for k in range(len(ry)):
+        pr = x[:, ry[k]:ry[k] + b, rx[k]:rx[k] + b]
+        pc = x[:, cy[k]:cy[k] + b, cx[k]:cx[k] + b]
+        den = np.sqrt((pr * pr).sum() * (pc * pc).sum())
+        out[k] = -((pr * pc).sum() / den) if den > 0 else 0.0
+    return out
+
+
+def check_ncc(img, b, s, Wn, K, gi, gd, oi, od, exact, iy_range=None, where=""):
+    """NCC parity. exact (uint8): idx equal to the oracle's (order included), d_NCC within
+    float32 rounding. Float input: the f32 rule of check_f32 with an absolute tolerance."""
+    gi, gd, oi, od = (np.asarray(x) for x in (gi, gd, oi, od))
+    assert gi.shape == oi.shape, (gi.shape, oi.shape)
+    if exact:
+        bad = np.argwhere(gi != oi)
+        assert bad.size == 0, f"{where}: {len(bad)} idx mismatches, first at {bad[:3].tolist()}: " \
+            f"gpu {gi[tuple(bad[0][:-1])].tolist()} vs oracle {oi[tuple(bad[0][:-1])].tolist()}"
+        fin = np.isfinite(od)
+        assert (np.isfinite(gd) == fin).all(), f"{where}: padding mismatch"
+        assert np.max(np.abs(gd[fin] - od[fin]), initial=0) <= 2e-6, f"{where}: d_NCC off"
+        return
+    C, H, W = img.shape
+    ny, nx = oracle.grid(H, W, b, s)
+    iy0, iy1 = iy_range if iy_range is not None else (0, ny)
+    refs = (iy1 - iy0) * nx
+    lo, hi = -(Wn // 2), Wn - 1 - Wn // 2
+    for r in range(refs):
+        ry, rx = (iy0 + r // nx) * s, (r % nx) * s
+        ncand = (min(H - b, ry + hi) - max(0, ry + lo) + 1) * (min(W - b, rx + hi) - max(0, rx + lo) + 1)
+        k = min(ncand, K)
+        g = gi[r, :k]
+        assert (gi[r, k:] == -1).all() and len(set(g.tolist())) == k, f"{where}: ref {r} slots"
+        gcy, gcx = g // W, g % W
+        assert ((gcy - ry >= lo) & (gcy - ry <= hi) & (gcx - rx >= lo) & (gcx - rx <= hi)).all()
+        D = pair_ncc(img, b, [ry] * k, [rx] * k, gcy, gcx)
+        assert np.max(np.abs(gd[r, :k] - D)) <= NCC_ATOL, f"{where}: ref {r} d_NCC off"
+        d = gd[r, :k].astype(np.float64)
+        assert ((d[1:] > d[:-1]) | ((d[1:] == d[:-1]) & (g[1:] > g[:-1]))).all(), f"{where}: ref {r} order"
+        gs, os_ = set(g.tolist()), set(oi[r, :k].tolist())
+        if gs != os_:
+            dK = od[r, k - 1]
+            dmap = dict(zip(oi[r, :k].tolist(), od[r, :k].tolist()))
+            dmap.update(zip(g.tolist(), D.tolist()))
+            for c in gs ^ os_:
+                assert abs(dmap[c] - dK) <= NCC_ATOL, f"{where}: ref {r} set differs beyond tolerance"

@@ -574,3 +574,86 @@ def test_group_padding_and_c5_sample():
     for f in (0, 63):
         ii = idx[f:f + 1, sel].cpu().numpy()
         np.testing.assert_array_equal(Y[f:f + 1, sel].cpu().numpy(), oracle.group(xs[f:f + 1], ii, cfg.b))
+
+
+# ------------------------------------------------------------------ NCC metric (Eq. 4)
+def _ncc_run(x, b, s, Wn, K, dtype):
+    from paper_2006_13714_b200.bm import Plan
+    N, C, H, W = x.shape
+    p = Plan(H, W, C, b, s, Wn, K, dtype, metric="ncc")
+    gi, gd = _run(p, x)
+    return p, gi, gd
+
+
+def _ncc_cases(n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shapes = [(4, 8), (3, 8), (1, 7), (2, 8)]
+    out = []
+    while len(out) < n:
+        s, b = shapes[len(out) % 4]
+        H, W = int(rng.integers(b, 90)), int(rng.integers(b, 130))
+        Wn, K = int(rng.integers(1, 46)), int(rng.integers(1, 25))
+        C = int(rng.choice([1, 1, 3]))
+        dtype = ["u8", "f32"][len(out) % 2]
+        if ((H - b) // s + 1) * ((W - b) // s + 1) * Wn * Wn * C > 2e7:
+            continue
+        out.append((dtype, s, b, C, H, W, Wn, K))
+    return out
+
+
+@pytest.mark.parametrize("case", _ncc_cases(16, 606))
+def test_ncc_random_sweep(case):
+    from tests.parity import check_ncc
+    dtype, s, b, C, H, W, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 2, C, H, W, dtype)
+    p, gi, gd = _ncc_run(x, b, s, Wn, K, dtype)
+    oi, od = oracle.ncc(x, b, s, Wn, K)
+    for n in range(2):
+        check_ncc(x[n], b, s, Wn, K, gi[n], gd[n], oi[n], od[n], exact=dtype == "u8", where=f"ncc {case} img{n}")
+
+
+@pytest.mark.parametrize("kind", ["zeros", "constant", "periodic", "scaled"])
+def test_ncc_ties_and_degenerate(kind):
+    """Zero-norm patches (NCC := 0), all-ties images, periodic tilings and exact scaled copies:
+    the exact uint8 ordering must reproduce the oracle's tie-breaks."""
+    from tests.parity import check_ncc
+    rng = np.random.Generator(np.random.PCG64(15))
+    if kind == "zeros":
+        x = rng.integers(0, 256, size=(1, 1, 48, 70), dtype=np.uint8)
+        x[:, :, 10:30, 20:50] = 0
+    elif kind == "constant":
+        x = np.full((1, 1, 48, 70), 77, dtype=np.uint8)
+    elif kind == "periodic":
+        x = np.tile(rng.integers(0, 256, size=(8, 8), dtype=np.uint8), (6, 9))[None, None].copy()
+    else:
+        base = rng.integers(1, 64, size=(48, 35), dtype=np.uint8)
+        x = np.concatenate([base, base * 2], axis=1)[None, None].copy()
+    p, gi, gd = _ncc_run(x, 8, 4, 21, 16, "u8")
+    oi, od = oracle.ncc(x, 8, 4, 21, 16)
+    check_ncc(x[0], 8, 4, 21, 16, gi[0], gd[0], oi[0], od[0], exact=True, where=f"ncc {kind}")
+
+
+def test_ncc_configs_and_rejects():
+    """c5 frames (u8, exact) and c2 (f32) with the NCC metric; unsupported geometry is refused."""
+    from paper_2006_13714_b200.bm import Plan, ScError
+    from tests.parity import check_ncc
+    cfg = synth.CONFIGS["c5"]
+    x = synth.make_input(cfg, n_frames=2)
+    p, gi, gd = _ncc_run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, "u8")
+    for r0, r1 in [(0, 2), (p.ny - 2, p.ny)]:
+        oi, od = oracle.ncc(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=(1, 2), rows=(r0, r1))
+        sl = slice(r0 * p.nx, r1 * p.nx)
+        check_ncc(x[1], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[1, sl], gd[1, sl], oi[0], od[0], exact=True,
+                  where=f"ncc c5 rows {r0}:{r1}")
+    cfg = synth.CONFIGS["c2"]
+    x = synth.make_input(cfg)
+    p, gi, gd = _ncc_run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, "f32")
+    oi, od = oracle.ncc(x, cfg.b, cfg.s, cfg.Wn, cfg.K, rows=(80, 83))
+    sl = slice(80 * p.nx, 83 * p.nx)
+    check_ncc(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0, sl], gd[0, sl], oi[0], od[0], exact=False,
+              iy_range=(80, 83), where="ncc c2")
+    for args in [(64, 64, 1, 8, 5, 21, 16), (64, 64, 1, 8, 4, 21, 25)]:
+        with pytest.raises(ScError) as e:
+            Plan(*args, "u8", metric="ncc")
+        assert e.value.code == 2

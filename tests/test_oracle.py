@@ -17,7 +17,7 @@ import pytest
 
 import oracle
 from paper_2006_13714_b200 import synth
-from tests.bm_numpy import bm_np
+from tests.bm_numpy import bm_np, ncc_np
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "worked_3x3.json")
 
@@ -340,3 +340,72 @@ def test_group_column_norms_and_self_first(dtype):
     for r in range(ny * nx):
         ry, rx = (r // nx) * s, (r % nx) * s
         np.testing.assert_array_equal(Y[0, r, 0], x[0, :, ry:ry + b, rx:rx + b])
+
+
+# ---------------------------------------------------------------- NCC block matching (Eq. 4)
+def test_ncc_worked_example():
+    """NCC = C_i / (||X_i|| ||X_j||) from the hand-worked C and norms (worked_3x3.json, Lemma 1
+    P:294-297): 46/46, 58/sqrt(46*74), 82/sqrt(46*154), 94/sqrt(46*206) -> order 0, 1, 3, 4."""
+    g = json.load(open(GOLD))
+    img = np.array(g["image"], dtype=np.uint8)
+    Cm, nm = np.array(g["C"], float), np.array(g["norms"], float)
+    want = (Cm / np.sqrt(nm[0, 0] * nm)).ravel()
+    idx, dist = oracle.ncc(img, 2, 2, 3, 4)
+    np.testing.assert_array_equal(idx[0, 0], [0, 1, 3, 4])
+    np.testing.assert_allclose(-dist[0, 0], want[[0, 1, 2, 3]], rtol=1e-15)
+
+
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+@pytest.mark.parametrize("C,b,s,Wn,K", [(1, 3, 1, 5, 4), (1, 4, 2, 7, 9), (2, 2, 1, 4, 6), (1, 8, 4, 9, 16), (3, 3, 2, 17, 30)])
+def test_ncc_vs_numpy_bruteforce(dtype, C, b, s, Wn, K):
+    rng = _rng(500 + b * 7 + Wn)
+    x = synth.random_image(rng, 1, C, 12, 13, dtype)[0]
+    if dtype == "u8":
+        x[:, :3, :3] = 0  # zero-norm patches: NCC := 0 reading
+    idx, dist = oracle.ncc(x, b, s, Wn, K)
+    ni, nd = ncc_np(x, b, s, Wn, K)
+    np.testing.assert_array_equal(idx[0], ni)
+    np.testing.assert_allclose(dist[0], nd, rtol=0, atol=1e-12)
+
+
+def test_ncc_closed_forms():
+    # b = 1 on positive pixels: every NCC is 1 -> pure index order of the clipped window
+    x = (_rng(3).integers(1, 256, size=(1, 9, 10))).astype(np.uint8)
+    idx, dist = oracle.ncc(x, 1, 2, 5, 7)
+    ny, nx = oracle.grid(9, 10, 1, 2)
+    for r in range(ny * nx):
+        ry, rx = (r // nx) * 2, (r % nx) * 2
+        win = [cy * 10 + cx for cy in range(max(0, ry - 2), min(8, ry + 2) + 1)
+               for cx in range(max(0, rx - 2), min(9, rx + 2) + 1)]
+        np.testing.assert_array_equal(idx[0, r], win[:7])
+    assert (dist == -1.0).all()
+    # an all-zero reference: NCC := 0 for every candidate -> index order
+    z = np.zeros((1, 12, 12), np.uint8)
+    z[:, 6:, :] = 200
+    idx, dist = oracle.ncc(z, 4, 4, 5, 3)
+    assert (dist[0, 0] == 0).all() and idx[0, 0].tolist() == [0, 1, 2]
+
+
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_ncc_invariants(dtype):
+    """Self is the best (NCC = 1, Cauchy-Schwarz) on data without scaled copies; NCC is invariant
+    to a positive scale of the image (Eq. 4), exactly in the integer ordering."""
+    rng = _rng(41)
+    x = synth.random_image(rng, 1, 2, 21, 23, dtype)[0]
+    if dtype == "u8":
+        x = np.maximum(x, 1).astype(np.uint8)
+    idx, dist = oracle.ncc(x, 4, 3, 9, 10)
+    ny, nx = oracle.grid(21, 23, 4, 3)
+    t = np.arange(ny * nx)
+    np.testing.assert_array_equal(idx[0, :, 0], (t // nx) * 3 * 23 + (t % nx) * 3)
+    np.testing.assert_allclose(dist[0, :, 0], -1.0, atol=1e-12)
+    assert (np.diff(dist[0], axis=1) >= 0).all()
+    if dtype == "u8":
+        y = (x // 2).astype(np.uint8) * 2  # even values: y/2 is an exact scale of y
+        i1, d1 = oracle.ncc(y, 4, 3, 9, 10)
+        i2, d2 = oracle.ncc((y // 2).astype(np.uint8), 4, 3, 9, 10)
+    else:
+        i1, d1 = oracle.ncc(x, 4, 3, 9, 10)
+        i2, d2 = oracle.ncc((x * np.float32(4.0)), 4, 3, 9, 10)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_allclose(d1, d2, atol=1e-12)
