@@ -64,8 +64,11 @@ __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 
 #define SCBM_BOX_MINB 2  // CTAs per SM the register allocation targets (tuning builds override)
 #endif
 
-template <int NY, int VY, int KR>
+// WPC: the staged row pitch in words when known at compile time (0 = runtime a.WP); a constant
+// pitch turns the candidate-row loads into [register + immediate] LDS (no per-load address math)
+template <int NY, int VY, int KR, int WPC = 0>
 __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) bm_box_kernel(BoxArgs a) {
+  const int WP = WPC > 0 ? WPC : a.WP;
   extern __shared__ __align__(16) uint32_t sm[];
   constexpr int NR = 4 * NY + 4;   // patch rows of the lane's NY references
   constexpr int NT = NR + VY - 1;  // candidate rows per (dy block, dx)
@@ -80,7 +83,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   // region bytes [4w+k, 4w+k+3] as int8 x' = x ^ 0x80 = x - 128 (0 outside the image).
   const uint8_t* img = a.imgs + size_t(f) * a.H * a.W;
   for (int e = threadIdx.x; e < a.PL; e += blockDim.x) {
-    const int r = e / a.WP, w = e - r * a.WP;
+    const int r = e / WP, w = e - r * WP;
     const int y = Ybase + r, x = Xbase + 4 * w;
     uint32_t u0 = 0u, u1 = 0u;
     if (y >= 0 && y < a.H) {
@@ -116,9 +119,9 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   uint32_t R[NR];
   {
     const int off = -a.lo;
-    const uint32_t* src = sm + (off & 3) * a.PL + rr0 * a.WP + lane + (off >> 2);
+    const uint32_t* src = sm + (off & 3) * a.PL + rr0 * WP + lane + (off >> 2);
 #pragma unroll
-    for (int r = 0; r < NR; ++r) R[r] = src[r * a.WP];
+    for (int r = 0; r < NR; ++r) R[r] = src[r * WP];
   }
   bool ref_ok[NY];
   int32_t nr[NY];  // ||X_i||^2 of the centred reference (left strip + lane l+1's right strip)
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       any_row |= rows[q] != 0u;
     }
     if (!any_row) continue;  // warp-uniform
-    const uint32_t* cbase = sm + (rr0 + dy0) * a.WP + lane;
+    const uint32_t* cbase = sm + (rr0 + dy0) * WP + lane;
     // a4 survivors of two consecutive offset groups are inserted together (fewer, fuller rounds:
     // a round lasts as long as the busiest lane); the bits of group h sit at h*VY .. h*VY+VY-1
     // and its distances in scratch rows q*2VY + h*VY + i
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       const uint32_t* col = cbase + (off & 3) * a.PL + (off >> 2);
       uint32_t Cw[NT];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) Cw[t] = col[t * a.WP];
+      for (int t = 0; t < NT; ++t) Cw[t] = col[t * WP];
       // a1 in registers: P[t] = sum_{u < t} |candidate strip row u|^2 (a dp4a prefix chain),
       // so the strip norm of offset i of reference q is P[4q+i+8] - P[4q+i]
       int P[NT + 1];
@@ -321,10 +324,10 @@ size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
   return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
 }
 
-template <int NY, int VY, int KR>
+template <int NY, int VY, int KR, int WPC = 0>
 cudaError_t launch_box_t(const BoxArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + kBoxWarps * NY - 1) / (kBoxWarps * NY);
-  auto k = bm_box_kernel<NY, VY, KR>;
+  auto k = bm_box_kernel<NY, VY, KR, WPC>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<dim3(a.tiles_x * tiles_y, F), kBoxWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
@@ -359,7 +362,8 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   const size_t smem = box_layout(g, 2, vy, kr, &a);
   cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  if (kr == 16 && vy == 11) e = launch_box_t<2, 11, 16>(a, F, smem, st);
+  if (kr == 16 && vy == 11 && a.WP == 40) e = launch_box_t<2, 11, 16, 40>(a, F, smem, st);  // Wn 29..33 (c5)
+  else if (kr == 16 && vy == 11) e = launch_box_t<2, 11, 16>(a, F, smem, st);
   else if (kr == 16 && vy == 7) e = launch_box_t<2, 7, 16>(a, F, smem, st);
   else if (kr == 16) e = launch_box_t<2, 8, 16>(a, F, smem, st);
   else if (vy == 11) e = launch_box_t<2, 11, 32>(a, F, smem, st);
