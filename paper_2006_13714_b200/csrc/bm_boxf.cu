@@ -78,6 +78,10 @@ template <bool EXACT>
 __device__ __forceinline__ bool ncc_better(const NccItem& x, const NccItem& y) {
   if (x.idx < 0 || y.idx < 0) return y.idx < 0 && x.idx >= 0;
   if constexpr (EXACT) {
+    // the double NCC values decide unless they are within rounding of each other; then the
+    // exact 128-bit comparison of sign(C) C^2 n_other (n_r is common) does
+    const double df = x.f - y.f;
+    if (fabs(df) > 1e-12 * fmax(fabs(x.f), fabs(y.f))) return df > 0.0;
     const __int128 lx = (__int128)(x.c < 0 ? -x.c : x.c) * x.c * y.n;
     const __int128 ly = (__int128)(y.c < 0 ? -y.c : y.c) * y.c * x.n;
     if (lx != ly) return lx > ly;
@@ -97,9 +101,9 @@ __device__ __forceinline__ NccItem shfl_item(const NccItem& v, int src_lane_xor)
 // warp bitonic sort, best first, one item per lane
 template <bool EXACT>
 __device__ NccItem warp_sort_ncc(NccItem x, int lane) {
-#pragma unroll 1
+#pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll 1
+#pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       const NccItem p = shfl_item(x, j);
       const bool lower = (lane & j) == 0, up = (lane & k) == 0;
