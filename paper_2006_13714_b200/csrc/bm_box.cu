@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "ncc.cuh"
 #include "regtopk.cuh"
 #include "sc_internal.h"
 
@@ -45,7 +46,7 @@ struct BoxArgs {
   const uint8_t* imgs;  // [F][H][W]
   int32_t* idx_out;     // [F][band refs][K]
   int32_t* dist_out;
-  int H, W, Wn, K, lo, hi, nx, iy_begin, iy_end, tiles_x;
+  int H, W, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
   int RH, WP, PL;  // staged region rows, words per region row, words per byte-shifted copy
   int nblk;        // dy blocks of VY offsets
   int scr;         // per-warp scratch words
@@ -66,7 +67,18 @@ __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 
 
 // WPC: the staged row pitch in words when known at compile time (0 = runtime a.WP); a constant
 // pitch turns the candidate-row loads into [register + immediate] LDS (no per-load address math)
-template <int NY, int VY, int KR, int WPC = 0>
+// dp4a on the staged words: signed int8 (centred, L2) or unsigned uint8 (raw, NCC)
+template <bool U>
+__device__ __forceinline__ int dp4(uint32_t x, uint32_t y, int acc) {
+  if constexpr (U) return int(__dp4a(x, y, uint32_t(acc)));
+  else return __dp4a(int(x), int(y), acc);
+}
+
+// NCC (SC_METRIC_NCC, Eq. 4): the same block sums on RAW bytes (unsigned dp4a, exact); a lane
+// forms C = U_l + U_{l+1} and n_c = D_l + D_{l+1} (two shuffles), filters on the float score
+// sqrt(n_r) - C / sqrt(n_c) >= 0 with quantised 32-bit keys (rel + 1, 0 sentinels), keeps K + 8
+// and re-ranks them exactly (ncc.cuh) from the staged bytes.
+template <int NY, int VY, int KR, int WPC = 0, bool NCC = false>
 __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) bm_box_kernel(BoxArgs a) {
   const int WP = WPC > 0 ? WPC : a.WP;
   extern __shared__ __align__(16) uint32_t sm[];
@@ -89,13 +101,13 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     if (y >= 0 && y < a.H) {
       const uint8_t* row = img + size_t(y) * a.W;
       if (x >= 0 && x + 8 <= a.W && (reinterpret_cast<uintptr_t>(row + x) & 3) == 0) {
-        u0 = __ldg(reinterpret_cast<const uint32_t*>(row + x)) ^ 0x80808080u;
-        u1 = __ldg(reinterpret_cast<const uint32_t*>(row + x + 4)) ^ 0x80808080u;
+        u0 = __ldg(reinterpret_cast<const uint32_t*>(row + x)) ^ (NCC ? 0u : 0x80808080u);
+        u1 = __ldg(reinterpret_cast<const uint32_t*>(row + x + 4)) ^ (NCC ? 0u : 0x80808080u);
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int xx = x + j;
-          const uint32_t v = (xx >= 0 && xx < a.W) ? uint32_t(row[xx] ^ 0x80u) : 0u;
+          const uint32_t v = (xx >= 0 && xx < a.W) ? uint32_t(row[xx] ^ (NCC ? 0u : 0x80u)) : 0u;
           if (j < 4) u0 |= v << (8 * j);
           else u1 |= v << (8 * (j - 4));
         }
@@ -126,17 +138,25 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   bool ref_ok[NY];
   int32_t nr[NY];  // ||X_i||^2 of the centred reference (left strip + lane l+1's right strip)
   int thr[NY];     // largest d' = d - ||X_i||^2 that may still enter the reference's top-K
+  float thrf[NY];  // NCC: largest filter score that may still enter the top-(K+8)
+  float nrs[NY];   // NCC: sqrt(n_r)
   RegTopK32<KR> rt[NY];
   const Key32 key32{a.rb, a.dsat};
 #pragma unroll
   for (int q = 0; q < NY; ++q) {
     int n = 0;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) n = __dp4a(int(R[4 * q + r]), int(R[4 * q + r]), n);
+    for (int r = 0; r < 8; ++r) n = dp4<NCC>(R[4 * q + r], R[4 * q + r], n);
     nr[q] = n + __shfl_down_sync(0xffffffffu, n, 1);
     ref_ok[q] = lane_ok && iy0 + q < a.iy_end;
     rt[q].init();
     thr[q] = int(a.dsat) - nr[q];
+    thrf[q] = __int_as_float(0x7f800000);
+    nrs[q] = sqrtf(float(nr[q]));
+    if constexpr (NCC) {  // 0 sentinels: the (K+8)-th key sits in r[KR-1]
+#pragma unroll
+      for (int k = 0; k < KR; ++k) rt[q].r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
+    }
   }
   uint32_t* scratch = sm + 4 * a.PL + warp * a.scr;
 
@@ -175,11 +195,23 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             const int i = 31 - __clz(bits | 1u);  // any survivor (insertion order is irrelevant)
             const uint32_t d = sc[32 * i];        // safe address for every lane
             const int rel = i < VY ? rel0p + i * a.Wn : rel0c + (i - VY) * a.Wn;
-            const uint32_t key = bits ? (min(d, a.dsat) << a.rb) | uint32_t(rel) : 0xffffffffu;
+            uint32_t key;
+            if constexpr (NCC)  // float bits of the score, quantised; rel + 1 (0 = sentinel)
+              key = bits ? ((d >> (a.rb - 1)) << a.rb) | uint32_t(rel + 1) : 0xffffffffu;
+            else
+              key = bits ? (min(d, a.dsat) << a.rb) | uint32_t(rel) : 0xffffffffu;
             bits &= ~(1u << i);
             rt[q].insert(key);
           }
-          thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
+          if constexpr (NCC) {
+            const uint32_t kth = rt[q].r[KR - 1];
+            if (kth != 0xffffffffu) {  // largest score of the (K+8)-th key's quantum + margin
+              const float smax = __uint_as_float(((kth >> a.rb) << (a.rb - 1)) | ((1u << (a.rb - 1)) - 1u));
+              thrf[q] = fmaf(smax, 1.0f + 1e-5f, 1e-30f);
+            }
+          } else {
+            thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
+          }
           __syncwarp();
         }
         pend[q] = 0u;
@@ -198,7 +230,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       int P[NT + 1];
       P[0] = 0;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) P[t + 1] = __dp4a(int(Cw[t]), int(Cw[t]), P[t]);
+      for (int t = 0; t < NT; ++t) P[t + 1] = dp4<NCC>(Cw[t], Cw[t], P[t]);
       // a2: block sums -> left-strip cross terms U[q][i] of reference q at offset (dy0 + i, dx)
       int U[NY][VY];
 #pragma unroll
@@ -206,17 +238,17 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         if constexpr (NY == 1) {
           int acc = 0;
 #pragma unroll
-          for (int r = 0; r < 8; ++r) acc = __dp4a(int(R[r]), int(Cw[r + i]), acc);
+          for (int r = 0; r < 8; ++r) acc = dp4<NCC>(R[r], Cw[r + i], acc);
           U[0][i] = acc;
         } else {
           int m = 0;  // middle rows 4..7, shared by both references
 #pragma unroll
-          for (int r = 4; r < 8; ++r) m = __dp4a(int(R[r]), int(Cw[r + i]), m);
+          for (int r = 4; r < 8; ++r) m = dp4<NCC>(R[r], Cw[r + i], m);
           int t0 = m, t1 = m;
 #pragma unroll
-          for (int r = 0; r < 4; ++r) t0 = __dp4a(int(R[r]), int(Cw[r + i]), t0);
+          for (int r = 0; r < 4; ++r) t0 = dp4<NCC>(R[r], Cw[r + i], t0);
 #pragma unroll
-          for (int r = 8; r < 12; ++r) t1 = __dp4a(int(R[r]), int(Cw[r + i]), t1);
+          for (int r = 8; r < 12; ++r) t1 = dp4<NCC>(R[r], Cw[r + i], t1);
           U[0][i] = t0;
           U[1][i] = t1;
         }
@@ -232,18 +264,29 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         // slack t = thr - d' (>= 0: the candidate may enter the top-K); fail bits = sign bits
         int t[VY];
         unsigned fails = 0u;
+        if constexpr (NCC) {
 #pragma unroll
-        for (int i = VY - 1; i >= 0; --i) {
-          const int e = D[4 * q + i] - 2 * U[q][i];
-          t[i] = thr[q] - e - __shfl_down_sync(0xffffffffu, e, 1);
-          fails = (fails << 1) + (uint32_t(t[i]) >> 31);
+          for (int i = VY - 1; i >= 0; --i) {
+            const int cc = U[q][i] + __shfl_down_sync(0xffffffffu, U[q][i], 1);      // C
+            const int nn = D[4 * q + i] + __shfl_down_sync(0xffffffffu, D[4 * q + i], 1);  // n_c
+            const float sc = nrs[q] - (nn > 0 ? float(cc) * rsqrtf(float(nn)) : 0.f);
+            t[i] = __float_as_int(fmaxf(sc, 0.f));
+            fails = (fails << 1) + (__float_as_uint(thrf[q] - sc) >> 31);
+          }
+        } else {
+#pragma unroll
+          for (int i = VY - 1; i >= 0; --i) {
+            const int e = D[4 * q + i] - 2 * U[q][i];
+            t[i] = thr[q] - e - __shfl_down_sync(0xffffffffu, e, 1);
+            fails = (fails << 1) + (uint32_t(t[i]) >> 31);
+          }
         }
         const unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);
         if (__any_sync(0xffffffffu, bits != 0u)) {
           uint32_t* sc = scratch + q * (64 * VY) + half * (32 * VY) + lane;
           const int dthr = thr[q] + nr[q];  // d = d' + ||X_i||^2 = dthr - t (exact, >= 0)
 #pragma unroll
-          for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(dthr - t[i]);
+          for (int i = 0; i < VY; ++i) sc[32 * i] = NCC ? uint32_t(t[i]) : uint32_t(dthr - t[i]);
           pend[q] |= bits << (half * VY);
         }
       }
@@ -259,10 +302,63 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     if (half == 1) flush(0);  // a lone last group (its bits are in the first half)
   }
 
-  // ---- a6: exact references -> staged rows of K keys -> coalesced (idx, dist) stores;
-  // references whose K-th key is saturated or unfilled -> the fix-up list
   const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
   const int nref = min(kBoxRefsX, a.nx - ix_first);
+  if constexpr (NCC) {
+    // ---- a5 + a6 (NCC): per reference, the kept K + 8 candidates re-scored EXACTLY from the staged
+    // raw bytes (C, n_c, n_r by unsigned dp4a), one warp bitonic sort (ncc.cuh), K (idx, -NCC)
+    const uint32_t relmask = (1u << a.rb) - 1u;
+    const int roff = -a.lo;
+#pragma unroll
+    for (int q = 0; q < NY; ++q) {
+      const int iy = iy0 + q;
+      if (iy >= a.iy_end) break;  // warp-uniform
+      const size_t row0 = size_t(f) * band_refs + size_t(iy - a.iy_begin) * a.nx + ix_first;
+      __syncwarp();
+      if (lane_ok) {
+#pragma unroll
+        for (int k = 0; k < KR; ++k) scratch[lane * (KR + 1) + k] = rt[q].r[k];
+      }
+      __syncwarp();
+      const int ry = 4 * iy;
+      const uint32_t* refbase = sm + (roff & 3) * a.PL + (rr0 + 4 * q) * WP + (roff >> 2);
+      for (int j = 0; j < nref; ++j) {
+        const uint32_t kk = lane < KR ? scratch[j * (KR + 1) + lane] : 0xffffffffu;
+        const bool have = kk != 0u && kk != 0xffffffffu;
+        const int rel = have ? int(kk & relmask) - 1 : 0;
+        const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+        const int cy = ry + dyy + a.lo, cx = (ix_first + j) * 4 + dxx + a.lo;
+        const int ccol = cx - Xbase;  // region byte column of the candidate (>= 0)
+        const uint32_t* cbase2 = sm + (ccol & 3) * a.PL + (cy - Ybase) * WP + (ccol >> 2);
+        int ci = 0, nci = 0, nri = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const uint32_t rv = refbase[r * WP + j + w];
+            const uint32_t cv = have ? cbase2[r * WP + w] : 0u;
+            ci = dp4<true>(rv, cv, ci);
+            nci = dp4<true>(cv, cv, nci);
+            nri = dp4<true>(rv, rv, nri);
+          }
+        NccItem it;
+        it.idx = have ? cy * a.W + cx : -1;
+        const bool zero = nri == 0 || nci == 0;
+        it.c = zero ? 0 : ci;
+        it.n = zero ? 1 : nci;
+        it.f = (zero || !have) ? 0.0 : double(ci) / sqrt(double(nri) * double(nci));
+        it = warp_sort_ncc<true>(it, lane);
+        if (lane < a.K) {
+          a.idx_out[(row0 + j) * a.K + lane] = it.idx;
+          reinterpret_cast<float*>(a.dist_out)[(row0 + j) * a.K + lane] =
+              it.idx < 0 ? __int_as_float(0x7f800000) : float(-it.f);
+        }
+      }
+    }
+    return;
+  }
+  // ---- a6: exact references -> staged rows of K keys -> coalesced (idx, dist) stores;
+  // references whose K-th key is saturated or unfilled -> the fix-up list
 #pragma unroll
   for (int q = 0; q < NY; ++q) {
     const int iy = iy0 + q;
@@ -324,10 +420,10 @@ size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
   return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
 }
 
-template <int NY, int VY, int KR, int WPC = 0>
+template <int NY, int VY, int KR, int WPC = 0, bool NCC = false>
 cudaError_t launch_box_t(const BoxArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + kBoxWarps * NY - 1) / (kBoxWarps * NY);
-  auto k = bm_box_kernel<NY, VY, KR, WPC>;
+  auto k = bm_box_kernel<NY, VY, KR, WPC, NCC>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<dim3(a.tiles_x * tiles_y, F), kBoxWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
@@ -340,6 +436,8 @@ int box_key_bits(const Geometry& g) { return std::max(2, key32_rel_bits(g.Wn)); 
 bool box_supported(const Geometry& g) {
   if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.s != 4 || g.C != 1 || g.K > 32) return false;
   if (key32_rel_bits(g.Wn) > 11) return false;  // keeps >= 21 distance bits in the 32-bit keys
+  if (g.metric == SC_METRIC_NCC && (g.KP > 32 || (1 << key32_rel_bits(g.Wn)) <= g.Wn * g.Wn))
+    return false;  // NCC: K + 8 <= 32 register keys, rel + 1 must fit
   BoxArgs a{};
   return box_layout(g, 2, box_vy(g), 32, &a) <= 227 * 1024;
 }
@@ -351,15 +449,23 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   a.imgs = static_cast<const uint8_t*>(imgs);
   a.idx_out = idx_out;
   a.dist_out = static_cast<int32_t*>(dist_out);
-  a.H = g.H; a.W = g.W; a.Wn = g.Wn; a.K = g.K; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
+  a.H = g.H; a.W = g.W; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.tiles_x = (g.nx + kBoxRefsX - 1) / kBoxRefsX;
   a.rb = box_key_bits(g);
   a.dsat = uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
   a.fix_count = p.ws.fix_count;
   a.fix_list = p.ws.fix_list;
-  const int vy = box_vy(g), kr = g.K <= 16 ? 16 : 32;
+  const int vy = box_vy(g), kr = g.KP <= 16 ? 16 : 32;
   const size_t smem = box_layout(g, 2, vy, kr, &a);
+  if (g.metric == SC_METRIC_NCC) {  // K + 8 <= 32: no saturation, no fix-up
+    if (launches) *launches += 1;
+    if (vy == 11 && a.WP == 40 && g.KP <= 24) return launch_box_t<2, 11, 24, 40, true>(a, F, box_layout(g, 2, vy, 24, &a), st);
+    if (vy == 11 && a.WP == 40) return launch_box_t<2, 11, 32, 40, true>(a, F, smem, st);
+    if (vy == 11) return launch_box_t<2, 11, 32, 0, true>(a, F, smem, st);
+    if (vy == 7) return launch_box_t<2, 7, 32, 0, true>(a, F, smem, st);
+    return launch_box_t<2, 8, 32, 0, true>(a, F, smem, st);
+  }
   cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   if (kr == 16 && vy == 11 && a.WP == 40) e = launch_box_t<2, 11, 16, 40>(a, F, smem, st);  // Wn 29..33 (c5)

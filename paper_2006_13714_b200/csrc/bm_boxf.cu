@@ -26,6 +26,7 @@
 // be lost if more than KP - K = 8 others lie within one quantum (~1e-4 relative) of it.
 #include <algorithm>
 
+#include "ncc.cuh"
 #include "regtopk.cuh"
 #include "sc_internal.h"
 #include "topk.cuh"
@@ -65,54 +66,6 @@ __device__ __forceinline__ float hcombine(float ef, float ep) {
     for (int j = 1; j < NS - 1; ++j) acc += __shfl_down_sync(0xffffffffu, ef, j);
     return acc + __shfl_down_sync(0xffffffffu, ep, NS - 1);
   }
-}
-
-// One candidate of the NCC re-rank (a5 for the NCC metric): exact integer cross term / squared
-// norm for uint8 input (compared by cross-multiplication in 128 bits), double NCC for float.
-struct NccItem {
-  long long c, n;  // uint8: C, ||X_c||^2 (NCC := 0 for zero norms: c = 0, n = 1)
-  double f;        // NCC value (float input: the comparison key)
-  int idx;         // -1: empty slot (sorts last)
-};
-template <bool EXACT>
-__device__ __forceinline__ bool ncc_better(const NccItem& x, const NccItem& y) {
-  if (x.idx < 0 || y.idx < 0) return y.idx < 0 && x.idx >= 0;
-  if constexpr (EXACT) {
-    // the double NCC values decide unless they are within rounding of each other; then the
-    // exact 128-bit comparison of sign(C) C^2 n_other (n_r is common) does
-    const double df = x.f - y.f;
-    if (fabs(df) > 1e-12 * fmax(fabs(x.f), fabs(y.f))) return df > 0.0;
-    const __int128 lx = (__int128)(x.c < 0 ? -x.c : x.c) * x.c * y.n;
-    const __int128 ly = (__int128)(y.c < 0 ? -y.c : y.c) * y.c * x.n;
-    if (lx != ly) return lx > ly;
-  } else {
-    if (x.f != y.f) return x.f > y.f;
-  }
-  return x.idx < y.idx;
-}
-__device__ __forceinline__ NccItem shfl_item(const NccItem& v, int src_lane_xor) {
-  NccItem o;
-  o.c = __shfl_xor_sync(0xffffffffu, v.c, src_lane_xor);
-  o.n = __shfl_xor_sync(0xffffffffu, v.n, src_lane_xor);
-  o.f = __shfl_xor_sync(0xffffffffu, v.f, src_lane_xor);
-  o.idx = __shfl_xor_sync(0xffffffffu, v.idx, src_lane_xor);
-  return o;
-}
-// warp bitonic sort, best first, one item per lane
-template <bool EXACT>
-__device__ NccItem warp_sort_ncc(NccItem x, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const NccItem p = shfl_item(x, j);
-      const bool lower = (lane & j) == 0, up = (lane & k) == 0;
-      const bool p_better = ncc_better<EXACT>(p, x);
-      // ascending (best first) when up: the lower lane keeps the better item
-      if ((lower == up) ? p_better : !p_better && ncc_better<EXACT>(x, p)) x = p;
-    }
-  }
-  return x;
 }
 
 template <int S, int BK, int VY, int KR, bool C1, bool NCC, typename TIN>
@@ -336,7 +289,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
       NccItem it;
       it.c = 0; it.n = 1; it.f = 0.0; it.idx = -1;
       double nrd = 0.0, cd = 0.0, ncd = 0.0;
-      long long nri = 0, ci = 0, nci = 0;
+      int nri = 0, ci = 0, nci = 0;
       int cy = 0, cx = 0;
       const bool have = kk != 0u && kk != 0xffffffffu;
       if (have) {

@@ -164,7 +164,7 @@ sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, in
   g.NFS = (long long)(g.My + 2 * g.NPAD) * g.Mxp;
   g.metric = metric;
   g.KP = (dtype == SC_DTYPE_F32 || metric == SC_METRIC_NCC) ? K + kRescoreMargin : K;
-  if (metric == SC_METRIC_NCC && !boxf_supported(g)) {  // NCC runs on the float box kernel only
+  if (metric == SC_METRIC_NCC && !boxf_supported(g) && !box_supported(g)) {  // NCC: box kernels only
     delete p;
     return SC_ERR_UNSUPPORTED;
   }
@@ -205,7 +205,8 @@ sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, in
   // f32, one channel, (s, b) in {(3,8), (1,7), (4,8), (2,8)}, K + 8 <= 80 (c2, c3): the float
   // box-sum matcher
   if (boxf_supported(g)) p->kernel = SC_KERNEL_BOXF;
-  if (metric == SC_METRIC_NCC) p->kernel = SC_KERNEL_BOXF;
+  if (metric == SC_METRIC_NCC)  // uint8 stride 4: the dp4a box kernel; else the float one
+    p->kernel = (box_supported(g) && (box_ctas >= 16 || !boxf_supported(g))) ? SC_KERNEL_BOX : SC_KERNEL_BOXF;
 
   const size_t SP = size_t((W + 15) / 16 * 16);
   cudaError_t e = cudaSuccess;
@@ -375,7 +376,7 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
 
 sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
-  if (p->g.metric == SC_METRIC_NCC && kernel != SC_KERNEL_BOXF) return SC_ERR_UNSUPPORTED;
+  if (p->g.metric == SC_METRIC_NCC && kernel != SC_KERNEL_BOXF && kernel != SC_KERNEL_BOX) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_BOX && !box_supported(p->g)) return SC_ERR_UNSUPPORTED;

@@ -638,9 +638,11 @@ def test_ncc_configs_and_rejects():
     """c5 frames (u8, exact) and c2 (f32) with the NCC metric; unsupported geometry is refused."""
     from paper_2006_13714_b200.bm import Plan, ScError
     from tests.parity import check_ncc
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX
     cfg = synth.CONFIGS["c5"]
     x = synth.make_input(cfg, n_frames=2)
     p, gi, gd = _ncc_run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, "u8")
+    assert p.info()["kernel"] == SC_KERNEL_BOX
     for r0, r1 in [(0, 2), (p.ny - 2, p.ny)]:
         oi, od = oracle.ncc(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=(1, 2), rows=(r0, r1))
         sl = slice(r0 * p.nx, r1 * p.nx)
@@ -657,3 +659,18 @@ def test_ncc_configs_and_rejects():
         with pytest.raises(ScError) as e:
             Plan(*args, "u8", metric="ncc")
         assert e.value.code == 2
+
+
+@pytest.mark.parametrize("kernel", ["box", "boxf"])
+def test_ncc_u8_both_kernels(kernel):
+    """uint8 stride-4 NCC on the dp4a box kernel (default) and on the float box kernel."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX, SC_KERNEL_BOXF, Plan
+    from tests.parity import check_ncc
+    rng = np.random.Generator(np.random.PCG64(16))
+    x = synth.random_image(rng, 2, 1, 90, 160, "u8")
+    p = Plan(90, 160, 1, 8, 4, 25, 20, "u8", metric="ncc")
+    p.set_kernel(SC_KERNEL_BOX if kernel == "box" else SC_KERNEL_BOXF)
+    gi, gd = _run(p, x)
+    oi, od = oracle.ncc(x, 8, 4, 25, 20)
+    for n in range(2):
+        check_ncc(x[n], 8, 4, 25, 20, gi[n], gd[n], oi[n], od[n], exact=True, where=f"ncc {kernel} img{n}")
