@@ -66,6 +66,14 @@ class ClockSampler:
             self.rows.append([v.strip() for v in line.split(",")])
 
     def __exit__(self, *exc):
+        if not self.rows:  # timed region shorter than one sampling period: one synchronous sample
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([v.strip() for v in line.split(",")])
+            except Exception:
+                pass
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -95,9 +103,10 @@ def _dist_env():
     return ws, rank, local
 
 
-def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1)):
+def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1), metric="l2"):
     """Time the oracle on a bounded sample of the workload: reference rows of image 0."""
     import oracle
+    run = oracle.ncc if metric == "ncc" else oracle.bm
     from paper_2006_13714_b200 import synth  # noqa: F401
     ny = (cfg.H - cfg.b) // cfg.s + 1
     nx = (cfg.W - cfg.b) // cfg.s + 1
@@ -111,11 +120,11 @@ def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1)):
     # calibrate on one row, then size the sample (starting at the top rows) to ~target_s seconds
     mid = 0
     t0 = time.perf_counter()
-    oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(ny // 2, ny // 2 + 1))
+    run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(ny // 2, ny // 2 + 1))
     dt = max(time.perf_counter() - t0, 1e-3)
     rows = int(max(1, min(ny, target_s / dt)))
     t0 = time.perf_counter()
-    oracle.bm(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(mid, mid + rows))
+    run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=images, rows=(mid, mid + rows))
     dt = time.perf_counter() - t0
     p = pairs(mid, mid + rows)
     return {"value": p / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
@@ -394,7 +403,7 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu, _, _ = _cpu_sample(cfg, x_host, target_s=args.ref_step_s * 2)
+        cpu, _, _ = _cpu_sample(cfg, x_host, target_s=args.ref_step_s * 2, metric=args.metric)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

@@ -78,9 +78,17 @@ __device__ __forceinline__ int dp4(uint32_t x, uint32_t y, int acc) {
 // forms C = U_l + U_{l+1} and n_c = D_l + D_{l+1} (two shuffles), filters on the float score
 // sqrt(n_r) - C / sqrt(n_c) >= 0 with quantised 32-bit keys (rel + 1, 0 sentinels), keeps K + 8
 // and re-ranks them exactly (ncc.cuh) from the staged bytes.
-template <int NY, int VY, int KR, int WPC = 0, bool NCC = false>
+// WNC: the window side when known at compile time (0 = runtime): the window geometry, key widths
+// and loop bounds then become immediates (no per-round constant reloads in the survivor loop)
+template <int NY, int VY, int KR, int WPC = 0, bool NCC = false, int WNC = 0>
 __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) bm_box_kernel(BoxArgs a) {
   const int WP = WPC > 0 ? WPC : a.WP;
+  constexpr int kRB = WNC > 0 ? (WNC * WNC <= 2 ? 2 : 32 - __builtin_clz(unsigned(WNC * WNC - 1))) : 0;
+  const int Wn = WNC > 0 ? WNC : a.Wn;
+  const int lo = WNC > 0 ? -(WNC / 2) : a.lo, hi = WNC > 0 ? WNC - 1 - WNC / 2 : a.hi;
+  const int nblk = WNC > 0 ? (WNC + VY - 1) / VY : a.nblk;
+  const int rbits = WNC > 0 ? (kRB < 2 ? 2 : kRB) : a.rb;
+  const uint32_t dsat = WNC > 0 ? uint32_t((uint64_t(1) << (32 - (kRB < 2 ? 2 : kRB))) - 1) : a.dsat;
   extern __shared__ __align__(16) uint32_t sm[];
   constexpr int NR = 4 * NY + 4;   // patch rows of the lane's NY references
   constexpr int NT = NR + VY - 1;  // candidate rows per (dy block, dx)
@@ -89,7 +97,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   const int iy_first = a.iy_begin + ty * (kBoxWarps * NY);
   const int ix_first = tx * kBoxRefsX;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int Ybase = iy_first * 4 + a.lo, Xbase = ix_first * 4 + a.lo;
+  const int Ybase = iy_first * 4 + lo, Xbase = ix_first * 4 + lo;
 
   // ---- a0: four byte-shifted copies of the centred region. Copy k, row r, word w holds
   // region bytes [4w+k, 4w+k+3] as int8 x' = x ^ 0x80 = x - 128 (0 outside the image).
@@ -125,12 +133,12 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   const int ix = ix_first + lane;
   const bool lane_ok = lane < kBoxRefsX && ix < a.nx;
   const int rx = ix * 4;
-  const int rr0 = (iy0 - iy_first) * 4 - a.lo;  // region row of image row 4 * iy0
+  const int rr0 = (iy0 - iy_first) * 4 - lo;  // region row of image row 4 * iy0
 
   // the lane's 4-column strip of its references' patch rows (reference side, aligned)
   uint32_t R[NR];
   {
-    const int off = -a.lo;
+    const int off = -lo;
     const uint32_t* src = sm + (off & 3) * a.PL + rr0 * WP + lane + (off >> 2);
 #pragma unroll
     for (int r = 0; r < NR; ++r) R[r] = src[r * WP];
@@ -141,7 +149,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   float thrf[NY];  // NCC: largest filter score that may still enter the top-(K+8)
   float nrs[NY];   // NCC: sqrt(n_r)
   RegTopK32<KR> rt[NY];
-  const Key32 key32{a.rb, a.dsat};
+  const Key32 key32{rbits, dsat};
 #pragma unroll
   for (int q = 0; q < NY; ++q) {
     int n = 0;
@@ -150,7 +158,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     nr[q] = n + __shfl_down_sync(0xffffffffu, n, 1);
     ref_ok[q] = lane_ok && iy0 + q < a.iy_end;
     rt[q].init();
-    thr[q] = int(a.dsat) - nr[q];
+    thr[q] = int(dsat) - nr[q];
     thrf[q] = __int_as_float(0x7f800000);
     nrs[q] = sqrtf(float(nr[q]));
     if constexpr (NCC) {  // 0 sentinels: the (K+8)-th key sits in r[KR-1]
@@ -160,19 +168,19 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   }
   uint32_t* scratch = sm + 4 * a.PL + warp * a.scr;
 
-  const int b0 = (0 - a.lo) / VY;  // dy block holding dy = 0
-  const int span = max(-a.lo, a.hi);
-  for (int kb = 0; kb < 2 * a.nblk; ++kb) {
+  const int b0 = (0 - lo) / VY;  // dy block holding dy = 0
+  const int span = max(-lo, hi);
+  for (int kb = 0; kb < 2 * nblk; ++kb) {
     const int bb = b0 + centre_out(kb);
-    if (bb < 0 || bb >= a.nblk) continue;
-    const int dy0 = a.lo + bb * VY;
+    if (bb < 0 || bb >= nblk) continue;
+    const int dy0 = lo + bb * VY;
     // offsets dy0 + i inside the window (dy <= hi) whose candidate row lies in [0, H-b]
     unsigned rows[NY];
     bool any_row = false;
 #pragma unroll
     for (int q = 0; q < NY; ++q) {
       const int cy0 = 4 * (iy0 + q) + dy0;  // candidate row of offset i = 0
-      const int ilo = max(0, -cy0), ihi = min(min(VY - 1, a.hi - dy0), a.H - 8 - cy0);
+      const int ilo = max(0, -cy0), ihi = min(min(VY - 1, hi - dy0), a.H - 8 - cy0);
       rows[q] = ihi >= ilo ? (((2u << ihi) - 1u) & ~((1u << ilo) - 1u)) : 0u;
       any_row |= rows[q] != 0u;
     }
@@ -194,19 +202,19 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           while (__any_sync(0xffffffffu, bits != 0u)) {
             const int i = 31 - __clz(bits | 1u);  // any survivor (insertion order is irrelevant)
             const uint32_t d = sc[32 * i];        // safe address for every lane
-            const int rel = i < VY ? rel0p + i * a.Wn : rel0c + (i - VY) * a.Wn;
+            const int rel = i < VY ? rel0p + i * Wn : rel0c + (i - VY) * Wn;
             uint32_t key;
             if constexpr (NCC)  // float bits of the score, quantised; rel + 1 (0 = sentinel)
-              key = bits ? ((d >> (a.rb - 1)) << a.rb) | uint32_t(rel + 1) : 0xffffffffu;
+              key = bits ? ((d >> (rbits - 1)) << rbits) | uint32_t(rel + 1) : 0xffffffffu;
             else
-              key = bits ? (min(d, a.dsat) << a.rb) | uint32_t(rel) : 0xffffffffu;
+              key = bits ? (min(d, dsat) << rbits) | uint32_t(rel) : 0xffffffffu;
             bits &= ~(1u << i);
             rt[q].insert(key);
           }
           if constexpr (NCC) {
             const uint32_t kth = rt[q].r[KR - 1];
             if (kth != 0xffffffffu) {  // largest score of the (K+8)-th key's quantum + margin
-              const float smax = __uint_as_float(((kth >> a.rb) << (a.rb - 1)) | ((1u << (a.rb - 1)) - 1u));
+              const float smax = __uint_as_float(((kth >> rbits) << (rbits - 1)) | ((1u << (rbits - 1)) - 1u));
               thrf[q] = fmaf(smax, 1.0f + 1e-5f, 1e-30f);
             }
           } else {
@@ -219,8 +227,8 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     };
     for (int kx = 0; kx <= 2 * span; ++kx) {
       const int dx = centre_out(kx);
-      if (dx < a.lo || dx > a.hi) continue;
-      const int off = dx - a.lo;
+      if (dx < lo || dx > hi) continue;
+      const int off = dx - lo;
       const uint32_t* col = cbase + (off & 3) * a.PL + (off >> 2);
       uint32_t Cw[NT];
 #pragma unroll
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           pend[q] |= bits << (half * VY);
         }
       }
-      const int rel0 = (dy0 - a.lo) * a.Wn + off;
+      const int rel0 = (dy0 - lo) * Wn + off;
       if (half == 0) {
         rel0p = rel0;
         half = 1;
@@ -307,8 +315,8 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   if constexpr (NCC) {
     // ---- a5 + a6 (NCC): per reference, the kept K + 8 candidates re-scored EXACTLY from the staged
     // raw bytes (C, n_c, n_r by unsigned dp4a), one warp bitonic sort (ncc.cuh), K (idx, -NCC)
-    const uint32_t relmask = (1u << a.rb) - 1u;
-    const int roff = -a.lo;
+    const uint32_t relmask = (1u << rbits) - 1u;
+    const int roff = -lo;
 #pragma unroll
     for (int q = 0; q < NY; ++q) {
       const int iy = iy0 + q;
@@ -326,8 +334,8 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         const uint32_t kk = lane < KR ? scratch[j * (KR + 1) + lane] : 0xffffffffu;
         const bool have = kk != 0u && kk != 0xffffffffu;
         const int rel = have ? int(kk & relmask) - 1 : 0;
-        const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
-        const int cy = ry + dyy + a.lo, cx = (ix_first + j) * 4 + dxx + a.lo;
+        const int dyy = rel / Wn, dxx = rel - dyy * Wn;
+        const int cy = ry + dyy + lo, cx = (ix_first + j) * 4 + dxx + lo;
         const int ccol = cx - Xbase;  // region byte column of the candidate (>= 0)
         const uint32_t* cbase2 = sm + (ccol & 3) * a.PL + (cy - Ybase) * WP + (ccol >> 2);
         int ci = 0, nci = 0, nri = 0;
@@ -383,8 +391,8 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       }
       if (e < nref * a.K) {
         const int rel = key32.rel(kk);
-        const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
-        a.idx_out[row0 * a.K + e] = (ry + dyy + a.lo) * a.W + (ix_first + j) * 4 + dxx + a.lo;
+        const int dyy = rel / Wn, dxx = rel - dyy * Wn;
+        a.idx_out[row0 * a.K + e] = (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
         a.dist_out[row0 * a.K + e] = key32.dist(kk);
       }
     }
@@ -400,8 +408,8 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       const int j = e / a.K, k = e - j * a.K;
       const uint32_t kk = scratch[j * (KR + 1) + k];
       const int rel = key32.rel(kk);
-      const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
-      a.idx_out[row0 * a.K + e] = (ry + dyy + a.lo) * a.W + (ix_first + j) * 4 + dxx + a.lo;
+      const int dyy = rel / Wn, dxx = rel - dyy * Wn;
+      a.idx_out[row0 * a.K + e] = (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
       a.dist_out[row0 * a.K + e] = key32.dist(kk);
     }
     __syncwarp();
@@ -420,10 +428,10 @@ size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
   return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
 }
 
-template <int NY, int VY, int KR, int WPC = 0, bool NCC = false>
+template <int NY, int VY, int KR, int WPC = 0, bool NCC = false, int WNC = 0>
 cudaError_t launch_box_t(const BoxArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + kBoxWarps * NY - 1) / (kBoxWarps * NY);
-  auto k = bm_box_kernel<NY, VY, KR, WPC, NCC>;
+  auto k = bm_box_kernel<NY, VY, KR, WPC, NCC, WNC>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<dim3(a.tiles_x * tiles_y, F), kBoxWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
@@ -460,6 +468,7 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   const size_t smem = box_layout(g, 2, vy, kr, &a);
   if (g.metric == SC_METRIC_NCC) {  // K + 8 <= 32: no saturation, no fix-up
     if (launches) *launches += 1;
+    if (g.Wn == 33 && g.KP <= 24) return launch_box_t<2, 11, 24, 40, true, 33>(a, F, box_layout(g, 2, vy, 24, &a), st);
     if (vy == 11 && a.WP == 40 && g.KP <= 24) return launch_box_t<2, 11, 24, 40, true>(a, F, box_layout(g, 2, vy, 24, &a), st);
     if (vy == 11 && a.WP == 40) return launch_box_t<2, 11, 32, 40, true>(a, F, smem, st);
     if (vy == 11) return launch_box_t<2, 11, 32, 0, true>(a, F, smem, st);
@@ -468,7 +477,8 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   }
   cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  if (kr == 16 && vy == 11 && a.WP == 40) e = launch_box_t<2, 11, 16, 40>(a, F, smem, st);  // Wn 29..33 (c5)
+  if (kr == 16 && g.Wn == 33) e = launch_box_t<2, 11, 16, 40, false, 33>(a, F, smem, st);  // c5: all constant
+  else if (kr == 16 && vy == 11 && a.WP == 40) e = launch_box_t<2, 11, 16, 40>(a, F, smem, st);  // Wn 29..33
   else if (kr == 16 && vy == 11) e = launch_box_t<2, 11, 16>(a, F, smem, st);
   else if (kr == 16 && vy == 7) e = launch_box_t<2, 7, 16>(a, F, smem, st);
   else if (kr == 16) e = launch_box_t<2, 8, 16>(a, F, smem, st);
