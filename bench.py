@@ -172,6 +172,51 @@ def _config_obj(cfg, args):
             "l2": "flushed between timed steps (256 MiB write); working set > L2"}
 
 
+def bench_nlm(args, cfg, plan, x, ws, rank, local, dist):
+    """NLM weights (Eq. 2 via Prop. 1) of one image per rank: weights/s, dense-table bytes vs HBM."""
+    import torch
+    info = plan.info()
+    h = args.nlm_h or (np.sqrt(cfg.b * cfg.b * cfg.C) * (25.0 if cfg.dtype == "u8" else 0.1))
+    img = x[:1]
+    out = torch.empty((info["n_refs"], cfg.Wn * cfg.Wn), dtype=torch.float32, device=x.device)
+    for _ in range(args.warmup):
+        plan.nlm_weights(img, h, out=out)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = plan.info()["launches"]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            starts[k].record(stream)
+            plan.nlm_weights(img, h, out=out)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    ms = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    pairs = info["total_candidates"]
+    table = out.numel() * 4
+    peaks = _peaks()
+    gbs = 3 * table / (ms / 1e3) / 1e9  # distances written, re-read, weights written
+    if rank == 0:
+        line = {"metric": "NLM weights/sec", "op": "nlm", "value": pairs * ws / (ms / 1e3), "unit": "weights/s",
+                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": dict(_config_obj(cfg, args), nlm_h=h, images=1),
+                "roofline": {"bound": "hbm", "kernel": "lanes dense + nlm_normalize", "achieved": gbs,
+                             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
+                             "traffic": None, "algorithmic_bytes_per_step": 3 * table},
+                "gpu_launches": int(plan.info()["launches"] - launches0), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def bench_group(args, cfg, plan, x, idx, ws, rank, local, dist):
     """Patch grouping Y_i of the run's idx table: gathered bytes/s vs HBM."""
     import torch
@@ -231,8 +276,10 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--metric", default="l2", choices=["l2", "ncc"],
                     help="l2: Euclidean BM, Eq. 3 (the headline); ncc: normalised cross-correlation, Eq. 4")
-    ap.add_argument("--op", default="bm", choices=["bm", "group"],
-                    help="bm: the block-matching hot path (default); group: patch grouping Y_i of its output")
+    ap.add_argument("--op", default="bm", choices=["bm", "group", "nlm"],
+                    help="bm: the block-matching hot path (default); group: patch grouping Y_i of its "
+                         "output; nlm: NLM weights (Eq. 2) of the config's first image")
+    ap.add_argument("--nlm-h", type=float, default=0.0, help="NLM bandwidth (default: 1.0 * sqrt(b^2 C) * value scale)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf"],
                     help="force the matching kernel (default: the plan's choice)")
     args = ap.parse_args()
@@ -277,6 +324,8 @@ def main():
     torch.cuda.synchronize()
     if args.op == "group":
         return bench_group(args, cfg, plan, x, idx, ws, rank, local, dist)
+    if args.op == "nlm":
+        return bench_nlm(args, cfg, plan, x, ws, rank, local, dist)
 
     plan.set_timing(True)
     plan.get_timing()

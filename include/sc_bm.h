@@ -158,6 +158,17 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t plan, const void* h_imgs, int64_t n_imag
 sc_status_t sc_bm_group(sc_bm_plan_t plan, const void* imgs, int64_t n_images, const int32_t* idx,
                         void* groups_out, sc_stream_t stream);
 
+/*
+ * NLM weights (Eq. 2, via Proposition 1) of ONE image:
+ *     weights_out[i][(dy-lo)*Wn + (dx-lo)] = exp(-||X_j - X_i||_F^2 / h^2) / Theta_i
+ * over reference i's clipped window (0 in clipped slots; every row sums to 1), float32
+ * [n_refs][Wn*Wn], device pointers (img 16-byte, weights_out 4-byte aligned), h > 0 the NLM
+ * bandwidth (the paper's b in Eq. 2). The window distances come from the Self-Convolution
+ * identity (Lemma 2), written into weights_out and normalised in place. L2 plans only.
+ */
+sc_status_t sc_bm_nlm_weights(sc_bm_plan_t plan, const void* img, float h, float* weights_out,
+                              sc_stream_t stream);
+
 /* Plan geometry and bookkeeping. */
 sc_status_t sc_bm_plan_info(sc_bm_plan_t plan, sc_bm_info_t* info);
 

@@ -49,6 +49,7 @@ def lib():
         L.sco_pair_dist.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
         L.sco_num_threads.restype = ci
         L.sco_ncc_rows.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, dp, ci]
+        L.sco_nlm_weights.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ctypes.c_double, dp, ci]
         _lib = L
     return _lib
 
@@ -119,6 +120,22 @@ def ncc(img: np.ndarray, b: int, s: int, Wn: int, K: int, *, images=None, rows=N
     if rc != 0:
         raise ValueError("oracle.ncc: invalid arguments")
     return idx, dist
+
+
+def nlm_weights(img: np.ndarray, b: int, s: int, Wn: int, h: float, nthreads: int = 0) -> np.ndarray:
+    """NLM weights (Eq. 2) over each reference's clipped window, one image [C,H,W]:
+    [refs, Wn*Wn] float64, 0 in clipped slots, rows summing to 1."""
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None]
+    C, H, W = a.shape
+    ny, nx = grid(H, W, b, s)
+    out = np.empty((ny * nx, Wn * Wn), dtype=np.float64)
+    rc = lib().sco_nlm_weights(a.ctypes.data, _dtype_code(a), C, H, W, b, s, Wn, float(h),
+                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), nthreads)
+    if rc != 0:
+        raise ValueError("oracle.nlm_weights: invalid arguments")
+    return out
 
 
 def bm_dense(img: np.ndarray, b: int, s: int, Wn: int, nthreads: int = 0) -> np.ndarray:

@@ -387,6 +387,53 @@ int sco_ncc_rows(const void* imgs, int dtype, int C, int H, int W, int b, int s,
     return 0;
 }
 
+/*
+ * NLM weights, Eq. 2 restricted to the search window (footnote 2,
+ * PAPER.md:280; the SAME clipped window as BM):
+ *   s_i(j) = exp(-||X_j - X_i||_F^2 / h^2) / Theta_i,  Theta_i = sum_j exp(-||X_j - X_i||^2 / h^2)
+ * with direct-difference distances (double). out[n_refs][Wn*Wn], slot (dy-lo)*Wn + (dx-lo), 0 in
+ * clipped slots. The common factor exp(d_min / h^2) is taken out of numerator and Theta_i
+ * (s_i(j) = exp(-(d_j - d_min)/h^2) / sum_k exp(-(d_k - d_min)/h^2): the same ratio) so that
+ * large d / h^2 cannot underflow to 0/0. One image.
+ */
+int sco_nlm_weights(const void* img, int dtype, int C, int H, int W, int b, int s, int Wn, double h,
+                    double* out, int nthreads) {
+    if (!img || !out || b < 1 || s < 1 || Wn < 1 || H < b || W < b || !(h > 0.0)) return -1;
+    const int ny = grid_n(H, b, s), nx = grid_n(W, b, s);
+    const int lo = -(Wn / 2);
+    const int nslot = Wn * Wn;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel for schedule(dynamic, 16)
+    for (long long t = 0; t < (long long)ny * nx; ++t) {
+        const int ry = (int)(t / nx) * s, rx = (int)(t % nx) * s;
+        double* row = &out[t * nslot];
+        double dmin = INFINITY;
+        for (int a = 0; a < Wn; ++a)
+            for (int c = 0; c < Wn; ++c) {
+                const int cy = ry + lo + a, cx = rx + lo + c;
+                double* o = &row[a * Wn + c];
+                if (cy < 0 || cx < 0 || cy > H - b || cx > W - b) {
+                    *o = -1.0;
+                    continue;
+                }
+                int64_t di;
+                patch_dist(img, dtype, C, H, W, b, ry, rx, cy, cx, &di, o);
+                if (*o < dmin) dmin = *o;
+            }
+        double theta = 0.0;
+        for (int k = 0; k < nslot; ++k) {
+            row[k] = row[k] < 0.0 ? 0.0 : exp(-(row[k] - dmin) / (h * h));
+            theta += row[k];
+        }
+        for (int k = 0; k < nslot; ++k) row[k] /= theta;
+    }
+    return 0;
+}
+
 int sco_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

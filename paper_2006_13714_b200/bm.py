@@ -22,7 +22,8 @@ STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_UNSUPPORTED",
 SC_METRIC_L2, SC_METRIC_NCC = 0, 1
 EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
-            "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group"]
+            "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group",
+            "sc_bm_nlm_weights"]
 
 
 class ScError(RuntimeError):
@@ -77,6 +78,7 @@ def load_library():
     L.sc_bm_set_timing.argtypes = [vp, i32]
     L.sc_bm_get_timing.argtypes = [vp, ctypes.POINTER(Timing)]
     L.sc_bm_group.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.sc_bm_nlm_weights.argtypes = [vp, vp, ctypes.c_float, vp, vp]
     for fn in EXPORTED:
         if fn != "sc_status_string":
             getattr(L, fn).restype = ci
@@ -215,6 +217,16 @@ class Plan:
         _check("sc_bm_group", self._lib.sc_bm_group(
             self._h, ctypes.c_void_p(imgs.data_ptr()), n, ctypes.c_void_p(idx.data_ptr()),
             ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def nlm_weights(self, img, h, out=None, stream=None):
+        """NLM weights of one image [C,H,W] (or [1,C,H,W]): float32 [n_refs, Wn*Wn], rows sum to 1."""
+        import torch
+        img = self._check_img(img)[0]
+        if out is None:
+            out = torch.empty((self.n_refs, self.Wn * self.Wn), dtype=torch.float32, device=img.device)
+        _check("sc_bm_nlm_weights", self._lib.sc_bm_nlm_weights(
+            self._h, ctypes.c_void_p(img.data_ptr()), float(h), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
     # ------------------------------------------------------------------ test exports

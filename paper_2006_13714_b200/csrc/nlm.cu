@@ -1,0 +1,66 @@
+// nlm.cu -- NLM weights (the "next" row SURVEY.md 8f rank 3): Eq. 2
+//     s_i(j) = exp(-||X_j - X_i||_F^2 / h^2) / Theta_i,   Theta_i = sum_j exp(-||X_j - X_i||^2 / h^2)
+// over the reference's clipped search window (footnote 2), computed the paper's
+// way (Proposition 1): the window distances come from the Self-Convolution
+// identity (the matcher's dense mode writes n_c + n_r - 2 C_i for every window slot, Lemma 2), and
+// this kernel turns each reference's row into normalised weights in place.
+//
+// Stabilisation: the row minimum d_min is subtracted before the exponential -- exp(-(d - d_min)/h^2)
+// has the same ratio (numerator and Theta share the factor exp(d_min / h^2)) and cannot underflow
+// to 0/0. One warp per reference row, coalesced, in place (int32 u8 distances / float distances ->
+// float weights of the same size).
+#include <math.h>
+
+#include <algorithm>
+
+#include "sc_internal.h"
+
+namespace scbm {
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) nlm_normalize(void* rows, long long n_refs, int slots, float inv_h2) {
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_refs; r += nw) {
+    T* d = static_cast<T*>(rows) + r * slots;
+    float* w = static_cast<float*>(rows) + r * slots;
+    float dmin = __int_as_float(0x7f800000);
+    for (int k = lane; k < slots; k += 32) {
+      const float v = float(d[k]);
+      // clipped slots hold -1; a float identity distance may round slightly below 0 (clamped)
+      if (v > -0.5f) dmin = fminf(dmin, fmaxf(v, 0.f));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    float theta = 0.f;
+    for (int k = lane; k < slots; k += 32) {
+      const float v = float(d[k]);
+      const float e = v > -0.5f ? expf(-(fmaxf(v, 0.f) - dmin) * inv_h2) : 0.f;
+      w[k] = e;  // in place: the same slot, read before it is written by this lane
+      theta += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) theta += __shfl_xor_sync(0xffffffffu, theta, o);
+    const float inv = 1.f / theta;
+    for (int k = lane; k < slots; k += 32) w[k] *= inv;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_nlm_normalize(const sc_bm_plan_s& p, void* rows, float h, cudaStream_t st, int64_t* launches) {
+  const Geometry& g = p.g;
+  const long long n_refs = (long long)g.ny * g.nx;
+  const int slots = g.Wn * g.Wn;
+  const float inv_h2 = 1.f / (h * h);
+  const long long blocks = std::min<long long>((n_refs + 7) / 8, (long long)p.sm_count * 16);
+  if (launches) *launches += 1;
+  if (g.dtype == SC_DTYPE_U8)
+    nlm_normalize<int32_t><<<unsigned(blocks), 256, 0, st>>>(rows, n_refs, slots, inv_h2);
+  else
+    nlm_normalize<float><<<unsigned(blocks), 256, 0, st>>>(rows, n_refs, slots, inv_h2);
+  return cudaGetLastError();
+}
+
+}  // namespace scbm

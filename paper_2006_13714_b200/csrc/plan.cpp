@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <new>
@@ -269,6 +270,20 @@ sc_status_t sc_bm_run_dense_debug(sc_bm_plan_t p, const void* img, void* dist_al
   if (s != SC_OK) return s;
   return enqueue(p, img, 1, 0, p->g.ny, nullptr, nullptr, dist_all,
                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+sc_status_t sc_bm_nlm_weights(sc_bm_plan_t p, const void* img, float h, float* weights_out, sc_stream_t stream) {
+  if (!p || !img || !weights_out || !(h > 0.f) || !std::isfinite(h)) return SC_ERR_INVALID_ARGUMENT;
+  if (p->g.metric != SC_METRIC_L2) return SC_ERR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(img) & 15) != 0 || (reinterpret_cast<uintptr_t>(weights_out) & 3) != 0)
+    return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // the window distances of every reference (Self-Convolution identity), written into the output
+  s = enqueue(p, img, 1, 0, p->g.ny, nullptr, nullptr, weights_out, st);
+  if (s != SC_OK) return s;
+  return cuda_status(launch_nlm_normalize(*p, weights_out, h, st, &p->launches));
 }
 
 sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_stream_t stream) {

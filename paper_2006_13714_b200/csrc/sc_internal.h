@@ -113,6 +113,9 @@ bool box_supported(const Geometry& g);
 cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
 
+// nlm.cu: NLM weights (Eq. 2 / Prop. 1) from a dense window-distance table, normalised in place.
+cudaError_t launch_nlm_normalize(const sc_bm_plan_s& p, void* rows, float h, cudaStream_t st, int64_t* launches);
+
 // group.cu: patch grouping Y_i from a run's idx table.
 cudaError_t launch_group(const sc_bm_plan_s& p, const void* imgs, int64_t n_images, const int32_t* idx,
                          void* out, cudaStream_t st, int64_t* launches);

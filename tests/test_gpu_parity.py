@@ -674,3 +674,31 @@ def test_ncc_u8_both_kernels(kernel):
     oi, od = oracle.ncc(x, 8, 4, 25, 20)
     for n in range(2):
         check_ncc(x[n], 8, 4, 25, 20, gi[n], gd[n], oi[n], od[n], exact=True, where=f"ncc {kernel} img{n}")
+
+
+# ------------------------------------------------------------------ NLM weights (Eq. 2 / Prop. 1)
+@pytest.mark.parametrize("dtype,C,H,W,b,s,Wn,h", [("u8", 1, 64, 64, 8, 4, 21, 300.0), ("u8", 1, 50, 77, 5, 2, 13, 120.0),
+                                                   ("f32", 1, 48, 52, 7, 2, 15, 0.6), ("f32", 3, 30, 41, 4, 3, 9, 0.5),
+                                                   ("u8", 2, 40, 40, 8, 3, 17, 1e6)])
+def test_nlm_weights_match_oracle(dtype, C, H, W, b, s, Wn, h):
+    rng = np.random.Generator(np.random.PCG64(H + W + b + C))
+    x = synth.random_image(rng, 1, C, H, W, dtype)[0]
+    p = _plan((H, W, C, b, s, Wn, 1), dtype)
+    got = p.nlm_weights(torch.from_numpy(x).cuda(), h).cpu().numpy().astype(np.float64)
+    want = oracle.nlm_weights(x, b, s, Wn, h)
+    np.testing.assert_allclose(got.sum(1), 1.0, rtol=2e-5)
+    assert (got[want == 0] == 0).all()  # clipped slots (float32 may also underflow tiny weights to 0)
+    # float32 weights of the identity distances: relative 1e-4 on weights above 1e-6 of the row
+    m = want > 1e-6
+    np.testing.assert_allclose(got[m], want[m], rtol=1e-4, atol=1e-9)
+
+
+def test_nlm_c2_full_image():
+    cfg = synth.CONFIGS["c2"]
+    x = synth.make_input(cfg)[0]
+    p = _plan(cfg)
+    h = 25.0 / 255.0 * 8  # a sigma-scaled bandwidth for the 8x8 noisy patches
+    got = p.nlm_weights(torch.from_numpy(x).cuda(), h).cpu().numpy().astype(np.float64)
+    want = oracle.nlm_weights(x, cfg.b, cfg.s, cfg.Wn, h)
+    m = want > 1e-6
+    np.testing.assert_allclose(got[m], want[m], rtol=1e-4, atol=1e-9)

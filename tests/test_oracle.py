@@ -409,3 +409,45 @@ def test_ncc_invariants(dtype):
         i2, d2 = oracle.ncc((x * np.float32(4.0)), 4, 3, 9, 10)
     np.testing.assert_array_equal(i1, i2)
     np.testing.assert_allclose(d1, d2, atol=1e-12)
+
+
+# ---------------------------------------------------------------- NLM weights (Eq. 2, Prop. 1)
+def test_nlm_worked_example():
+    """Eq. 2 on the hand-worked distances d = [0, 4, 36, 64] of ref (0,0) (worked_3x3.json) with
+    h^2 = 16: s = exp(-d/16) / sum exp(-d/16); the 3x3 window's 5 clipped slots are 0."""
+    g = json.load(open(GOLD))
+    img = np.array(g["image"], dtype=np.uint8)
+    w = oracle.nlm_weights(img, 2, 2, 3, 4.0)[0].reshape(3, 3)
+    e = np.exp(-np.array(g["d"], float) / 16.0)
+    np.testing.assert_allclose(w[1:, 1:], e / e.sum(), rtol=1e-14)
+    assert (w[0, :] == 0).all() and (w[:, 0] == 0).all()
+
+
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_nlm_limits_and_invariants(dtype):
+    """Rows sum to 1; h -> inf gives uniform weights over the clipped window; h -> 0 puts all the
+    weight on the nearest candidate (the BM top-1, the reference itself on duplicate-free data);
+    the weights are the softmax of -d/h^2 over the window (checked against oracle.bm_dense)."""
+    rng = _rng(61)
+    x = synth.random_image(rng, 1, 2, 20, 23, dtype)[0]
+    b, s, Wn = 4, 3, 7
+    w = oracle.nlm_weights(x, b, s, Wn, 40.0 if dtype == "u8" else 0.4)
+    np.testing.assert_allclose(w.sum(1), 1.0, rtol=1e-12)
+    dense = oracle.bm_dense(x, b, s, Wn)
+    valid = dense >= 0
+    assert ((w > 0) == valid).all()
+    wu = oracle.nlm_weights(x, b, s, Wn, 1e12)
+    np.testing.assert_allclose(wu, valid / valid.sum(1, keepdims=True), rtol=1e-9)
+    w0 = oracle.nlm_weights(x, b, s, Wn, 1e-3)
+    top1, _ = oracle.bm(x, b, s, Wn, 1)
+    ny, nx = oracle.grid(20, 23, b, s)
+    lo = -(Wn // 2)
+    for r in range(ny * nx):
+        ry, rx = (r // nx) * s, (r % nx) * s
+        cy, cx = divmod(int(top1[0, r, 0]), 23)
+        assert w0[r, (cy - ry - lo) * Wn + (cx - rx - lo)] == pytest.approx(1.0)
+        assert (cy, cx) == (ry, rx)
+    h = 40.0 if dtype == "u8" else 0.4
+    z = np.where(valid, -dense / h ** 2, -np.inf)
+    sm = np.exp(z - z.max(1, keepdims=True))
+    np.testing.assert_allclose(w, sm / sm.sum(1, keepdims=True), rtol=1e-12, atol=1e-300)
