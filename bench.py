@@ -168,7 +168,7 @@ def _config_obj(cfg, args):
     return {"workload": cfg.name, "images": cfg.N, "channels": cfg.C, "H": cfg.H, "W": cfg.W,
             "input_dtype": "u8" if cfg.dtype == "u8" else "f32", "patch": cfg.b, "stride": cfg.s,
             "window": cfg.Wn, "K": cfg.K, "sharding": "frames" if cfg.N > 1 else "replicas",
-            "similarity": getattr(args, "metric", "l2"),
+            "similarity": getattr(args, "metric", "l2"), "temporal_radius": getattr(args, "temporal", 0),
             "l2": "flushed between timed steps (256 MiB write); working set > L2"}
 
 
@@ -279,6 +279,8 @@ def main():
     ap.add_argument("--op", default="bm", choices=["bm", "group", "nlm"],
                     help="bm: the block-matching hot path (default); group: patch grouping Y_i of its "
                          "output; nlm: NLM weights (Eq. 2) of the config's first image")
+    ap.add_argument("--temporal", type=int, default=0,
+                    help="3D / temporal search radius T: candidates in frames f-T..f+T of the batch")
     ap.add_argument("--nlm-h", type=float, default=0.0, help="NLM bandwidth (default: 1.0 * sqrt(b^2 C) * value scale)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf"],
                     help="force the matching kernel (default: the plan's choice)")
@@ -312,6 +314,8 @@ def main():
     del x_all
     x = torch.from_numpy(x_host).cuda()
     plan = Plan(cfg.H, cfg.W, cfg.C, cfg.b, cfg.s, cfg.Wn, cfg.K, cfg.dtype, metric=args.metric)
+    if args.temporal > 0:
+        plan.set_temporal(args.temporal)
     if args.kernel != "auto":
         plan.set_kernel({"simt": 0, "tc": 1, "warp": 2, "box": 3, "boxf": 4}[args.kernel])
     info = plan.info()
@@ -359,6 +363,9 @@ def main():
     pairs_per_image = info["total_candidates"]
     n_images_total = cfg.N if cfg.N > 1 else ws
     pairs_step = pairs_per_image * n_images_total
+    if args.temporal > 0:  # every reference also searches the frames f-T..f+T of its rank's shard
+        frames_searched = sum(min(nloc - 1, f + args.temporal) - max(0, f - args.temporal) + 1 for f in range(nloc))
+        pairs_step = pairs_per_image * frames_searched * ws
     refs_step = info["n_refs"] * n_images_total
     value = pairs_step / (ms / 1e3)
 
@@ -369,8 +376,9 @@ def main():
     # product image once, s^2 C per pair (its 4x4 block sums are shared by 2 x 2 references)
     # (c5); the float box kernel correlates one s-column strip per reference and offset, b s C
     mac_pair = {3: cfg.s * cfg.s * cfg.C, 4: cfg.b * cfg.s * cfg.C}.get(info["kernel"], cfg.b * cfg.b * cfg.C)
-    macs_launch = pairs_per_image * nloc * mac_pair  # algorithmic MACs per rank-step
-    macs_direct = pairs_per_image * nloc * cfg.b * cfg.b * cfg.C
+    pairs_rank = pairs_step // max(1, ws) if args.temporal > 0 else pairs_per_image * nloc
+    macs_launch = pairs_rank * mac_pair  # algorithmic MACs per rank-step
+    macs_direct = pairs_rank * cfg.b * cfg.b * cfg.C
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if info["kernel"] == 1:
         peak = 2.0 * peaks["bf16_tflops"]  # int8 tcgen05 = 2x the measured bf16 (guide's nominal ratio)
@@ -413,7 +421,7 @@ def main():
 
     # end-to-end through the public API with host buffers (pinned), copies inside the timing
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.temporal == 0:  # the host path has no temporal mode
         xh = torch.from_numpy(x_host).pin_memory()
         hi = torch.empty((nloc, info["n_refs"], cfg.K), dtype=torch.int32).pin_memory()
         hd = torch.empty((nloc, info["n_refs"], cfg.K),

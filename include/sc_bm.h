@@ -169,6 +169,16 @@ sc_status_t sc_bm_group(sc_bm_plan_t plan, const void* imgs, int64_t n_images, c
 sc_status_t sc_bm_nlm_weights(sc_bm_plan_t plan, const void* img, float h, float* weights_out,
                               sc_stream_t stream);
 
+/*
+ * 3D / temporal search (the video setting of PAPER.md:661, 697): with T > 0, the candidates of a
+ * reference in image f of a sc_bm_run_batch / sc_bm_run_rows call are the window positions of
+ * images f-T .. f+T of that call (clipped to the batch), and idx_out holds the BATCH-GLOBAL
+ * index frame * H * W + cy * W + cx (ties by it: earlier frames first). uint8, b = 8, stride 4,
+ * one channel, L2 metric, (2T+1) Wn^2 <= 4096 (else SC_ERR_UNSUPPORTED); T = 0 (default)
+ * restores per-image search. sc_bm_run_host is unsupported with T > 0.
+ */
+sc_status_t sc_bm_set_temporal(sc_bm_plan_t plan, int32_t T);
+
 /* Plan geometry and bookkeeping. */
 sc_status_t sc_bm_plan_info(sc_bm_plan_t plan, sc_bm_info_t* info);
 

@@ -49,6 +49,7 @@ def lib():
         L.sco_pair_dist.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
         L.sco_num_threads.restype = ci
         L.sco_ncc_rows.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, dp, ci]
+        L.sco_bm_temporal.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, vp, ci]
         L.sco_nlm_weights.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ctypes.c_double, dp, ci]
         _lib = L
     return _lib
@@ -119,6 +120,22 @@ def ncc(img: np.ndarray, b: int, s: int, Wn: int, K: int, *, images=None, rows=N
                             dist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), nthreads)
     if rc != 0:
         raise ValueError("oracle.ncc: invalid arguments")
+    return idx, dist
+
+
+def bm_temporal(img: np.ndarray, b: int, s: int, Wn: int, K: int, T: int, nthreads: int = 0):
+    """Temporal BM over a batch [N, C, H, W]: candidates in frames f-T..f+T; idx batch-global
+    (frame * H * W + cy * W + cx). Returns (idx int32, dist int32 | float64) [N, refs, K]."""
+    a = np.ascontiguousarray(img)
+    N, C, H, W = a.shape
+    ny, nx = grid(H, W, b, s)
+    idx = np.empty((N, ny * nx, K), dtype=np.int32)
+    code = _dtype_code(a)
+    dist = np.empty((N, ny * nx, K), dtype=np.int32 if code == U8 else np.float64)
+    rc = lib().sco_bm_temporal(a.ctypes.data, code, N, C, H, W, b, s, Wn, K, T,
+                               idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), dist.ctypes.data, nthreads)
+    if rc != 0:
+        raise ValueError("oracle.bm_temporal: invalid arguments")
     return idx, dist
 
 

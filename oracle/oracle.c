@@ -388,6 +388,75 @@ int sco_ncc_rows(const void* imgs, int dtype, int C, int H, int W, int b, int s,
 }
 
 /*
+ * 3D / temporal block matching (the video setting of PAPER.md:661, 697):
+ * Eq. 3 with the candidate set of a reference in frame f = the clipped window positions of
+ * frames f-T .. f+T of the batch (clipped to [0, n_img)), idx = frame * H * W + cy * W + cx
+ * (batch-global), ties by (d, idx). uint8 / float as sco_bm_rows; all references of all frames.
+ */
+int sco_bm_temporal(const void* imgs, int dtype, int n_img, int C, int H, int W, int b, int s, int Wn,
+                    int K, int T, int32_t* idx_out, void* dist_out, int nthreads) {
+    if (!imgs || !idx_out || !dist_out || b < 1 || s < 1 || Wn < 1 || K < 1 || C < 1 || H < b ||
+        W < b || n_img < 1 || T < 0)
+        return -1;
+    const int ny = grid_n(H, b, s), nx = grid_n(W, b, s);
+    const int lo = -(Wn / 2), hi = Wn - 1 - Wn / 2;
+    const long long refs_per_img = (long long)ny * nx, total = refs_per_img * n_img;
+    const size_t img_elems = (size_t)C * H * W;
+    const size_t esz = dtype == SCO_U8 ? 1 : dtype == SCO_F32 ? 4 : 8;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel
+    {
+        sco_key* keys = (sco_key*)malloc(sizeof(sco_key) * (size_t)Wn * (size_t)Wn * (size_t)(2 * T + 1));
+#pragma omp for schedule(dynamic, 16)
+        for (long long t = 0; t < total; ++t) {
+            const int f = (int)(t / refs_per_img);
+            const long long j = t % refs_per_img;
+            const int ry = (int)(j / nx) * s, rx = (int)(j % nx) * s;
+            const int cy0 = ry + lo < 0 ? 0 : ry + lo, cy1 = ry + hi > H - b ? H - b : ry + hi;
+            const int cx0 = rx + lo < 0 ? 0 : rx + lo, cx1 = rx + hi > W - b ? W - b : rx + hi;
+            const char* rimg = (const char*)imgs + (size_t)f * img_elems * esz;
+            int cnt = 0;
+            for (int fr = f - T; fr <= f + T; ++fr) {
+                if (fr < 0 || fr >= n_img) continue;
+                const char* cimg = (const char*)imgs + (size_t)fr * img_elems * esz;
+                for (int cy = cy0; cy <= cy1; ++cy)
+                    for (int cx = cx0; cx <= cx1; ++cx) {
+                        /* direct differences between frame f's reference and frame fr's candidate */
+                        int64_t acc = 0;
+                        double accd = 0.0;
+                        for (int c = 0; c < C; ++c)
+                            for (int l = 0; l < b; ++l)
+                                for (int m = 0; m < b; ++m) {
+                                    const size_t base = (size_t)c * H * W;
+                                    const double vr = px(rimg, dtype, base + (size_t)(ry + l) * W + rx + m);
+                                    const double vc = px(cimg, dtype, base + (size_t)(cy + l) * W + cx + m);
+                                    accd += (vr - vc) * (vr - vc);
+                                    if (dtype == SCO_U8) acc += (int64_t)(vr - vc) * (int64_t)(vr - vc);
+                                }
+                        keys[cnt].di = acc;
+                        keys[cnt].d = accd;
+                        keys[cnt].idx = (int32_t)((long long)fr * H * W + (long long)cy * W + cx);
+                        ++cnt;
+                    }
+            }
+            qsort(keys, (size_t)cnt, sizeof(sco_key), dtype == SCO_U8 ? cmp_key_int : cmp_key_dbl);
+            const long long o = t * K;
+            for (int k = 0; k < K; ++k) {
+                idx_out[o + k] = k < cnt ? keys[k].idx : -1;
+                if (dtype == SCO_U8) ((int32_t*)dist_out)[o + k] = k < cnt ? (int32_t)keys[k].di : INT32_MAX;
+                else ((double*)dist_out)[o + k] = k < cnt ? keys[k].d : INFINITY;
+            }
+        }
+        free(keys);
+    }
+    return 0;
+}
+
+/*
  * NLM weights, Eq. 2 restricted to the search window (footnote 2,
  * PAPER.md:280; the SAME clipped window as BM):
  *   s_i(j) = exp(-||X_j - X_i||_F^2 / h^2) / Theta_i,  Theta_i = sum_j exp(-||X_j - X_i||^2 / h^2)

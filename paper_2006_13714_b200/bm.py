@@ -23,7 +23,7 @@ SC_METRIC_L2, SC_METRIC_NCC = 0, 1
 EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
             "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group",
-            "sc_bm_nlm_weights"]
+            "sc_bm_nlm_weights", "sc_bm_set_temporal"]
 
 
 class ScError(RuntimeError):
@@ -79,6 +79,7 @@ def load_library():
     L.sc_bm_get_timing.argtypes = [vp, ctypes.POINTER(Timing)]
     L.sc_bm_group.argtypes = [vp, vp, i64, vp, vp, vp]
     L.sc_bm_nlm_weights.argtypes = [vp, vp, ctypes.c_float, vp, vp]
+    L.sc_bm_set_temporal.argtypes = [vp, i32]
     for fn in EXPORTED:
         if fn != "sc_status_string":
             getattr(L, fn).restype = ci
@@ -139,6 +140,10 @@ class Plan:
         out = Timing()
         _check("sc_bm_get_timing", self._lib.sc_bm_get_timing(self._h, ctypes.byref(out)))
         return {k: getattr(out, k) for k, _ in out._fields_}
+
+    def set_temporal(self, T: int):
+        """Temporal search radius over the frames of a batch call (idx becomes batch-global)."""
+        _check("sc_bm_set_temporal", self._lib.sc_bm_set_temporal(self._h, T))
 
     def set_kernel(self, kernel: int):
         _check("sc_bm_set_kernel", self._lib.sc_bm_set_kernel(self._h, kernel))

@@ -50,6 +50,9 @@ struct BoxArgs {
   int RH, WP, PL;  // staged region rows, words per region row, words per byte-shifted copy
   int nblk;        // dy blocks of VY offsets
   int scr;         // per-warp scratch words
+  int T;           // temporal search radius (0: the reference's own frame only)
+  int n_frames;    // frames reachable from imgs (temporal search: the whole batch)
+  int frame0;      // batch index of the launch's first reference frame (temporal search)
   int rb;          // 32-bit keys: window-relative index bits
   uint32_t dsat;   // 32-bit keys: distance saturation value
   int* fix_count;
@@ -80,7 +83,12 @@ __device__ __forceinline__ int dp4(uint32_t x, uint32_t y, int acc) {
 // and re-ranks them exactly (ncc.cuh) from the staged bytes.
 // WNC: the window side when known at compile time (0 = runtime): the window geometry, key widths
 // and loop bounds then become immediates (no per-round constant reloads in the survivor loop)
-template <int NY, int VY, int KR, int WPC = 0, bool NCC = false, int WNC = 0>
+// TEMP (3D / temporal search): the candidates of a reference in frame f are
+// the window positions of frames f-T .. f+T of the batch (PAPER.md:661/697's video setting); the
+// region is restaged per frame (time offsets visited centre-out: 0, +1, -1, ...), the keys'
+// window-relative index becomes (tau + T) Wn^2 + slot, and idx is the batch-global
+// frame * H * W + cy * W + cx.
+template <int NY, int VY, int KR, int WPC = 0, bool NCC = false, int WNC = 0, bool TEMP = false>
 __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) bm_box_kernel(BoxArgs a) {
   const int WP = WPC > 0 ? WPC : a.WP;
   constexpr int kRB = WNC > 0 ? (WNC * WNC <= 2 ? 2 : 32 - __builtin_clz(unsigned(WNC * WNC - 1))) : 0;
@@ -101,7 +109,9 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
 
   // ---- a0: four byte-shifted copies of the centred region. Copy k, row r, word w holds
   // region bytes [4w+k, 4w+k+3] as int8 x' = x ^ 0x80 = x - 128 (0 outside the image).
-  const uint8_t* img = a.imgs + size_t(f) * a.H * a.W;
+  const int fref = TEMP ? a.frame0 + f : f;  // frame of the references (index into imgs)
+  auto stage = [&](int frame) {
+  const uint8_t* img = a.imgs + size_t(frame) * a.H * a.W;
   for (int e = threadIdx.x; e < a.PL; e += blockDim.x) {
     const int r = e / WP, w = e - r * WP;
     const int y = Ybase + r, x = Xbase + 4 * w;
@@ -126,10 +136,13 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     sm[2 * a.PL + e] = __funnelshift_r(u0, u1, 16);
     sm[3 * a.PL + e] = __funnelshift_r(u0, u1, 24);
   }
+  };
+  stage(fref);
   __syncthreads();
 
   const int iy0 = iy_first + warp * NY;
-  if (iy0 >= a.iy_end) return;
+  const bool wact = iy0 < a.iy_end;  // warp-uniform (temporal: every warp joins the restaging)
+  if (!TEMP && !wact) return;
   const int ix = ix_first + lane;
   const bool lane_ok = lane < kBoxRefsX && ix < a.nx;
   const int rx = ix * 4;
@@ -170,6 +183,19 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
 
   const int b0 = (0 - lo) / VY;  // dy block holding dy = 0
   const int span = max(-lo, hi);
+  const int nt = TEMP ? 2 * a.T + 1 : 1;
+  for (int kt = 0; kt < nt; ++kt) {  // time offsets, centre-out (TEMP only; else one pass)
+  const int tau = centre_out(kt);
+  if (TEMP) {
+    if (fref + tau < 0 || fref + tau >= a.n_frames) continue;  // CTA-uniform
+    if (kt > 0) {
+      __syncthreads();  // every warp is done with the previous frame's region
+      stage(fref + tau);
+      __syncthreads();
+    }
+    if (!wact) continue;
+  }
+  const int relt = TEMP ? (tau + a.T) * Wn * Wn : 0;  // window-relative index offset of this frame
   for (int kb = 0; kb < 2 * nblk; ++kb) {
     const int bb = b0 + centre_out(kb);
     if (bb < 0 || bb >= nblk) continue;
@@ -298,7 +324,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           pend[q] |= bits << (half * VY);
         }
       }
-      const int rel0 = (dy0 - lo) * Wn + off;
+      const int rel0 = relt + (dy0 - lo) * Wn + off;
       if (half == 0) {
         rel0p = rel0;
         half = 1;
@@ -309,6 +335,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     }
     if (half == 1) flush(0);  // a lone last group (its bits are in the first half)
   }
+  }  // time offsets
 
   const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
   const int nref = min(kBoxRefsX, a.nx - ix_first);
@@ -390,9 +417,12 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         if (kq == k) kk = v;
       }
       if (e < nref * a.K) {
-        const int rel = key32.rel(kk);
+        int rel = key32.rel(kk);
+        const int tsl = TEMP ? rel / (Wn * Wn) : 0;  // frame slot tau + T
+        rel -= tsl * Wn * Wn;
         const int dyy = rel / Wn, dxx = rel - dyy * Wn;
-        a.idx_out[row0 * a.K + e] = (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
+        a.idx_out[row0 * a.K + e] = (TEMP ? (fref + tsl - a.T) * a.H * a.W : 0) +
+                                    (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
         a.dist_out[row0 * a.K + e] = key32.dist(kk);
       }
     }
@@ -407,9 +437,12 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     for (int e = lane; e < nref * a.K; e += 32) {
       const int j = e / a.K, k = e - j * a.K;
       const uint32_t kk = scratch[j * (KR + 1) + k];
-      const int rel = key32.rel(kk);
+      int rel = key32.rel(kk);
+      const int tsl = TEMP ? rel / (Wn * Wn) : 0;  // frame slot tau + T
+      rel -= tsl * Wn * Wn;
       const int dyy = rel / Wn, dxx = rel - dyy * Wn;
-      a.idx_out[row0 * a.K + e] = (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
+      a.idx_out[row0 * a.K + e] = (TEMP ? (fref + tsl - a.T) * a.H * a.W : 0) +
+                                  (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
       a.dist_out[row0 * a.K + e] = key32.dist(kk);
     }
     __syncwarp();
@@ -428,10 +461,10 @@ size_t box_layout(const Geometry& g, int NY, int VY, int KR, BoxArgs* a) {
   return size_t(4 * a->PL + kBoxWarps * a->scr) * 4;
 }
 
-template <int NY, int VY, int KR, int WPC = 0, bool NCC = false, int WNC = 0>
+template <int NY, int VY, int KR, int WPC = 0, bool NCC = false, int WNC = 0, bool TEMP = false>
 cudaError_t launch_box_t(const BoxArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + kBoxWarps * NY - 1) / (kBoxWarps * NY);
-  auto k = bm_box_kernel<NY, VY, KR, WPC, NCC, WNC>;
+  auto k = bm_box_kernel<NY, VY, KR, WPC, NCC, WNC, TEMP>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<dim3(a.tiles_x * tiles_y, F), kBoxWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
@@ -440,6 +473,17 @@ cudaError_t launch_box_t(const BoxArgs& a, int F, size_t smem, cudaStream_t st) 
 }  // namespace
 
 int box_key_bits(const Geometry& g) { return std::max(2, key32_rel_bits(g.Wn)); }
+
+// temporal search: the window-relative index spans (2T+1) Wn^2 slots
+int box_key_bits_t(const Geometry& g, int T) {
+  int rb = 2;
+  while ((1 << rb) < (2 * T + 1) * g.Wn * g.Wn) ++rb;
+  return rb;
+}
+
+bool box_temporal_supported(const Geometry& g, int T) {
+  return T == 0 || (g.metric == SC_METRIC_L2 && box_supported(g) && box_key_bits_t(g, T) <= 12);
+}
 
 bool box_supported(const Geometry& g) {
   if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.s != 4 || g.C != 1 || g.K > 32) return false;
@@ -466,6 +510,25 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   a.fix_list = p.ws.fix_list;
   const int vy = box_vy(g), kr = g.KP <= 16 ? 16 : 32;
   const size_t smem = box_layout(g, 2, vy, kr, &a);
+  if (p.T > 0) {  // temporal search (L2): batch-wide frame access, wider keys, runtime geometry
+    a.imgs = static_cast<const uint8_t*>(p.batch_base);
+    a.T = p.T;
+    a.frame0 = int(p.batch_f0);
+    a.n_frames = int(p.batch_n);
+    a.rb = box_key_bits_t(g, p.T);
+    a.dsat = uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
+    cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    if (kr == 16 && vy == 11) e = launch_box_t<2, 11, 16, 0, false, 0, true>(a, F, smem, st);
+    else if (kr == 16 && vy == 7) e = launch_box_t<2, 7, 16, 0, false, 0, true>(a, F, smem, st);
+    else if (kr == 16) e = launch_box_t<2, 8, 16, 0, false, 0, true>(a, F, smem, st);
+    else if (vy == 11) e = launch_box_t<2, 11, 32, 0, false, 0, true>(a, F, smem, st);
+    else if (vy == 7) e = launch_box_t<2, 7, 32, 0, false, 0, true>(a, F, smem, st);
+    else e = launch_box_t<2, 8, 32, 0, false, 0, true>(a, F, smem, st);
+    if (launches) *launches += 2;
+    if (e != cudaSuccess) return e;
+    return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
+  }
   if (g.metric == SC_METRIC_NCC) {  // K + 8 <= 32: no saturation, no fix-up
     if (launches) *launches += 1;
     if (g.Wn == 33 && g.KP <= 24) return launch_box_t<2, 11, 24, 40, true, 33>(a, F, box_layout(g, 2, vy, 24, &a), st);

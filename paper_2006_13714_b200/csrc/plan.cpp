@@ -92,6 +92,9 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
     cudaError_t e = box ? cudaSuccess : launch_norm(*p, src, F, st, &p->launches);
     if (e != cudaSuccess) return cuda_status(e);
     if (ev) cudaEventRecord(ev[1], st);
+    p->batch_base = imgs;  // temporal search reads the neighbouring frames of the whole batch
+    p->batch_f0 = f0;
+    p->batch_n = n;
     int32_t* io = idx ? idx + f0 * out_elems : nullptr;
     void* dd = dist ? static_cast<char*>(dist) + f0 * out_elems * 4 : nullptr;
     if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
@@ -302,6 +305,7 @@ sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_s
 sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images, int32_t* h_idx,
                            void* h_dist, sc_stream_t stream) {
   if (!p || !h_imgs || !h_idx || !h_dist || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (p->T > 0) return SC_ERR_UNSUPPORTED;  // chunked staging has no neighbouring frames
   sc_status_t s = check_device(p);
   if (s != SC_OK) return s;
   if (n_images == 0) return SC_OK;
@@ -389,8 +393,17 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
   return SC_OK;
 }
 
+sc_status_t sc_bm_set_temporal(sc_bm_plan_t p, int32_t T) {
+  if (!p || T < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (T > 0 && !box_temporal_supported(p->g, T)) return SC_ERR_UNSUPPORTED;
+  p->T = T;
+  if (T > 0) p->kernel = SC_KERNEL_BOX;  // the only matcher with a temporal window
+  return SC_OK;
+}
+
 sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
+  if (p->T > 0 && kernel != SC_KERNEL_BOX) return SC_ERR_UNSUPPORTED;
   if (p->g.metric == SC_METRIC_NCC && kernel != SC_KERNEL_BOXF && kernel != SC_KERNEL_BOX) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;

@@ -72,6 +72,9 @@ struct sc_bm_plan_s {
   scbm::HostStaging host;
   scbm::Timing timing;
   int64_t launches = 0;
+  int T = 0;                          // temporal search radius (sc_bm_set_temporal)
+  const void* batch_base = nullptr;   // temporal search: the run's whole batch ...
+  int64_t batch_f0 = 0, batch_n = 0;  // ... the current chunk's first frame and the batch size
   int64_t min_cand = 0, max_cand = 0, total_cand = 0;
 };
 
@@ -110,6 +113,7 @@ size_t lanes_smem_bytes(const Geometry& g, int nwy);
 
 // bm_box.cu: the box-sum matcher (SC_KERNEL_BOX; u8, b = 8, s = 4, C = 1, K <= 32).
 bool box_supported(const Geometry& g);
+bool box_temporal_supported(const Geometry& g, int T);
 cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
 

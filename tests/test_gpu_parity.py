@@ -702,3 +702,53 @@ def test_nlm_c2_full_image():
     want = oracle.nlm_weights(x, cfg.b, cfg.s, cfg.Wn, h)
     m = want > 1e-6
     np.testing.assert_allclose(got[m], want[m], rtol=1e-4, atol=1e-9)
+
+
+# ------------------------------------------------------------------ 3D / temporal search
+@pytest.mark.parametrize("N,H,W,Wn,K,T", [(4, 70, 150, 21, 16, 1), (5, 60, 97, 15, 12, 2), (3, 90, 130, 33, 16, 1),
+                                          (2, 40, 64, 9, 32, 1), (6, 48, 80, 13, 8, 3)])
+def test_temporal_matches_oracle(N, H, W, Wn, K, T):
+    rng = np.random.Generator(np.random.PCG64(N * H + W + T))
+    x = synth.random_image(rng, N, 1, H, W, "u8")
+    p = _plan((H, W, 1, 8, 4, Wn, K), "u8")
+    p.set_temporal(T)
+    gi, gd = _run(p, x)
+    oi, od = oracle.bm_temporal(x, 8, 4, Wn, K, T)
+    check_u8(gi, gd, oi, od, f"temporal N{N} {H}x{W} Wn{Wn} K{K} T{T}")
+
+
+def test_temporal_c5_frames_and_saturation():
+    """The c5 video (random-walk crops): every reference's K best over frames f-1..f+1, bit-exact
+    on sampled rows; a saturated video exercises the temporal fix-up."""
+    cfg = synth.CONFIGS["c5"]
+    x = synth.make_input(cfg, n_frames=3)
+    p = _plan(cfg)
+    p.set_temporal(1)
+    gi, gd = _run(p, x)
+    oi, od = oracle.bm_temporal(x[:, :, :64, :], cfg.b, cfg.s, cfg.Wn, cfg.K, 1)  # rows whose windows stay in 64 rows
+    nx = p.nx
+    for f in range(3):
+        for r in range(3):  # reference rows 0..2 of the crop see the same candidates as in the full frame
+            sl = slice(r * nx, (r + 1) * nx)
+            go = gi[f, sl].copy()
+            fr, pix = go // (cfg.H * cfg.W), go % (cfg.H * cfg.W)
+            remap = fr * (64 * cfg.W) + pix  # batch-global idx of the 64-row crop
+            np.testing.assert_array_equal(remap, oi[f, sl])
+            np.testing.assert_array_equal(gd[f, sl], od[f, sl])
+    rng = np.random.Generator(np.random.PCG64(3))
+    xs = (rng.integers(0, 2, size=(3, 1, 48, 96)) * 255).astype(np.uint8)
+    p = _plan((48, 96, 1, 8, 4, 21, 16), "u8")
+    p.set_temporal(1)
+    gi, gd = _run(p, xs)
+    oi, od = oracle.bm_temporal(xs, 8, 4, 21, 16, 1)
+    check_u8(gi, gd, oi, od, "temporal saturated")
+
+
+def test_temporal_rejects():
+    from paper_2006_13714_b200.bm import ScError
+    for args, dt, T in [((64, 64, 1, 8, 3, 21, 16), "u8", 1), ((64, 64, 1, 8, 4, 33, 16), "u8", 2),
+                        ((64, 64, 1, 8, 4, 21, 16), "f32", 1)]:
+        p = _plan(args, dt)
+        with pytest.raises(ScError) as e:
+            p.set_temporal(T)
+        assert e.value.code == 2

@@ -17,7 +17,7 @@ import pytest
 
 import oracle
 from paper_2006_13714_b200 import synth
-from tests.bm_numpy import bm_np, ncc_np
+from tests.bm_numpy import all_patches as _all_patches, bm_np, ncc_np
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "worked_3x3.json")
 
@@ -451,3 +451,46 @@ def test_nlm_limits_and_invariants(dtype):
     z = np.where(valid, -dense / h ** 2, -np.inf)
     sm = np.exp(z - z.max(1, keepdims=True))
     np.testing.assert_allclose(w, sm / sm.sum(1, keepdims=True), rtol=1e-12, atol=1e-300)
+
+
+# ---------------------------------------------------------------- 3D / temporal search
+def test_temporal_reduces_to_spatial_and_exhaustive():
+    """T = 0 is per-frame BM (idx offset by frame * H * W); T = 1 on a tiny video equals an
+    independent numpy brute force over the stacked candidate sets."""
+    rng = _rng(71)
+    x = rng.integers(0, 256, size=(3, 1, 12, 13), dtype=np.uint8)
+    i0, d0 = oracle.bm_temporal(x, 4, 2, 5, 6, 0)
+    i1, d1 = oracle.bm(x, 4, 2, 5, 6)
+    np.testing.assert_array_equal(i0, i1 + (np.arange(3) * 12 * 13)[:, None, None])
+    np.testing.assert_array_equal(d0, d1)
+    it, dt = oracle.bm_temporal(x, 4, 2, 5, 7, 1)
+    P = [_all_patches(x[f].astype(np.int64), 4) for f in range(3)]
+    ny, nx = oracle.grid(12, 13, 4, 2)
+    for f in range(3):
+        for r in range(ny * nx):
+            ry, rx = (r // nx) * 2, (r % nx) * 2
+            cand = []
+            for fr in range(max(0, f - 1), min(2, f + 1) + 1):
+                for cy in range(max(0, ry - 2), min(8, ry + 2) + 1):
+                    for cx in range(max(0, rx - 2), min(9, rx + 2) + 1):
+                        d = int(((P[f][ry, rx] - P[fr][cy, cx]) ** 2).sum())
+                        cand.append((d, fr * 156 + cy * 13 + cx))
+            cand.sort()
+            np.testing.assert_array_equal(it[f, r], [c[1] for c in cand[:7]])
+            np.testing.assert_array_equal(dt[f, r], [c[0] for c in cand[:7]])
+
+
+def test_temporal_translated_video():
+    """A sequence of pure translations: the best match of a reference in frame f within frame f+1
+    is the translated position, at distance 0 (the motion-compensated neighbour)."""
+    base = _rng(72).integers(0, 256, size=(40, 44), dtype=np.uint8)
+    x = np.stack([base[2 * f:2 * f + 30, f:f + 32] for f in range(3)])[:, None].copy()
+    idx, dist = oracle.bm_temporal(x, 8, 4, 9, 3, 1)
+    ny, nx = oracle.grid(30, 32, 8, 4)
+    for r in range(ny * nx):
+        ry, rx = (r // nx) * 4, (r % nx) * 4
+        if ry + 2 > 30 - 8 or rx + 1 > 32 - 8:  # the motion-compensated position leaves frame 0
+            continue
+        # frame 1's content at (y, x) is frame 0's at (y + 2, x + 1): frame 1 ref -> frame 0 (ry+2, rx+1)
+        want = 0 * 30 * 32 + (ry + 2) * 32 + rx + 1
+        assert want in idx[1, r].tolist() and dist[1, r, 0] == 0
