@@ -225,15 +225,23 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         unsigned bits = pend[q];
         if (__any_sync(0xffffffffu, bits != 0u)) {
           const uint32_t* sc = scratch + q * (64 * VY) + lane;
+          const int relB = rel0c - VY * Wn;
+          const uint32_t sc_s = uint32_t(__cvta_generic_to_shared(sc));
           while (__any_sync(0xffffffffu, bits != 0u)) {
-            const int i = 31 - __clz(bits | 1u);  // any survivor (insertion order is irrelevant)
-            const uint32_t d = sc[32 * i];        // safe address for every lane
-            const int rel = i < VY ? rel0p + i * Wn : rel0c + (i - VY) * Wn;
+            // any survivor (insertion order is irrelevant): the highest set bit (bfind; ~0 if none,
+            // clamped to a valid scratch row so the unconditional load of every lane stays in bounds);
+            // lanes without a survivor insert the no-op key ~0 (branch-free round)
+            uint32_t pos, d;
+            asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(bits));
+            const int i = int(min(pos, uint32_t(2 * VY - 1)));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sc_s + 128u * uint32_t(i)));
+            const int rel = (i < VY ? rel0p : relB) + i * Wn;
+            const uint32_t none = bits ? 0u : 0xffffffffu;
             uint32_t key;
             if constexpr (NCC)  // float bits of the score, quantised; rel + 1 (0 = sentinel)
-              key = bits ? ((d >> (rbits - 1)) << rbits) | uint32_t(rel + 1) : 0xffffffffu;
+              key = (((d >> (rbits - 1)) << rbits) | uint32_t(rel + 1)) | none;
             else
-              key = bits ? (min(d, dsat) << rbits) | uint32_t(rel) : 0xffffffffu;
+              key = ((min(d, dsat) << rbits) | uint32_t(rel)) | none;
             bits &= ~(1u << i);
             rt[q].insert(key);
           }
