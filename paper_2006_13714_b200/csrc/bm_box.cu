@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           const uint32_t* sc = scratch + q * (64 * VY) + lane;
           const int relB = rel0c - VY * Wn;
           const uint32_t sc_s = uint32_t(__cvta_generic_to_shared(sc));
+          const uint32_t dthr = uint32_t(thr[q] + nr[q]);  // L2: d = dthr - staged slack
           while (__any_sync(0xffffffffu, bits != 0u)) {
             // any survivor (insertion order is irrelevant): the highest set bit (bfind; ~0 if none,
             // clamped to a valid scratch row so the unconditional load of every lane stays in bounds);
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             if constexpr (NCC)  // float bits of the score, quantised; rel + 1 (0 = sentinel)
               key = (((d >> (rbits - 1)) << rbits) | uint32_t(rel + 1)) | none;
             else
-              key = ((min(d, dsat) << rbits) | uint32_t(rel)) | none;
+              key = ((min(dthr - d, dsat) << rbits) | uint32_t(rel)) | none;
             bits &= ~(1u << i);
             rt[q].insert(key);
           }
@@ -326,9 +327,10 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         const unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);
         if (__any_sync(0xffffffffu, bits != 0u)) {
           uint32_t* sc = scratch + q * (64 * VY) + half * (32 * VY) + lane;
-          const int dthr = thr[q] + nr[q];  // d = d' + ||X_i||^2 = dthr - t (exact, >= 0)
+          // the slack t is staged; the flush recovers d = d' + ||X_i||^2 = (thr + n_r) - t (exact,
+          // thr does not change between the two staged groups of a flush)
 #pragma unroll
-          for (int i = 0; i < VY; ++i) sc[32 * i] = NCC ? uint32_t(t[i]) : uint32_t(dthr - t[i]);
+          for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(t[i]);
           pend[q] |= bits << (half * VY);
         }
       }
