@@ -314,14 +314,14 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             const int nn = D[4 * q + i] + __shfl_down_sync(0xffffffffu, D[4 * q + i], 1);  // n_c
             const float sc = nrs[q] - (nn > 0 ? float(cc) * rsqrtf(float(nn)) : 0.f);
             t[i] = __float_as_int(fmaxf(sc, 0.f));
-            fails = (fails << 1) + (__float_as_uint(thrf[q] - sc) >> 31);
+            fails = __funnelshift_l(__float_as_uint(thrf[q] - sc), fails, 1);  // (fails << 1) | sign
           }
         } else {
 #pragma unroll
           for (int i = VY - 1; i >= 0; --i) {
             const int e = D[4 * q + i] - 2 * U[q][i];
             t[i] = thr[q] - e - __shfl_down_sync(0xffffffffu, e, 1);
-            fails = (fails << 1) + (uint32_t(t[i]) >> 31);
+            fails = __funnelshift_l(uint32_t(t[i]), fails, 1);  // (fails << 1) | sign(t): one SHF
           }
         }
         const unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
           dpv[i] = hcombine<NS, WL, S>(ef, ep);  // d' = n_c - 2 C
         }
         // slack thr - d' >= 0 (or +inf): the candidate may enter the top-KP
-        fails = (fails << 1) + (__float_as_uint(thr - dpv[i]) >> 31);
+        fails = __funnelshift_l(__float_as_uint(thr - dpv[i]), fails, 1);  // (fails << 1) | sign
       }
       unsigned bits = ~fails & ((lane_ok && colok) ? rows : 0u);
       if (__any_sync(0xffffffffu, bits != 0u)) {
