@@ -457,6 +457,20 @@ def main():
         tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device="cuda")
         dist.all_reduce(tg, op=dist.ReduceOp.MAX)
         gather = {"ms": tg.item(), "bytes_per_rank": int(2 * gi.numel() * 4), "backend": "nccl"}
+        # compute + gather pipelined per frame chunk (the gather of chunk c overlaps chunk c+1)
+        from paper_2006_13714_b200.dist import run_frames_pipelined
+        chunk = max(1, nloc // 4)
+        if nloc % chunk == 0:
+            dist.barrier()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record()
+            run_frames_pipelined(lambda fr: plan.run(fr), x, rank, ws, chunk, local=True)
+            p1.record()
+            torch.cuda.synchronize()
+            tp = torch.tensor([p0.elapsed_time(p1)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+            gather["compute_plus_gather_pipelined_ms"] = tp.item()
+            gather["chunk_frames"] = chunk
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

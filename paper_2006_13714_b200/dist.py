@@ -86,3 +86,45 @@ def run_bands_sharded(run_rows: Callable, img, n_ref_rows: int, n_ref_x: int, ra
     counts = [(e - s) * n_ref_x for s, e in balanced_ranges(n_ref_rows, world)]
     gi, gd = gather_tables([idx[0], dist_[0]], counts, group)
     return gi[None], gd[None]
+
+
+def run_frames_pipelined(run: Callable, frames, rank: int, world: int, chunk: int, group=None,
+                         local: bool = False):
+    """Frame-parallel BM with the table gather pipelined behind the compute.
+
+    Each rank owns frames [rank * per, (rank + 1) * per) (per = n / world, n divisible by
+    world * chunk) and processes them in chunks of `chunk` frames; right after chunk c is
+    enqueued, its tables are all-gathered ASYNCHRONOUSLY (NCCL runs on its own stream and waits
+    for the chunk's kernels only), so the gather of chunk c overlaps the compute of chunk c+1.
+    Returns the full tables [n, ...] in global frame order. local=True: `frames` already is this
+    rank's shard (n = world * len(frames)).
+    """
+    import torch
+    import torch.distributed as dist
+    n = frames.shape[0] * (world if local else 1)
+    if n % (world * chunk) != 0:
+        raise ValueError("run_frames_pipelined: n_frames must be a multiple of world * chunk")
+    per = n // world
+    a = 0 if local else rank * per
+    pending = []
+    for c0 in range(0, per, chunk):
+        idx, dist_ = run(frames[a + c0:a + c0 + chunk])
+        outs = []
+        works = []
+        for t in (idx, dist_):
+            full = torch.empty((world * chunk,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            works.append(dist.all_gather_into_tensor(full, t.contiguous(), group=group, async_op=True))
+            outs.append(full)
+        pending.append((c0, outs, works))
+    res = [None, None]
+    parts = [[None] * n, [None] * n]
+    for c0, outs, works in pending:
+        for w in works:
+            w.wait()
+        for k in range(2):
+            for r in range(world):
+                for j in range(chunk):
+                    parts[k][r * per + c0 + j] = outs[k][r * chunk + j]
+    for k in range(2):
+        res[k] = torch.stack(parts[k], 0)
+    return res[0], res[1]

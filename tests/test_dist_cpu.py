@@ -52,6 +52,15 @@ def _worker(rank, world, port, mode, q):
 
             gi, gd = sdist.run_frames_sharded(run, frames, rank, world)
             wi, wd = oracle.bm(frames, b, s, Wn, K)
+        elif mode == "pipelined":
+            frames = rng.integers(0, 256, size=(4 * world, 1, 20, 23), dtype=np.uint8)
+
+            def run(local):
+                i, d = oracle.bm(local, b, s, Wn, K)
+                return torch.from_numpy(i), torch.from_numpy(d)
+
+            gi, gd = sdist.run_frames_pipelined(run, frames, rank, world, chunk=2)
+            wi, wd = oracle.bm(frames, b, s, Wn, K)
         else:
             img = rng.random((1, 2, 31, 22)).astype(np.float32)
             ny, nx = oracle.grid(31, 22, b, s)
@@ -68,7 +77,7 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["frames", "bands"])
+@pytest.mark.parametrize("mode", ["frames", "bands", "pipelined"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_gather_equals_single_process(mode, world):
     import torch.multiprocessing as mp
