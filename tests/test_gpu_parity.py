@@ -752,3 +752,17 @@ def test_temporal_rejects():
         with pytest.raises(ScError) as e:
             p.set_temporal(T)
         assert e.value.code == 2
+
+
+def test_temporal_row_bands_match_full_run():
+    """Row bands (the multi-GPU spatial split) with temporal search = the matching rows of the full run."""
+    rng = np.random.Generator(np.random.PCG64(17))
+    x = torch.from_numpy(synth.random_image(rng, 3, 1, 96, 150, "u8")).cuda()
+    p = _plan((96, 150, 1, 8, 4, 21, 16), "u8")
+    p.set_temporal(1)
+    fi, fd = p.run(x)
+    for r0, r1 in [(0, 3), (5, 17), (20, p.ny)]:
+        bi, bd = p.run_rows(x, r0, r1)
+        torch.cuda.synchronize()
+        sl = slice(r0 * p.nx, r1 * p.nx)
+        assert torch.equal(bi, fi[:, sl]) and torch.equal(bd, fd[:, sl]), (r0, r1)
