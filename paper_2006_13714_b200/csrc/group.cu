@@ -36,6 +36,8 @@ struct GroupArgs {
   long long n_patches;  // n * refs * K (< 2^31)
   size_t img_elems;     // n * C * H * W (bound for the aligned word loads)
   FastDiv fdW, fdImg;   // divide by W (pixel index -> row), by refs * K (patch -> image)
+  FastDiv fdHW;         // divide by H * W: batch-global idx (3D / temporal runs) -> frame
+  int global_idx;       // idx entries are frame * H * W + pixel (sc_bm_set_temporal), not per image
 };
 
 #ifndef SCBM_GROUP_UNROLL
@@ -80,8 +82,14 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
       const int j = jv[u];
       {
         if (j >= 0) {
-          const uint32_t cy = a.fdW.div(uint32_t(j)), cx = uint32_t(j) - cy * uint32_t(a.W);
-          const uint32_t img = a.fdImg.div(uint32_t(p));
+          uint32_t img, pix = uint32_t(j);
+          if (a.global_idx) {
+            img = a.fdHW.div(pix);
+            pix -= img * uint32_t(a.H * a.W);
+          } else {
+            img = a.fdImg.div(uint32_t(p));
+          }
+          const uint32_t cy = a.fdW.div(pix), cx = pix - cy * uint32_t(a.W);
           off[u] = (size_t(img) * a.C + c) * plane + size_t(cy + l) * a.W + cx;
         }
       }
@@ -142,6 +150,127 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
   }
 }
 
+// Region-staged gather (the default for per-image idx tables): a CTA owns a TRY x TRX tile of
+// references of one image, stages the union of their search windows (+ patch extent) in shared
+// memory with coalesced loads -- every matched patch lies inside it -- and then writes the tile's
+// groups: one warp per reference, lanes over its K C b patch rows, consecutive lanes consecutive
+// rows (contiguous output), patch rows read from shared memory (uint8, b % 4 == 0: aligned words
+// + funnel shifts). The image is read once per tile instead of once per matched patch row.
+struct StagedArgs {
+  int s, lo, hi, nx, ny, TRY, TRX, tiles_x, RH, RWp;  // RWp: region row pitch in elements
+  FastDiv fdPP, fdB;                                 // divide by vectors per patch, by b
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedArgs sa) {
+  extern __shared__ __align__(16) uint8_t gsm[];
+  T* reg = reinterpret_cast<T*>(gsm);
+  const int f = blockIdx.y;
+  const int ty = blockIdx.x / sa.tiles_x, tx = blockIdx.x - ty * sa.tiles_x;
+  const int iy_first = ty * sa.TRY, ix_first = tx * sa.TRX;
+  const int iy_n = min(sa.TRY, sa.ny - iy_first), ix_n = min(sa.TRX, sa.nx - ix_first);
+  const int Ybase = iy_first * sa.s + sa.lo, Xbase = ix_first * sa.s + sa.lo;
+  const size_t plane = size_t(a.H) * a.W;
+  const T* img = static_cast<const T*>(a.imgs) + size_t(f) * a.C * plane;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int per_plane = sa.RH * sa.RWp;
+  for (int row = warp; row < a.C * sa.RH; row += nwarps) {  // warp per region row, lanes along it
+    const int c = row / sa.RH, r = row - c * sa.RH, y = Ybase + r;
+    const bool yin = y >= 0 && y < a.H;
+    const T* src = img + c * plane + size_t(yin ? y : 0) * a.W;
+    T* d = reg + c * per_plane + r * sa.RWp;
+    for (int x = lane; x < sa.RWp; x += 32) {
+      const int xx = Xbase + x;
+      d[x] = (yin && xx >= 0 && xx < a.W) ? __ldg(src + xx) : T(0);
+    }
+  }
+  __syncthreads();
+  const int R = a.C * a.b;  // patch rows
+  const long long n_refs = (long long)sa.ny * sa.nx;
+  // item -> (patch k, first element e0 of the patch's R b elements): a 16-byte vector (two 8-byte
+  // rows for uint8 b = 8, four floats for float32 b % 4 == 0), a whole patch row otherwise. Consecutive lanes write consecutive output bytes.
+  const int vec = sizeof(T) == 1 ? (a.b == 8 ? 16 : a.b) : (a.b % 4 == 0 ? 4 : a.b);
+  const int per_patch = R * a.b / vec, items = a.K * per_patch;
+  for (int t = warp; t < iy_n * ix_n; t += nwarps) {
+    const int ty2 = t / ix_n;
+    const int iy = iy_first + ty2, ix = ix_first + t - ty2 * ix_n;
+    const long long ref = (long long)f * n_refs + (long long)iy * sa.nx + ix;
+    T* out_ref = static_cast<T*>(a.out) + size_t(ref * a.K) * R * a.b;
+    for (int it = lane; it < items; it += 32) {
+      const int k = int(sa.fdPP.div(uint32_t(it)));
+      const int e0 = (it - k * per_patch) * vec;  // element within the patch: (c, l, m) row-major
+      const int rr = int(sa.fdB.div(uint32_t(e0))), m0 = e0 - rr * a.b;
+      const int c = rr / a.b, l = rr - c * a.b;
+      const int j = __ldg(a.idx + ref * a.K + k);
+      T* dst = out_ref + size_t(k) * R * a.b + e0;
+      if (j < 0) {
+        if (vec * sizeof(T) == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+        else for (int m = 0; m < vec; ++m) dst[m] = T(0);
+        continue;
+      }
+      const uint32_t cy = a.fdW.div(uint32_t(j)), cx = uint32_t(j) - cy * uint32_t(a.W);
+      const int ry = int(cy) - Ybase, rx = int(cx) - Xbase;
+      if (ry < 0 || ry + a.b > sa.RH || rx < 0 || rx + a.b + 4 > sa.RWp) {  // outside the tile's windows
+        const T* src = img + c * plane + size_t(cy + l) * a.W + cx + m0;  // (an idx not from this plan)
+        const int nrow = (vec == 16 && sizeof(T) == 1 && a.b == 8) ? 2 : 1, per_row = vec / nrow;
+        for (int q = 0; q < nrow; ++q)
+          for (int m = 0; m < per_row; ++m) dst[q * a.b + m] = src[q * a.W + m];
+        continue;
+      }
+      const int ro = c * per_plane + (ry + l) * sa.RWp + rx + m0;  // region offset of the first element
+      if constexpr (sizeof(T) == 1) {
+        if (vec == 16 && a.b == 8) {  // two 8-byte patch rows: aligned words + funnel shifts
+          uint32_t o[4];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int rq = ro + q * sa.RWp;
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(gsm) + (rq >> 2);
+            const int sh = 8 * (rq & 3);
+            const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+            o[2 * q] = __funnelshift_r(w0, w1, sh);
+            o[2 * q + 1] = __funnelshift_r(w1, w2, sh);
+          }
+          __stcs(reinterpret_cast<uint4*>(dst), make_uint4(o[0], o[1], o[2], o[3]));
+          continue;
+        }
+      } else {
+        if (vec == 4 && a.b % 4 == 0) {
+          __stcs(reinterpret_cast<float4*>(dst), make_float4(reg[ro], reg[ro + 1], reg[ro + 2], reg[ro + 3]));
+          continue;
+        }
+      }
+      for (int m = 0; m < vec; ++m) dst[m] = reg[ro + m];  // one patch row
+    }
+  }
+}
+
+template <typename T>
+cudaError_t launch_group_staged_t(const GroupArgs& a, const sc_bm_plan_s& p, int64_t n_images, cudaStream_t st) {
+  const Geometry& g = p.g;
+  StagedArgs sa{};
+  sa.s = g.s; sa.lo = g.lo; sa.hi = g.hi; sa.nx = g.nx; sa.ny = g.ny;
+  const int vec = sizeof(T) == 1 ? (g.b == 8 ? 16 : g.b) : (g.b % 4 == 0 ? 4 : g.b);
+  sa.fdPP = FastDiv(uint32_t(g.C * g.b * g.b / vec));
+  sa.fdB = FastDiv(uint32_t(g.b));
+  size_t bytes = 0;
+  // 16 x 32 reference tiles, halved while the region exceeds 96 KB or the grid is under 4 waves
+  // of CTAs on the SMs (small images)
+  for (int t = 0;; ++t) {
+    sa.TRY = std::max(1, 16 >> (t / 2)), sa.TRX = std::max(1, 32 >> ((t + 1) / 2));
+    sa.RH = (sa.TRY - 1) * g.s + g.Wn + g.b - 1;
+    sa.RWp = ((sa.TRX - 1) * g.s + g.Wn + g.b - 1 + 4 + 3) & ~3;  // + 1 word of slack for the funnel
+    bytes = size_t(g.C) * sa.RH * sa.RWp * sizeof(T) + 16;
+    const long long ctas = (long long)((g.nx + sa.TRX - 1) / sa.TRX) * ((g.ny + sa.TRY - 1) / sa.TRY) * n_images;
+    if ((bytes <= 96 * 1024 && ctas >= 4LL * p.sm_count) || sa.TRY * sa.TRX <= 4) break;
+  }
+  if (bytes > 96 * 1024) return cudaErrorInvalidValue;
+  sa.tiles_x = (g.nx + sa.TRX - 1) / sa.TRX;
+  const int tiles_y = (g.ny + sa.TRY - 1) / sa.TRY;
+  cudaFuncSetAttribute(group_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  group_staged_kernel<T><<<dim3(sa.tiles_x * tiles_y, unsigned(n_images)), 256, bytes, st>>>(a, sa);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_group_t(const GroupArgs& a, int sm_count, cudaStream_t st) {
   const int ppb = 256 / (a.C * a.b);
@@ -166,7 +295,15 @@ cudaError_t launch_group(const sc_bm_plan_s& p, const void* imgs, int64_t n_imag
   if (a.n_patches >= (1ll << 31)) return cudaErrorInvalidValue;  // 32-bit patch / pixel indices
   a.fdW = FastDiv(uint32_t(g.W));
   a.fdImg = FastDiv(uint32_t(n_refs * g.K));
+  a.fdHW = FastDiv(uint32_t(g.H * g.W));
+  a.global_idx = p.T > 0;
   if (launches) *launches += 1;
+  if (p.T == 0 && n_images <= 65535) {  // per-image idx: the region-staged gather
+    cudaError_t e = g.dtype == SC_DTYPE_U8 ? launch_group_staged_t<uint8_t>(a, p, n_images, st)
+                                           : launch_group_staged_t<float>(a, p, n_images, st);
+    if (e != cudaErrorInvalidValue) return e;
+    cudaGetLastError();
+  }
   if (g.dtype == SC_DTYPE_U8) return launch_group_t<uint8_t>(a, p.sm_count, st);
   return launch_group_t<float>(a, p.sm_count, st);
 }

@@ -554,6 +554,23 @@ def test_group_matches_oracle(dtype, C, H, W, b, s, Wn, K):
     np.testing.assert_array_equal(Y.cpu().numpy(), oracle.group(x, idx.cpu().numpy(), b))
 
 
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+def test_group_arbitrary_idx(dtype):
+    # idx not produced by a search (any patch of the image, -1 holes): the staged gather must fall
+    # back to global reads for candidates outside a tile's windows; ragged tiles in both directions
+    H, W, C, b, s, Wn, K = 150, 203, 2, 8, 4, 9, 7
+    rng = np.random.Generator(np.random.PCG64(11))
+    x = synth.random_image(rng, 3, C, H, W, dtype)
+    p = _plan((H, W, C, b, s, Wn, K), dtype)
+    cy = rng.integers(0, H - b + 1, (3, p.n_refs, K))
+    cx = rng.integers(0, W - b + 1, (3, p.n_refs, K))
+    ii = (cy * W + cx).astype(np.int32)
+    ii[rng.random(ii.shape) < 0.1] = -1
+    t = torch.from_numpy(x).cuda()
+    Y = p.group(t, torch.from_numpy(ii).cuda())
+    np.testing.assert_array_equal(Y.cpu().numpy(), oracle.group(x, ii, b))
+
+
 def test_group_padding_and_c5_sample():
     # K > window candidates: -1 entries -> zero columns
     rng = np.random.Generator(np.random.PCG64(3))
@@ -715,6 +732,23 @@ def test_temporal_matches_oracle(N, H, W, Wn, K, T):
     gi, gd = _run(p, x)
     oi, od = oracle.bm_temporal(x, 8, 4, Wn, K, T)
     check_u8(gi, gd, oi, od, f"temporal N{N} {H}x{W} Wn{Wn} K{K} T{T}")
+
+
+def test_group_temporal_idx():
+    # a 3D / temporal run's idx is batch-global (frame * H * W + pixel); for C = 1 that is the pixel
+    # index of the frames stacked vertically, so the oracle groups the stacked image
+    N, H, W = 4, 52, 75
+    rng = np.random.Generator(np.random.PCG64(17))
+    x = synth.random_image(rng, N, 1, H, W, "u8")
+    p = _plan((H, W, 1, 8, 4, 15, 12), "u8")
+    p.set_temporal(1)
+    t = torch.from_numpy(x).cuda()
+    idx, _ = p.run(t)
+    ii = idx.cpu().numpy()
+    assert (ii // (H * W) != np.arange(N)[:, None, None]).any()  # some matches in neighbouring frames
+    Y = p.group(t, idx).cpu().numpy()
+    ref = oracle.group(x.reshape(1, 1, N * H, W), ii.reshape(1, -1, 12), 8)
+    np.testing.assert_array_equal(Y.reshape(ref.shape), ref)
 
 
 def test_temporal_c5_frames_and_saturation():
