@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
 // + funnel shifts). The image is read once per tile instead of once per matched patch row.
 struct StagedArgs {
   int s, lo, hi, nx, ny, TRY, TRX, tiles_x, RH, RWp;  // RWp: region row pitch in elements
-  FastDiv fdPP, fdB;                                 // divide by vectors per patch, by b
+  int tab_off;                                       // byte offset of the item table in shared memory
 };
 
 template <typename T>
@@ -186,61 +186,79 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
   }
   __syncthreads();
   const int R = a.C * a.b;  // patch rows
+  // Items of a reference's contiguous output segment (K patches of R b elements): a 16-byte vector
+  // (two 8-byte rows for uint8 b = 8, four floats for float32 b % 4 == 0), one element otherwise;
+  // lane i writes items i, i + 32, ... so consecutive lanes write consecutive bytes. tab[e] is the
+  // region offset of item e of a patch; wb[k] the region offset of match k of the current reference.
+  const int vec = sizeof(T) == 1 ? (a.b == 8 ? 16 : 1) : (a.b % 4 == 0 ? 4 : 1);
+  const int ppv = R * a.b / vec, items = a.K * ppv;
+  int* tab = reinterpret_cast<int*>(gsm + sa.tab_off);
+  int* wb = tab + ppv + warp * a.K;
+  for (int e = threadIdx.x; e < ppv; e += blockDim.x) {
+    const int el = e * vec, rr = el / a.b, m = el - rr * a.b, c = rr / a.b, l = rr - c * a.b;
+    tab[e] = c * per_plane + l * sa.RWp + m;
+  }
+  __syncthreads();
+  const int kstep = 32 / ppv, estep = 32 - kstep * ppv;
+  const int k_lane = lane / ppv, e_lane = lane - k_lane * ppv;
   const long long n_refs = (long long)sa.ny * sa.nx;
-  // item -> (patch k, first element e0 of the patch's R b elements): a 16-byte vector (two 8-byte
-  // rows for uint8 b = 8, four floats for float32 b % 4 == 0), a whole patch row otherwise. Consecutive lanes write consecutive output bytes.
-  const int vec = sizeof(T) == 1 ? (a.b == 8 ? 16 : a.b) : (a.b % 4 == 0 ? 4 : a.b);
-  const int per_patch = R * a.b / vec, items = a.K * per_patch;
   for (int t = warp; t < iy_n * ix_n; t += nwarps) {
     const int ty2 = t / ix_n;
     const int iy = iy_first + ty2, ix = ix_first + t - ty2 * ix_n;
     const long long ref = (long long)f * n_refs + (long long)iy * sa.nx + ix;
-    T* out_ref = static_cast<T*>(a.out) + size_t(ref * a.K) * R * a.b;
-    for (int it = lane; it < items; it += 32) {
-      const int k = int(sa.fdPP.div(uint32_t(it)));
-      const int e0 = (it - k * per_patch) * vec;  // element within the patch: (c, l, m) row-major
-      const int rr = int(sa.fdB.div(uint32_t(e0))), m0 = e0 - rr * a.b;
-      const int c = rr / a.b, l = rr - c * a.b;
+    for (int k = lane; k < a.K; k += 32) {  // match k -> region offset; -1: no match; <= -2: outside
       const int j = __ldg(a.idx + ref * a.K + k);
-      T* dst = out_ref + size_t(k) * R * a.b + e0;
-      if (j < 0) {
-        if (vec * sizeof(T) == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
-        else for (int m = 0; m < vec; ++m) dst[m] = T(0);
-        continue;
+      int v = -1;
+      if (j >= 0) {
+        const uint32_t cy = a.fdW.div(uint32_t(j)), cx = uint32_t(j) - cy * uint32_t(a.W);
+        const int ry = int(cy) - Ybase, rx = int(cx) - Xbase;
+        const bool in = ry >= 0 && ry + a.b <= sa.RH && rx >= 0 && rx + a.b + 4 <= sa.RWp;
+        v = in ? ry * sa.RWp + rx : -2 - j;  // outside the tile's windows: an idx not from this plan
       }
-      const uint32_t cy = a.fdW.div(uint32_t(j)), cx = uint32_t(j) - cy * uint32_t(a.W);
-      const int ry = int(cy) - Ybase, rx = int(cx) - Xbase;
-      if (ry < 0 || ry + a.b > sa.RH || rx < 0 || rx + a.b + 4 > sa.RWp) {  // outside the tile's windows
-        const T* src = img + c * plane + size_t(cy + l) * a.W + cx + m0;  // (an idx not from this plan)
-        const int nrow = (vec == 16 && sizeof(T) == 1 && a.b == 8) ? 2 : 1, per_row = vec / nrow;
-        for (int q = 0; q < nrow; ++q)
-          for (int m = 0; m < per_row; ++m) dst[q * a.b + m] = src[q * a.W + m];
-        continue;
-      }
-      const int ro = c * per_plane + (ry + l) * sa.RWp + rx + m0;  // region offset of the first element
-      if constexpr (sizeof(T) == 1) {
-        if (vec == 16 && a.b == 8) {  // two 8-byte patch rows: aligned words + funnel shifts
-          uint32_t o[4];
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int rq = ro + q * sa.RWp;
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(gsm) + (rq >> 2);
-            const int sh = 8 * (rq & 3);
-            const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
-            o[2 * q] = __funnelshift_r(w0, w1, sh);
-            o[2 * q + 1] = __funnelshift_r(w1, w2, sh);
-          }
-          __stcs(reinterpret_cast<uint4*>(dst), make_uint4(o[0], o[1], o[2], o[3]));
-          continue;
-        }
-      } else {
-        if (vec == 4 && a.b % 4 == 0) {
-          __stcs(reinterpret_cast<float4*>(dst), make_float4(reg[ro], reg[ro + 1], reg[ro + 2], reg[ro + 3]));
-          continue;
-        }
-      }
-      for (int m = 0; m < vec; ++m) dst[m] = reg[ro + m];  // one patch row
+      wb[k] = v;
     }
+    __syncwarp();
+    T* out_ref = static_cast<T*>(a.out) + size_t(ref * a.K) * R * a.b;
+    int k = k_lane, e = e_lane;
+    for (int it = lane; it < items; it += 32) {
+      const int base = wb[k];
+      T* dst = out_ref + (k * ppv + e) * vec;
+      if (base < 0) {
+        const int el = e * vec, rr = el / a.b, m0 = el - rr * a.b, c = rr / a.b, l = rr - c * a.b;
+        const int j = -2 - base;
+        const uint32_t cy = a.fdW.div(uint32_t(max(j, 0))), cx = uint32_t(max(j, 0)) - cy * uint32_t(a.W);
+        const T* src = img + c * plane + size_t(cy + l) * a.W + cx + m0;
+        const int nrow = (vec == 16 && sizeof(T) == 1) ? 2 : 1, per_row = vec / nrow;
+        for (int q = 0; q < nrow; ++q)
+          for (int m = 0; m < per_row; ++m) dst[q * a.b + m] = base == -1 ? T(0) : src[size_t(q) * a.W + m];
+      } else {
+        const int ro = base + tab[e];
+        if constexpr (sizeof(T) == 1) {
+          if (vec == 16) {  // two 8-byte patch rows: aligned words + funnel shifts
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int rq = ro + q * sa.RWp;
+              const uint32_t* w = reinterpret_cast<const uint32_t*>(gsm) + (rq >> 2);
+              const int sh = 8 * (rq & 3);
+              const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+              o[2 * q] = __funnelshift_r(w0, w1, sh);
+              o[2 * q + 1] = __funnelshift_r(w1, w2, sh);
+            }
+            __stcs(reinterpret_cast<uint4*>(dst), make_uint4(o[0], o[1], o[2], o[3]));
+          } else {
+            *dst = reg[ro];
+          }
+        } else {
+          if (vec == 4) __stcs(reinterpret_cast<float4*>(dst), make_float4(reg[ro], reg[ro + 1], reg[ro + 2], reg[ro + 3]));
+          else __stcs(dst, reg[ro]);
+        }
+      }
+      e += estep;
+      k += kstep;
+      if (e >= ppv) e -= ppv, ++k;
+    }
+    __syncwarp();
   }
 }
 
@@ -249,9 +267,8 @@ cudaError_t launch_group_staged_t(const GroupArgs& a, const sc_bm_plan_s& p, int
   const Geometry& g = p.g;
   StagedArgs sa{};
   sa.s = g.s; sa.lo = g.lo; sa.hi = g.hi; sa.nx = g.nx; sa.ny = g.ny;
-  const int vec = sizeof(T) == 1 ? (g.b == 8 ? 16 : g.b) : (g.b % 4 == 0 ? 4 : g.b);
-  sa.fdPP = FastDiv(uint32_t(g.C * g.b * g.b / vec));
-  sa.fdB = FastDiv(uint32_t(g.b));
+  const int vec = sizeof(T) == 1 ? (g.b == 8 ? 16 : 1) : (g.b % 4 == 0 ? 4 : 1);
+  const size_t extra = size_t(g.C * g.b * g.b / vec + 8 * g.K) * sizeof(int);  // item table + 8 warps' bases
   size_t bytes = 0;
   // 16 x 32 reference tiles, halved while the region exceeds 96 KB or the grid is under 4 waves
   // of CTAs on the SMs (small images)
@@ -259,7 +276,8 @@ cudaError_t launch_group_staged_t(const GroupArgs& a, const sc_bm_plan_s& p, int
     sa.TRY = std::max(1, 16 >> (t / 2)), sa.TRX = std::max(1, 32 >> ((t + 1) / 2));
     sa.RH = (sa.TRY - 1) * g.s + g.Wn + g.b - 1;
     sa.RWp = ((sa.TRX - 1) * g.s + g.Wn + g.b - 1 + 4 + 3) & ~3;  // + 1 word of slack for the funnel
-    bytes = size_t(g.C) * sa.RH * sa.RWp * sizeof(T) + 16;
+    sa.tab_off = int((size_t(g.C) * sa.RH * sa.RWp * sizeof(T) + 16 + 15) & ~size_t(15));
+    bytes = size_t(sa.tab_off) + extra;
     const long long ctas = (long long)((g.nx + sa.TRX - 1) / sa.TRX) * ((g.ny + sa.TRY - 1) / sa.TRY) * n_images;
     if ((bytes <= 96 * 1024 && ctas >= 4LL * p.sm_count) || sa.TRY * sa.TRX <= 4) break;
   }
