@@ -158,10 +158,11 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
 // + funnel shifts). The image is read once per tile instead of once per matched patch row.
 struct StagedArgs {
   int s, lo, hi, nx, ny, TRY, TRX, tiles_x, RH, RWp;  // RWp: region row pitch in elements
-  int tab_off;                                       // byte offset of the item table in shared memory
+  int tab_off, tab_len;                              // item table: byte offset in shared memory, entries
 };
 
-template <typename T>
+// BT: match-table entry type (int16_t when every region offset fits).
+template <typename T, typename BT>
 __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedArgs sa) {
   extern __shared__ __align__(16) uint8_t gsm[];
   T* reg = reinterpret_cast<T*>(gsm);
@@ -174,11 +175,60 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
   const T* img = static_cast<const T*>(a.imgs) + size_t(f) * a.C * plane;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int per_plane = sa.RH * sa.RWp;
+  const long long n_refs = (long long)sa.ny * sa.nx;
+  const int n_tile = iy_n * ix_n;
+  const long long ref00 = (long long)f * n_refs + (long long)iy_first * sa.nx + ix_first;  // tile's first ref
+  // Match table of the tile: bases[t K + k] = region offset of match k of tile reference t
+  // (t row-major over the tile), -1 for no match, -2 for a match outside the staged region
+  // (an idx not from this plan). The idx rows of a tile row are contiguous: coalesced loads,
+  // kMatchBatch in flight per thread.
+  BT* bases = reinterpret_cast<BT*>(reinterpret_cast<int*>(gsm + sa.tab_off) + sa.tab_len);
+  {
+    constexpr int kMatchBatch = 8;
+    const int rowK = ix_n * a.K, nq = iy_n * rowK;
+    const float inv_rowK = 1.0f / float(rowK);
+    for (int q0 = threadIdx.x; q0 < nq; q0 += kMatchBatch * blockDim.x) {
+      int jv[kMatchBatch];
+#pragma unroll
+      for (int u = 0; u < kMatchBatch; ++u) {
+        const int q = q0 + u * blockDim.x;
+        int r = __float2int_rz(float(q) * inv_rowK), e = q - r * rowK;  // q / rowK, corrected below
+        if (e < 0) --r, e += rowK;
+        if (e >= rowK) ++r, e -= rowK;
+        jv[u] = q < nq ? __ldg(a.idx + (ref00 + (long long)r * sa.nx) * a.K + e) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < kMatchBatch; ++u) {
+        const int q = q0 + u * blockDim.x, j = jv[u];
+        int v = -1;
+        if (j >= 0) {
+          const uint32_t cy = a.fdW.div(uint32_t(j)), cx = uint32_t(j) - cy * uint32_t(a.W);
+          const int ry = int(cy) - Ybase, rx = int(cx) - Xbase;
+          const bool in = ry >= 0 && ry + a.b <= sa.RH && rx >= 0 && rx + a.b + 4 <= sa.RWp;
+          v = in ? ry * sa.RWp + rx : -2;
+        }
+        if (q < nq) bases[q] = BT(v);
+      }
+    }
+  }
+  const size_t img_end = a.img_elems - size_t(f) * a.C * plane;  // elements of img[] from this image on
   for (int row = warp; row < a.C * sa.RH; row += nwarps) {  // warp per region row, lanes along it
     const int c = row / sa.RH, r = row - c * sa.RH, y = Ybase + r;
     const bool yin = y >= 0 && y < a.H;
     const T* src = img + c * plane + size_t(yin ? y : 0) * a.W;
     T* d = reg + c * per_plane + r * sa.RWp;
+    if constexpr (sizeof(T) == 1) {  // interior rows: aligned 4-byte loads + funnel shifts
+      const size_t g0 = c * plane + size_t(y) * a.W + Xbase;
+      if (yin && Xbase >= 0 && Xbase + sa.RWp <= a.W && g0 + sa.RWp + 4 <= img_end) {
+        const uint8_t* rp = reinterpret_cast<const uint8_t*>(img) + g0;
+        const int mis = int(reinterpret_cast<uintptr_t>(rp) & 3);
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(rp - mis);
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(d);
+        for (int x4 = lane; x4 < sa.RWp / 4; x4 += 32)
+          d32[x4] = __funnelshift_r(__ldg(wp + x4), __ldg(wp + x4 + 1), 8 * mis);
+        continue;
+      }
+    }
     for (int x = lane; x < sa.RWp; x += 32) {
       const int xx = Xbase + x;
       d[x] = (yin && xx >= 0 && xx < a.W) ? __ldg(src + xx) : T(0);
@@ -193,7 +243,6 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
   const int vec = sizeof(T) == 1 ? (a.b == 8 ? 16 : 1) : (a.b % 4 == 0 ? 4 : 1);
   const int ppv = R * a.b / vec, items = a.K * ppv;
   int* tab = reinterpret_cast<int*>(gsm + sa.tab_off);
-  int* wb = tab + ppv + warp * a.K;
   for (int e = threadIdx.x; e < ppv; e += blockDim.x) {
     const int el = e * vec, rr = el / a.b, m = el - rr * a.b, c = rr / a.b, l = rr - c * a.b;
     tab[e] = c * per_plane + l * sa.RWp + m;
@@ -201,23 +250,12 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
   __syncthreads();
   const int kstep = 32 / ppv, estep = 32 - kstep * ppv;
   const int k_lane = lane / ppv, e_lane = lane - k_lane * ppv;
-  const long long n_refs = (long long)sa.ny * sa.nx;
-  for (int t = warp; t < iy_n * ix_n; t += nwarps) {
-    const int ty2 = t / ix_n;
-    const int iy = iy_first + ty2, ix = ix_first + t - ty2 * ix_n;
-    const long long ref = (long long)f * n_refs + (long long)iy * sa.nx + ix;
-    for (int k = lane; k < a.K; k += 32) {  // match k -> region offset; -1: no match; <= -2: outside
-      const int j = __ldg(a.idx + ref * a.K + k);
-      int v = -1;
-      if (j >= 0) {
-        const uint32_t cy = a.fdW.div(uint32_t(j)), cx = uint32_t(j) - cy * uint32_t(a.W);
-        const int ry = int(cy) - Ybase, rx = int(cx) - Xbase;
-        const bool in = ry >= 0 && ry + a.b <= sa.RH && rx >= 0 && rx + a.b + 4 <= sa.RWp;
-        v = in ? ry * sa.RWp + rx : -2 - j;  // outside the tile's windows: an idx not from this plan
-      }
-      wb[k] = v;
-    }
-    __syncwarp();
+  int ty_w = warp / ix_n, tx_w = warp - ty_w * ix_n;  // this warp's current tile reference
+  for (int t = warp; t < n_tile; t += nwarps) {
+    const long long ref = ref00 + (long long)ty_w * sa.nx + tx_w;
+    const BT* wb = bases + t * a.K;
+    tx_w += nwarps;
+    while (tx_w >= ix_n) tx_w -= ix_n, ++ty_w;
     T* out_ref = static_cast<T*>(a.out) + size_t(ref * a.K) * R * a.b;
     int k = k_lane, e = e_lane;
     for (int it = lane; it < items; it += 32) {
@@ -225,7 +263,7 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
       T* dst = out_ref + (k * ppv + e) * vec;
       if (base < 0) {
         const int el = e * vec, rr = el / a.b, m0 = el - rr * a.b, c = rr / a.b, l = rr - c * a.b;
-        const int j = -2 - base;
+        const int j = base == -1 ? 0 : __ldg(a.idx + ref * a.K + k);  // (an idx not from this plan)
         const uint32_t cy = a.fdW.div(uint32_t(max(j, 0))), cx = uint32_t(max(j, 0)) - cy * uint32_t(a.W);
         const T* src = img + c * plane + size_t(cy + l) * a.W + cx + m0;
         const int nrow = (vec == 16 && sizeof(T) == 1) ? 2 : 1, per_row = vec / nrow;
@@ -258,9 +296,13 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
       k += kstep;
       if (e >= ppv) e -= ppv, ++k;
     }
-    __syncwarp();
   }
 }
+
+#ifndef SCBM_GROUP_SMEM
+#define SCBM_GROUP_SMEM 96
+#endif
+constexpr size_t kGroupSmem = size_t(SCBM_GROUP_SMEM) * 1024;  // shared-memory budget of a tile
 
 template <typename T>
 cudaError_t launch_group_staged_t(const GroupArgs& a, const sc_bm_plan_s& p, int64_t n_images, cudaStream_t st) {
@@ -268,24 +310,36 @@ cudaError_t launch_group_staged_t(const GroupArgs& a, const sc_bm_plan_s& p, int
   StagedArgs sa{};
   sa.s = g.s; sa.lo = g.lo; sa.hi = g.hi; sa.nx = g.nx; sa.ny = g.ny;
   const int vec = sizeof(T) == 1 ? (g.b == 8 ? 16 : 1) : (g.b % 4 == 0 ? 4 : 1);
-  const size_t extra = size_t(g.C * g.b * g.b / vec + 8 * g.K) * sizeof(int);  // item table + 8 warps' bases
+  sa.tab_len = (g.C * g.b * g.b / vec + 3) & ~3;
   size_t bytes = 0;
-  // 16 x 32 reference tiles, halved while the region exceeds 96 KB or the grid is under 4 waves
-  // of CTAs on the SMs (small images)
+  bool short_bases = false;
+  // 16 x 32 reference tiles, halved while region + tables exceed kGroupSmem, the tile writes more
+  // than max(1 MB, 8 x its shared memory) of groups (measured: c3's 70 float patches per reference
+  // prefer 8 x 8 tiles) or the grid is under 4 waves of CTAs on the SMs (small images)
   for (int t = 0;; ++t) {
     sa.TRY = std::max(1, 16 >> (t / 2)), sa.TRX = std::max(1, 32 >> ((t + 1) / 2));
     sa.RH = (sa.TRY - 1) * g.s + g.Wn + g.b - 1;
     sa.RWp = ((sa.TRX - 1) * g.s + g.Wn + g.b - 1 + 4 + 3) & ~3;  // + 1 word of slack for the funnel
     sa.tab_off = int((size_t(g.C) * sa.RH * sa.RWp * sizeof(T) + 16 + 15) & ~size_t(15));
-    bytes = size_t(sa.tab_off) + extra;
+    short_bases = size_t(sa.RH) * sa.RWp <= 32767;  // match offsets (within one channel plane) fit int16
+    bytes = size_t(sa.tab_off) + size_t(sa.tab_len) * sizeof(int) +
+            size_t(sa.TRY) * sa.TRX * g.K * (short_bases ? 2 : 4);
     const long long ctas = (long long)((g.nx + sa.TRX - 1) / sa.TRX) * ((g.ny + sa.TRY - 1) / sa.TRY) * n_images;
-    if ((bytes <= 96 * 1024 && ctas >= 4LL * p.sm_count) || sa.TRY * sa.TRX <= 4) break;
+    const size_t out_bytes = size_t(sa.TRY) * sa.TRX * g.K * g.C * g.b * g.b * sizeof(T);  // groups per CTA
+    const bool small_out = out_bytes <= std::max(size_t(1) << 20, 8 * bytes);  // else: staging amortised enough
+    if ((bytes <= kGroupSmem && ctas >= 4LL * p.sm_count && small_out) || sa.TRY * sa.TRX <= 4) break;
   }
   if (bytes > 96 * 1024) return cudaErrorInvalidValue;
   sa.tiles_x = (g.nx + sa.TRX - 1) / sa.TRX;
   const int tiles_y = (g.ny + sa.TRY - 1) / sa.TRY;
-  cudaFuncSetAttribute(group_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-  group_staged_kernel<T><<<dim3(sa.tiles_x * tiles_y, unsigned(n_images)), 256, bytes, st>>>(a, sa);
+  const dim3 grid(sa.tiles_x * tiles_y, unsigned(n_images));
+  if (short_bases) {
+    cudaFuncSetAttribute(group_staged_kernel<T, int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    group_staged_kernel<T, int16_t><<<grid, 256, bytes, st>>>(a, sa);
+  } else {
+    cudaFuncSetAttribute(group_staged_kernel<T, int>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    group_staged_kernel<T, int><<<grid, 256, bytes, st>>>(a, sa);
+  }
   return cudaGetLastError();
 }
 
