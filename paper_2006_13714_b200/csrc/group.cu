@@ -161,9 +161,11 @@ struct StagedArgs {
   int tab_off, tab_len;                              // item table: byte offset in shared memory, entries
 };
 
-// BT: match-table entry type (int16_t when every region offset fits).
-template <typename T, typename BT>
+// BT: match-table entry type (int16_t when every region offset fits); BFIX: compile-time patch
+// size (0: a.b at run time).
+template <typename T, typename BT, int BFIX>
 __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedArgs sa) {
+  const int bb = BFIX ? BFIX : a.b;
   extern __shared__ __align__(16) uint8_t gsm[];
   T* reg = reinterpret_cast<T*>(gsm);
   const int f = blockIdx.y;
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
         if (j >= 0) {
           const uint32_t cy = a.fdW.div(uint32_t(j)), cx = uint32_t(j) - cy * uint32_t(a.W);
           const int ry = int(cy) - Ybase, rx = int(cx) - Xbase;
-          const bool in = ry >= 0 && ry + a.b <= sa.RH && rx >= 0 && rx + a.b + 4 <= sa.RWp;
+          const bool in = ry >= 0 && ry + bb <= sa.RH && rx >= 0 && rx + bb + 4 <= sa.RWp;
           v = in ? ry * sa.RWp + rx : -2;
         }
         if (q < nq) bases[q] = BT(v);
@@ -235,66 +237,78 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
     }
   }
   __syncthreads();
-  const int R = a.C * a.b;  // patch rows
+  const int R = a.C * bb;  // patch rows
   // Items of a reference's contiguous output segment (K patches of R b elements): a 16-byte vector
   // (two 8-byte rows for uint8 b = 8, four floats for float32 b % 4 == 0), one element otherwise;
   // lane i writes items i, i + 32, ... so consecutive lanes write consecutive bytes. tab[e] is the
   // region offset of item e of a patch; wb[k] the region offset of match k of the current reference.
-  const int vec = sizeof(T) == 1 ? (a.b == 8 ? 16 : 1) : (a.b % 4 == 0 ? 4 : 1);
-  const int ppv = R * a.b / vec, items = a.K * ppv;
+  const int vec = sizeof(T) == 1 ? (bb == 8 ? 16 : 1) : (bb % 4 == 0 ? 4 : 1);
+  const int ppv = R * bb / vec, items = a.K * ppv;
   int* tab = reinterpret_cast<int*>(gsm + sa.tab_off);
   for (int e = threadIdx.x; e < ppv; e += blockDim.x) {
-    const int el = e * vec, rr = el / a.b, m = el - rr * a.b, c = rr / a.b, l = rr - c * a.b;
+    const int el = e * vec, rr = el / bb, m = el - rr * bb, c = rr / bb, l = rr - c * bb;
     tab[e] = c * per_plane + l * sa.RWp + m;
   }
   __syncthreads();
   const int kstep = 32 / ppv, estep = 32 - kstep * ppv;
   const int k_lane = lane / ppv, e_lane = lane - k_lane * ppv;
+  const uint32_t* reg32 = reinterpret_cast<const uint32_t*>(gsm);
+  // one item: region offset ro (base < 0: no match / outside the region), destination dst
+  auto put = [&](int base, int te, int e, T* dst, long long ref, int k) {
+    if (base < 0) {
+      const int el = e * vec, rr = el / bb, m0 = el - rr * bb, c = rr / bb, l = rr - c * bb;
+      const int j = base == -1 ? 0 : __ldg(a.idx + ref * a.K + k);  // (an idx not from this plan)
+      const uint32_t cy = a.fdW.div(uint32_t(max(j, 0))), cx = uint32_t(max(j, 0)) - cy * uint32_t(a.W);
+      const T* src = img + c * plane + size_t(cy + l) * a.W + cx + m0;
+      const int nrow = (vec == 16 && sizeof(T) == 1) ? 2 : 1, per_row = vec / nrow;
+      for (int q = 0; q < nrow; ++q)
+        for (int m = 0; m < per_row; ++m) dst[q * bb + m] = base == -1 ? T(0) : src[size_t(q) * a.W + m];
+      return;
+    }
+    const int ro = base + te;
+    if constexpr (sizeof(T) == 1) {
+      if (vec == 16) {  // two 8-byte patch rows: aligned words + funnel shifts
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int rq = ro + q * sa.RWp;
+          const uint32_t* w = reg32 + (rq >> 2);
+          const int sh = 8 * (rq & 3);
+          const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+          o[2 * q] = __funnelshift_r(w0, w1, sh);
+          o[2 * q + 1] = __funnelshift_r(w1, w2, sh);
+        }
+        __stcs(reinterpret_cast<uint4*>(dst), make_uint4(o[0], o[1], o[2], o[3]));
+      } else {
+        *dst = reg[ro];
+      }
+    } else {
+      if (vec == 4) __stcs(reinterpret_cast<float4*>(dst), make_float4(reg[ro], reg[ro + 1], reg[ro + 2], reg[ro + 3]));
+      else __stcs(dst, reg[ro]);
+    }
+  };
+  const int ref_elems = a.K * R * bb;                      // group elements per reference
+  T* out_tile = static_cast<T*>(a.out) + size_t(ref00) * ref_elems;
   int ty_w = warp / ix_n, tx_w = warp - ty_w * ix_n;  // this warp's current tile reference
   for (int t = warp; t < n_tile; t += nwarps) {
-    const long long ref = ref00 + (long long)ty_w * sa.nx + tx_w;
+    const int rofs = ty_w * sa.nx + tx_w;  // reference - ref00
+    const long long ref = ref00 + rofs;
     const BT* wb = bases + t * a.K;
     tx_w += nwarps;
     while (tx_w >= ix_n) tx_w -= ix_n, ++ty_w;
-    T* out_ref = static_cast<T*>(a.out) + size_t(ref * a.K) * R * a.b;
-    int k = k_lane, e = e_lane;
-    for (int it = lane; it < items; it += 32) {
-      const int base = wb[k];
-      T* dst = out_ref + (k * ppv + e) * vec;
-      if (base < 0) {
-        const int el = e * vec, rr = el / a.b, m0 = el - rr * a.b, c = rr / a.b, l = rr - c * a.b;
-        const int j = base == -1 ? 0 : __ldg(a.idx + ref * a.K + k);  // (an idx not from this plan)
-        const uint32_t cy = a.fdW.div(uint32_t(max(j, 0))), cx = uint32_t(max(j, 0)) - cy * uint32_t(a.W);
-        const T* src = img + c * plane + size_t(cy + l) * a.W + cx + m0;
-        const int nrow = (vec == 16 && sizeof(T) == 1) ? 2 : 1, per_row = vec / nrow;
-        for (int q = 0; q < nrow; ++q)
-          for (int m = 0; m < per_row; ++m) dst[q * a.b + m] = base == -1 ? T(0) : src[size_t(q) * a.W + m];
-      } else {
-        const int ro = base + tab[e];
-        if constexpr (sizeof(T) == 1) {
-          if (vec == 16) {  // two 8-byte patch rows: aligned words + funnel shifts
-            uint32_t o[4];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int rq = ro + q * sa.RWp;
-              const uint32_t* w = reinterpret_cast<const uint32_t*>(gsm) + (rq >> 2);
-              const int sh = 8 * (rq & 3);
-              const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
-              o[2 * q] = __funnelshift_r(w0, w1, sh);
-              o[2 * q + 1] = __funnelshift_r(w1, w2, sh);
-            }
-            __stcs(reinterpret_cast<uint4*>(dst), make_uint4(o[0], o[1], o[2], o[3]));
-          } else {
-            *dst = reg[ro];
-          }
-        } else {
-          if (vec == 4) __stcs(reinterpret_cast<float4*>(dst), make_float4(reg[ro], reg[ro + 1], reg[ro + 2], reg[ro + 3]));
-          else __stcs(dst, reg[ro]);
-        }
+    T* out_ref = out_tile + (long long)rofs * ref_elems;
+    if (estep == 0) {  // ppv divides 32: every lane keeps its item e and strides over the matches
+      const int te = tab[e_lane];
+      T* dst = out_ref + lane * vec;
+      for (int k = k_lane; k < a.K; k += kstep, dst += 32 * vec) put(int(wb[k]), te, e_lane, dst, ref, k);
+    } else {
+      int k = k_lane, e = e_lane;
+      for (int it = lane; it < items; it += 32) {
+        put(int(wb[k]), tab[e], e, out_ref + it * vec, ref, k);
+        e += estep;
+        k += kstep;
+        if (e >= ppv) e -= ppv, ++k;
       }
-      e += estep;
-      k += kstep;
-      if (e >= ppv) e -= ppv, ++k;
     }
   }
 }
@@ -333,12 +347,16 @@ cudaError_t launch_group_staged_t(const GroupArgs& a, const sc_bm_plan_s& p, int
   sa.tiles_x = (g.nx + sa.TRX - 1) / sa.TRX;
   const int tiles_y = (g.ny + sa.TRY - 1) / sa.TRY;
   const dim3 grid(sa.tiles_x * tiles_y, unsigned(n_images));
-  if (short_bases) {
-    cudaFuncSetAttribute(group_staged_kernel<T, int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    group_staged_kernel<T, int16_t><<<grid, 256, bytes, st>>>(a, sa);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    kern<<<grid, 256, bytes, st>>>(a, sa);
+  };
+  if (g.b == 8) {
+    if (short_bases) go(group_staged_kernel<T, int16_t, 8>);
+    else go(group_staged_kernel<T, int, 8>);
   } else {
-    cudaFuncSetAttribute(group_staged_kernel<T, int>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    group_staged_kernel<T, int><<<grid, 256, bytes, st>>>(a, sa);
+    if (short_bases) go(group_staged_kernel<T, int16_t, 0>);
+    else go(group_staged_kernel<T, int, 0>);
   }
   return cudaGetLastError();
 }
