@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   int thr[NY];     // largest d' = d - ||X_i||^2 that may still enter the reference's top-K
   float thrf[NY];  // NCC: largest filter score that may still enter the top-(K+8)
   float nrs[NY];   // NCC: sqrt(n_r)
+  float gsq[NY];   // NCC: the filter's bound on C^2 / n_c (0: keep everything)
   RegTopK32<KR> rt[NY];
   const Key32 key32{rbits, dsat};
 #pragma unroll
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     thr[q] = int(dsat) - nr[q];
     thrf[q] = __int_as_float(0x7f800000);
     nrs[q] = sqrtf(float(nr[q]));
+    gsq[q] = 0.f;
     if constexpr (NCC) {  // 0 sentinels: the (K+8)-th key sits in r[KR-1]
 #pragma unroll
       for (int k = 0; k < KR; ++k) rt[q].r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
@@ -234,8 +236,14 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             // lanes without a survivor insert the no-op key ~0 (branch-free round)
             uint32_t pos, d;
             asm("bfind.u32 %0, %1;" : "=r"(pos) : "r"(bits));
-            const int i = int(min(pos, uint32_t(2 * VY - 1)));
+            const int i = int(min(pos, uint32_t(NCC ? VY - 1 : 2 * VY - 1)));
             asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sc_s + 128u * uint32_t(i)));
+            if constexpr (NCC) {  // staged C and n_c -> filter score sqrt(n_r) - C / sqrt(n_c) (float bits)
+              uint32_t nw;
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nw) : "r"(sc_s + 128u * uint32_t(i + VY)));
+              const float sc = nrs[q] - (nw > 0u ? float(d) * rsqrtf(float(nw)) : 0.f);
+              d = __float_as_uint(fmaxf(sc, 0.f));
+            }
             const int rel = (i < VY ? rel0p : relB) + i * Wn;
             const uint32_t none = bits ? 0u : 0xffffffffu;
             uint32_t key;
@@ -251,6 +259,8 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             if (kth != 0xffffffffu) {  // largest score of the (K+8)-th key's quantum + margin
               const float smax = __uint_as_float(((kth >> rbits) << (rbits - 1)) | ((1u << (rbits - 1)) - 1u));
               thrf[q] = fmaf(smax, 1.0f + 1e-5f, 1e-30f);
+              const float g = nrs[q] - thrf[q];  // keep iff C / sqrt(n_c) >= g, i.e. C^2 >= g^2 n_c (C >= 0)
+              gsq[q] = g > 0.f ? g * g * (1.0f - 1e-6f) : 0.f;
             }
           } else {
             thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
@@ -308,13 +318,20 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         int t[VY];
         unsigned fails = 0u;
         if constexpr (NCC) {
+          // raw bytes: 0 <= C, n_c < 2^22, so both convert exactly by the 2^23 magic-number trick and
+          // the filter sqrt(n_r) - C / sqrt(n_c) <= thrf needs no square root: C^2 - gsq n_c >= 0
+          // (gsq carries a 1e-6 relative margin, so rounding never drops a candidate). C and n_c
+          // are staged for the flush, which scores the survivors.
+          uint32_t* sc = scratch + q * (64 * VY) + lane;
 #pragma unroll
           for (int i = VY - 1; i >= 0; --i) {
             const int cc = U[q][i] + __shfl_down_sync(0xffffffffu, U[q][i], 1);      // C
             const int nn = D[4 * q + i] + __shfl_down_sync(0xffffffffu, D[4 * q + i], 1);  // n_c
-            const float sc = nrs[q] - (nn > 0 ? float(cc) * rsqrtf(float(nn)) : 0.f);
-            t[i] = __float_as_int(fmaxf(sc, 0.f));
-            fails = __funnelshift_l(__float_as_uint(thrf[q] - sc), fails, 1);  // (fails << 1) | sign
+            const float fc = __int_as_float(0x4B000000 | cc) - 8388608.f;
+            const float fn = __int_as_float(0x4B000000 | nn) - 8388608.f;
+            sc[32 * i] = uint32_t(cc);
+            sc[32 * (i + VY)] = uint32_t(nn);
+            fails = __funnelshift_l(__float_as_uint(fmaf(-gsq[q], fn, fc * fc)), fails, 1);
           }
         } else {
 #pragma unroll
@@ -325,7 +342,9 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           }
         }
         const unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);
-        if (__any_sync(0xffffffffu, bits != 0u)) {
+        if constexpr (NCC) {
+          pend[q] |= bits;
+        } else if (__any_sync(0xffffffffu, bits != 0u)) {
           uint32_t* sc = scratch + q * (64 * VY) + half * (32 * VY) + lane;
           // the slack t is staged; the flush recovers d = d' + ||X_i||^2 = (thr + n_r) - t (exact,
           // thr does not change between the two staged groups of a flush)
@@ -335,7 +354,10 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         }
       }
       const int rel0 = relt + (dy0 - lo) * Wn + off;
-      if (half == 0) {
+      if constexpr (NCC) {  // one group per flush: the scratch holds its C and n_c
+        rel0p = rel0;
+        flush(0);
+      } else if (half == 0) {
         rel0p = rel0;
         half = 1;
       } else {
@@ -392,7 +414,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         it.c = zero ? 0 : ci;
         it.n = zero ? 1 : nci;
         it.f = (zero || !have) ? 0.0 : double(ci) / sqrt(double(nri) * double(nci));
-        it = warp_sort_ncc<true>(it, lane);
+        it = warp_rank_ncc<true>(it, lane);
         if (lane < a.K) {
           a.idx_out[(row0 + j) * a.K + lane] = it.idx;
           reinterpret_cast<float*>(a.dist_out)[(row0 + j) * a.K + lane] =

@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
           it.f = double(float(den > 0.0 ? cd / den : 0.0));
         }
       }
-      it = warp_sort_ncc<EXACT>(it, lane);
+      it = warp_rank_ncc<EXACT>(it, lane);
       if (lane < a.K) {
         a.idx_out[(row0 + j) * a.K + lane] = it.idx;
         a.dist_out[(row0 + j) * a.K + lane] = it.idx < 0 ? __int_as_float(0x7f800000) : float(-it.f);

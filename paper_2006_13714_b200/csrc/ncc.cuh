@@ -56,5 +56,57 @@ __device__ __noinline__ NccItem warp_sort_ncc(NccItem x, int lane) {
   return x;
 }
 
+// The same order at a fraction of the cost: a warp bitonic sort of 64-bit keys (order-preserving
+// bits of float(-f), then idx) that carries only the source lane, the items fetched once at the
+// end; float(-f) is monotone in f, so the key order can disagree with ncc_better only between
+// neighbours whose float keys are equal or whose f are within the exact path's rounding band --
+// those are repaired by odd-even transposition passes with the full comparator (rarely entered).
+template <bool EXACT>
+__device__ __forceinline__ NccItem warp_rank_ncc(const NccItem x, int lane) {
+  uint32_t hi = 0xffffffffu, lo = 0xffffffffu;  // empty slots sort last
+  if (x.idx >= 0) {
+    const uint32_t u = __float_as_uint(float(-x.f) + 0.0f);  // -0 -> +0 (ncc_better: equal)
+    hi = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    lo = uint32_t(x.idx);
+  }
+  int src = lane;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t phi = __shfl_xor_sync(0xffffffffu, hi, j), plo = __shfl_xor_sync(0xffffffffu, lo, j);
+      const int psrc = __shfl_xor_sync(0xffffffffu, src, j);
+      const bool p_less = phi < hi || (phi == hi && plo < lo);
+      const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
+      if (take_min == p_less) hi = phi, lo = plo, src = psrc;
+    }
+  }
+  NccItem y;
+  y.c = __shfl_sync(0xffffffffu, x.c, src);
+  y.n = __shfl_sync(0xffffffffu, x.n, src);
+  y.f = __shfl_sync(0xffffffffu, x.f, src);
+  y.idx = __shfl_sync(0xffffffffu, x.idx, src);
+  // neighbours the keys may have mis-ordered
+  const uint32_t nhi = __shfl_down_sync(0xffffffffu, hi, 1);
+  const double nf = __shfl_down_sync(0xffffffffu, y.f, 1);
+  const int nidx = __shfl_down_sync(0xffffffffu, y.idx, 1);
+  bool amb = lane < 31 && y.idx >= 0 && nidx >= 0 && nhi == hi;
+  if constexpr (EXACT) amb |= lane < 31 && y.idx >= 0 && nidx >= 0 && fabs(y.f - nf) <= 1e-12 * fmax(fabs(y.f), fabs(nf));
+  if (__any_sync(0xffffffffu, amb)) {
+    for (int pass = 0, quiet = 0; quiet < 2; ++pass) {
+      const int ph = pass & 1;
+      const int partner = ((lane & 1) == ph) ? min(lane + 1, 31) : max(lane - 1, 0);
+      NccItem p;
+      p.c = __shfl_sync(0xffffffffu, y.c, partner);
+      p.n = __shfl_sync(0xffffffffu, y.n, partner);
+      p.f = __shfl_sync(0xffffffffu, y.f, partner);
+      p.idx = __shfl_sync(0xffffffffu, y.idx, partner);
+      const bool swap = partner != lane && (partner > lane ? ncc_better<EXACT>(p, y) : ncc_better<EXACT>(y, p));
+      if (swap) y = p;
+      quiet = __any_sync(0xffffffffu, swap) ? 0 : quiet + 1;
+    }
+  }
+  return y;
+}
 
 }  // namespace scbm
