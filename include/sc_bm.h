@@ -220,6 +220,13 @@ sc_status_t sc_bm_norm_map(sc_bm_plan_t plan, const void* img, void* norm_out, s
 sc_status_t sc_bm_run_dense_debug(sc_bm_plan_t plan, const void* img, void* dist_all,
                                   sc_stream_t stream);
 
+/*
+ * Test export: the number of references the LAST matching launch of the plan (its last frame
+ * chunk) sent to the exact fix-up kernel (u8 L2: saturated or unfilled 32-bit keys; NCC: key
+ * quantisation that could hide a top-K candidate). Synchronises the device; host pointer.
+ */
+sc_status_t sc_bm_debug_fix_count(sc_bm_plan_t plan, int32_t* count_out);
+
 #ifdef __cplusplus
 }
 #endif

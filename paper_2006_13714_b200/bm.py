@@ -23,7 +23,7 @@ SC_METRIC_L2, SC_METRIC_NCC = 0, 1
 EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
             "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group",
-            "sc_bm_nlm_weights", "sc_bm_set_temporal"]
+            "sc_bm_nlm_weights", "sc_bm_set_temporal", "sc_bm_debug_fix_count"]
 
 
 class ScError(RuntimeError):
@@ -75,6 +75,7 @@ def load_library():
     L.sc_status_string.restype = ctypes.c_char_p
     L.sc_bm_norm_map.argtypes = [vp, vp, vp, vp]
     L.sc_bm_run_dense_debug.argtypes = [vp, vp, vp, vp]
+    L.sc_bm_debug_fix_count.argtypes = [vp, ctypes.POINTER(i32)]
     L.sc_bm_set_timing.argtypes = [vp, i32]
     L.sc_bm_get_timing.argtypes = [vp, ctypes.POINTER(Timing)]
     L.sc_bm_group.argtypes = [vp, vp, i64, vp, vp, vp]
@@ -252,6 +253,12 @@ class Plan:
         _check("sc_bm_run_dense_debug", self._lib.sc_bm_run_dense_debug(
             self._h, ctypes.c_void_p(img.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
+
+    def debug_fix_count(self):
+        """References the last matching launch sent to the exact fix-up kernel (test export)."""
+        n = ctypes.c_int32(0)
+        _check("sc_bm_debug_fix_count", self._lib.sc_bm_debug_fix_count(self._h, ctypes.byref(n)))
+        return n.value
 
 
 def status_string(code: int) -> str:

@@ -414,7 +414,20 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         it.c = zero ? 0 : ci;
         it.n = zero ? 1 : nci;
         it.f = (zero || !have) ? 0.0 : double(ci) / sqrt(double(nri) * double(nci));
+        // the kept keys were quantised (2^-(rbits-1)... relative): when the worst kept key's quantum
+        // could still hold a score as good as the exact K-th one, a dropped candidate might belong
+        // to the top-K -> exact re-rank over the whole window (fixup.cu)
+        const uint32_t klast = __shfl_sync(0xffffffffu, kk, KR - 1);
         it = warp_rank_ncc<true>(it, lane);
+        const double fK = __shfl_sync(0xffffffffu, it.f, a.K - 1);
+        if (lane == 0 && klast != 0u && klast != 0xffffffffu && nri > 0) {
+          const float smin = __uint_as_float((klast >> rbits) << (rbits - 1));  // quantum minimum
+          const double nrd = sqrt(double(nri)), scK = nrd * (1.0 - fK);         // exact K-th score
+          if (double(smin) <= scK * (1.0 + 1e-5) + 1e-6 * nrd) {
+            const int pos = atomicAdd(a.fix_count, 1);
+            a.fix_list[pos] = int(row0 + j);
+          }
+        }
         if (lane < a.K) {
           a.idx_out[(row0 + j) * a.K + lane] = it.idx;
           reinterpret_cast<float*>(a.dist_out)[(row0 + j) * a.K + lane] =
@@ -561,14 +574,18 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
     if (e != cudaSuccess) return e;
     return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
   }
-  if (g.metric == SC_METRIC_NCC) {  // K + 8 <= 32: no saturation, no fix-up
-    if (launches) *launches += 1;
-    if (g.Wn == 33 && g.KP <= 24) return launch_box_t<2, 11, 24, 40, true, 33>(a, F, box_layout(g, 2, vy, 24, &a), st);
-    if (vy == 11 && a.WP == 40 && g.KP <= 24) return launch_box_t<2, 11, 24, 40, true>(a, F, box_layout(g, 2, vy, 24, &a), st);
-    if (vy == 11 && a.WP == 40) return launch_box_t<2, 11, 32, 40, true>(a, F, smem, st);
-    if (vy == 11) return launch_box_t<2, 11, 32, 0, true>(a, F, smem, st);
-    if (vy == 7) return launch_box_t<2, 7, 32, 0, true>(a, F, smem, st);
-    return launch_box_t<2, 8, 32, 0, true>(a, F, smem, st);
+  if (g.metric == SC_METRIC_NCC) {  // K + 8 <= 32; references the key quantisation leaves open -> fix-up
+    cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    if (g.Wn == 33 && g.KP <= 24) e = launch_box_t<2, 11, 24, 40, true, 33>(a, F, box_layout(g, 2, vy, 24, &a), st);
+    else if (vy == 11 && a.WP == 40 && g.KP <= 24) e = launch_box_t<2, 11, 24, 40, true>(a, F, box_layout(g, 2, vy, 24, &a), st);
+    else if (vy == 11 && a.WP == 40) e = launch_box_t<2, 11, 32, 40, true>(a, F, smem, st);
+    else if (vy == 11) e = launch_box_t<2, 11, 32, 0, true>(a, F, smem, st);
+    else if (vy == 7) e = launch_box_t<2, 7, 32, 0, true>(a, F, smem, st);
+    else e = launch_box_t<2, 8, 32, 0, true>(a, F, smem, st);
+    if (launches) *launches += 2;
+    if (e != cudaSuccess) return e;
+    return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
   }
   cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;

@@ -46,6 +46,8 @@ struct BoxfArgs {
   int scr;          // per-warp scratch words (survivor staging [+ output staging | + heaps])
   int hp;           // heap pitch (words per reference) when the top-KP lives in shared heaps
   int rb;           // window-relative index bits of the 32-bit keys
+  int* fix_count;   // references the key quantisation leaves open -> exact fix-up (fixup.cu)
+  int* fix_list;
 };
 
 __device__ __forceinline__ int centre_out_f(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
@@ -329,7 +331,20 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
           it.f = double(float(den > 0.0 ? cd / den : 0.0));
         }
       }
+      // the worst kept key's quantum could still hold a score as good as the exact K-th one:
+      // a dropped candidate might belong to the top-K -> exact re-rank of the window (fixup.cu)
+      const uint32_t klast = __shfl_sync(0xffffffffu, kk, KR - 1);
       it = warp_rank_ncc<EXACT>(it, lane);
+      const double fK = __shfl_sync(0xffffffffu, it.f, a.K - 1);
+      const double nrq = EXACT ? double(nri) : nrd;
+      if (lane == 0 && klast != 0u && klast != 0xffffffffu && nrq > 0.0) {
+        const float smin = __uint_as_float((klast >> rb) << (rb - 1));  // quantum minimum
+        const double nrs_d = sqrt(nrq), scK = nrs_d * (1.0 - fK);     // exact K-th filter score
+        if (double(smin) <= scK * (1.0 + 1e-5) + 1e-6 * nrs_d) {
+          const int pos = atomicAdd(a.fix_count, 1);
+          a.fix_list[pos] = int(row0 + j);
+        }
+      }
       if (lane < a.K) {
         a.idx_out[(row0 + j) * a.K + lane] = it.idx;
         a.dist_out[(row0 + j) * a.K + lane] = it.idx < 0 ? __int_as_float(0x7f800000) : float(-it.f);
@@ -366,6 +381,25 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
         key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * a.W + cx);
       }
       top.merge(key, lane);
+    }
+    {  // worst kept key vs the exact K-th distance (see the NCC branch; fp32 filter error margin)
+      uint64_t kv = kKeyInf;
+#pragma unroll
+      for (int sl = 0; sl < NJ; ++sl)
+        if (sl == (a.K - 1) / 32) kv = top.v[sl];
+      kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
+      const float nrj = __shfl_sync(0xffffffffu, nr, j);
+      uint32_t klast;
+      if constexpr (HEAP) klast = heap[(j - min(lane, RX - 1)) * a.hp + 1];  // max-heap root
+      else klast = scratch[j * (KR + 1) + KR - 1];
+      if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf) {
+        const float dK = __uint_as_float(uint32_t(kv >> 32));
+        const float smin = __uint_as_float((klast >> rb) << (rb - 1));
+        if (smin <= fmaf(dK, 1.0f + 1e-5f, 4e-6f * (nrj + dK))) {
+          const int pos = atomicAdd(a.fix_count, 1);
+          a.fix_list[pos] = int(row0 + j);
+        }
+      }
     }
 #pragma unroll
     for (int sl = 0; sl < NJ; ++sl) {
@@ -429,10 +463,13 @@ bool boxf_supported(const Geometry& g) {
   return boxf_layout(g, kr, &a) <= (g.C == 1 ? 113 : 227) * 1024;
 }
 
-cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
-                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
+namespace {
+cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                               int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
   const Geometry& g = p.g;
   BoxfArgs a{};
+  a.fix_count = p.ws.fix_count;
+  a.fix_list = p.ws.fix_list;
   a.imgs = imgs;
   a.idx_out = idx_out;
   a.dist_out = static_cast<float*>(dist_out);
@@ -468,6 +505,17 @@ cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int i
   SCBM_BOXF_CASE(2, 8)
 #undef SCBM_BOXF_CASE
   return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_bm_boxf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
+  // matcher, then the exact fix-up of the references its quantised keys leave open
+  cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = launch_boxf_kernel(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st, launches);
+  if (e != cudaSuccess) return e;
+  if (launches) *launches += 1;
+  return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
 }
 
 }  // namespace scbm

@@ -275,6 +275,15 @@ sc_status_t sc_bm_run_dense_debug(sc_bm_plan_t p, const void* img, void* dist_al
                  reinterpret_cast<cudaStream_t>(stream));
 }
 
+sc_status_t sc_bm_debug_fix_count(sc_bm_plan_t p, int32_t* count_out) {
+  if (!p || !count_out) return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(count_out, p->ws.fix_count, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  return cuda_status(e);
+}
+
 sc_status_t sc_bm_nlm_weights(sc_bm_plan_t p, const void* img, float h, float* weights_out, sc_stream_t stream) {
   if (!p || !img || !weights_out || !(h > 0.f) || !std::isfinite(h)) return SC_ERR_INVALID_ARGUMENT;
   if (p->g.metric != SC_METRIC_L2) return SC_ERR_UNSUPPORTED;

@@ -630,10 +630,11 @@ def test_ncc_random_sweep(case):
         check_ncc(x[n], b, s, Wn, K, gi[n], gd[n], oi[n], od[n], exact=dtype == "u8", where=f"ncc {case} img{n}")
 
 
-@pytest.mark.parametrize("kind", ["zeros", "constant", "periodic", "scaled"])
+@pytest.mark.parametrize("kind", ["zeros", "constant", "periodic", "scaled", "near_scaled"])
 def test_ncc_ties_and_degenerate(kind):
-    """Zero-norm patches (NCC := 0), all-ties images, periodic tilings and exact scaled copies:
-    the exact uint8 ordering must reproduce the oracle's tie-breaks."""
+    """Zero-norm patches (NCC := 0), all-ties images, periodic tilings, exact scaled copies and
+    rounded near-scaled copies (NCC within rounding of 1): the exact uint8 ordering must reproduce
+    the oracle's tie-breaks; references whose quantised keys cannot decide go to the fix-up."""
     from tests.parity import check_ncc
     rng = np.random.Generator(np.random.PCG64(15))
     if kind == "zeros":
@@ -643,12 +644,50 @@ def test_ncc_ties_and_degenerate(kind):
         x = np.full((1, 1, 48, 70), 77, dtype=np.uint8)
     elif kind == "periodic":
         x = np.tile(rng.integers(0, 256, size=(8, 8), dtype=np.uint8), (6, 9))[None, None].copy()
-    else:
+    elif kind == "scaled":
         base = rng.integers(1, 64, size=(48, 35), dtype=np.uint8)
         x = np.concatenate([base, base * 2], axis=1)[None, None].copy()
+    else:
+        tile = rng.integers(60, 200, size=(8, 8)).astype(np.float64)
+        gains = rng.uniform(0.9, 1.1, size=(6, 9))
+        x = np.clip(np.round(np.kron(gains, np.ones((8, 8))) * np.tile(tile, (6, 9))), 0, 255)
+        x = x.astype(np.uint8)[None, None].copy()
     p, gi, gd = _ncc_run(x, 8, 4, 21, 16, "u8")
     oi, od = oracle.ncc(x, 8, 4, 21, 16)
     check_ncc(x[0], 8, 4, 21, 16, gi[0], gd[0], oi[0], od[0], exact=True, where=f"ncc {kind}")
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX
+    p.set_kernel(SC_KERNEL_BOX)  # the dp4a kernel and its fix-up (small images default to the float kernel)
+    gi, gd = _run(p, x)
+    check_ncc(x[0], 8, 4, 21, 16, gi[0], gd[0], oi[0], od[0], exact=True, where=f"ncc {kind} box")
+    if kind == "constant":  # every candidate ties at NCC = 1: the float keys cannot order them
+        assert p.debug_fix_count() > 0
+
+
+@pytest.mark.parametrize("metric", ["l2", "ncc"])
+def test_boxf_quantised_key_fixup(metric):
+    """The float box kernel's 32-bit keys quantise the score (~1e-4 relative): on a constant image
+    every candidate ties, the worst kept key cannot separate the K-th candidate from dropped ones,
+    so every reference goes to the exact fix-up -- whose output must still satisfy the parity rule;
+    a tiny-noise image mixes flagged and unflagged references."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOXF, Plan
+    from tests.parity import check_ncc
+    H, W, b, s, Wn, K = 40, 56, 8, 3, 15, 12
+    rng = np.random.Generator(np.random.PCG64(21))
+    for kind in ("constant", "tiny_noise"):
+        x = np.full((1, 1, H, W), 0.5 if metric == "l2" else 0.7, dtype=np.float32)
+        if kind == "tiny_noise":
+            x += (rng.standard_normal(x.shape) * 1e-3).astype(np.float32)
+        p = Plan(H, W, 1, b, s, Wn, K, "f32", metric=metric)
+        p.set_kernel(SC_KERNEL_BOXF)
+        gi, gd = _run(p, x)
+        if kind == "constant":
+            assert p.debug_fix_count() == p.n_refs
+        if metric == "l2":
+            oi, od = oracle.bm(x, b, s, Wn, K)
+            check_f32(x[0], b, s, Wn, K, gi[0], gd[0], oi[0], od[0], where=f"boxf fixup {kind}")
+        else:
+            oi, od = oracle.ncc(x, b, s, Wn, K)
+            check_ncc(x[0], b, s, Wn, K, gi[0], gd[0], oi[0], od[0], exact=False, where=f"boxf ncc fixup {kind}")
 
 
 def test_ncc_configs_and_rejects():
