@@ -371,11 +371,14 @@ def main():
 
     # roofline of the dominant kernel (the fused cross-term / top-K kernel)
     peaks = _peaks()
-    # algorithmic MACs per candidate pair: the direct cross term is b^2 C
-    # multiply-adds; the box-sum kernel evaluates each product of the shifted
-    # product image once, s^2 C per pair (its 4x4 block sums are shared by 2 x 2 references)
-    # (c5); the float box kernel correlates one s-column strip per reference and offset, b s C
-    mac_pair = {3: cfg.s * cfg.s * cfg.C, 4: cfg.b * cfg.s * cfg.C}.get(info["kernel"], cfg.b * cfg.b * cfg.C)
+    # algorithmic MACs per candidate pair = SURVEY.md 8d's per-unit figure MAC_alg: the cross term
+    # of Eq. 5 is b^2 C multiply-adds per (reference, candidate) pair. The
+    # kernels EXECUTE fewer: the box-sum kernel forms each product of the shifted product image
+    # once, s^2 C per pair (its 4x4 block sums are shared by 2 x 2 references, c5); the float box
+    # kernel correlates one s-column strip per reference and offset, b s C per pair. Both are
+    # reported (frac_executed = the executed MACs at the same peak).
+    mac_pair = cfg.b * cfg.b * cfg.C
+    mac_exec = {3: cfg.s * cfg.s * cfg.C, 4: cfg.b * cfg.s * cfg.C}.get(info["kernel"], mac_pair)
     pairs_rank = pairs_step // max(1, ws) if args.temporal > 0 else pairs_per_image * nloc
     macs_launch = pairs_rank * mac_pair  # algorithmic MACs per rank-step
     macs_direct = pairs_rank * cfg.b * cfg.b * cfg.C
@@ -407,7 +410,9 @@ def main():
             "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
             "peak_source": peak_note, "kernel_ms_per_step": match_ms, "norm_ms_per_step": norm_ms,
             "kernel_share_of_step": match_ms / ms if ms > 0 else None,
-            "algorithmic_ops_per_launch": 2.0 * macs_launch, "macs_per_pair": mac_pair}
+            "algorithmic_ops_per_launch": 2.0 * macs_launch, "macs_per_pair": mac_pair,
+            "executed_macs_per_pair": mac_exec,
+            "frac_executed": (achieved * mac_exec / mac_pair / peak) if achieved else None}
     # the north_star's roofline: direct b^2 C MACs per pair at the int8 / fp32 peak vs image +
     # output bytes at HBM bandwidth (whichever is slower), against the measured step time
     if cfg.dtype == "u8":
