@@ -389,15 +389,17 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       __syncwarp();
       const int ry = 4 * iy;
       const uint32_t* refbase = sm + (roff & 3) * a.PL + (rr0 + 4 * q) * WP + (roff >> 2);
+      const int kskip = KR - a.KP;  // leading 0 sentinels: lane k takes the k-th kept key
       for (int j = 0; j < nref; ++j) {
-        const uint32_t kk = lane < KR ? scratch[j * (KR + 1) + lane] : 0xffffffffu;
+        const uint32_t kk = lane < a.KP ? scratch[j * (KR + 1) + kskip + lane] : 0xffffffffu;
         const bool have = kk != 0u && kk != 0xffffffffu;
         const int rel = have ? int(kk & relmask) - 1 : 0;
         const int dyy = rel / Wn, dxx = rel - dyy * Wn;
         const int cy = ry + dyy + lo, cx = (ix_first + j) * 4 + dxx + lo;
         const int ccol = cx - Xbase;  // region byte column of the candidate (>= 0)
         const uint32_t* cbase2 = sm + (ccol & 3) * a.PL + (cy - Ybase) * WP + (ccol >> 2);
-        int ci = 0, nci = 0, nri = 0;
+        int ci = 0, nci = 0;
+        const int nri = __shfl_sync(0xffffffffu, nr[q], j);  // ||X_i||^2 (raw bytes), lane j's reference
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -406,7 +408,6 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             const uint32_t cv = have ? cbase2[r * WP + w] : 0u;
             ci = dp4<true>(rv, cv, ci);
             nci = dp4<true>(cv, cv, nci);
-            nri = dp4<true>(rv, rv, nri);
           }
         NccItem it;
         it.idx = have ? cy * a.W + cx : -1;
@@ -417,8 +418,8 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         // the kept keys were quantised (2^-(rbits-1)... relative): when the worst kept key's quantum
         // could still hold a score as good as the exact K-th one, a dropped candidate might belong
         // to the top-K -> exact re-rank over the whole window (fixup.cu)
-        const uint32_t klast = __shfl_sync(0xffffffffu, kk, KR - 1);
-        it = warp_rank_ncc<true>(it, lane);
+        const uint32_t klast = __shfl_sync(0xffffffffu, kk, a.KP - 1);
+        it = warp_repair_ncc<true>(it, lane);  // kept keys arrive in (quantised score, idx) order
         const double fK = __shfl_sync(0xffffffffu, it.f, a.K - 1);
         if (lane == 0 && klast != 0u && klast != 0xffffffffu && nri > 0) {
           const float smin = __uint_as_float((klast >> rbits) << (rbits - 1));  // quantum minimum

@@ -282,12 +282,13 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const size_t row0 = size_t(f) * band_refs + size_t(iy0 - a.iy_begin) * a.nx + ix_first;
   constexpr int NJ = (KR + 31) / 32;
   if constexpr (NCC) {
-    // a5 (NCC): exact cross terms / norms of the KP (<= 32) kept candidates, warp bitonic sort
-    // (exact 128-bit comparisons for uint8), write K (idx, d_NCC = -NCC)
+    // a5 (NCC): exact cross terms / norms of the KP (<= 32) kept candidates, which arrive in key
+    // order; exact neighbour checks + odd-even repair (128-bit comparisons for uint8, ncc.cuh),
+    // write K (idx, d_NCC = -NCC)
     constexpr bool EXACT = sizeof(TIN) == 1;
     for (int j = 0; j < nref; ++j) {
       const int rxj = (ix_first + j) * S;
-      const uint32_t kk = lane < KR ? scratch[j * (KR + 1) + lane] : 0xffffffffu;
+      const uint32_t kk = lane < a.KP ? scratch[j * (KR + 1) + (KR - a.KP) + lane] : 0xffffffffu;  // skip 0 sentinels
       NccItem it;
       it.c = 0; it.n = 1; it.f = 0.0; it.idx = -1;
       double nrd = 0.0, cd = 0.0, ncd = 0.0;
@@ -333,8 +334,8 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
       }
       // the worst kept key's quantum could still hold a score as good as the exact K-th one:
       // a dropped candidate might belong to the top-K -> exact re-rank of the window (fixup.cu)
-      const uint32_t klast = __shfl_sync(0xffffffffu, kk, KR - 1);
-      it = warp_rank_ncc<EXACT>(it, lane);
+      const uint32_t klast = __shfl_sync(0xffffffffu, kk, a.KP - 1);
+      it = warp_repair_ncc<EXACT>(it, lane);  // kept keys arrive in (quantised score, idx) order
       const double fK = __shfl_sync(0xffffffffu, it.f, a.K - 1);
       const double nrq = EXACT ? double(nri) : nrd;
       if (lane == 0 && klast != 0u && klast != 0xffffffffu && nrq > 0.0) {

@@ -109,4 +109,32 @@ __device__ __forceinline__ NccItem warp_rank_ncc(const NccItem x, int lane) {
   return y;
 }
 
+// Items that arrive already ordered by a monotone approximation of the key (the kept quantised
+// filter keys, empty slots last): one check of every neighbour pair with the full comparator, and
+// odd-even transposition passes only when some pair is out of order -- the passes are a complete
+// sort, so the result is exact however far the approximation was off.
+template <bool EXACT>
+__device__ __forceinline__ NccItem warp_repair_ncc(NccItem y, int lane) {
+  auto fetch = [&](int src) {
+    NccItem p;
+    p.c = __shfl_sync(0xffffffffu, y.c, src);
+    p.n = __shfl_sync(0xffffffffu, y.n, src);
+    p.f = __shfl_sync(0xffffffffu, y.f, src);
+    p.idx = __shfl_sync(0xffffffffu, y.idx, src);
+    return p;
+  };
+  const NccItem nx = fetch(min(lane + 1, 31));
+  const bool bad = lane < 31 && ncc_better<EXACT>(nx, y);
+  if (!__any_sync(0xffffffffu, bad)) return y;
+  for (int pass = 0, quiet = 0; quiet < 2; ++pass) {
+    const int ph = pass & 1;
+    const int partner = ((lane & 1) == ph) ? min(lane + 1, 31) : max(lane - 1, 0);
+    const NccItem p = fetch(partner);
+    const bool swap = partner != lane && (partner > lane ? ncc_better<EXACT>(p, y) : ncc_better<EXACT>(y, p));
+    if (swap) y = p;
+    quiet = __any_sync(0xffffffffu, swap) ? 0 : quiet + 1;
+  }
+  return y;
+}
+
 }  // namespace scbm
