@@ -476,6 +476,24 @@ def main():
             dist.all_reduce(tp, op=dist.ReduceOp.MAX)
             gather["compute_plus_gather_pipelined_ms"] = tp.item()
             gather["chunk_frames"] = chunk
+        # the gather fused into the matcher's epilogue: every rank's kernels store their rows
+        # straight into rank 0's tables through CUDA IPC / NVLink peer mappings (dist.PeerTables)
+        if args.temporal == 0:
+            from paper_2006_13714_b200.dist import PeerTables
+            pt = PeerTables(plan, nloc * ws, rank, ws)
+            for _ in range(2):  # warm the mapping
+                pt.run(x)
+            pt.finish()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record()
+            pt.run(x)
+            q1.record()
+            torch.cuda.synchronize()
+            tq = torch.tensor([q0.elapsed_time(q1)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tq, op=dist.ReduceOp.MAX)
+            pt.finish()
+            gather["compute_plus_peer_store_ms"] = tq.item()
+            del pt
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

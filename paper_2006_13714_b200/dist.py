@@ -128,3 +128,56 @@ def run_frames_pipelined(run: Callable, frames, rank: int, world: int, chunk: in
     for k in range(2):
         res[k] = torch.stack(parts[k], 0)
     return res[0], res[1]
+
+
+class PeerTables:
+    """The gather fused into the matcher's epilogue ("fused peer-store epilogue").
+
+    The root rank allocates the FULL result tables [n, n_refs, K]; their CUDA IPC handles are
+    broadcast over the process group and every other rank maps them into its own address space
+    (NVLink peer memory on an NVSwitch node). Each rank then runs the matcher on its frames with
+    the output pointers aimed at its rows of the root's tables: the kernels' coalesced (idx, dist)
+    row stores -- and the fix-up's -- go straight over NVLink, overlapped with the matching itself;
+    there is no separate collective pass. ``finish()`` (device sync + barrier) makes the root's
+    tables complete. NCCL's ``all_gather_into_tensor`` (``gather_tables``) stays the reference path.
+
+    Only the product plumbing lives here: handles travel as pickled torch IPC records
+    (``torch.multiprocessing.reductions``), the writes are the CUDA kernels' own stores.
+    """
+
+    def __init__(self, plan, n_frames: int, rank: int, world: int, root: int = 0, group=None):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.plan, self.n, self.rank, self.world, self.root, self.group = plan, n_frames, rank, world, root, group
+        self.range = frame_shard(n_frames, rank, world)
+        if rank == root:
+            self.idx, self.dist = plan.alloc_out(n_frames)
+            recs = [reduce_tensor(self.idx), reduce_tensor(self.dist)] if world > 1 else None
+        else:
+            recs = None
+        box = [recs]
+        if world > 1:
+            dist.broadcast_object_list(box, src=root, group=group)
+        if rank != root:
+            (f_i, a_i), (f_d, a_d) = box[0]
+            self.idx, self.dist = f_i(*a_i), f_d(*a_d)  # the root's tables, mapped (cudaIpcOpenMemHandle)
+        if self.idx.shape != (n_frames, plan.n_refs, plan.K):
+            raise RuntimeError("PeerTables: mapped tables have an unexpected shape")
+
+    def run(self, local_frames, stream=None):
+        """Match this rank's frames [a, b) straight into rows [a, b) of the root's tables."""
+        a, b = self.range
+        if local_frames.shape[0] != b - a:
+            raise ValueError("PeerTables.run: expected this rank's frame shard")
+        if b > a:
+            self.plan.run(local_frames, out=(self.idx[a:b], self.dist[a:b]), stream=stream)
+
+    def finish(self):
+        """Every rank's stores have landed: on return the root's tables are complete."""
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        return (self.idx, self.dist) if self.rank == self.root else None
