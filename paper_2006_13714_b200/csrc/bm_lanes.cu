@@ -465,7 +465,8 @@ int vy_for(const Geometry& g) {
 int lanes_r32_slots(const Geometry& g);
 namespace {
 
-size_t lanes_smem(const Geometry& g, int NWY, int VY, LanesArgs* a) {
+// r32: the register top-K instantiation (no norm tile, no heaps); dense tables always use heaps' layout
+size_t lanes_smem(const Geometry& g, int NWY, int VY, bool r32, LanesArgs* a) {
   const bool u8 = g.dtype == SC_DTYPE_U8;
   const int BK = bk_for(g.b, u8);
   const int pad = BK - g.b;
@@ -486,8 +487,8 @@ size_t lanes_smem(const Geometry& g, int NWY, int VY, LanesArgs* a) {
   const int NW = 31 * g.s + g.Wn;
   a->NQ = (NW + a->NP - 1) / a->NP + 1;
   a->NHp = (NWY - 1) * g.s + g.Wn + 2 * (VY - 1);
-  a->norm_words = lanes_r32_slots(g) > 0 ? 0 : ((a->NP * a->NHp * a->NQ + 3) & ~3);
-  a->list_pitch = lanes_r32_slots(g) > 0 ? 0 : (g.KP | 1);  // the register top-K path needs no heaps
+  a->norm_words = r32 ? 0 : ((a->NP * a->NHp * a->NQ + 3) & ~3);
+  a->list_pitch = r32 ? 0 : (g.KP | 1);  // the register top-K path needs no heaps
   size_t bytes = size_t(a->img_words + a->norm_words) * 4;
   bytes += size_t(NWY) * 32 * a->list_pitch * 8;  // reference lists
   bytes += size_t(NWY) * 32 * 16 * 4;           // survivor queues (64 x 12 B) / R32 scratch (32 x 16 x 4 B)
@@ -543,7 +544,7 @@ int lanes_warps_for(const Geometry& g, int sm_count, int n_images) {
   // 8 reference rows per CTA unless shared memory or the grid size says fewer
   for (int nwy : {8, 4, 2, 1}) {
     LanesArgs a{};
-    const size_t sm = lanes_smem(g, nwy, vy_for(g), &a);
+    const size_t sm = lanes_smem(g, nwy, vy_for(g), lanes_r32_slots(g) > 0, &a);
     const long long ctas = (long long)((g.ny + nwy - 1) / nwy) * ((g.nx + 31) / 32) * n_images;
     if (sm <= 110 * 1024 && ctas >= 4LL * sm_count) return nwy;
     if (nwy == 1) return 1;
@@ -553,7 +554,7 @@ int lanes_warps_for(const Geometry& g, int sm_count, int n_images) {
 
 size_t lanes_smem_bytes(const Geometry& g, int nwy) {
   LanesArgs a{};
-  return lanes_smem(g, nwy, vy_for(g), &a);
+  return lanes_smem(g, nwy, vy_for(g), lanes_r32_slots(g) > 0, &a);
 }
 
 // Register 32-bit top-K eligibility (u8, exact patch side 8, K <= 32, Wn^2 <= 2^11 so that the
@@ -581,8 +582,9 @@ cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int 
   a.NWY = p.lanes_nwy;
   a.tiles_x = (g.nx + 31) / 32;
   const int vy = vy_for(g);
-  const size_t smem = lanes_smem(g, a.NWY, vy, &a);
-  const int kr = dense ? 0 : lanes_r32_slots(g);
+  const int kr = dense ? 0 : lanes_r32_slots(g);  // dense tables: the heap instantiation's layout
+  const size_t smem = lanes_smem(g, a.NWY, vy, kr > 0, &a);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   a.rb = key32_rel_bits(g.Wn);
   a.dsat = (a.rb >= 32) ? 0u : uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
   a.fix_count = p.ws.fix_count;

@@ -18,6 +18,7 @@
 //   a5 re-score  f32 only: the best KP = K+8 keys are re-scored by direct differences
 //                sum (x_r - x_c)^2 in fp32 from the uncentred input and re-sorted.
 //   a6 output    coalesced stores of K idx + K dist per reference; u8 dist = d' + n_r exact.
+#include "nlm.cuh"
 #include "sc_internal.h"
 #include "topk.cuh"
 
@@ -31,7 +32,8 @@ struct SimtArgs {
   const void* norm;   // [F][My][Mx] int32 / float (centred norm map)
   int32_t* idx_out;   // [F][band refs][K]
   void* dist_out;     // [F][band refs][K]
-  void* dense;        // debug: [refs][Wn*Wn] (one image) or nullptr
+  void* dense;        // dense tables: [refs][Wn*Wn] (one image) or nullptr
+  float nlm_inv_h2;   // > 0: normalise each dense row into NLM weights in the epilogue (nlm.cuh)
   int H, W, C, b, s, Wn, K, KP, lo, hi, nx, My, Mx;
   long long nfs;      // norm-map frame stride
   int iy_begin, iy_end;
@@ -192,7 +194,13 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
       }
     }
   }
-  if (a.dense) return;
+  if (a.dense) {
+    if (a.nlm_inv_h2 > 0.f) {  // fused NLM epilogue: the warp's own row, just written (L2-hot)
+      __syncwarp();
+      nlm_normalize_row<T>(dense_row, a.Wn * a.Wn, a.nlm_inv_h2, lane);
+    }
+    return;
+  }
   if (cnt > 0) smem_list_merge<NJ>(lst, buf, cnt, a.KP, lane);
 
   const size_t out_base = (size_t(f) * ((a.iy_end - a.iy_begin) * a.nx) + ref_band) * a.K;
@@ -428,6 +436,7 @@ cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int i
   a.idx_out = idx_out;
   a.dist_out = dist_out;
   a.dense = dense;
+  a.nlm_inv_h2 = dense ? p.nlm_inv_h2 : 0.f;
   a.H = g.H; a.W = g.W; a.C = g.C; a.b = g.b; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
   a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
   a.nfs = g.NFS;

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 
+#include "nlm.cuh"
 #include "sc_internal.h"
 
 namespace scbm {
@@ -22,29 +23,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) nlm_normalize(void* rows, long long n_refs, int slots, float inv_h2) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_refs; r += nw) {
-    T* d = static_cast<T*>(rows) + r * slots;
-    float* w = static_cast<float*>(rows) + r * slots;
-    float dmin = __int_as_float(0x7f800000);
-    for (int k = lane; k < slots; k += 32) {
-      const float v = float(d[k]);
-      // clipped slots hold -1; a float identity distance may round slightly below 0 (clamped)
-      if (v > -0.5f) dmin = fminf(dmin, fmaxf(v, 0.f));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
-    float theta = 0.f;
-    for (int k = lane; k < slots; k += 32) {
-      const float v = float(d[k]);
-      const float e = v > -0.5f ? expf(-(fmaxf(v, 0.f) - dmin) * inv_h2) : 0.f;
-      w[k] = e;  // in place: the same slot, read before it is written by this lane
-      theta += e;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) theta += __shfl_xor_sync(0xffffffffu, theta, o);
-    const float inv = 1.f / theta;
-    for (int k = lane; k < slots; k += 32) w[k] *= inv;
-  }
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_refs; r += nw)
+    nlm_normalize_row<T>(static_cast<T*>(rows) + r * slots, slots, inv_h2, lane);
 }
 
 }  // namespace

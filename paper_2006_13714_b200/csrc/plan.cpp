@@ -103,7 +103,10 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
       e = launch_bm_box(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_BOXF && dense == nullptr)
       e = launch_bm_boxf(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
-    else if (p->kernel == SC_KERNEL_SIMT_WARP)
+    else if (p->kernel == SC_KERNEL_SIMT_WARP ||
+             (dense != nullptr && (p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF)))
+      // dense tables (NLM weights, debug): one warp per reference, lanes along its window row, so
+      // the [refs][Wn^2] rows are written contiguously
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
     else
       e = launch_bm_lanes(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
@@ -292,9 +295,14 @@ sc_status_t sc_bm_nlm_weights(sc_bm_plan_t p, const void* img, float h, float* w
   sc_status_t s = check_device(p);
   if (s != SC_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  // the window distances of every reference (Self-Convolution identity), written into the output
+  // the window distances of every reference (Self-Convolution identity), written into the output;
+  // the one-warp-per-reference dense matcher normalises its own row in its epilogue (nlm.cuh),
+  // the lanes matcher (an explicit SC_KERNEL_SIMT choice) is followed by nlm_normalize
+  const bool fused = p->kernel == SC_KERNEL_SIMT_WARP || p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF;
+  p->nlm_inv_h2 = fused ? 1.f / (h * h) : 0.f;
   s = enqueue(p, img, 1, 0, p->g.ny, nullptr, nullptr, weights_out, st);
-  if (s != SC_OK) return s;
+  p->nlm_inv_h2 = 0.f;
+  if (s != SC_OK || fused) return s;
   return cuda_status(launch_nlm_normalize(*p, weights_out, h, st, &p->launches));
 }
 

@@ -60,10 +60,14 @@ def test_norm_map(dtype, C, H, W, b):
 @pytest.mark.parametrize("dtype", ["u8", "f32"])
 @pytest.mark.parametrize("C,H,W,b,s,Wn", [(1, 64, 64, 8, 4, 21), (1, 40, 45, 7, 1, 13), (4, 36, 41, 8, 3, 17),
                                           (1, 20, 20, 3, 2, 30), (2, 33, 29, 12, 5, 9)])
-def test_dense_cross_term(dtype, C, H, W, b, s, Wn):
+@pytest.mark.parametrize("kernel", ["default", "lanes", "warp"])
+def test_dense_cross_term(dtype, C, H, W, b, s, Wn, kernel):
+    from paper_2006_13714_b200.bm import SC_KERNEL_SIMT, SC_KERNEL_SIMT_WARP
     rng = np.random.Generator(np.random.PCG64(7 * H + W))
     x = synth.random_image(rng, 1, C, H, W, dtype)[0]
     p = _plan((H, W, C, b, s, Wn, 1), dtype)
+    if kernel != "default":  # the lanes matcher's dense mode (heap layout even where u8 b = 8 uses registers)
+        p.set_kernel(SC_KERNEL_SIMT if kernel == "lanes" else SC_KERNEL_SIMT_WARP)
     got = p.dense_debug(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
     want = oracle.bm_dense(x, b, s, Wn)
     np.testing.assert_array_equal(got == -1, want == -1)
@@ -736,10 +740,16 @@ def test_ncc_u8_both_kernels(kernel):
 @pytest.mark.parametrize("dtype,C,H,W,b,s,Wn,h", [("u8", 1, 64, 64, 8, 4, 21, 300.0), ("u8", 1, 50, 77, 5, 2, 13, 120.0),
                                                    ("f32", 1, 48, 52, 7, 2, 15, 0.6), ("f32", 3, 30, 41, 4, 3, 9, 0.5),
                                                    ("u8", 2, 40, 40, 8, 3, 17, 1e6)])
-def test_nlm_weights_match_oracle(dtype, C, H, W, b, s, Wn, h):
+@pytest.mark.parametrize("kernel", ["default", "lanes"])
+def test_nlm_weights_match_oracle(dtype, C, H, W, b, s, Wn, h, kernel):
+    """default: the one-warp-per-reference dense matcher with the fused normalisation epilogue;
+    lanes: the lanes dense matcher followed by the stand-alone nlm_normalize kernel."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_SIMT
     rng = np.random.Generator(np.random.PCG64(H + W + b + C))
     x = synth.random_image(rng, 1, C, H, W, dtype)[0]
     p = _plan((H, W, C, b, s, Wn, 1), dtype)
+    if kernel == "lanes":
+        p.set_kernel(SC_KERNEL_SIMT)
     got = p.nlm_weights(torch.from_numpy(x).cuda(), h).cpu().numpy().astype(np.float64)
     want = oracle.nlm_weights(x, b, s, Wn, h)
     np.testing.assert_allclose(got.sum(1), 1.0, rtol=2e-5)
