@@ -155,6 +155,31 @@ def nlm_weights(img: np.ndarray, b: int, s: int, Wn: int, h: float, nthreads: in
     return out
 
 
+def nlm_average(img: np.ndarray, b: int, s: int, Wn: int, h: float, *, refs=None) -> np.ndarray:
+    """NL-means estimate of every reference patch: X_i ~ sum_j s_i(j) X_j (after
+    Eq. 2), the weights s_i(j) of nlm_weights over the clipped window, X_j the raw input patches.
+    One image [C,H,W] -> [refs, C, b, b] float64 (refs: optional list of reference numbers).
+    Plain loops over the definition (small images or sampled references)."""
+    a = np.asarray(img)
+    if a.ndim == 2:
+        a = a[None]
+    C, H, W = a.shape
+    ny, nx = grid(H, W, b, s)
+    w = nlm_weights(a, b, s, Wn, h)
+    lo = -(Wn // 2)
+    sel = range(ny * nx) if refs is None else refs
+    out = np.zeros((len(sel), C, b, b), dtype=np.float64)
+    x = a.astype(np.float64)
+    for o, r in enumerate(sel):
+        ry, rx = (r // nx) * s, (r % nx) * s
+        for slot in range(Wn * Wn):
+            if w[r, slot] == 0.0:
+                continue
+            cy, cx = ry + lo + slot // Wn, rx + lo + slot % Wn
+            out[o] += w[r, slot] * x[:, cy:cy + b, cx:cx + b]
+    return out
+
+
 def bm_dense(img: np.ndarray, b: int, s: int, Wn: int, nthreads: int = 0) -> np.ndarray:
     """Every window distance of one image [C,H,W]: [refs, Wn*Wn] float64, -1 where clipped."""
     a = np.ascontiguousarray(img)

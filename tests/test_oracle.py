@@ -453,6 +453,34 @@ def test_nlm_limits_and_invariants(dtype):
     np.testing.assert_allclose(w, sm / sm.sum(1, keepdims=True), rtol=1e-12, atol=1e-300)
 
 
+def test_nlm_average_pins():
+    """The NL-means patch estimate: h -> inf gives the plain mean of the clipped
+    window's patches (a numpy brute force with its own window clipping); h -> 0 returns the
+    reference patch itself (duplicate-free data: the unique zero distance); a constant image is a
+    fixed point; scaling the image scales the estimate (the weights of x*c at h*c equal x's)."""
+    rng = _rng(63)
+    x = synth.random_image(rng, 1, 2, 18, 21, "f32")[0]
+    b, s, Wn = 4, 3, 7
+    ny, nx = oracle.grid(18, 21, b, s)
+    lo, hi = -(Wn // 2), Wn - 1 - Wn // 2
+    mu = oracle.nlm_average(x, b, s, Wn, 1e12)
+    for r in range(ny * nx):
+        ry, rx = (r // nx) * s, (r % nx) * s
+        ps = [x[:, cy:cy + b, cx:cx + b].astype(np.float64)
+              for cy in range(max(0, ry + lo), min(18 - b, ry + hi) + 1)
+              for cx in range(max(0, rx + lo), min(21 - b, rx + hi) + 1)]
+        np.testing.assert_allclose(mu[r], np.mean(ps, 0), rtol=1e-9)
+    z = oracle.nlm_average(x, b, s, Wn, 1e-3)
+    for r in range(ny * nx):
+        ry, rx = (r // nx) * s, (r % nx) * s
+        np.testing.assert_allclose(z[r], x[:, ry:ry + b, rx:rx + b], rtol=1e-12)
+    c = np.full((1, 12, 13), 37, dtype=np.uint8)
+    np.testing.assert_allclose(oracle.nlm_average(c, 4, 2, 5, 10.0), 37.0, rtol=1e-12)
+    y = (x * np.float32(2.0)).astype(np.float32)
+    np.testing.assert_allclose(oracle.nlm_average(y, b, s, Wn, 0.8, refs=[0, 5, 11]),
+                               2.0 * oracle.nlm_average(x, b, s, Wn, 0.4, refs=[0, 5, 11]), rtol=1e-9)
+
+
 # ---------------------------------------------------------------- 3D / temporal search
 def test_temporal_reduces_to_spatial_and_exhaustive():
     """T = 0 is per-frame BM (idx offset by frame * H * W); T = 1 on a tiny video equals an
