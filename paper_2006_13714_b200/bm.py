@@ -23,7 +23,7 @@ SC_METRIC_L2, SC_METRIC_NCC = 0, 1
 EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
             "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group",
-            "sc_bm_nlm_weights", "sc_bm_set_temporal", "sc_bm_debug_fix_count"]
+            "sc_bm_nlm_weights", "sc_bm_set_temporal", "sc_bm_debug_fix_count", "sc_bm_nlm_average"]
 
 
 class ScError(RuntimeError):
@@ -76,6 +76,7 @@ def load_library():
     L.sc_bm_norm_map.argtypes = [vp, vp, vp, vp]
     L.sc_bm_run_dense_debug.argtypes = [vp, vp, vp, vp]
     L.sc_bm_debug_fix_count.argtypes = [vp, ctypes.POINTER(i32)]
+    L.sc_bm_nlm_average.argtypes = [vp, vp, ctypes.c_float, vp, vp]
     L.sc_bm_set_timing.argtypes = [vp, i32]
     L.sc_bm_get_timing.argtypes = [vp, ctypes.POINTER(Timing)]
     L.sc_bm_group.argtypes = [vp, vp, i64, vp, vp, vp]
@@ -252,6 +253,17 @@ class Plan:
                           dtype=torch.int32 if self.dtype == "u8" else torch.float32, device=img.device)
         _check("sc_bm_run_dense_debug", self._lib.sc_bm_run_dense_debug(
             self._h, ctypes.c_void_p(img.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def nlm_average(self, img, h, out=None, stream=None):
+        """NL-means estimate of every reference patch (sum_j s_i(j) X_j), one image [C,H,W] (or
+        [1,C,H,W]): float32 [n_refs, C, b, b]; the weights are never materialised."""
+        import torch
+        img = self._check_img(img)[0]
+        if out is None:
+            out = torch.empty((self.n_refs, self.C, self.b, self.b), dtype=torch.float32, device=img.device)
+        _check("sc_bm_nlm_average", self._lib.sc_bm_nlm_average(
+            self._h, ctypes.c_void_p(img.data_ptr()), float(h), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
     def debug_fix_count(self):

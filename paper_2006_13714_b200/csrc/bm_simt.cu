@@ -34,6 +34,7 @@ struct SimtArgs {
   void* dist_out;     // [F][band refs][K]
   void* dense;        // dense tables: [refs][Wn*Wn] (one image) or nullptr
   float nlm_inv_h2;   // > 0: normalise each dense row into NLM weights in the epilogue (nlm.cuh)
+  float* avg_out;     // NL-means estimate [band refs][C][b][b] (AVG instantiation), 1 / h^2 in nlm_inv_h2
   int H, W, C, b, s, Wn, K, KP, lo, hi, nx, My, Mx;
   long long nfs;      // norm-map frame stride
   int iy_begin, iy_end;
@@ -123,7 +124,9 @@ template <> struct Path<uint8_t> {
   __device__ static uint32_t ord(int32_t v) { return ord_i32(v); }
 };
 
-template <typename In, int BK, int VY, int NJ, bool ONE_CH>
+// AVG (NL-means, sc_bm_nlm_average): patch elements per lane, ceil(b^2 C / 32) rounded up to
+// 2, 4 or 8 (b^2 C <= 256); 0 = block matching / dense tables
+template <typename In, int BK, int VY, int NJ, bool ONE_CH, int AVG>
 __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_band, int iy, int ix,
                                             const uint32_t* __restrict__ tile,
                                             const typename Path<In>::T* __restrict__ ntile,
@@ -154,6 +157,29 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
     for (int i = lane; i < a.Wn * a.Wn; i += 32) dense_row[i] = T(-1);
     __syncwarp();
   }
+  // NL-means estimate (AVG, PAPER.md:252 after Eq. 2): X_i ~ sum_j s_i(j) X_j over the clipped
+  // window, fused -- no weight table. Streaming softmax over the candidate blocks: running minimum
+  // distance m (weights exp(-(d - m)/h^2) <= 1, rescaled when m drops), lane-partial Theta, and
+  // the weighted sum of the raw candidate patches with lanes over the b^2 C patch elements.
+  // The candidate pixels come from the CTA's staged (centred) tile; the centring constant is added
+  // back after the normalisation (sum_j s_i(j) (x'_j + c) = sum_j s_i(j) x'_j + c).
+  constexpr int EPL = AVG > 0 ? AVG : 1;
+  float avg_acc[EPL];
+  int avg_c[EPL], avg_l[EPL], avg_m[EPL];  // element -> (channel, row, column); channel -1: none
+  float m_run = __int_as_float(0x7f800000), theta = 0.f;
+  if constexpr (AVG > 0) {
+    const int bb2 = b * b;
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      const int e = lane + 32 * k;
+      const int c = e / bb2, l = (e - c * bb2) / b, m = e - c * bb2 - l * b;
+      const bool in = e < bb2 * a.C;
+      avg_c[k] = in ? c : 0;  // out-of-patch elements read a valid pixel and are never stored
+      avg_l[k] = in ? l : 0;
+      avg_m[k] = in ? m : 0;
+      avg_acc[k] = 0.f;
+    }
+  }
 
   for (int base = 0; base < nitems; base += 32) {
     const int item = base + lane;
@@ -168,6 +194,58 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
     for (int c = 0; c < nch; ++c) {
       if (!ONE_CH) P::template load_ref<BK>(R, tile, a, c, ry - Y0, rx - X0);
       P::template cross<BK, VY>(acc, R, tile, a, c, cy - Y0, cx - X0);
+    }
+    if constexpr (AVG > 0) {
+      float dv[VY], wv[VY];
+      float bmin = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int i = 0; i < VY; ++i) {
+        const int cyi = cy + i;
+        const bool ok = ivalid && cyi <= cy1;
+        const T nc = ntile[(cyi - Y0) * a.NWp + (cx - X0)];
+        dv[i] = ok ? fmaxf(float(nc - T(2) * acc[i] + nr), 0.f) : __int_as_float(0x7f800000);
+        bmin = fminf(bmin, dv[i]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bmin = fminf(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+      if (bmin < m_run) {  // warp-uniform: rescale what was accumulated against the old minimum
+        const float sc = expf(-(m_run - bmin) * a.nlm_inv_h2);
+        theta *= sc;
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) avg_acc[k] *= sc;
+        m_run = bmin;
+      }
+      unsigned any = 0u;
+#pragma unroll
+      for (int i = 0; i < VY; ++i) {
+        wv[i] = dv[i] < __int_as_float(0x7f800000) ? expf(-(dv[i] - m_run) * a.nlm_inv_h2) : 0.f;
+        theta += wv[i];
+        any |= (wv[i] > 0.f ? 1u : 0u) << i;
+      }
+      // every lane's candidates in turn: broadcast weights and position, lanes over patch elements
+      // (zero weights of clipped rows multiply finite staged pixels: no branch, loads batched)
+      for (unsigned lanes = __ballot_sync(0xffffffffu, any != 0u); lanes; lanes &= lanes - 1) {
+        const int L = __ffs(lanes) - 1;
+        const int yL = __shfl_sync(0xffffffffu, cy, L) - Y0, xL = __shfl_sync(0xffffffffu, cx, L) - X0;
+        float wj[VY];
+#pragma unroll
+        for (int i = 0; i < VY; ++i) wj[i] = __shfl_sync(0xffffffffu, wv[i], L);
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) {
+          const int y = yL + avg_l[k], x = xL + avg_m[k];
+          if constexpr (sizeof(In) == 1) {  // packed centred bytes: copy x & 3, byte 0 of word x >> 2
+            const uint32_t* col = P::plane(tile, a, avg_c[k], x & 3) + y * a.WP + (x >> 2);
+#pragma unroll
+            for (int i = 0; i < VY; ++i)
+              avg_acc[k] = fmaf(wj[i], float(int8_t(col[i * a.WP] & 0xffu)), avg_acc[k]);
+          } else {
+            const float* col = reinterpret_cast<const float*>(tile) + (size_t(avg_c[k]) * a.RHp + y) * a.RWp + x;
+#pragma unroll
+            for (int i = 0; i < VY; ++i) avg_acc[k] = fmaf(wj[i], col[i * a.RWp], avg_acc[k]);
+          }
+        }
+      }
+      continue;
     }
 #pragma unroll
     for (int i = 0; i < VY; ++i) {
@@ -193,6 +271,16 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
         __syncwarp();
       }
     }
+  }
+  if constexpr (AVG > 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) theta += __shfl_xor_sync(0xffffffffu, theta, o);
+    const float inv = 1.f / theta, centre = sizeof(In) == 1 ? 128.f : 0.5f;
+    float* out = a.avg_out + size_t(ref_band) * a.C * b * b;
+#pragma unroll
+    for (int k = 0; k < EPL; ++k)
+      if (lane + 32 * k < a.C * b * b) out[lane + 32 * k] = fmaf(avg_acc[k], inv, centre);
+    return;
   }
   if (a.dense) {
     if (a.nlm_inv_h2 > 0.f) {  // fused NLM epilogue: the warp's own row, just written (L2-hot)
@@ -259,7 +347,7 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
   }
 }
 
-template <typename In, int BK, int VY, int NJ, bool ONE_CH>
+template <typename In, int BK, int VY, int NJ, bool ONE_CH, int AVG>
 __global__ void __launch_bounds__(256) bm_simt_kernel(SimtArgs a) {
   using T = typename Path<In>::T;
   extern __shared__ __align__(16) uint32_t smem_u32[];
@@ -325,20 +413,20 @@ __global__ void __launch_bounds__(256) bm_simt_kernel(SimtArgs a) {
   for (int r = warp; r < ty_n * tx_n; r += nwarps) {
     const int iy = iy_first + r / tx_n, ix = ix_first + r % tx_n;
     const int ref_band = (iy - a.iy_begin) * a.nx + ix;
-    process_ref<In, BK, VY, NJ, ONE_CH>(a, f, ref_band, iy, ix, tile, ntile, buf, Y0, X0, lane);
+    process_ref<In, BK, VY, NJ, ONE_CH, AVG>(a, f, ref_band, iy, ix, tile, ntile, buf, Y0, X0, lane);
   }
 }
 
-template <typename In, int BK, int VY, int NJ>
+template <typename In, int BK, int VY, int NJ, int AVG = 0>
 cudaError_t launch_t(const SimtArgs& a, int F, size_t smem, cudaStream_t st) {
   const int tiles_y = (a.iy_end - a.iy_begin + a.TRY - 1) / a.TRY;
   dim3 grid(a.tiles_x * tiles_y, F);
   if (a.C == 1) {
-    auto k = bm_simt_kernel<In, BK, VY, NJ, true>;
+    auto k = bm_simt_kernel<In, BK, VY, NJ, true, AVG>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k<<<grid, 256, smem, st>>>(a);
   } else {
-    auto k = bm_simt_kernel<In, BK, VY, NJ, false>;
+    auto k = bm_simt_kernel<In, BK, VY, NJ, false, AVG>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k<<<grid, 256, smem, st>>>(a);
   }
@@ -349,6 +437,12 @@ int nj_for(int KP) { return KP <= 32 ? 1 : KP <= 64 ? 2 : KP <= 96 ? 3 : 5; }
 
 template <typename In, int BK, int VY, bool SPEC>
 cudaError_t dispatch_nj(const SimtArgs& a, int F, size_t smem, cudaStream_t st) {
+  if (a.avg_out) {  // NL-means: no lists; elements per lane for b^2 C <= 64 / 128 / 256
+    const int n = a.b * a.b * a.C;
+    if (n <= 64) return launch_t<In, BK, VY, 1, 2>(a, F, smem, st);
+    if (n <= 128) return launch_t<In, BK, VY, 1, 4>(a, F, smem, st);
+    return launch_t<In, BK, VY, 1, 8>(a, F, smem, st);
+  }
   const int nj = nj_for(a.KP);
   if constexpr (SPEC) {
     if (nj == 1) return launch_t<In, BK, VY, 1>(a, F, smem, st);
@@ -436,7 +530,8 @@ cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int i
   a.idx_out = idx_out;
   a.dist_out = dist_out;
   a.dense = dense;
-  a.nlm_inv_h2 = dense ? p.nlm_inv_h2 : 0.f;
+  a.nlm_inv_h2 = (dense || p.nlm_avg_out) ? p.nlm_inv_h2 : 0.f;
+  a.avg_out = static_cast<float*>(p.nlm_avg_out);
   a.H = g.H; a.W = g.W; a.C = g.C; a.b = g.b; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP;
   a.lo = g.lo; a.hi = g.hi; a.nx = g.nx; a.My = g.My; a.Mx = g.Mxp;  // Mx = norm-map row pitch
   a.nfs = g.NFS;

@@ -76,7 +76,8 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
   const Geometry& g = p->g;
   const size_t img_bytes = size_t(g.C) * g.H * g.W * elem_size(g.dtype);
   const size_t out_elems = size_t(iy_end - iy_begin) * g.nx * g.K;
-  const int chunk = ((p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr) ? p->FB : p->F;
+  const bool avg = p->nlm_avg_out != nullptr;  // sc_bm_nlm_average: the one-warp-per-reference matcher
+  const int chunk = ((p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr && !avg) ? p->FB : p->F;
   for (int64_t f0 = 0; f0 < n; f0 += chunk) {
     const int F = int(std::min<int64_t>(chunk, n - f0));
     const void* src = static_cast<const char*>(imgs) + f0 * img_bytes;
@@ -88,7 +89,7 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
       cudaEventRecord(ev[0], st);
     }
     // the box-sum matcher forms the norms in registers; every other matcher reads the norm map
-    const bool box = (p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr;
+    const bool box = (p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr && !avg;
     cudaError_t e = box ? cudaSuccess : launch_norm(*p, src, F, st, &p->launches);
     if (e != cudaSuccess) return cuda_status(e);
     if (ev) cudaEventRecord(ev[1], st);
@@ -97,7 +98,9 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
     p->batch_n = n;
     int32_t* io = idx ? idx + f0 * out_elems : nullptr;
     void* dd = dist ? static_cast<char*>(dist) + f0 * out_elems * 4 : nullptr;
-    if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
+    if (avg)
+      e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, nullptr, st, &p->launches);
+    else if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
       e = launch_bm_tc(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_BOX && dense == nullptr)
       e = launch_bm_box(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
@@ -304,6 +307,23 @@ sc_status_t sc_bm_nlm_weights(sc_bm_plan_t p, const void* img, float h, float* w
   p->nlm_inv_h2 = 0.f;
   if (s != SC_OK || fused) return s;
   return cuda_status(launch_nlm_normalize(*p, weights_out, h, st, &p->launches));
+}
+
+sc_status_t sc_bm_nlm_average(sc_bm_plan_t p, const void* img, float h, float* out, sc_stream_t stream) {
+  if (!p || !img || !out || !(h > 0.f) || !std::isfinite(h)) return SC_ERR_INVALID_ARGUMENT;
+  if (p->g.metric != SC_METRIC_L2 || p->g.b * p->g.b * p->g.C > 256) return SC_ERR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(img) & 15) != 0 || (reinterpret_cast<uintptr_t>(out) & 3) != 0)
+    return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  // window distances from the Self-Convolution identity, weights and the weighted patch sum fused
+  // in the one-warp-per-reference matcher's epilogue (bm_simt.cu, AVG): no weight table
+  p->nlm_inv_h2 = 1.f / (h * h);
+  p->nlm_avg_out = out;
+  s = enqueue(p, img, 1, 0, p->g.ny, nullptr, nullptr, nullptr, reinterpret_cast<cudaStream_t>(stream));
+  p->nlm_avg_out = nullptr;
+  p->nlm_inv_h2 = 0.f;
+  return s;
 }
 
 sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_stream_t stream) {

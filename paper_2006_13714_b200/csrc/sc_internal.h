@@ -73,7 +73,8 @@ struct sc_bm_plan_s {
   scbm::Timing timing;
   int64_t launches = 0;
   int T = 0;                          // temporal search radius (sc_bm_set_temporal)
-  float nlm_inv_h2 = 0.f;             // > 0 while sc_bm_nlm_weights runs the fused dense epilogue
+  float nlm_inv_h2 = 0.f;             // > 0 while sc_bm_nlm_weights / sc_bm_nlm_average run
+  void* nlm_avg_out = nullptr;        // set while sc_bm_nlm_average runs (float [refs][C][b][b])
   const void* batch_base = nullptr;   // temporal search: the run's whole batch ...
   int64_t batch_f0 = 0, batch_n = 0;  // ... the current chunk's first frame and the batch size
   int64_t min_cand = 0, max_cand = 0, total_cand = 0;

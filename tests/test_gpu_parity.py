@@ -770,6 +770,41 @@ def test_nlm_c2_full_image():
     np.testing.assert_allclose(got[m], want[m], rtol=1e-4, atol=1e-9)
 
 
+@pytest.mark.parametrize("dtype,C,H,W,b,s,Wn,h", [("u8", 1, 64, 64, 8, 4, 21, 300.0), ("f32", 1, 48, 52, 7, 2, 15, 0.6),
+                                                   ("f32", 3, 30, 41, 4, 3, 9, 0.5), ("u8", 2, 40, 40, 8, 3, 17, 1e6),
+                                                   ("u8", 1, 33, 47, 5, 1, 11, 60.0), ("f32", 4, 36, 36, 8, 3, 13, 0.3)])
+def test_nlm_average_matches_oracle(dtype, C, H, W, b, s, Wn, h):
+    """The fused NL-means estimate (no weight table): float32 identity distances and weights,
+    so relative 1e-4 of the image's value range; h -> inf gives the window mean, h -> 0 the
+    reference patch."""
+    rng = np.random.Generator(np.random.PCG64(H * W + C))
+    x = synth.random_image(rng, 1, C, H, W, dtype)[0]
+    p = _plan((H, W, C, b, s, Wn, 1), dtype)
+    t = torch.from_numpy(x).cuda()
+    scale = 255.0 if dtype == "u8" else 1.0
+    for hh in (h, 1e12, 1e-3 * scale):
+        got = p.nlm_average(t, hh).cpu().numpy().astype(np.float64)
+        want = oracle.nlm_average(x, b, s, Wn, hh)
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-4 * scale, err_msg=f"h={hh}")
+
+
+def test_nlm_average_c2_sampled_and_rejects():
+    from paper_2006_13714_b200.bm import Plan, ScError
+    cfg = synth.CONFIGS["c2"]
+    x = synth.make_input(cfg)[0]
+    p = _plan(cfg)
+    h = 25.0 / 255.0 * 8
+    got = p.nlm_average(torch.from_numpy(x).cuda(), h).cpu().numpy().astype(np.float64)
+    sel = list(np.random.Generator(np.random.PCG64(9)).choice(p.n_refs, 40, replace=False))
+    want = oracle.nlm_average(x, cfg.b, cfg.s, cfg.Wn, h, refs=sel)
+    np.testing.assert_allclose(got[sel], want, rtol=0, atol=1e-4)
+    with pytest.raises(ScError):  # b^2 C > 256
+        Plan(40, 40, 8, 8, 4, 9, 4, "f32").nlm_average(torch.zeros((8, 40, 40), device="cuda"), 1.0)
+    with pytest.raises(ScError):  # NCC plans
+        Plan(40, 40, 1, 8, 4, 9, 4, "u8", metric="ncc").nlm_average(
+            torch.zeros((1, 40, 40), dtype=torch.uint8, device="cuda"), 1.0)
+
+
 # ------------------------------------------------------------------ 3D / temporal search
 @pytest.mark.parametrize("N,H,W,Wn,K,T", [(4, 70, 150, 21, 16, 1), (5, 60, 97, 15, 12, 2), (3, 90, 130, 33, 16, 1),
                                           (2, 40, 64, 9, 32, 1), (6, 48, 80, 13, 8, 3)])
