@@ -6,9 +6,10 @@
 // column k = vecT of the full-depth patch, stored channel-major ([C][b][b], reading R13),
 // in the input dtype and uncentred. idx = -1 (fewer than K candidates) -> a zero column.
 //
-// Pure gather: HBM-bound on the writes (c5: 8.4 GB of groups per 64 frames), so threads write
-// consecutive patch rows (8-byte stores for u8 b = 8, 16-byte stores for f32 b % 4 = 0) and read
-// the image through L1/L2 (each image row segment is reused by the many groups that contain it).
+// Pure gather, HBM-bound on the writes (c5: 8.4 GB of groups per 64 frames). Two kernels:
+// group_staged_kernel (default, per-image idx) stages each reference tile's windows in shared
+// memory and writes every group segment with 16-byte streaming stores; group_kernel (batch-global
+// temporal idx, tiles that do not fit) reads the image through L1/L2, one thread per patch row.
 #include <algorithm>
 
 #include "sc_internal.h"
@@ -152,10 +153,11 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
 
 // Region-staged gather (the default for per-image idx tables): a CTA owns a TRY x TRX tile of
 // references of one image, stages the union of their search windows (+ patch extent) in shared
-// memory with coalesced loads -- every matched patch lies inside it -- and then writes the tile's
-// groups: one warp per reference, lanes over its K C b patch rows, consecutive lanes consecutive
-// rows (contiguous output), patch rows read from shared memory (uint8, b % 4 == 0: aligned words
-// + funnel shifts). The image is read once per tile instead of once per matched patch row.
+// memory with coalesced loads -- every matched patch lies inside it -- converts the tile's idx
+// rows into region offsets (a shared match table), then writes the tile's groups: one warp per
+// reference, whose K C b b elements are one contiguous output segment; lanes take 16-byte items
+// (two 8-byte u8 rows via aligned words + funnel shifts, or four floats) or single elements,
+// consecutive lanes consecutive bytes. The image is read once per tile instead of once per match.
 struct StagedArgs {
   int s, lo, hi, nx, ny, TRY, TRX, tiles_x, RH, RWp;  // RWp: region row pitch in elements
   int tab_off, tab_len;                              // item table: byte offset in shared memory, entries
