@@ -884,3 +884,31 @@ def test_temporal_row_bands_match_full_run():
         torch.cuda.synchronize()
         sl = slice(r0 * p.nx, r1 * p.nx)
         assert torch.equal(bi, fi[:, sl]) and torch.equal(bd, fd[:, sl]), (r0, r1)
+
+
+# ------------------------------------------------------------------ CUDA-graph capture
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c5"])
+def test_run_is_graph_capturable(cfg_name):
+    """sc_bm_run* never allocates or synchronises: one step captured into a CUDA graph and
+    replayed on new input equals the eager run (box / float box / warp matchers + fix-up)."""
+    cfg = synth.CONFIGS[cfg_name]
+    n = 2 if cfg_name == "c5" else cfg.N
+    x = torch.from_numpy(synth.make_input(cfg, n_frames=n) if cfg_name == "c5" else synth.make_input(cfg)).cuda()
+    p = _plan(cfg)
+    idx, dist = p.alloc_out(x.shape[0])
+    xin = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        p.run(xin.copy_(x), out=(idx, dist), stream=s)  # warm-up outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        p.run(xin, out=(idx, dist), stream=s)
+    y = torch.flip(x, dims=[-1]).contiguous()  # a different input for the replay
+    xin.copy_(y)
+    g.replay()
+    torch.cuda.synchronize()
+    wi, wd = p.run(y)
+    torch.cuda.synchronize()
+    assert torch.equal(idx, wi) and torch.equal(dist, wd)
