@@ -295,6 +295,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gather", action="store_true", help="also time an NCCL all-gather of the tables")
+    ap.add_argument("--graph", action="store_true", help="also time the step replayed from a CUDA graph")
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--metric", default="l2", choices=["l2", "ncc"],
                     help="l2: Euclidean BM, Eq. 3 (the headline); ncc: normalised cross-correlation, Eq. 4")
@@ -382,6 +383,29 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, match_ms, norm_ms = t.tolist()
 
+    # the same step captured once into a CUDA graph and replayed (launch-bound small configs)
+    graph = None
+    if args.graph:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            plan.run(x, out=(idx, dst), stream=gs)
+        torch.cuda.synchronize()
+        gst = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        gen = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            gst[k].record(stream)
+            g.replay()
+            gen[k].record(stream)
+        torch.cuda.synchronize()
+        gms = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in zip(gst, gen)]))], dtype=torch.float64,
+                           device="cuda")
+        if dist:
+            dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        graph = {"ms_per_step": gms.item(), "note": "one captured plan.run replayed per step (torch.cuda.CUDAGraph)"}
+
     pairs_per_image = info["total_candidates"]
     n_images_total = cfg.N if cfg.N > 1 else ws
     pairs_step = pairs_per_image * n_images_total
@@ -390,6 +414,8 @@ def main():
         pairs_step = pairs_per_image * frames_searched * ws
     refs_step = info["n_refs"] * n_images_total
     value = pairs_step / (ms / 1e3)
+    if graph:
+        graph["value"] = pairs_step / (graph["ms_per_step"] / 1e3)
 
     # roofline of the dominant kernel (the fused cross-term / top-K kernel)
     peaks = _peaks()
@@ -528,7 +554,7 @@ def main():
                 "dtype": _dtype_name(cfg), "data": "synthetic", "config": _config_obj(cfg, args),
                 "ref_patches_per_s": refs_step / (ms / 1e3), "candidate_pairs_per_step": pairs_step,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk.summary(), "gather": gather,
+                "clocks": clk.summary(), "gather": gather, "graph": graph,
                 "kernel": info["kernel"], "frames_per_chunk": info["frames_per_chunk"], "metric_kind": args.metric}
         print(json.dumps(line), flush=True)
     if dist:
