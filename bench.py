@@ -38,40 +38,75 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML thread (every ~2 ms,
+    so even a 100 ms region gets dozens of samples); `nvidia-smi -lms` if NVML is unavailable."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    def __init__(self, gpu_index: int, period_s: float = 0.002):
+        self.gpu, self.period = gpu_index, period_s
         self.proc = None
-        self.rows = []
+        self.nvml = None
+        self.rows = []  # (sm_mhz, max_mhz, set of active reason names)
+        self._stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.nvml = (pynvml, h, bits)
+            self._sample_nvml()  # one sample as the region starts
+            self._t = threading.Thread(target=self._loop_nvml, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t = threading.Thread(target=self._read_smi, daemon=True)
             self._t.start()
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
+    def _sample_nvml(self):
+        pynvml, h, bits = self.nvml
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.rows.append((float(sm), float(mx), {n for n, b in bits.items() if r & b}))
+
+    def _loop_nvml(self):
+        while not self._stop.wait(self.period):
+            try:
+                self._sample_nvml()
+            except Exception:
+                return
+
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.rows.append([v.strip() for v in line.split(",")])
+            r = [v.strip() for v in line.split(",")]
+            if len(r) >= 9 and r[1].replace(".", "").isdigit():
+                self.rows.append((float(r[1]), float(r[2]),
+                                  {n for i, n in enumerate(self.NAMES) if r[5 + i].lower() == "active"}))
 
     def __exit__(self, *exc):
-        if not self.rows:  # timed region shorter than one sampling period: one synchronous sample
+        self._stop.set()
+        if self.nvml is not None:
+            self._t.join(timeout=1)
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([v.strip() for v in line.split(",")])
+                self._sample_nvml()  # one sample as the region ends
             except Exception:
                 pass
         if self.proc is not None:
@@ -84,16 +119,10 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        reasons = set().union(*[r[2] for r in self.rows])
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def _dist_env():
