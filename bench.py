@@ -374,9 +374,18 @@ def main():
     idx, dst = plan.alloc_out(nloc)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
+    halo = args.temporal > 0 and ws > 1 and cfg.N > 1  # temporal search across frame shards
+
+    def step():
+        if halo:  # the T-frame halo exchange (NCCL point-to-point) + the window run, both timed
+            from paper_2006_13714_b200.dist import run_temporal_sharded
+            run_temporal_sharded(lambda ext, a0, a1, off: plan.run_temporal(ext, a0, a1, off, out=(idx, dst)),
+                                 x, rank, ws, cfg.N, args.temporal)
+        else:
+            plan.run(x, out=(idx, dst))
 
     for _ in range(args.warmup):
-        plan.run(x, out=(idx, dst))
+        step()
     torch.cuda.synchronize()
     if args.op == "group":
         return bench_group(args, cfg, plan, x, idx, ws, rank, local, dist)
@@ -395,7 +404,7 @@ def main():
         for k in range(args.steps):
             flush.fill_(k & 0xFF)  # L2 flush outside the step's events
             starts[k].record(stream)
-            plan.run(x, out=(idx, dst))
+            step()
             ends[k].record(stream)
         torch.cuda.synchronize()
     if dist:
@@ -438,9 +447,12 @@ def main():
     pairs_per_image = info["total_candidates"]
     n_images_total = cfg.N if cfg.N > 1 else ws
     pairs_step = pairs_per_image * n_images_total
-    if args.temporal > 0:  # every reference also searches the frames f-T..f+T of its rank's shard
-        frames_searched = sum(min(nloc - 1, f + args.temporal) - max(0, f - args.temporal) + 1 for f in range(nloc))
-        pairs_step = pairs_per_image * frames_searched * ws
+    if args.temporal > 0:  # every reference also searches the frames f-T..f+T of the video
+        nvid = cfg.N if cfg.N > 1 else 1
+        T_ = args.temporal
+        fs = [min(nvid - 1, f + T_) - max(0, f - T_) + 1 for f in range(nvid)]
+        pairs_step = pairs_per_image * sum(fs) * (1 if cfg.N > 1 else ws)
+        pairs_rank_t = pairs_per_image * (sum(fs[f0:f0 + nloc]) if cfg.N > 1 else fs[0])
     refs_step = info["n_refs"] * n_images_total
     value = pairs_step / (ms / 1e3)
     if graph:
@@ -456,7 +468,7 @@ def main():
     # reported (frac_executed = the executed MACs at the same peak).
     mac_pair = cfg.b * cfg.b * cfg.C
     mac_exec = {3: cfg.s * cfg.s * cfg.C, 4: cfg.b * cfg.s * cfg.C}.get(info["kernel"], mac_pair)
-    pairs_rank = pairs_step // max(1, ws) if args.temporal > 0 else pairs_per_image * nloc
+    pairs_rank = pairs_rank_t if args.temporal > 0 else pairs_per_image * nloc
     macs_launch = pairs_rank * mac_pair  # algorithmic MACs per rank-step
     macs_direct = pairs_rank * cfg.b * cfg.b * cfg.C
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)

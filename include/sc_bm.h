@@ -179,6 +179,20 @@ sc_status_t sc_bm_nlm_weights(sc_bm_plan_t plan, const void* img, float h, float
  */
 sc_status_t sc_bm_set_temporal(sc_bm_plan_t plan, int32_t T);
 
+/*
+ * Temporal search over part of a batch (a frame shard plus its halo): references from frames
+ * [f_begin, f_end) of the n_images-frame batch imgs [n_images][C][H][W]; the candidates of a
+ * reference in frame f are the clipped window positions of frames max(0, f-T) .. min(n_images-1,
+ * f+T) of that batch (T from sc_bm_set_temporal, > 0, else SC_ERR_UNSUPPORTED). idx_out /
+ * dist_out hold f_end - f_begin frames ([f][n_refs][K], as sc_bm_run_batch); idx is
+ * (frame + frame_offset) * H * W + cy * W + cx, so a rank whose buffer starts at global frame
+ * frame_offset (its halo) reports global indices. frame_offset >= 0 and the largest idx must fit
+ * int32 (SC_ERR_INVALID_ARGUMENT otherwise). Device pointers, asynchronous on `stream`.
+ */
+sc_status_t sc_bm_run_temporal(sc_bm_plan_t plan, const void* imgs, int64_t n_images, int64_t f_begin,
+                               int64_t f_end, int64_t frame_offset, int32_t* idx_out, void* dist_out,
+                               sc_stream_t stream);
+
 /* Plan geometry and bookkeeping. */
 sc_status_t sc_bm_plan_info(sc_bm_plan_t plan, sc_bm_info_t* info);
 

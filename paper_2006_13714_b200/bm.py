@@ -23,7 +23,8 @@ SC_METRIC_L2, SC_METRIC_NCC = 0, 1
 EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
             "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group",
-            "sc_bm_nlm_weights", "sc_bm_set_temporal", "sc_bm_debug_fix_count", "sc_bm_nlm_average"]
+            "sc_bm_nlm_weights", "sc_bm_set_temporal", "sc_bm_debug_fix_count", "sc_bm_nlm_average",
+            "sc_bm_run_temporal"]
 
 
 class ScError(RuntimeError):
@@ -77,6 +78,7 @@ def load_library():
     L.sc_bm_run_dense_debug.argtypes = [vp, vp, vp, vp]
     L.sc_bm_debug_fix_count.argtypes = [vp, ctypes.POINTER(i32)]
     L.sc_bm_nlm_average.argtypes = [vp, vp, ctypes.c_float, vp, vp]
+    L.sc_bm_run_temporal.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp]
     L.sc_bm_set_timing.argtypes = [vp, i32]
     L.sc_bm_get_timing.argtypes = [vp, ctypes.POINTER(Timing)]
     L.sc_bm_group.argtypes = [vp, vp, i64, vp, vp, vp]
@@ -254,6 +256,16 @@ class Plan:
         _check("sc_bm_run_dense_debug", self._lib.sc_bm_run_dense_debug(
             self._h, ctypes.c_void_p(img.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
+
+    def run_temporal(self, imgs, f_begin, f_end, frame_offset=0, out=None, stream=None):
+        """Temporal search (set_temporal(T) first) for the reference frames [f_begin, f_end) of the
+        batch imgs, candidates from every frame of it; idx = (frame + frame_offset) * H * W + pixel."""
+        imgs = self._check_img(imgs)
+        idx, dist = out if out is not None else self.alloc_out(f_end - f_begin)
+        _check("sc_bm_run_temporal", self._lib.sc_bm_run_temporal(
+            self._h, ctypes.c_void_p(imgs.data_ptr()), imgs.shape[0], f_begin, f_end, frame_offset,
+            ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
+        return idx, dist
 
     def nlm_average(self, img, h, out=None, stream=None):
         """NL-means estimate of every reference patch (sum_j s_i(j) X_j), one image [C,H,W] (or

@@ -53,6 +53,7 @@ struct BoxArgs {
   int T;           // temporal search radius (0: the reference's own frame only)
   int n_frames;    // frames reachable from imgs (temporal search: the whole batch)
   int frame0;      // batch index of the launch's first reference frame (temporal search)
+  int idx_foff;    // temporal search: frame offset added to the batch-global idx (halo buffers)
   int rb;          // 32-bit keys: window-relative index bits
   uint32_t dsat;   // 32-bit keys: distance saturation value
   int* fix_count;
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         const int tsl = TEMP ? rel / (Wn * Wn) : 0;  // frame slot tau + T
         rel -= tsl * Wn * Wn;
         const int dyy = rel / Wn, dxx = rel - dyy * Wn;
-        a.idx_out[row0 * a.K + e] = (TEMP ? (fref + tsl - a.T) * a.H * a.W : 0) +
+        a.idx_out[row0 * a.K + e] = (TEMP ? (fref + tsl - a.T + a.idx_foff) * a.H * a.W : 0) +
                                     (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
         a.dist_out[row0 * a.K + e] = key32.dist(kk);
       }
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       const int tsl = TEMP ? rel / (Wn * Wn) : 0;  // frame slot tau + T
       rel -= tsl * Wn * Wn;
       const int dyy = rel / Wn, dxx = rel - dyy * Wn;
-      a.idx_out[row0 * a.K + e] = (TEMP ? (fref + tsl - a.T) * a.H * a.W : 0) +
+      a.idx_out[row0 * a.K + e] = (TEMP ? (fref + tsl - a.T + a.idx_foff) * a.H * a.W : 0) +
                                   (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
       a.dist_out[row0 * a.K + e] = key32.dist(kk);
     }
@@ -561,6 +562,7 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
     a.T = p.T;
     a.frame0 = int(p.batch_f0);
     a.n_frames = int(p.batch_n);
+    a.idx_foff = int(p.idx_frame_off);
     a.rb = box_key_bits_t(g, p.T);
     a.dsat = uint32_t((uint64_t(1) << (32 - a.rb)) - 1);
     cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);

@@ -25,6 +25,7 @@ struct FixArgs {
   int H, W, C, b, s, K, lo, hi, nx, iy_begin, iy_end;
   int T, n_frames, frame0;  // temporal search: frames fref-T..fref+T of the batch at imgs
   int ncc;                  // SC_METRIC_NCC: exact NCC re-rank (K <= 32), dist_out = -NCC (float)
+  int idx_foff;             // temporal search: frame offset added to the batch-global idx
 };
 
 // NCC (Eq. 4): a reference whose kept top-(K+8) could have lost a top-K candidate to the 32-bit
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(FixArgs a) {
             }
           }
         // idx: frame-local without temporal search, batch-global with it
-        const int idx = (a.T > 0 ? fr * int(plane) : 0) + cy * a.W + cx;
+        const int idx = (a.T > 0 ? (fr + a.idx_foff) * int(plane) : 0) + cy * a.W + cx;
         const uint32_t dbits = U8 ? uint32_t(di) : __float_as_uint(df);  // d >= 0: monotone bits
         key = (uint64_t(dbits) << 32) | uint32_t(idx);
       }
@@ -190,6 +191,7 @@ cudaError_t launch_fixup(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
     a.imgs = p.batch_base;
     a.frame0 = int(p.batch_f0);
     a.n_frames = int(p.batch_n);
+    a.idx_foff = int(p.idx_frame_off);
   } else {
     a.frame0 = 0;
     a.n_frames = 1 << 30;

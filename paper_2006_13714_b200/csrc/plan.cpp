@@ -72,14 +72,18 @@ void free_host(sc_bm_plan_s* p) {
 // Enqueue norm + match for images [0, n) of imgs, chunked so the norm workspace of a chunk
 // stays resident in L2 while its matching kernel runs.
 sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, int iy_end,
-                    int32_t* idx, void* dist, void* dense, cudaStream_t st) {
+                    int32_t* idx, void* dist, void* dense, cudaStream_t st, int64_t f_begin = 0,
+                    int64_t f_end = -1) {
+  // reference frames [f_begin, f_end) of the n-frame batch at imgs (outputs start at f_begin);
+  // temporal search reads candidates from every frame of the batch
+  if (f_end < 0) f_end = n;
   const Geometry& g = p->g;
   const size_t img_bytes = size_t(g.C) * g.H * g.W * elem_size(g.dtype);
   const size_t out_elems = size_t(iy_end - iy_begin) * g.nx * g.K;
   const bool avg = p->nlm_avg_out != nullptr;  // sc_bm_nlm_average: the one-warp-per-reference matcher
   const int chunk = ((p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr && !avg) ? p->FB : p->F;
-  for (int64_t f0 = 0; f0 < n; f0 += chunk) {
-    const int F = int(std::min<int64_t>(chunk, n - f0));
+  for (int64_t f0 = f_begin; f0 < f_end; f0 += chunk) {
+    const int F = int(std::min<int64_t>(chunk, f_end - f0));
     const void* src = static_cast<const char*>(imgs) + f0 * img_bytes;
     cudaEvent_t* ev = nullptr;
     Timing& tm = p->timing;
@@ -96,8 +100,8 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
     p->batch_base = imgs;  // temporal search reads the neighbouring frames of the whole batch
     p->batch_f0 = f0;
     p->batch_n = n;
-    int32_t* io = idx ? idx + f0 * out_elems : nullptr;
-    void* dd = dist ? static_cast<char*>(dist) + f0 * out_elems * 4 : nullptr;
+    int32_t* io = idx ? idx + (f0 - f_begin) * out_elems : nullptr;
+    void* dd = dist ? static_cast<char*>(dist) + (f0 - f_begin) * out_elems * 4 : nullptr;
     if (avg)
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, nullptr, st, &p->launches);
     else if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
@@ -258,6 +262,25 @@ sc_status_t sc_bm_run_rows(sc_bm_plan_t p, const void* imgs, int64_t n_images, i
   if (n_images == 0 || iy_end == iy_begin) return SC_OK;
   return enqueue(p, imgs, n_images, iy_begin, iy_end, idx_out, dist_out, nullptr,
                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+sc_status_t sc_bm_run_temporal(sc_bm_plan_t p, const void* imgs, int64_t n_images, int64_t f_begin,
+                               int64_t f_end, int64_t frame_offset, int32_t* idx_out, void* dist_out,
+                               sc_stream_t stream) {
+  if (!p || !imgs || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
+  if (f_begin < 0 || f_end > n_images || f_end < f_begin) return SC_ERR_INVALID_ARGUMENT;
+  if (p->T == 0) return SC_ERR_UNSUPPORTED;  // sc_bm_run_batch on imgs + f_begin frames does it
+  if (frame_offset < 0 || (frame_offset + n_images) * int64_t(p->g.H) * p->g.W > (int64_t(1) << 31))
+    return SC_ERR_INVALID_ARGUMENT;  // the offset batch-global idx must stay int32
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  if (f_end == f_begin) return SC_OK;
+  p->idx_frame_off = frame_offset;
+  s = enqueue(p, imgs, n_images, 0, p->g.ny, idx_out, dist_out, nullptr, reinterpret_cast<cudaStream_t>(stream),
+              f_begin, f_end);
+  p->idx_frame_off = 0;
+  return s;
 }
 
 sc_status_t sc_bm_run_batch(sc_bm_plan_t p, const void* imgs, int64_t n_images, int32_t* idx_out,

@@ -77,6 +77,7 @@ struct sc_bm_plan_s {
   void* nlm_avg_out = nullptr;        // set while sc_bm_nlm_average runs (float [refs][C][b][b])
   const void* batch_base = nullptr;   // temporal search: the run's whole batch ...
   int64_t batch_f0 = 0, batch_n = 0;  // ... the current chunk's first frame and the batch size
+  int64_t idx_frame_off = 0;          // sc_bm_run_temporal: frame offset of the batch-global idx
   int64_t min_cand = 0, max_cand = 0, total_cand = 0;
 };
 

@@ -181,3 +181,46 @@ class PeerTables:
         if self.world > 1:
             dist.barrier(group=self.group)
         return (self.idx, self.dist) if self.rank == self.root else None
+
+
+def temporal_halo(local, rank: int, world: int, T: int, group=None):
+    """The one real data exchange of the method: 3D / temporal search on
+    frame shards needs, for the references of a rank's first and last frames, the T neighbouring
+    frames held by the adjacent ranks. Every rank sends its first T frames to rank-1 and its last
+    T to rank+1 (point-to-point NCCL over NVLink on GPUs; gloo in the CPU tests) and returns the
+    extended buffer [left halo | own frames | right halo] plus the halo sizes (0 at the ends).
+    T must not exceed the shard size (each halo comes from one neighbour)."""
+    import torch
+    import torch.distributed as dist
+    n = local.shape[0]
+    if T > n and world > 1:
+        raise ValueError("temporal_halo: T larger than the frame shard")
+    left = T if rank > 0 else 0
+    right = T if rank < world - 1 else 0
+    if world == 1 or T == 0:
+        return local, 0, 0
+    shape = tuple(local.shape[1:])
+    rl = torch.empty((left,) + shape, dtype=local.dtype, device=local.device)
+    rr = torch.empty((right,) + shape, dtype=local.dtype, device=local.device)
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, local[:T].contiguous(), rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, rl, rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, local[n - T:].contiguous(), rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, rr, rank + 1, group))
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    return torch.cat([rl, local, rr], 0).contiguous(), left, right
+
+
+def run_temporal_sharded(run_window: Callable, local, rank: int, world: int, n_frames: int, T: int, group=None):
+    """Frame-sharded temporal search with the halo exchange. `run_window(ext, f_begin, f_end,
+    frame_offset) -> (idx, dist)` is the plan's ``run_temporal`` (references from ext frames
+    [f_begin, f_end), candidates from all of ext, idx offset to global frames) on GPUs. Returns this
+    rank's tables for its own frames, with global (whole-video) idx."""
+    a, b = frame_shard(n_frames, rank, world)
+    if local.shape[0] != b - a:
+        raise ValueError("run_temporal_sharded: expected this rank's frame shard")
+    ext, left, _ = temporal_halo(local, rank, world, T, group)
+    return run_window(ext, left, left + (b - a), a - left)

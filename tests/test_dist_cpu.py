@@ -92,3 +92,48 @@ def test_sharded_gather_equals_single_process(mode, world):
         assert p.exitcode == 0
     res = sorted(q.get(timeout=5) for _ in range(world))
     assert all(ok for _, ok in res), res
+
+
+def _temporal_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.Generator(np.random.PCG64(5))
+        n, H, W, b, s, Wn, K, T = 7, 20, 23, 4, 2, 7, 6, 2
+        video = rng.integers(0, 256, size=(n, 1, H, W), dtype=np.uint8)
+        a, e = sdist.frame_shard(n, rank, world)
+
+        def run_window(ext, f0, f1, foff):  # the oracle standing in for plan.run_temporal
+            i, d = oracle.bm_temporal(ext.numpy(), b, s, Wn, K, T)
+            i = i[f0:f1]
+            i = np.where(i >= 0, i + foff * H * W, i)
+            return i, d[f0:f1]
+
+        gi, gd = sdist.run_temporal_sharded(run_window, torch.from_numpy(video[a:e]), rank, world, n, T)
+        wi, wd = oracle.bm_temporal(video, b, s, Wn, K, T)
+        q.put((rank, bool(np.array_equal(gi, wi[a:e]) and np.array_equal(gd, wd[a:e]))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_temporal_halo_equals_single_process(world):
+    """Temporal search on frame shards with the T-frame halo exchange (point-to-point) reproduces
+    the whole-video search for every rank's frames, global idx included."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_temporal_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(ok for _, ok in res), res

@@ -835,6 +835,36 @@ def test_group_temporal_idx():
     np.testing.assert_array_equal(Y.reshape(ref.shape), ref)
 
 
+def test_run_temporal_frame_ranges():
+    """sc_bm_run_temporal: references of frames [f_begin, f_end) of a batch, candidates from all of
+    it, idx offset by frame_offset -- the per-rank call of the sharded temporal search on its
+    halo-extended buffer (emulated here by slicing the video: the exchange itself is tested with
+    gloo in test_dist_cpu.py); a saturated video exercises the offset in the fix-up."""
+    from paper_2006_13714_b200 import dist as sdist
+    from paper_2006_13714_b200.bm import ScError
+    rng = np.random.Generator(np.random.PCG64(29))
+    N, H, W, Wn, K, T = 7, 60, 97, 15, 12, 2
+    for kind in ("random", "saturated"):
+        if kind == "random":
+            x = synth.random_image(rng, N, 1, H, W, "u8")
+        else:
+            x = (rng.integers(0, 2, size=(N, 1, H, W)) * 255).astype(np.uint8)
+        oi, od = oracle.bm_temporal(x, 8, 4, Wn, K, T)
+        p = _plan((H, W, 1, 8, 4, Wn, K), "u8")
+        p.set_temporal(T)
+        t = torch.from_numpy(x).cuda()
+        for world in (2, 3):
+            for r in range(world):
+                a, b = sdist.frame_shard(N, r, world)
+                lo_, hi_ = max(0, a - T), min(N, b + T)  # what the halo exchange assembles
+                gi, gd = p.run_temporal(t[lo_:hi_].clone(), a - lo_, b - lo_, lo_)  # a fresh (aligned) buffer
+                torch.cuda.synchronize()
+                np.testing.assert_array_equal(gi.cpu().numpy(), oi[a:b], err_msg=f"{kind} world {world} rank {r}")
+                np.testing.assert_array_equal(gd.cpu().numpy(), od[a:b])
+    with pytest.raises(ScError):
+        _plan((H, W, 1, 8, 4, Wn, K), "u8").run_temporal(t, 0, 2)  # T = 0
+
+
 def test_temporal_c5_frames_and_saturation():
     """The c5 video (random-walk crops): every reference's K best over frames f-1..f+1, bit-exact
     on sampled rows; a saturated video exercises the temporal fix-up."""
