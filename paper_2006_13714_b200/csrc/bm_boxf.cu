@@ -436,7 +436,10 @@ int boxf_rel_bits(int Wn) {
   return rb;
 }
 
-int boxf_kr(const Geometry& g) { return g.KP <= 32 ? 32 : g.KP <= 48 ? 48 : g.KP <= 80 ? 80 : 0; }
+// register list length: the smallest instantiated size >= KP (an insertion costs 2 KR - 1 IMNMX)
+int boxf_kr(const Geometry& g) {
+  return g.KP <= 24 ? 24 : g.KP <= 32 ? 32 : g.KP <= 40 ? 40 : g.KP <= 48 ? 48 : g.KP <= 80 ? 80 : 0;
+}
 
 template <int S, int BK, int KR, bool NCC = false, typename TIN = float>
 cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st) {
@@ -484,9 +487,13 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
   if (launches) *launches += 1;
   if (g.metric == SC_METRIC_NCC) {  // KP <= 32: register lists, exact re-rank
 #define SCBM_NCC_CASE(S_, B_)                                                                          \
-  if (g.s == S_ && g.b == B_)                                                                          \
+  if (g.s == S_ && g.b == B_) {                                                                        \
+    if (kr == 24)                                                                                      \
+      return g.dtype == SC_DTYPE_U8 ? launch_boxf_t<S_, B_, 24, true, uint8_t>(a, F, smem, st)         \
+                                    : launch_boxf_t<S_, B_, 24, true, float>(a, F, smem, st);          \
     return g.dtype == SC_DTYPE_U8 ? launch_boxf_t<S_, B_, 32, true, uint8_t>(a, F, smem, st)           \
-                                  : launch_boxf_t<S_, B_, 32, true, float>(a, F, smem, st);
+                                  : launch_boxf_t<S_, B_, 32, true, float>(a, F, smem, st);            \
+  }
     SCBM_NCC_CASE(3, 8)
     SCBM_NCC_CASE(1, 7)
     SCBM_NCC_CASE(4, 8)
@@ -496,7 +503,9 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
   }
 #define SCBM_BOXF_CASE(S_, B_)                                                    \
   if (g.s == S_ && g.b == B_) {                                                   \
+    if (kr == 24) return launch_boxf_t<S_, B_, 24>(a, F, smem, st);               \
     if (kr == 32) return launch_boxf_t<S_, B_, 32>(a, F, smem, st);               \
+    if (kr == 40) return launch_boxf_t<S_, B_, 40>(a, F, smem, st);               \
     if (kr == 48) return launch_boxf_t<S_, B_, 48>(a, F, smem, st);               \
     return launch_boxf_t<S_, B_, 80>(a, F, smem, st);                             \
   }

@@ -457,7 +457,8 @@ def test_box_default_and_rejects_unsupported():
 def _boxf_fits(s, b, Wn, K, C=1):
     """Mirror of boxf_supported's shared-memory / key-width rule (bm_boxf.cu)."""
     ns = -(-b // s)
-    kr = 32 if K + 8 <= 32 else 48 if K + 8 <= 48 else 80 if K + 8 <= 80 else 0
+    kp = K + 8
+    kr = next((r for r in (24, 32, 40, 48, 80) if kp <= r), 0)
     rb = max(1, (Wn * Wn).bit_length())
     if kr == 0 or rb > 12:
         return False
