@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
   }
   // (helper lanes RX..31 never insert; they alias lane RX-1's heap for the root reads)
-  uint32_t* heap = reinterpret_cast<uint32_t*>(smf + nch * a.PL) + warp * a.scr + 32 * VY + min(lane, RX - 1) * a.hp;
+  uint32_t* heap = reinterpret_cast<uint32_t*>(smf + nch * a.PL) + warp * a.scr + 64 * VY + min(lane, RX - 1) * a.hp;
   if constexpr (HEAP) {
     if (lane < RX)
       for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
@@ -155,6 +155,45 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
 
   const int b0 = (0 - a.lo) / VY;
   const int span = max(-a.lo, a.hi);
+  unsigned pend = 0u;  // survivor bits of the staged group(s)
+  int half = 0, rel1p = 0;
+  auto flush = [&](int rel1c) {
+    unsigned bits = pend;
+    pend = 0u;
+    if (!__any_sync(0xffffffffu, bits != 0u)) return;
+    const uint32_t* sc = scratch + lane;
+    while (__any_sync(0xffffffffu, bits != 0u)) {
+      const int i = 31 - __clz(bits | 1u);
+      const uint32_t q = sc[32 * i] >> (rb - 1);
+      const int rel1 = i < VY ? rel1p + i * a.Wn : rel1c + (i - VY) * a.Wn;
+      const uint32_t key = bits ? (q << rb) | uint32_t(rel1) : 0xffffffffu;
+      bits &= ~(1u << i);
+      if constexpr (HEAP) {
+        if (key < heap[1]) {  // replace the root, sift down (children of i: 2i, 2i+1)
+          int h = 1;
+          for (int c = 2; c <= a.KP; c = 2 * h) {
+            const uint32_t v0 = heap[c];
+            const uint32_t v1 = c + 1 <= a.KP ? heap[c + 1] : 0u;
+            const int cb = v1 > v0 ? c + 1 : c;
+            const uint32_t big = max(v0, v1);
+            if (big <= key) break;
+            heap[h] = big;
+            h = cb;
+          }
+          heap[h] = key;
+        }
+      } else {
+        rt.insert(key);
+      }
+    }
+    const uint32_t kth = HEAP ? heap[1] : rt.r[KR - 1];
+    if (kth != 0xffffffffu) {
+      // largest distance whose key can still tie the KP-th key, plus a rounding margin
+      const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
+      thr = fmaf(dmax, 1.0f + (NCC ? 1e-5f : 1e-6f), -nadd) + 1e-30f;
+    }
+    __syncwarp();
+  };
   for (int kb = 0; kb < 2 * a.nblk; ++kb) {
     const int bb = b0 + centre_out_f(kb);
     if (bb < 0 || bb >= a.nblk) continue;
@@ -227,43 +266,28 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
         // slack thr - d' >= 0 (or +inf): the candidate may enter the top-KP
         fails = __funnelshift_l(__float_as_uint(thr - dpv[i]), fails, 1);  // (fails << 1) | sign
       }
-      unsigned bits = ~fails & ((lane_ok && colok) ? rows : 0u);
+      const unsigned bits = ~fails & ((lane_ok && colok) ? rows : 0u);
+      // survivors of two consecutive offset groups are inserted together (fewer, fuller rounds:
+      // a round lasts as long as the busiest lane); group h's distances sit in scratch rows
+      // h*VY .. h*VY+VY-1 and its bits at the same positions of pend
       if (__any_sync(0xffffffffu, bits != 0u)) {
-        uint32_t* sc = scratch + lane;
+        uint32_t* sc = scratch + half * (32 * VY) + lane;
 #pragma unroll
         for (int i = 0; i < VY; ++i) sc[32 * i] = __float_as_uint(fmaxf(dpv[i] + nadd, 0.f));
-        const int rel1 = (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
-        while (__any_sync(0xffffffffu, bits != 0u)) {
-          const int i = 31 - __clz(bits | 1u);
-          const uint32_t q = sc[32 * i] >> (rb - 1);
-          const uint32_t key = bits ? (q << rb) | uint32_t(rel1 + i * a.Wn) : 0xffffffffu;
-          bits &= ~(1u << i);
-          if constexpr (HEAP) {
-            if (key < heap[1]) {  // replace the root, sift down (children of i: 2i, 2i+1)
-              int h = 1;
-              for (int c = 2; c <= a.KP; c = 2 * h) {
-                const uint32_t v0 = heap[c];
-                const uint32_t v1 = c + 1 <= a.KP ? heap[c + 1] : 0u;
-                const int cb = v1 > v0 ? c + 1 : c;
-                const uint32_t big = max(v0, v1);
-                if (big <= key) break;
-                heap[h] = big;
-                h = cb;
-              }
-              heap[h] = key;
-            }
-          } else {
-            rt.insert(key);
-          }
-        }
-        const uint32_t kth = HEAP ? heap[1] : rt.r[KR - 1];
-        if (kth != 0xffffffffu) {
-          // largest distance whose key can still tie the KP-th key, plus a rounding margin
-          const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
-          thr = fmaf(dmax, 1.0f + (NCC ? 1e-5f : 1e-6f), -nadd) + 1e-30f;
-        }
-        __syncwarp();
+        pend |= bits << (half * VY);
       }
+      const int rel1 = (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
+      if (half == 0) {
+        rel1p = rel1;
+        half = 1;
+      } else {
+        flush(rel1);
+        half = 0;
+      }
+    }
+    if (half == 1) {  // a lone last group (its bits are in the first half)
+      flush(0);
+      half = 0;
     }
   }
 
@@ -425,7 +449,7 @@ size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) {
   a->RWp = 32 * g.s + g.Wn - 1 + 1;
   a->PL = a->RH * a->RWp;
   a->hp = (g.KP + 1) | 1;  // heap pitch: 1-indexed heap, odd pitch
-  a->scr = KR > 48 ? 32 * kFVY + rx * a->hp : std::max(32 * kFVY, rx * (KR + 1));
+  a->scr = KR > 48 ? 64 * kFVY + rx * a->hp : std::max(64 * kFVY, rx * (KR + 1));  // 2 staged groups
   return size_t(g.C * a->PL + kFWarps * a->scr) * 4;
 }
 
