@@ -375,7 +375,11 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
   const size_t out_elems = size_t(g.ny) * g.nx * g.K;
   cudaError_t e = cudaSuccess;
   if (!h.ready) {
-    h.F = p->F;
+    // frames per pipeline stage: small enough that filling (first H2D + match) and draining (last
+    // D2H) the pipeline stay short against the PCIe-bound copies (~48 MB of results per stage),
+    // at most the plan's workspace chunk
+    const size_t out_frame = out_elems * 8;
+    h.F = int(std::max<size_t>(1, std::min<size_t>(size_t(p->F), (size_t(48) << 20) / std::max<size_t>(out_frame, 1))));
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
       e = cudaMalloc(&h.d_img[i], img_bytes * h.F);
       if (e == cudaSuccess) e = cudaMalloc(&h.d_idx[i], out_elems * 4 * h.F);
@@ -406,16 +410,26 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
     if (e != cudaSuccess) return cuda_status(e);
     cudaEventRecord(h.ev_in[slot], h.copy_in);
     cudaStreamWaitEvent(st, h.ev_in[slot], 0);
-    s = enqueue(p, h.d_img[slot], F, 0, g.ny, h.d_idx[slot], h.d_dist[slot], nullptr, st);
-    if (s != SC_OK) return s;
-    cudaEventRecord(h.ev_done[slot], st);
-    cudaStreamWaitEvent(h.copy_out, h.ev_done[slot], 0);
-    e = cudaMemcpyAsync(h_idx + f0 * out_elems, h.d_idx[slot], out_elems * 4 * F,
-                        cudaMemcpyDeviceToHost, h.copy_out);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(static_cast<char*>(h_dist) + f0 * out_elems * 4, h.d_dist[slot],
-                          out_elems * 4 * F, cudaMemcpyDeviceToHost, h.copy_out);
-    if (e != cudaSuccess) return cuda_status(e);
+    // one-frame stages with a large table (c3: 143 MB) are split into reference-row bands so the
+    // D2H of band b overlaps the matching of band b+1
+    const size_t row_elems = size_t(g.nx) * g.K;
+    const size_t stage_bytes = size_t(48) << 20;
+    const int nb = F == 1 ? int(std::max<size_t>(1, std::min<size_t>(size_t(g.ny), (out_elems * 8 + stage_bytes - 1) / stage_bytes))) : 1;
+    for (int bi = 0; bi < nb; ++bi) {
+      const int y0 = int(int64_t(g.ny) * bi / nb), y1 = int(int64_t(g.ny) * (bi + 1) / nb);
+      const size_t off = size_t(y0) * row_elems, cnt = (nb == 1 ? out_elems * F : size_t(y1 - y0) * row_elems);
+      s = enqueue(p, h.d_img[slot], F, nb == 1 ? 0 : y0, nb == 1 ? g.ny : y1, h.d_idx[slot] + off,
+                  static_cast<char*>(h.d_dist[slot]) + off * 4, nullptr, st);
+      if (s != SC_OK) return s;
+      cudaEventRecord(h.ev_done[slot], st);
+      cudaStreamWaitEvent(h.copy_out, h.ev_done[slot], 0);
+      e = cudaMemcpyAsync(h_idx + f0 * out_elems + off, h.d_idx[slot] + off, cnt * 4, cudaMemcpyDeviceToHost,
+                          h.copy_out);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(static_cast<char*>(h_dist) + (f0 * out_elems + off) * 4,
+                            static_cast<char*>(h.d_dist[slot]) + off * 4, cnt * 4, cudaMemcpyDeviceToHost, h.copy_out);
+      if (e != cudaSuccess) return cuda_status(e);
+    }
     cudaEventRecord(h.ev_out[slot], h.copy_out);
   }
   e = cudaStreamSynchronize(h.copy_out);

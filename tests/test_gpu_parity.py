@@ -235,11 +235,14 @@ def test_rows_band_matches_full():
     assert torch.equal(bi[0], fi[0, sl]) and torch.equal(bd[0], fd[0, sl])
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
 def test_host_path_matches_device(name):
+    """The pipelined host path (H2D / match / D2H stages: several frames per stage, one frame,
+    or reference-row bands of one frame when its table is large -- c3) equals the device run."""
     cfg = synth.CONFIGS[name]
-    xn = synth.make_input(cfg)
-    xn = np.concatenate([xn] * 3)  # several chunks
+    xn = synth.make_input(cfg, n_frames=5) if name == "c5" else synth.make_input(cfg)
+    if name in ("c1", "c2"):
+        xn = np.concatenate([xn] * 3)  # several chunks
     p = _plan(cfg)
     di, dd = p.run(torch.from_numpy(xn).cuda())
     hi, hd = p.run_host(torch.from_numpy(xn).pin_memory())
