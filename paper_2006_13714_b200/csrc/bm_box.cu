@@ -31,6 +31,7 @@
 // coalesced (a warp's 31 references are contiguous in the output).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "ncc.cuh"
 #include "regtopk.cuh"
@@ -221,7 +222,10 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     unsigned pend[NY];
 #pragma unroll
     for (int q = 0; q < NY; ++q) pend[q] = 0u;
-    int half = 0, rel0p = 0;
+    int rel0p = 0;
+    unsigned rmask[NY];  // window rows of this dy block x reference validity
+#pragma unroll
+    for (int q = 0; q < NY; ++q) rmask[q] = ref_ok[q] ? rows[q] : 0u;
     auto flush = [&](int rel0c) {
 #pragma unroll
       for (int q = 0; q < NY; ++q) {
@@ -271,9 +275,9 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         pend[q] = 0u;
       }
     };
-    for (int kx = 0; kx <= 2 * span; ++kx) {
-      const int dx = centre_out(kx);
-      if (dx < lo || dx > hi) continue;
+    // one offset group (fixed dx, offsets dy0 .. dy0+VY-1) into staging half H (compile time)
+    auto group = [&](int dx, auto hc) -> int {
+      constexpr int H = decltype(hc)::value;
       const int off = dx - lo;
       const uint32_t* col = cbase + (off & 3) * a.PL + (off >> 2);
       uint32_t Cw[NT];
@@ -342,31 +346,38 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             fails = __funnelshift_l(uint32_t(t[i]), fails, 1);  // (fails << 1) | sign(t): one SHF
           }
         }
-        const unsigned bits = ~fails & ((ref_ok[q] && colok) ? rows[q] : 0u);
+        const unsigned bits = ~fails & (colok ? rmask[q] : 0u);
         if constexpr (NCC) {
           pend[q] |= bits;
         } else if (__any_sync(0xffffffffu, bits != 0u)) {
-          uint32_t* sc = scratch + q * (64 * VY) + half * (32 * VY) + lane;
+          uint32_t* sc = scratch + q * (64 * VY) + H * (32 * VY) + lane;
           // the slack t is staged; the flush recovers d = d' + ||X_i||^2 = (thr + n_r) - t (exact,
           // thr does not change between the two staged groups of a flush)
 #pragma unroll
           for (int i = 0; i < VY; ++i) sc[32 * i] = uint32_t(t[i]);
-          pend[q] |= bits << (half * VY);
+          pend[q] |= bits << (H * VY);
         }
       }
-      const int rel0 = relt + (dy0 - lo) * Wn + off;
-      if constexpr (NCC) {  // one group per flush: the scratch holds its C and n_c
-        rel0p = rel0;
+      return relt + (dy0 - lo) * Wn + off;  // window-relative index of offset (dy0, dx)
+    };
+    // dx centre-out (0, 1, -1, 2, -2, ...), consecutive pairs (-j, j+1) staged in the two halves
+    // and flushed together; a lone group (window edge) flushes alone. NCC: one group per flush
+    // (the scratch holds its C and n_c).
+    if constexpr (NCC) {
+      for (int kx = 0; kx <= 2 * span; ++kx) {
+        const int dx = centre_out(kx);
+        if (dx < lo || dx > hi) continue;
+        rel0p = group(dx, std::integral_constant<int, 0>{});
         flush(0);
-      } else if (half == 0) {
-        rel0p = rel0;
-        half = 1;
-      } else {
-        flush(rel0);
-        half = 0;
+      }
+    } else {
+      for (int j = 0; j <= span; ++j) {
+        const bool va = -j >= lo, vb = j + 1 <= hi;
+        if (!va && !vb) continue;  // warp-uniform
+        rel0p = group(va ? -j : j + 1, std::integral_constant<int, 0>{});
+        flush(va && vb ? group(j + 1, std::integral_constant<int, 1>{}) : 0);
       }
     }
-    if (half == 1) flush(0);  // a lone last group (its bits are in the first half)
   }
   }  // time offsets
 
