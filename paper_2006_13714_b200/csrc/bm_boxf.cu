@@ -25,6 +25,7 @@
 // K (BASELINE.json north_star tolerance): a true top-K candidate can only
 // be lost if more than KP - K = 8 others lie within one quantum (~1e-4 relative) of it.
 #include <algorithm>
+#include <type_traits>
 
 #include "ncc.cuh"
 #include "regtopk.cuh"
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const int b0 = (0 - a.lo) / VY;
   const int span = max(-a.lo, a.hi);
   unsigned pend = 0u;  // survivor bits of the staged group(s)
-  int half = 0, rel1p = 0;
+  int rel1p = 0;
   auto flush = [&](int rel1c) {
     unsigned bits = pend;
     pend = 0u;
@@ -203,9 +204,10 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     if (ihi < ilo) continue;  // warp-uniform
     const unsigned rows = ((2u << ihi) - 1u) & ~((1u << ilo) - 1u);
     const float* cbase = smf + (rr0 + dy0) * a.RWp + rc0;
-    for (int kx = 0; kx <= 2 * span; ++kx) {
-      const int dx = centre_out_f(kx);
-      if (dx < a.lo || dx > a.hi) continue;
+    const unsigned rmask = lane_ok ? rows : 0u;
+    // one offset group (fixed dx, offsets dy0 .. dy0+VY-1) into staging half H (compile time)
+    auto group = [&](int dx, auto hc) -> int {
+      constexpr int H = decltype(hc)::value;
       const float* col = cbase + dx;
       // cross terms of the full / partial strip, and running squared-row sums for the norms
       float Tp[VY], Tr[VY];
@@ -266,28 +268,25 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
         // slack thr - d' >= 0 (or +inf): the candidate may enter the top-KP
         fails = __funnelshift_l(__float_as_uint(thr - dpv[i]), fails, 1);  // (fails << 1) | sign
       }
-      const unsigned bits = ~fails & ((lane_ok && colok) ? rows : 0u);
+      const unsigned bits = ~fails & (colok ? rmask : 0u);
       // survivors of two consecutive offset groups are inserted together (fewer, fuller rounds:
       // a round lasts as long as the busiest lane); group h's distances sit in scratch rows
       // h*VY .. h*VY+VY-1 and its bits at the same positions of pend
       if (__any_sync(0xffffffffu, bits != 0u)) {
-        uint32_t* sc = scratch + half * (32 * VY) + lane;
+        uint32_t* sc = scratch + H * (32 * VY) + lane;
 #pragma unroll
         for (int i = 0; i < VY; ++i) sc[32 * i] = __float_as_uint(fmaxf(dpv[i] + nadd, 0.f));
-        pend |= bits << (half * VY);
+        pend |= bits << (H * VY);
       }
-      const int rel1 = (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
-      if (half == 0) {
-        rel1p = rel1;
-        half = 1;
-      } else {
-        flush(rel1);
-        half = 0;
-      }
-    }
-    if (half == 1) {  // a lone last group (its bits are in the first half)
-      flush(0);
-      half = 0;
+      return (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
+    };
+    // dx centre-out (0, 1, -1, 2, -2, ...): pairs (-j, j+1) staged in the two halves and
+    // flushed together (a round lasts as long as the busiest lane); a lone group flushes alone
+    for (int j = 0; j <= span; ++j) {
+      const bool va = -j >= a.lo, vb = j + 1 <= a.hi;
+      if (!va && !vb) continue;  // warp-uniform
+      rel1p = group(va ? -j : j + 1, std::integral_constant<int, 0>{});
+      flush(va && vb ? group(j + 1, std::integral_constant<int, 1>{}) : 0);
     }
   }
 
