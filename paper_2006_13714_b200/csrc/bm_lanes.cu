@@ -406,6 +406,9 @@ __global__ void __launch_bounds__(256, KR > 0 ? 3 : 1) bm_lanes_kernel(LanesArgs
     for (int r = 0; r < n_ref_lanes; ++r) {
       const int rxr = (ix_first + r) * s;
       uint64_t* L = lists + size_t(warp * 32 + r) * a.list_pitch;
+      const float nr_r = __shfl_sync(0xffffffffu, float(nr), r);
+      const uint64_t kp_key = L[0];  // heap root: the KP-th identity key (kKeyInf: list not full)
+      __syncwarp();
       for (int k = lane; k < a.KP; k += 32) {
         const uint64_t key = L[k];
         if (key == kKeyInf) continue;
@@ -433,6 +436,22 @@ __global__ void __launch_bounds__(256, KR > 0 ? 3 : 1) bm_lanes_kernel(LanesArgs
         t.merge(k < a.KP ? L[k] : kKeyInf, lane);
       }
       const size_t o = (size_t(f) * band_refs + size_t(iy - a.iy_begin) * a.nx + ix_first + r) * a.K;
+      {  // identity-rounding check (bm_simt.cu a5): a hidden top-K candidate -> exact fix-up
+        uint64_t kk = kKeyInf;
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+          if (j == (a.K - 1) / 32) kk = t.v[j];
+        kk = __shfl_sync(0xffffffffu, kk, (a.K - 1) % 32);
+        if (lane == 0 && kp_key != kKeyInf && kk != kKeyInf) {
+          const float dK = __uint_as_float(uint32_t(kk >> 32));
+          const float dKP = unord_f32(uint32_t(kp_key >> 32)) + nr_r;
+          const float kappa = 2.f * float(b * b * a.C) * 5.96e-8f;
+          if (dKP - kappa * (6.f * fmaxf(nr_r, 0.f) + 4.f * dK) <= dK * (1.f + 1e-5f)) {
+            const int pos = atomicAdd(a.fix_count, 1);
+            a.fix_list[pos] = int(o / a.K);
+          }
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
         const int k = j * 32 + lane;
@@ -592,13 +611,15 @@ cudaError_t launch_bm_lanes(const sc_bm_plan_s& p, const void* imgs, int F, int 
   if (launches) *launches += 1;
   const int bk = bk_for(g.b, g.dtype == SC_DTYPE_U8);
   cudaError_t e;
-  if (kr > 0) {
+  // fix-up: u8 register keys (saturation), float top-K (identity rounding, see bm_simt.cu a5)
+  const bool fix = kr > 0 || (g.dtype == SC_DTYPE_F32 && dense == nullptr);
+  if (fix) {
     e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
   }
   if (g.dtype == SC_DTYPE_U8) e = dispatch<uint8_t>(a, F, smem, st, bk, vy, kr);
   else e = dispatch<float>(a, F, smem, st, bk, vy, kr);
-  if (e != cudaSuccess || kr == 0) return e;
+  if (e != cudaSuccess || !fix) return e;
   if (launches) *launches += 1;
   return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
 }

@@ -35,6 +35,8 @@ struct SimtArgs {
   void* dense;        // dense tables: [refs][Wn*Wn] (one image) or nullptr
   float nlm_inv_h2;   // > 0: normalise each dense row into NLM weights in the epilogue (nlm.cuh)
   float* avg_out;     // NL-means estimate [band refs][C][b][b] (AVG instantiation), 1 / h^2 in nlm_inv_h2
+  int* fix_count;     // float L2: references whose identity rounding could hide a top-K candidate
+  int* fix_list;      // (exact fix-up, fixup.cu); nullptr: no check
   int H, W, C, b, s, Wn, K, KP, lo, hi, nx, My, Mx;
   long long nfs;      // norm-map frame stride
   int iy_begin, iy_end;
@@ -308,6 +310,7 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
     // a5: re-score the best KP keys by direct differences from the uncentred input.
     const float* img = static_cast<const float*>(a.imgs) + size_t(f) * a.C * a.H * a.W;
     const size_t pl = size_t(a.H) * a.W;
+    const uint64_t kp_key = lst[a.KP - 1];  // the KP-th identity key (filter boundary)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       const int k = lane + 32 * j;
@@ -333,6 +336,21 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
     }
     __syncwarp();
     smem_list_sort<NJ>(lst, lane);
+    // A candidate the fp32 identity pushed beyond the KP-th key could still be a true top-K one
+    // when the identity's rounding (relative to the norms, ~b^2 C ulps: it matters only for
+    // near-degenerate data, e.g. b = 1 on smooth images) reaches the exact K-th distance: then
+    // the reference goes to the exact fix-up (fixup.cu). Threat candidates have d <= d_K, so
+    // n_c <= 2 n_r + 2 d_K and the identity's terms are <= 6 n_r + 4 d_K.
+    if (lane == 0 && kp_key != kKeyInf && a.fix_count != nullptr) {
+      const uint64_t kk = lst[a.K - 1];
+      const float dK = __uint_as_float(uint32_t(kk >> 32));
+      const float dKP = unord_f32(uint32_t(kp_key >> 32)) + nr;
+      const float kappa = 2.f * float(b * b * a.C) * 5.96e-8f;
+      if (kk != kKeyInf && dKP - kappa * (6.f * fmaxf(nr, 0.f) + 4.f * dK) <= dK * (1.f + 1e-5f)) {
+        const int pos = atomicAdd(a.fix_count, 1);
+        a.fix_list[pos] = int(size_t(f) * ((a.iy_end - a.iy_begin) * a.nx) + ref_band);
+      }
+    }
     float* dist = static_cast<float*>(a.dist_out);
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
@@ -541,7 +559,17 @@ cudaError_t launch_bm_simt(const sc_bm_plan_s& p, const void* imgs, int F, int i
   const size_t smem = smem_bytes(g, a.TRY, a.TRX, &a);
   if (launches) *launches += 1;
   if (g.dtype == SC_DTYPE_U8) return dispatch_b<uint8_t>(a, F, smem, st);
-  return dispatch_b<float>(a, F, smem, st);
+  const bool fix = dense == nullptr && a.avg_out == nullptr;  // float top-K: identity-rounding check
+  if (fix) {
+    a.fix_count = p.ws.fix_count;
+    a.fix_list = p.ws.fix_list;
+    cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = dispatch_b<float>(a, F, smem, st);
+  if (e != cudaSuccess || !fix) return e;
+  if (launches) *launches += 1;
+  return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
 }
 
 }  // namespace scbm
