@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         int t[VY];
         unsigned fails = 0u;
         if constexpr (NCC) {
-          // raw bytes: 0 <= C, n_c < 2^22, so both convert exactly by the 2^23 magic-number trick and
+          // raw bytes: 0 <= C, n_c < 2^22, so both convert to fp32 exactly and
           // the filter sqrt(n_r) - C / sqrt(n_c) <= thrf needs no square root: C^2 - gsq n_c >= 0
           // (gsq carries a 1e-6 relative margin, so rounding never drops a candidate). C and n_c
           // are staged for the flush, which scores the survivors.
@@ -332,8 +332,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           for (int i = VY - 1; i >= 0; --i) {
             const int cc = U[q][i] + __shfl_down_sync(0xffffffffu, U[q][i], 1);      // C
             const int nn = D[4 * q + i] + __shfl_down_sync(0xffffffffu, D[4 * q + i], 1);  // n_c
-            const float fc = __int_as_float(0x4B000000 | cc) - 8388608.f;
-            const float fn = __int_as_float(0x4B000000 | nn) - 8388608.f;
+            const float fc = __int2float_rn(cc), fn = __int2float_rn(nn);  // exact: < 2^24 (one I2FP each)
             sc[32 * i] = uint32_t(cc);
             sc[32 * (i + VY)] = uint32_t(nn);
             fails = __funnelshift_l(__float_as_uint(fmaf(-gsq[q], fn, fc * fc)), fails, 1);
