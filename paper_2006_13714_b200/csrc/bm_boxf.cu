@@ -145,14 +145,16 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
   }
   // (helper lanes RX..31 never insert; they alias lane RX-1's heap for the root reads)
-  uint32_t* heap = reinterpret_cast<uint32_t*>(smf + nch * a.PL) + warp * a.scr + 64 * VY + min(lane, RX - 1) * a.hp;
+  uint32_t* const scr0 = reinterpret_cast<uint32_t*>(smf + ((nch * a.PL + 1) & ~1));  // 8-byte aligned
+  uint32_t* heap = scr0 + warp * a.scr + 64 * VY + min(lane, RX - 1) * a.hp;
   if constexpr (HEAP) {
     if (lane < RX)
       for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
+    if (lane < RX) heap[a.KP + 1] = 0u;  // padding child: never the larger one
   }
   const int rb = a.rb;
   float thr = __int_as_float(0x7f800000);  // +inf: largest d' that may still enter the top-KP
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(smf + nch * a.PL) + warp * a.scr;
+  uint32_t* scratch = scr0 + warp * a.scr;
 
   const int b0 = (0 - a.lo) / VY;
   const int span = max(-a.lo, a.hi);
@@ -173,8 +175,9 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
         if (key < heap[1]) {  // replace the root, sift down (children of i: 2i, 2i+1)
           int h = 1;
           for (int c = 2; c <= a.KP; c = 2 * h) {
-            const uint32_t v0 = heap[c];
-            const uint32_t v1 = c + 1 <= a.KP ? heap[c + 1] : 0u;
+            // both children in one 8-byte load: rows are 8-byte aligned, c is even
+            const uint2 vv = *reinterpret_cast<const uint2*>(heap + c);
+            const uint32_t v0 = vv.x, v1 = vv.y;
             const int cb = v1 > v0 ? c + 1 : c;
             const uint32_t big = max(v0, v1);
             if (big <= key) break;
@@ -447,9 +450,11 @@ size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) {
   a->RH = (kFWarps - 1) * g.s + a->nblk * kFVY + g.b;
   a->RWp = 32 * g.s + g.Wn - 1 + 1;
   a->PL = a->RH * a->RWp;
-  a->hp = (g.KP + 1) | 1;  // heap pitch: 1-indexed heap, odd pitch
+  // heap pitch: 1-indexed heap + a padding child, = 2 (mod 4) words: 8-byte aligned rows whose
+  // 64-bit child loads hit distinct bank pairs across a half-warp
+  a->hp = ((g.KP + 2 + 1) & ~3) + 2;
   a->scr = KR > 48 ? 64 * kFVY + rx * a->hp : std::max(64 * kFVY, rx * (KR + 1));  // 2 staged groups
-  return size_t(g.C * a->PL + kFWarps * a->scr) * 4;
+  return size_t(((g.C * a->PL + 1) & ~1) + kFWarps * a->scr) * 4;  // scratch 8-byte aligned
 }
 
 // key bits of the window-relative index + 1 (values 1 .. Wn^2; 0 is the sentinel)

@@ -467,9 +467,9 @@ def _boxf_fits(s, b, Wn, K, C=1):
         return False
     nblk = -(-Wn // 8)
     pl = (7 * s + nblk * 8 + b) * (32 * s + Wn)
-    hp = (K + 9) | 1
+    hp = ((K + 8 + 3) & ~3) + 2
     scr = 512 + (33 - ns) * hp if kr == 80 else max(512, (33 - ns) * (kr + 1))
-    return (C * pl + 8 * scr) * 4 <= (113 if C == 1 else 227) * 1024
+    return (((C * pl + 1) & ~1) + 8 * scr) * 4 <= (113 if C == 1 else 227) * 1024
 
 
 def _boxf_cases(n, seed):
