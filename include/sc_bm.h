@@ -47,7 +47,9 @@
  *         integral image is uint32 (wrap-around, box sums exact), the cross term int32; all
  *         distances are exact integers -- bit-identical to the definition.
  *   f32 : values are centred by -0.5; the integral image is fp64; the cross term fp32; the
- *         top-(K+8) survivors are re-scored by direct differences in fp32 and re-sorted.
+ *         top-(K+m) survivors (m = 4, or 8 for K > 48) are re-scored by direct differences in
+ *         fp32 and re-sorted; references where the margin could hide a top-K candidate are
+ *         recomputed exactly over their whole window.
  *         Distances are within relative 1e-5 of the exact value (BASELINE.json north_star).
  */
 #ifndef SC_BM_H
@@ -100,7 +102,7 @@ typedef struct {
 #define SC_KERNEL_BOX 3        /* box-sum matcher: 4x4 block sums of the shifted product image
                                   (u8, b = 8, stride 4, C = 1, K <= 32; default where supported) */
 #define SC_KERNEL_BOXF 4       /* float box-sum matcher (f32, C = 1, (stride, b) in {(3,8), (1,7),
-                                  (4,8), (2,8)}, K + 8 <= 80; default where supported) */
+                                  (4,8), (2,8)}, K + m <= 80; default where supported) */
 
 /*
  * Create a plan. H, W: image size (H, W >= b, H*W < 2^31); C: channels (1..8); b: patch

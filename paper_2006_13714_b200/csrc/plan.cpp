@@ -14,10 +14,12 @@ using namespace scbm;
 
 namespace {
 
-// keys re-ranked beyond K: float L2 keeps 8 (c3's K = 70 window has near-ties
-// whose exact fix-up costs more than the margin saves), NCC 4 (measured: no c5 / c2 reference
-// reaches the quantisation fix-up; the shorter list saves 5 % on c5)
-constexpr int kRescoreMargin = 8;
+// keys re-ranked beyond K (every kernel checks whether the margin could have
+// hidden a top-K candidate and sends such references to the exact fix-up): 4 (measured on c2, c4,
+// c5-NCC: no reference reaches the fix-up, the shorter lists save 3-5 %), 8 for large K (c3's
+// K = 70: margin 4 sends near-tie references to the fix-up, which costs more than it saves)
+constexpr int kRescoreMargin = 4;
+constexpr int kRescoreMarginLargeK = 8;
 constexpr int kNccMargin = 4;
 
 sc_status_t cuda_status(cudaError_t e) {
@@ -181,7 +183,8 @@ sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, in
   g.Mxp = (g.Mx + 2 * g.NPAD + 3) & ~3;
   g.NFS = (long long)(g.My + 2 * g.NPAD) * g.Mxp;
   g.metric = metric;
-  g.KP = metric == SC_METRIC_NCC ? K + kNccMargin : dtype == SC_DTYPE_F32 ? K + kRescoreMargin : K;
+  g.KP = metric == SC_METRIC_NCC ? K + kNccMargin
+         : dtype == SC_DTYPE_F32 ? K + (K > 48 ? kRescoreMarginLargeK : kRescoreMargin) : K;
   if (metric == SC_METRIC_NCC && !boxf_supported(g) && !box_supported(g)) {  // NCC: box kernels only
     delete p;
     return SC_ERR_UNSUPPORTED;

@@ -460,14 +460,14 @@ def test_box_default_and_rejects_unsupported():
 def _boxf_fits(s, b, Wn, K, C=1):
     """Mirror of boxf_supported's shared-memory / key-width rule (bm_boxf.cu)."""
     ns = -(-b // s)
-    kp = K + 8
+    kp = K + (8 if K > 48 else 4)  # plan.cpp's re-rank margin
     kr = next((r for r in (24, 32, 40, 48, 80) if kp <= r), 0)
     rb = max(1, (Wn * Wn).bit_length())
     if kr == 0 or rb > 12:
         return False
     nblk = -(-Wn // 8)
     pl = (7 * s + nblk * 8 + b) * (32 * s + Wn)
-    hp = ((K + 8 + 3) & ~3) + 2
+    hp = ((kp + 3) & ~3) + 2
     scr = 512 + (33 - ns) * hp if kr == 80 else max(512, (33 - ns) * (kr + 1))
     return (((C * pl + 1) & ~1) + 8 * scr) * 4 <= (113 if C == 1 else 227) * 1024
 
