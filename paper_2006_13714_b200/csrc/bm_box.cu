@@ -593,10 +593,13 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
     if (g.Wn == 33 && g.KP <= 20) e = launch_box_t<2, 11, 20, 40, true, 33>(a, F, box_layout(g, 2, vy, 20, &a), st);
     else if (g.Wn == 33 && g.KP <= 24) e = launch_box_t<2, 11, 24, 40, true, 33>(a, F, box_layout(g, 2, vy, 24, &a), st);
     else if (vy == 11 && a.WP == 40 && g.KP <= 24) e = launch_box_t<2, 11, 24, 40, true>(a, F, box_layout(g, 2, vy, 24, &a), st);
-    else if (vy == 11 && a.WP == 40) e = launch_box_t<2, 11, 32, 40, true>(a, F, smem, st);
-    else if (vy == 11) e = launch_box_t<2, 11, 32, 0, true>(a, F, smem, st);
-    else if (vy == 7) e = launch_box_t<2, 7, 32, 0, true>(a, F, smem, st);
-    else e = launch_box_t<2, 8, 32, 0, true>(a, F, smem, st);
+    else {  // 32-key lists: the layout (per-warp scratch for the KR + 1 pitch) must match KR
+      const size_t smem32 = box_layout(g, 2, vy, 32, &a);
+      if (vy == 11 && a.WP == 40) e = launch_box_t<2, 11, 32, 40, true>(a, F, smem32, st);
+      else if (vy == 11) e = launch_box_t<2, 11, 32, 0, true>(a, F, smem32, st);
+      else if (vy == 7) e = launch_box_t<2, 7, 32, 0, true>(a, F, smem32, st);
+      else e = launch_box_t<2, 8, 32, 0, true>(a, F, smem32, st);
+    }
     if (launches) *launches += 2;
     if (e != cudaSuccess) return e;
     return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);

@@ -740,6 +740,22 @@ def test_ncc_u8_both_kernels(kernel):
         check_ncc(x[n], 8, 4, 25, 20, gi[n], gd[n], oi[n], od[n], exact=True, where=f"ncc {kernel} img{n}")
 
 
+@pytest.mark.parametrize("Wn,K", [(14, 4), (15, 2), (21, 8), (12, 12), (33, 28)])
+def test_ncc_box_small_lists(Wn, K):
+    """The dp4a NCC kernel's list sizes for every window-block geometry (VY 7 / 8 / 11): the
+    shared-memory layout must match the instantiated list length (found by tools/stress.py)."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_BOX, Plan
+    from tests.parity import check_ncc
+    rng = np.random.Generator(np.random.PCG64(Wn * 100 + K))
+    x = synth.random_image(rng, 2, 1, 55, 120, "u8")
+    p = Plan(55, 120, 1, 8, 4, Wn, K, "u8", metric="ncc")
+    p.set_kernel(SC_KERNEL_BOX)
+    gi, gd = _run(p, x)
+    oi, od = oracle.ncc(x, 8, 4, Wn, K)
+    for n in range(2):
+        check_ncc(x[n], 8, 4, Wn, K, gi[n], gd[n], oi[n], od[n], exact=True, where=f"ncc box Wn{Wn} K{K} img{n}")
+
+
 # ------------------------------------------------------------------ NLM weights (Eq. 2 / Prop. 1)
 @pytest.mark.parametrize("dtype,C,H,W,b,s,Wn,h", [("u8", 1, 64, 64, 8, 4, 21, 300.0), ("u8", 1, 50, 77, 5, 2, 13, 120.0),
                                                    ("f32", 1, 48, 52, 7, 2, 15, 0.6), ("f32", 3, 30, 41, 4, 3, 9, 0.5),
