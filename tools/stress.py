@@ -36,11 +36,14 @@ def image(rng, kind, N, C, H, W, dtype):
     return np.round(x).astype(np.uint8) if dtype == "u8" else x.astype(np.float32)
 
 
+FOCUS = os.environ.get("STRESS_FOCUS", "")  # "", "ncc" or "box" (u8 b=8 s=4: the dp4a kernels)
+
+
 def one(rng):
-    metric = rng.choice(["l2", "l2", "l2", "ncc"])
-    dtype = rng.choice(["u8", "f32"])
+    metric = "ncc" if FOCUS == "ncc" else rng.choice(["l2", "l2", "l2", "ncc"])
+    dtype = "u8" if FOCUS == "box" else rng.choice(["u8", "f32"])
     kind = rng.choice(["random", "binary", "smooth", "quantised"])
-    if metric == "l2" and dtype == "u8" and rng.random() < 0.6:  # the box kernel's geometry
+    if FOCUS == "box" or (dtype == "u8" and rng.random() < 0.6):  # the dp4a box kernel's geometry
         b, s, C = 8, 4, 1
     elif rng.random() < 0.5:  # the float box kernel's shapes
         s, b = [(3, 8), (1, 7), (4, 8), (2, 8)][rng.integers(0, 4)]
@@ -51,7 +54,7 @@ def one(rng):
     Wn = int(rng.integers(1, 40))
     K = int(rng.integers(1, 25 if metric == "ncc" else 40))
     N = int(rng.integers(1, 4))
-    kernel = rng.choice(["default", "box", "boxf", "warp", "lanes"])
+    kernel = "box" if FOCUS == "box" and rng.random() < 0.7 else rng.choice(["default", "box", "boxf", "warp", "lanes"])
     T = int(rng.integers(1, 3)) if (metric == "l2" and dtype == "u8" and b == 8 and s == 4 and C == 1
                                     and rng.random() < 0.25) else 0
     x = image(rng, kind, N, C, H, W, dtype)
