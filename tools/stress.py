@@ -69,9 +69,31 @@ def one(rng):
     except ScError:
         return "skip", desc
     t = torch.from_numpy(x).cuda()
-    gi, gd = p.run(t)
-    torch.cuda.synchronize()
-    gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
+    if rng.random() < 0.2 and not T:  # the pipelined host path instead of the device call
+        hi, hd = p.run_host(torch.from_numpy(x).pin_memory())
+        gi, gd = hi.numpy(), hd.numpy()
+    else:
+        gi, gd = p.run(t)
+        torch.cuda.synchronize()
+        gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
+    if rng.random() < 0.3:  # the next rows on the same plan: groups of this run, NLM weights / estimate
+        Y = p.group(t, torch.from_numpy(gi).cuda()).cpu().numpy()
+        if T:  # batch-global idx: the frames stacked vertically (C = 1)
+            want = oracle.group(x.reshape(1, 1, N * H, W), gi.reshape(1, -1, K), b).reshape(Y.shape)
+        else:
+            want = oracle.group(x, gi, b)
+        assert np.array_equal(Y, want), f"group mismatch: {desc}"
+        if metric == "l2" and not T and b * b * C <= 256:
+            h = float(rng.choice([0.3, 3.0, 1e6])) * (255.0 if dtype == "u8" else 1.0) * b
+            scale = 255.0 if dtype == "u8" else 1.0
+            w = p.nlm_weights(t[0], h).cpu().numpy().astype(np.float64)
+            ww = oracle.nlm_weights(x[0], b, s, Wn, h)
+            m = ww > 1e-6
+            assert np.allclose(w[m], ww[m], rtol=1e-4, atol=1e-9), f"nlm weights mismatch: {desc} h={h}"
+            a = p.nlm_average(t[0], h).cpu().numpy().astype(np.float64)
+            aa = oracle.nlm_average(x[0], b, s, Wn, h)
+            assert np.allclose(a, aa, rtol=0, atol=1e-4 * scale), f"nlm average mismatch: {desc} h={h}"
+
     if T:
         oi, od = oracle.bm_temporal(x, b, s, Wn, K, T)
         check_u8(gi, gd, oi, od, desc)
