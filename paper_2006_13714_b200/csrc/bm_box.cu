@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     // one offset group (fixed dx, offsets dy0 .. dy0+VY-1) into staging half H (compile time)
     auto group = [&](int dx, auto hc) -> int {
       constexpr int H = decltype(hc)::value;
+      (void)H;  // (NCC stages one group per flush)
       const int off = dx - lo;
       const uint32_t* col = cbase + (off & 3) * a.PL + (off >> 2);
       uint32_t Cw[NT];
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       for (int q = 0; q < NY; ++q) {
         // a3: d' = n_c - 2 C = E_l + E_{l+1}, E = strip norm - 2 * strip cross term
         // slack t = thr - d' (>= 0: the candidate may enter the top-K); fail bits = sign bits
-        int t[VY];
+        [[maybe_unused]] int t[VY];
         unsigned fails = 0u;
         if constexpr (NCC) {
           // raw bytes: 0 <= C, n_c < 2^22, so both convert to fp32 exactly and
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       }
     }
     return;
-  }
+  } else {
   // ---- a6: exact references -> staged rows of K keys -> coalesced (idx, dist) stores;
   // references whose K-th key is saturated or unfilled -> the fix-up list
 #pragma unroll
@@ -505,6 +506,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     __syncwarp();
 #endif
   }
+  }  // !NCC
 }
 
 int box_vy(const Geometry& g) { return g.Wn % 11 == 0 ? 11 : g.Wn % 7 == 0 ? 7 : g.Wn <= 8 ? 8 : 11; }

@@ -37,7 +37,6 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kEpiWarps + 1) * 32;
 constexpr int kRBY = 8, kRBX = 16;   // reference block (M = 128)
 constexpr int kTR = 8, kTC = 16;     // candidate tile: 8 rows x 16 columns (N = 128)
-constexpr int kBig = 0x3fffffff;     // norm of positions that are not candidates
 constexpr uint32_t kIdesc = sm100::idesc_i8(128, 128, /*a_mn=*/false, /*b_mn=*/true);
 
 struct TcArgs {
@@ -61,14 +60,6 @@ __device__ unsigned long long g_tc_stats[8];  // debug counters (SCBM_TC_DEBUG &
 __device__ unsigned long long g_tc_clk[8];    // debug cycle accumulators (SCBM_TC_DEBUG & 8)
 #define TCLK(i, t0) do { if (a.dbg & 8) { const long long _t = clock64(); if (lane == 0) atomicAdd(&g_tc_clk[i], (unsigned long long)(_t - (t0))); (t0) = _t; } } while (0)
 
-__device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
-// k-th index of a centre-out enumeration of [0, n)
-__device__ __forceinline__ int co_index(int k, int n) {
-  const int c = (n - 1) >> 1;
-  int idx = c + centre_out(k);
-  // for even n the enumeration c, c+1, c-1, ... stays in range for k < n
-  return idx;
-}
 
 __global__ void __launch_bounds__(kThreads, 2) bm_tc_i8_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -87,7 +78,6 @@ __global__ void __launch_bounds__(kThreads, 2) bm_tc_i8_kernel(TcArgs a) {
   const int NTI = (cyB - cyA) / kTR + 1;         // candidate row blocks
   const int RH = NTI * kTR + 7;                  // image rows of E
   const uint32_t RP = uint32_t(NC) * 128u;       // E row pitch (bytes)
-  const int NWc = NC * kTC;                      // norm-tile columns
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const uint32_t sbase = smem_addr(smem);
