@@ -200,6 +200,15 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     if (!wact) continue;
   }
   const int relt = TEMP ? (tau + a.T) * Wn * Wn : 0;  // window-relative index offset of this frame
+  // two phases over the dy blocks: the near offsets (dx pairs j < kNearPairs: |dx| <= 5) of every
+  // block first, then the rest -- the thresholds tighten sooner than with each block's whole dx
+  // range in turn (a c5 simulation: 5 % fewer survivor rounds)
+#ifndef SCBM_NEAR_PAIRS
+#define SCBM_NEAR_PAIRS 5
+#endif
+  constexpr int kNearPairs = SCBM_NEAR_PAIRS;
+  for (int ph = 0; ph < 2; ++ph) {
+  const int j_begin = ph == 0 ? 0 : kNearPairs, j_end = ph == 0 ? min(kNearPairs, span + 1) : span + 1;
   for (int kb = 0; kb < 2 * nblk; ++kb) {
     const int bb = b0 + centre_out(kb);
     if (bb < 0 || bb >= nblk) continue;
@@ -364,14 +373,14 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     // and flushed together; a lone group (window edge) flushes alone. NCC: one group per flush
     // (the scratch holds its C and n_c).
     if constexpr (NCC) {
-      for (int kx = 0; kx <= 2 * span; ++kx) {
+      for (int kx = 2 * j_begin; kx < 2 * j_end && kx <= 2 * span; ++kx) {
         const int dx = centre_out(kx);
         if (dx < lo || dx > hi) continue;
         rel0p = group(dx, std::integral_constant<int, 0>{});
         flush(0);
       }
     } else {
-      for (int j = 0; j <= span; ++j) {
+      for (int j = j_begin; j < j_end; ++j) {
         const bool va = -j >= lo, vb = j + 1 <= hi;
         if (!va && !vb) continue;  // warp-uniform
         rel0p = group(va ? -j : j + 1, std::integral_constant<int, 0>{});
@@ -379,6 +388,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       }
     }
   }
+  }  // phases
   }  // time offsets
 
   const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
