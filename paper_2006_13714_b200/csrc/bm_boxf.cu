@@ -198,6 +198,12 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     }
     __syncwarp();
   };
+  // two phases over the dy blocks: the near offsets (dx pairs j < 5) of every block first (as in
+  // the uint8 box kernel: thresholds tighten sooner; measured on c2 / c4). Heap lists (c3, K = 70)
+  // measured slower with the split: one phase.
+  const int kNearPairs = HEAP ? span + 1 : 5;
+  for (int ph = 0; ph < 2; ++ph) {
+  const int j_begin = ph == 0 ? 0 : kNearPairs, j_end = ph == 0 ? min(kNearPairs, span + 1) : span + 1;
   for (int kb = 0; kb < 2 * a.nblk; ++kb) {
     const int bb = b0 + centre_out_f(kb);
     if (bb < 0 || bb >= a.nblk) continue;
@@ -285,13 +291,14 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     };
     // dx centre-out (0, 1, -1, 2, -2, ...): pairs (-j, j+1) staged in the two halves and
     // flushed together (a round lasts as long as the busiest lane); a lone group flushes alone
-    for (int j = 0; j <= span; ++j) {
+    for (int j = j_begin; j < j_end; ++j) {
       const bool va = -j >= a.lo, vb = j + 1 <= a.hi;
       if (!va && !vb) continue;  // warp-uniform
       rel1p = group(va ? -j : j + 1, std::integral_constant<int, 0>{});
       flush(va && vb ? group(j + 1, std::integral_constant<int, 1>{}) : 0);
     }
   }
+  }  // phases
 
   // ---- a5 + a6: stage each reference's KP keys (register lists; the heaps already are in shared
   // memory), then per reference (warp-cooperative) re-score them by direct differences from the
