@@ -962,3 +962,20 @@ def test_run_is_graph_capturable(cfg_name):
     wi, wd = p.run(y)
     torch.cuda.synchronize()
     assert torch.equal(idx, wi) and torch.equal(dist, wd)
+
+
+def test_batch_larger_than_one_launch():
+    """More frames than one box-kernel launch takes (FB = 64): the chunked run (64 + 3 frames, the
+    second chunk's fix-up list and output offsets) equals per-frame runs."""
+    rng = np.random.Generator(np.random.PCG64(41))
+    N, H, W = 67, 96, 160
+    x = synth.random_image(rng, N, 1, H, W, "u8")
+    x[N - 1] = (rng.integers(0, 2, size=(1, H, W)) * 255).astype(np.uint8)  # saturating: fix-up in chunk 2
+    p = _plan((H, W, 1, 8, 4, 33, 16), "u8")
+    t = torch.from_numpy(x).cuda()
+    gi, gd = p.run(t)
+    for f in (0, 63, 64, 65, 66):
+        fi, fd = p.run(t[f:f + 1].clone())
+        assert torch.equal(gi[f], fi[0]) and torch.equal(gd[f], fd[0]), f
+    oi, od = oracle.bm(x, 8, 4, 33, 16, images=(N - 1, N))
+    check_u8(gi[N - 1:].cpu().numpy(), gd[N - 1:].cpu().numpy(), oi, od, "saturated frame in the second chunk")
