@@ -291,6 +291,11 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
   };
   const int ref_elems = a.K * R * bb;                      // group elements per reference
   T* out_tile = static_cast<T*>(a.out) + size_t(ref00) * ref_elems;
+  // float patches with an odd row length (c3: b = 7) are written as element pairs when every
+  // reference's segment starts 8-byte aligned (K C b^2 even)
+  const bool pair = sizeof(T) == 4 && vec == 1 && (ref_elems & 1) == 0;
+  const int pkstep = 64 / ppv, pestep = 64 - pkstep * ppv;  // 64 elements per warp iteration
+  const int k_pair = (2 * lane) / ppv, e_pair = 2 * lane - k_pair * ppv;
   int ty_w = warp / ix_n, tx_w = warp - ty_w * ix_n;  // this warp's current tile reference
   for (int t = warp; t < n_tile; t += nwarps) {
     const int rofs = ty_w * sa.nx + tx_w;  // reference - ref00
@@ -303,6 +308,31 @@ __global__ void __launch_bounds__(256) group_staged_kernel(GroupArgs a, StagedAr
       const int te = tab[e_lane];
       T* dst = out_ref + lane * vec;
       for (int k = k_lane; k < a.K; k += kstep, dst += 32 * vec) put(int(wb[k]), te, e_lane, dst, ref, k);
+    } else if (pair) {  // float, odd row length: element pairs -> one 8-byte store (segment is 8-B aligned)
+      int k0 = k_pair, e0 = e_pair;
+      for (int it = lane; 2 * it < ref_elems; it += 32) {
+        int k1 = k0, e1 = e0 + 1;
+        if (e1 == ppv) e1 = 0, ++k1;
+        T v[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = u ? k1 : k0, e = u ? e1 : e0;
+          const int base = int(wb[k]);
+          if (base >= 0) {
+            v[u] = reg[base + tab[e]];
+          } else {  // no match (0) / outside the staged region (global read)
+            const int j = base == -1 ? -1 : __ldg(a.idx + ref * a.K + k);
+            const int rr = e / bb, c = rr / bb, l = rr - c * bb, m = e - rr * bb;
+            const uint32_t cy = a.fdW.div(uint32_t(max(j, 0))), cx = uint32_t(max(j, 0)) - cy * uint32_t(a.W);
+            v[u] = j < 0 ? T(0) : img[c * plane + size_t(cy + l) * a.W + cx + m];
+          }
+        }
+        if constexpr (sizeof(T) == 4)
+          __stcs(reinterpret_cast<float2*>(out_ref + 2 * it), make_float2(float(v[0]), float(v[1])));
+        e0 += pestep;
+        k0 += pkstep;
+        if (e0 >= ppv) e0 -= ppv, ++k0;
+      }
     } else {
       int k = k_lane, e = e_lane;
       for (int it = lane; it < items; it += 32) {

@@ -562,11 +562,12 @@ def test_group_matches_oracle(dtype, C, H, W, b, s, Wn, K):
     np.testing.assert_array_equal(Y.cpu().numpy(), oracle.group(x, idx.cpu().numpy(), b))
 
 
-@pytest.mark.parametrize("dtype", ["u8", "f32"])
-def test_group_arbitrary_idx(dtype):
+@pytest.mark.parametrize("dtype,b", [("u8", 8), ("f32", 8), ("f32", 7), ("u8", 5)])
+def test_group_arbitrary_idx(dtype, b):
     # idx not produced by a search (any patch of the image, -1 holes): the staged gather must fall
     # back to global reads for candidates outside a tile's windows; ragged tiles in both directions
-    H, W, C, b, s, Wn, K = 150, 203, 2, 8, 4, 9, 7
+    # (f32 b = 7: the element-pair stores; u8 b = 5: single elements)
+    H, W, C, s, Wn, K = 150, 203, 2, 4, 9, 8
     rng = np.random.Generator(np.random.PCG64(11))
     x = synth.random_image(rng, 3, C, H, W, dtype)
     p = _plan((H, W, C, b, s, Wn, K), dtype)
