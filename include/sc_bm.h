@@ -172,6 +172,19 @@ sc_status_t sc_bm_nlm_weights(sc_bm_plan_t plan, const void* img, float h, float
                               sc_stream_t stream);
 
 /*
+ * NL-means estimate of every reference patch (PAPER.md:252, after Eq. 2): the weighted average
+ *     X_hat_i = sum_j s_i(j) X_j,   s_i(j) = exp(-||X_j - X_i||_F^2 / h^2) / Theta_i,
+ * j over the reference's clipped window (footnote 2, PAPER.md:280), the distances from the
+ * Self-Convolution identity (Proposition 1, PAPER.md:316-320), X_j the raw input patches.
+ * One image img [C][H][W] (device, 16-byte aligned) -> out [n_refs][C][b][b] float32 (device,
+ * 4-byte aligned), reference raster order. The weights are never materialised (streaming
+ * softmax in the matcher's epilogue). SC_ERR_UNSUPPORTED for the NCC metric or b*b*C > 256.
+ * Asynchronous on `stream`, never allocates.
+ */
+sc_status_t sc_bm_nlm_average(sc_bm_plan_t plan, const void* img, float h, float* out,
+                              sc_stream_t stream);
+
+/*
  * 3D / temporal search (the video setting of PAPER.md:661, 697): with T > 0, the candidates of a
  * reference in image f of a sc_bm_run_batch / sc_bm_run_rows call are the window positions of
  * images f-T .. f+T of that call (clipped to the batch), and idx_out holds the BATCH-GLOBAL
@@ -220,19 +233,6 @@ sc_status_t sc_bm_destroy(sc_bm_plan_t plan);
 
 /* Static string for a status code. */
 const char* sc_status_string(sc_status_t s);
-
-/*
- * NL-means estimate of every reference patch (PAPER.md:252, after Eq. 2): the weighted average
- *     X_hat_i = sum_j s_i(j) X_j,   s_i(j) = exp(-||X_j - X_i||_F^2 / h^2) / Theta_i,
- * j over the reference's clipped window (footnote 2, PAPER.md:280), the distances from the
- * Self-Convolution identity (Proposition 1, PAPER.md:316-320), X_j the raw input patches.
- * One image img [C][H][W] (device, 16-byte aligned) -> out [n_refs][C][b][b] float32 (device,
- * 4-byte aligned), reference raster order. The weights are never materialised (streaming
- * softmax in the matcher's epilogue). SC_ERR_UNSUPPORTED for the NCC metric or b*b*C > 256.
- * Asynchronous on `stream`, never allocates.
- */
-sc_status_t sc_bm_nlm_average(sc_bm_plan_t plan, const void* img, float h, float* out,
-                              sc_stream_t stream);
 
 /*
  * Test export of step a1: the norm map h_X (.) h_X of the CENTRED image
