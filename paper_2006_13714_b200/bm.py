@@ -261,7 +261,8 @@ class Plan:
         """Temporal search (set_temporal(T) first) for the reference frames [f_begin, f_end) of the
         batch imgs, candidates from every frame of it; idx = (frame + frame_offset) * H * W + pixel."""
         imgs = self._check_img(imgs)
-        idx, dist = out if out is not None else self.alloc_out(f_end - f_begin)
+        # (the C ABI validates the range: an empty allocation for an invalid one)
+        idx, dist = out if out is not None else self.alloc_out(max(0, f_end - f_begin))
         _check("sc_bm_run_temporal", self._lib.sc_bm_run_temporal(
             self._h, ctypes.c_void_p(imgs.data_ptr()), imgs.shape[0], f_begin, f_end, frame_offset,
             ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))

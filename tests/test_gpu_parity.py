@@ -980,3 +980,34 @@ def test_batch_larger_than_one_launch():
         assert torch.equal(gi[f], fi[0]) and torch.equal(gd[f], fd[0]), f
     oi, od = oracle.bm(x, 8, 4, 33, 16, images=(N - 1, N))
     check_u8(gi[N - 1:].cpu().numpy(), gd[N - 1:].cpu().numpy(), oi, od, "saturated frame in the second chunk")
+
+
+def test_next_rows_argument_validation():
+    """Synchronous argument checks of the next rows' entry points (SC_ERR_INVALID_ARGUMENT = 1,
+    SC_ERR_UNSUPPORTED = 2): nothing is launched for a rejected call."""
+    from paper_2006_13714_b200.bm import Plan, ScError
+    p = Plan(64, 96, 1, 8, 4, 15, 8, "u8")
+    x = torch.zeros((3, 1, 64, 96), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ScError) as e:
+        p.run_temporal(x, 0, 2)  # T = 0
+    assert e.value.code == 2
+    p.set_temporal(1)
+    for args, kw in [((x, 2, 4), {}), ((x, 2, 1), {}), ((x, -1, 2), {}), ((x, 0, 2), {"frame_offset": -1})]:
+        with pytest.raises(ScError) as e:
+            p.run_temporal(*args, **kw)
+        assert e.value.code == 1, (args, kw)
+    with pytest.raises(ScError) as e:
+        p.nlm_weights(x[0], 0.0)
+    assert e.value.code == 1
+    with pytest.raises(ScError) as e:
+        p.nlm_average(x[0], -1.0)
+    assert e.value.code == 1
+    q = Plan(64, 96, 1, 8, 4, 15, 8, "u8", metric="ncc")
+    with pytest.raises(ScError) as e:
+        q.set_temporal(1)  # temporal search is L2-only
+    assert e.value.code == 2
+    idx, _ = Plan(64, 96, 1, 8, 4, 15, 8, "u8").run(x)
+    buf = torch.empty(idx.numel() * 64 + 16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ScError) as e:  # misaligned groups_out
+        Plan(64, 96, 1, 8, 4, 15, 8, "u8").group(x, idx, out=buf[1:1 + idx.numel() * 64].view(3, -1, 8, 1, 8, 8))
+    assert e.value.code == 1
