@@ -383,10 +383,14 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
   cudaError_t e = cudaSuccess;
   if (!h.ready) {
     // frames per pipeline stage: small enough that filling (first H2D + match) and draining (last
-    // D2H) the pipeline stay short against the PCIe-bound copies (~48 MB of results per stage),
+    // D2H) the pipeline stay short against the PCIe-bound copies (~24 MB of results per stage:
+    // one c5 frame; 48 and 100 MB measured 1-3 % slower),
     // at most the plan's workspace chunk
     const size_t out_frame = out_elems * 8;
-    h.F = int(std::max<size_t>(1, std::min<size_t>(size_t(p->F), (size_t(48) << 20) / std::max<size_t>(out_frame, 1))));
+#ifndef SCBM_HOST_STAGE_MB
+#define SCBM_HOST_STAGE_MB 24
+#endif
+    h.F = int(std::max<size_t>(1, std::min<size_t>(size_t(p->F), (size_t(SCBM_HOST_STAGE_MB) << 20) / std::max<size_t>(out_frame, 1))));
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
       e = cudaMalloc(&h.d_img[i], img_bytes * h.F);
       if (e == cudaSuccess) e = cudaMalloc(&h.d_idx[i], out_elems * 4 * h.F);
