@@ -602,7 +602,8 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
   if (g.metric == SC_METRIC_NCC) {  // K + 4 <= 32; references the key quantisation leaves open -> fix-up
     cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
-    if (g.Wn == 33 && g.KP <= 20) e = launch_box_t<2, 11, 20, 40, true, 33>(a, F, box_layout(g, 2, vy, 20, &a), st);
+    if (g.Wn == 33 && g.KP <= 18) e = launch_box_t<2, 11, 18, 40, true, 33>(a, F, box_layout(g, 2, vy, 18, &a), st);
+    else if (g.Wn == 33 && g.KP <= 20) e = launch_box_t<2, 11, 20, 40, true, 33>(a, F, box_layout(g, 2, vy, 20, &a), st);
     else if (g.Wn == 33 && g.KP <= 24) e = launch_box_t<2, 11, 24, 40, true, 33>(a, F, box_layout(g, 2, vy, 24, &a), st);
     else if (vy == 11 && a.WP == 40 && g.KP <= 24) e = launch_box_t<2, 11, 24, 40, true>(a, F, box_layout(g, 2, vy, 24, &a), st);
     else {  // 32-key lists: the layout (per-warp scratch for the KR + 1 pitch) must match KR

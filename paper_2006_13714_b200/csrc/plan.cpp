@@ -20,7 +20,10 @@ namespace {
 // K = 70: margin 4 sends near-tie references to the fix-up, which costs more than it saves)
 constexpr int kRescoreMargin = 4;
 constexpr int kRescoreMarginLargeK = 8;
-constexpr int kNccMargin = 4;
+// NCC: 2 for uint8 (the integer fix-up is cheap: c5 sends 489 of 8.2M references to it and
+// still gains 4 %), 4 for float input (its fp64 fix-up costs more than the shorter list saves)
+constexpr int kNccMarginU8 = 2;
+constexpr int kNccMarginF32 = 4;
 
 sc_status_t cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return SC_OK;
@@ -183,7 +186,7 @@ sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, in
   g.Mxp = (g.Mx + 2 * g.NPAD + 3) & ~3;
   g.NFS = (long long)(g.My + 2 * g.NPAD) * g.Mxp;
   g.metric = metric;
-  g.KP = metric == SC_METRIC_NCC ? K + kNccMargin
+  g.KP = metric == SC_METRIC_NCC ? K + (dtype == SC_DTYPE_U8 ? kNccMarginU8 : kNccMarginF32)
          : dtype == SC_DTYPE_F32 ? K + (K > 48 ? kRescoreMarginLargeK : kRescoreMargin) : K;
   if (metric == SC_METRIC_NCC && !boxf_supported(g) && !box_supported(g)) {  // NCC: box kernels only
     delete p;

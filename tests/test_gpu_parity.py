@@ -720,7 +720,7 @@ def test_ncc_configs_and_rejects():
     sl = slice(80 * p.nx, 83 * p.nx)
     check_ncc(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0, sl], gd[0, sl], oi[0], od[0], exact=False,
               iy_range=(80, 83), where="ncc c2")
-    for args in [(64, 64, 1, 8, 5, 21, 16), (64, 64, 1, 8, 4, 21, 29)]:
+    for args in [(64, 64, 1, 8, 5, 21, 16), (64, 64, 1, 8, 4, 21, 31)]:
         with pytest.raises(ScError) as e:
             Plan(*args, "u8", metric="ncc")
         assert e.value.code == 2
