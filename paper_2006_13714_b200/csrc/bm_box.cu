@@ -81,7 +81,7 @@ __device__ __forceinline__ int dp4(uint32_t x, uint32_t y, int acc) {
 
 // NCC (SC_METRIC_NCC, Eq. 4): the same block sums on RAW bytes (unsigned dp4a, exact); a lane
 // forms C = U_l + U_{l+1} and n_c = D_l + D_{l+1} (two shuffles), filters on the float score
-// sqrt(n_r) - C / sqrt(n_c) >= 0 with quantised 32-bit keys (rel + 1, 0 sentinels), keeps K + 4
+// sqrt(n_r) - C / sqrt(n_c) >= 0 with quantised 32-bit keys (rel + 1, 0 sentinels), keeps K + m
 // and re-ranks them exactly (ncc.cuh) from the staged bytes.
 // WNC: the window side when known at compile time (0 = runtime): the window geometry, key widths
 // and loop bounds then become immediates (no per-round constant reloads in the survivor loop)
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   bool ref_ok[NY];
   int32_t nr[NY];  // ||X_i||^2 of the centred reference (left strip + lane l+1's right strip)
   int thr[NY];     // largest d' = d - ||X_i||^2 that may still enter the reference's top-K
-  float thrf[NY];  // NCC: largest filter score that may still enter the top-(K+4)
+  float thrf[NY];  // NCC: largest filter score that may still enter the top-(K+m)
   float nrs[NY];   // NCC: sqrt(n_r)
   float gsq[NY];   // NCC: the filter's bound on C^2 / n_c (0: keep everything)
   RegTopK32<KR> rt[NY];
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     thrf[q] = __int_as_float(0x7f800000);
     nrs[q] = sqrtf(float(nr[q]));
     gsq[q] = 0.f;
-    if constexpr (NCC) {  // 0 sentinels: the (K+4)-th key sits in r[KR-1]
+    if constexpr (NCC) {  // 0 sentinels: the (K+m)-th key sits in r[KR-1]
 #pragma unroll
       for (int k = 0; k < KR; ++k) rt[q].r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
     }
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
           }
           if constexpr (NCC) {
             const uint32_t kth = rt[q].r[KR - 1];
-            if (kth != 0xffffffffu) {  // largest score of the (K+4)-th key's quantum + margin
+            if (kth != 0xffffffffu) {  // largest score of the (K+m)-th key's quantum + margin
               const float smax = __uint_as_float(((kth >> rbits) << (rbits - 1)) | ((1u << (rbits - 1)) - 1u));
               thrf[q] = fmaf(smax, 1.0f + 1e-5f, 1e-30f);
               const float g = nrs[q] - thrf[q];  // keep iff C / sqrt(n_c) >= g, i.e. C^2 >= g^2 n_c (C >= 0)
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
   const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
   const int nref = min(kBoxRefsX, a.nx - ix_first);
   if constexpr (NCC) {
-    // ---- a5 + a6 (NCC): per reference, the kept K + 4 candidates re-scored EXACTLY from the staged
+    // ---- a5 + a6 (NCC): per reference, the kept K + m candidates re-scored EXACTLY from the staged
     // raw bytes (C, n_c, n_r by unsigned dp4a), one warp bitonic sort (ncc.cuh), K (idx, -NCC)
     const uint32_t relmask = (1u << rbits) - 1u;
     const int roff = -lo;
@@ -558,7 +558,7 @@ bool box_supported(const Geometry& g) {
   if (g.dtype != SC_DTYPE_U8 || g.b != 8 || g.s != 4 || g.C != 1 || g.K > 32) return false;
   if (key32_rel_bits(g.Wn) > 11) return false;  // keeps >= 21 distance bits in the 32-bit keys
   if (g.metric == SC_METRIC_NCC && (g.KP > 32 || (1 << key32_rel_bits(g.Wn)) <= g.Wn * g.Wn))
-    return false;  // NCC: K + 4 <= 32 register keys, rel + 1 must fit
+    return false;  // NCC: K + m <= 32 register keys, rel + 1 must fit
   BoxArgs a{};
   return box_layout(g, 2, box_vy(g), 32, &a) <= 227 * 1024;
 }
@@ -599,7 +599,7 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
     if (e != cudaSuccess) return e;
     return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
   }
-  if (g.metric == SC_METRIC_NCC) {  // K + 4 <= 32; references the key quantisation leaves open -> fix-up
+  if (g.metric == SC_METRIC_NCC) {  // K + m <= 32; references the key quantisation leaves open -> fix-up
     cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     if (g.Wn == 33 && g.KP <= 18) e = launch_box_t<2, 11, 18, 40, true, 33>(a, F, box_layout(g, 2, vy, 18, &a), st);

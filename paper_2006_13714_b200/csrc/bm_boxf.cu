@@ -488,7 +488,7 @@ cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st
 }  // namespace
 
 bool boxf_supported(const Geometry& g) {
-  // L2: float images (uint8 L2 has the dp4a box kernel); NCC: both dtypes, K + 4 <= 32
+  // L2: float images (uint8 L2 has the dp4a box kernel); NCC: both dtypes, K + m <= 32
   if (g.metric == SC_METRIC_L2 && g.dtype != SC_DTYPE_F32) return false;
   if (g.metric == SC_METRIC_NCC && g.KP > 32) return false;
   const bool shape = (g.s == 3 && g.b == 8) || (g.s == 1 && g.b == 7) || (g.s == 4 && g.b == 8) ||
