@@ -502,8 +502,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         if (k < a.K) scratch[lane * (KR + 1) + k] = rt[q].r[k];
     }
     __syncwarp();
-    for (int e = lane; e < nref * a.K; e += 32) {
-      const int j = e / a.K, k = e - j * a.K;
+    auto emit = [&](int e, int j, int k) {
       const uint32_t kk = scratch[j * (KR + 1) + k];
       int rel = key32.rel(kk);
       const int tsl = TEMP ? rel / (Wn * Wn) : 0;  // frame slot tau + T
@@ -512,6 +511,14 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
       a.idx_out[row0 * a.K + e] = (TEMP ? (fref + tsl - a.T + a.idx_foff) * a.H * a.W : 0) +
                                   (ry + dyy + lo) * a.W + (ix_first + j) * 4 + dxx + lo;
       a.dist_out[row0 * a.K + e] = key32.dist(kk);
+    };
+    if (a.K == KR) {  // the list length is K (c5): element -> (reference, rank) by a constant divisor
+      for (int e = lane; e < nref * KR; e += 32) emit(e, e / KR, e % KR);
+    } else {
+      for (int e = lane; e < nref * a.K; e += 32) {
+        const int j = e / a.K;
+        emit(e, j, e - j * a.K);
+      }
     }
     __syncwarp();
 #endif
