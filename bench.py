@@ -125,6 +125,85 @@ class ClockSampler:
                 "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _launch_ranks(args) -> None:
+    """One process per GPU. Under torchrun (WORLD_SIZE set) the world must equal --gpus.
+    Without it, ``--gpus N > 1`` re-executes this script under torch.distributed.run with N
+    local ranks (127.0.0.1 rendezvous), refusing with a non-zero exit when fewer than N GPUs
+    are visible -- never a silent single-rank run reported as N GPUs."""
+    env_ws = os.environ.get("WORLD_SIZE")
+    if env_ws is not None:
+        if args.impl == "ours" and int(env_ws) != args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_ws}\n")
+            sys.exit(2)
+        return
+    if args.gpus <= 1 or args.impl == "reference":  # the reference arm runs on rank 0 only
+        return
+    if not args.selftest_cpu:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but only {have} GPU(s) visible\n")
+            sys.exit(3)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def selftest_cpu(args, cfg):
+    """CPU plumbing check of the multi-rank bench (tests/test_bench_cpu.py): the launcher, the
+    frame shards, barrier-bracketed timing with the max over ranks and the line's fields, on
+    gloo with a stand-in step (a numpy pass over a buffer sized by the shard). NOT a measurement."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2006_13714_b200.dist import balanced_ranges
+    ws, rank, _ = _dist_env()
+    if ws > 1:
+        tdist.init_process_group("gloo")
+    shards = balanced_ranges(cfg.N, ws)
+    f0, f1 = shards[rank]
+    buf = np.random.default_rng(rank).random((max(1, f1 - f0), 1 << 16))
+
+    def step():
+        return float(np.sort(buf, axis=1)[:, 0].sum())
+
+    for _ in range(args.warmup):
+        step()
+    if ws > 1:
+        tdist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    local_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    t = torch.tensor([local_ms, float(f1 - f0)], dtype=torch.float64)
+    if ws > 1:
+        tdist.barrier()
+        tm = t.clone()
+        tdist.all_reduce(tm, op=tdist.ReduceOp.MAX)
+        tn = t.clone()
+        tdist.all_reduce(tn, op=tdist.ReduceOp.SUM)
+        ms, frames = tm[0].item(), tn[1].item()
+    else:
+        ms, frames = local_ms, float(f1 - f0)
+    if rank == 0:
+        line = {"selftest": "cpu plumbing only (launcher, shards, max over ranks); not a measurement",
+                "metric": METRIC, "value": frames / (ms / 1e3), "unit": "frames/s (stand-in step)",
+                "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong" if cfg.N > 1 else "weak",
+                "config": dict(_config_obj(cfg, args), shards=shards), "frames_timed": frames}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
 def _dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -132,7 +211,7 @@ def _dist_env():
     return ws, rank, local
 
 
-def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1), metric="l2"):
+def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1), metric="l2", want_tables=False):
     """Time the oracle on a bounded sample of the workload: reference rows of image 0."""
     import oracle
     run = oracle.ncc if metric == "ncc" else oracle.bm
@@ -156,13 +235,47 @@ def _cpu_sample(cfg, x, target_s=8.0, images=(0, 1), metric="l2"):
     if rows == ny and x.shape[0] > 1:  # more than one frame's worth of CPU time: whole frames
         n_img = int(max(1, min(x.shape[0], -(-target_s // (dt * ny)))))  # ceil
     t0 = time.perf_counter()
-    run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=(0, n_img) if n_img > 1 else images, rows=(mid, mid + rows))
+    imgs = (0, n_img) if n_img > 1 else images
+    out = run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, images=imgs, rows=(mid, mid + rows))
     dt = time.perf_counter() - t0
     p = pairs(mid, mid + rows) * n_img
     what = (f"{cfg.name} images 0:{n_img} (all {ny} reference rows)" if n_img > 1 else
             f"{cfg.name} image 0, reference rows {mid}:{mid + rows} of {ny}")
-    return {"value": p / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{what} ({rows * nx * n_img} refs, {p} candidate pairs), {dt:.2f} s"}, p, dt
+    res = {"value": p / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"{what} ({rows * nx * n_img} refs, {p} candidate pairs), {dt:.2f} s"}
+    if want_tables:
+        return res, p, dt, (imgs, (mid, mid + rows), out)
+    return res, p, dt
+
+
+def _parity_of_sample(cfg, x_host, idx, dst, sample, metric):
+    """The bench checks what it times: the GPU tables of the frames / reference rows the
+    cpu_baseline leg just computed with the oracle, compared element by element (u8 bit-exact,
+    f32 by the 1e-5 rule of tests/parity.py)."""
+    from tests.parity import check_f32, check_ncc, check_u8
+    (i0, i1), (r0, r1), (oi, od) = sample
+    nx = (cfg.W - cfg.b) // cfg.s + 1
+    sl = slice(r0 * nx, r1 * nx)
+    gi = idx[i0:i1, sl].cpu().numpy()
+    gd = dst[i0:i1, sl].cpu().numpy()
+    what = f"images {i0}:{i1}, reference rows {r0}:{r1} ({(i1 - i0) * (r1 - r0) * nx} references)"
+    try:
+        if metric == "ncc":
+            for n in range(i1 - i0):
+                check_ncc(x_host[i0 + n], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[n], gd[n], oi[n], od[n],
+                          exact=cfg.dtype == "u8", iy_range=(r0, r1), where="bench")
+            rule = "idx bit-exact, d_NCC within 2e-6" if cfg.dtype == "u8" else "NCC tolerance rule"
+        elif cfg.dtype == "u8":
+            check_u8(gi, gd, oi, od, "bench")
+            rule = "idx and dist bit-exact"
+        else:
+            for n in range(i1 - i0):
+                check_f32(x_host[i0 + n], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[n], gd[n], oi[n], od[n],
+                          iy_range=(r0, r1), where="bench")
+            rule = "f32 rule: rel 1e-5, set differences only at the K-th distance"
+        return {"checked": what, "rule": rule, "result": "pass"}
+    except AssertionError as e:
+        return {"checked": what, "result": "FAIL", "detail": str(e)[:300]}
 
 
 def run_reference(args, cfg):
@@ -340,13 +453,18 @@ def main():
     ap.add_argument("--nlm-h", type=float, default=0.0, help="NLM bandwidth (default: 1.0 * sqrt(b^2 C) * value scale)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf"],
                     help="force the matching kernel (default: the plan's choice)")
+    ap.add_argument("--selftest-cpu", action="store_true",
+                    help="CPU check of the multi-rank plumbing (gloo, stand-in step); prints no measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    _launch_ranks(args)
 
     from paper_2006_13714_b200 import synth
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.selftest_cpu:
+        return selftest_cpu(args, cfg)
 
     import torch
     from paper_2006_13714_b200.bm import Plan
@@ -543,7 +661,7 @@ def main():
                "steps": e_steps, "timing": "wall clock around sc_bm_run_host (synchronous), max over ranks"}
 
     gather = None
-    if args.gather and dist:
+    if dist and (args.gather or (cfg.N > 1 and args.temporal == 0)):  # default at N > 1
         gi = torch.empty((ws * idx.shape[0],) + tuple(idx.shape[1:]), dtype=idx.dtype, device="cuda")
         gd = torch.empty_like(gi, dtype=dst.dtype)
         dist.barrier()
@@ -555,7 +673,32 @@ def main():
         torch.cuda.synchronize()
         tg = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device="cuda")
         dist.all_reduce(tg, op=dist.ReduceOp.MAX)
-        gather = {"ms": tg.item(), "bytes_per_rank": int(2 * gi.numel() * 4), "backend": "nccl"}
+        gather = {"ms": tg.item(), "bytes_per_rank": int(2 * gi.numel() * 4), "backend": "nccl",
+                  "equal_shards": bool(cfg.N % ws == 0)}
+        # end to end with the NCCL gather: pinned host frames -> HBM, the matcher, the all-gather
+        # of both tables (every rank ends with the whole batch's tables), device-timed per step,
+        # max over ranks
+        xp = torch.from_numpy(x_host).pin_memory()
+        e_steps = max(3, min(args.steps, 5))
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e_steps)]
+        dist.barrier()
+        torch.cuda.synchronize()
+        for a_, b_ in ev:
+            a_.record()
+            x.copy_(xp, non_blocking=True)
+            plan.run(x, out=(idx, dst))
+            dist.all_gather_into_tensor(gi, idx)
+            dist.all_gather_into_tensor(gd, dst)
+            b_.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([float(np.mean([a_.elapsed_time(b_) for a_, b_ in ev]))], dtype=torch.float64, device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        gather["h2d_compute_gather_ms"] = te.item()
+        gather["h2d_compute_gather_value"] = pairs_step / (te.item() / 1e3)
+        if e2e is not None:
+            e2e["nccl_gather"] = {"value": pairs_step / (te.item() / 1e3), "ms_per_step": te.item(),
+                                  "what": "pinned H2D of the rank's frames + matcher + NCCL all-gather of "
+                                          "idx and dist to every rank (device events, max over ranks)"}
         # compute + gather pipelined per frame chunk (the gather of chunk c overlaps chunk c+1)
         from paper_2006_13714_b200.dist import run_frames_pipelined
         chunk = max(1, nloc // 4)
@@ -589,11 +732,13 @@ def main():
             gather["compute_plus_peer_store_ms"] = tq.item()
             del pt
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and ws == 1 and not args.no_cpu:
         # the oracle on ~10-30 s of the same workload (whole frames where one frame takes less;
         # the middle-row calibration overestimates a frame, whose border rows have clipped windows)
-        cpu, _, _ = _cpu_sample(cfg, x_host, target_s=20.0, metric=args.metric)
+        cpu, _, _, sample = _cpu_sample(cfg, x_host, target_s=20.0, metric=args.metric, want_tables=True)
+        if args.temporal == 0:
+            parity = _parity_of_sample(cfg, x_host, idx, dst, sample, args.metric)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -602,7 +747,7 @@ def main():
                 "scaling": "strong" if cfg.N > 1 else "weak", "vs_baseline": None,
                 "dtype": _dtype_name(cfg), "data": "synthetic", "config": _config_obj(cfg, args),
                 "ref_patches_per_s": refs_step / (ms / 1e3), "candidate_pairs_per_step": pairs_step,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "gather": gather, "graph": graph,
                 "kernel": info["kernel"], "frames_per_chunk": info["frames_per_chunk"], "metric_kind": args.metric}
         print(json.dumps(line), flush=True)

@@ -118,16 +118,28 @@ sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K
 sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, int K,
                           sc_dtype_t dtype, sc_metric_t metric, sc_bm_plan_t* plan_out);
 
-/* One image [C][H][W] -> idx_out / dist_out [n_refs][K]. Device pointers; img 16-B aligned. */
+/*
+ * Block matching of one image (Eq. 3, over the window of footnote 2,
+ * PAPER.md:280; evaluated through Lemma 2, and Theorem 1):
+ * img [C][H][W] -> idx_out / dist_out [n_refs][K]. Device pointers; img 16-B aligned, outputs
+ * 4-B aligned. SC_ERR_INVALID_ARGUMENT for a null / misaligned pointer, SC_ERR_WRONG_DEVICE off
+ * the plan's device, SC_ERR_CUDA when the launch fails. Asynchronous on `stream`.
+ */
 sc_status_t sc_bm_run(sc_bm_plan_t plan, const void* img, int32_t* idx_out, void* dist_out,
                       sc_stream_t stream);
 
-/* n_images images [n][C][H][W] -> [n][n_refs][K]. Device pointers. */
+/*
+ * Block matching (Eq. 3; footnote 2) of n_images independent
+ * images [n][C][H][W] -> [n][n_refs][K] (the video batch of config c5; the paper's video
+ * setting). Device pointers, errors as sc_bm_run. With sc_bm_set_temporal(T > 0)
+ * idx is batch-global, so n_images * H * W must stay <= 2^31 (SC_ERR_INVALID_ARGUMENT).
+ */
 sc_status_t sc_bm_run_batch(sc_bm_plan_t plan, const void* imgs, int64_t n_images,
                             int32_t* idx_out, void* dist_out, sc_stream_t stream);
 
 /*
- * Row band (the multi-GPU partitioner's spatial split): only the
+ * Row band of Eq. 3: the multi-GPU partitioner's spatial split (DESIGN.md
+ * "Multi-GPU"; every reference is independent given its window, footnote 2): only the
  * references of reference-grid rows [iy_begin, iy_end) of each image; idx_out / dist_out
  * are [n_images][(iy_end - iy_begin) * n_ref_x][K]. The full image is read (replicated).
  */
@@ -190,7 +202,8 @@ sc_status_t sc_bm_nlm_average(sc_bm_plan_t plan, const void* img, float h, float
  * images f-T .. f+T of that call (clipped to the batch), and idx_out holds the BATCH-GLOBAL
  * index frame * H * W + cy * W + cx (ties by it: earlier frames first). uint8, b = 8, stride 4,
  * one channel, L2 metric, (2T+1) Wn^2 <= 4096 (else SC_ERR_UNSUPPORTED); T = 0 (default)
- * restores per-image search. sc_bm_run_host is unsupported with T > 0.
+ * restores per-image search and the matcher the plan used before T > 0 forced the box kernel.
+ * sc_bm_run_host is unsupported with T > 0.
  */
 sc_status_t sc_bm_set_temporal(sc_bm_plan_t plan, int32_t T);
 

@@ -168,6 +168,19 @@ class Plan:
             raise ValueError(f"image shape {tuple(imgs.shape)} does not match the plan")
         return imgs
 
+    def _check_out(self, out, n_images, refs, cuda):
+        """Output tables must be contiguous [n, refs, K] int32 idx + dist of the plan's dtype,
+        on the device (device paths) or in host memory (run_host): the C ABI writes
+        n * refs * K elements through the raw pointers."""
+        import torch
+        idx, dist = out
+        for name, t, want in (("idx", idx, torch.int32), ("dist", dist, self._dist_dtype())):
+            if not isinstance(t, torch.Tensor) or t.dtype != want or t.is_cuda != cuda or \
+                    not t.is_contiguous() or tuple(t.shape) != (n_images, refs, self.K):
+                raise ValueError(f"{name} must be a contiguous {'CUDA' if cuda else 'host'} {want} tensor "
+                                 f"of shape {(n_images, refs, self.K)}")
+        return idx, dist
+
     def alloc_out(self, n_images, rows=None):
         import torch
         refs = self.n_refs if rows is None else (rows[1] - rows[0]) * self.nx
@@ -179,7 +192,8 @@ class Plan:
     def run(self, imgs, out=None, stream=None):
         """Block matching on device tensors; returns (idx, dist) [N, n_refs, K]."""
         imgs = self._check_img(imgs)
-        idx, dist = out if out is not None else self.alloc_out(imgs.shape[0])
+        idx, dist = (self._check_out(out, imgs.shape[0], self.n_refs, True) if out is not None
+                     else self.alloc_out(imgs.shape[0]))
         _check("sc_bm_run_batch", self._lib.sc_bm_run_batch(
             self._h, ctypes.c_void_p(imgs.data_ptr()), imgs.shape[0], ctypes.c_void_p(idx.data_ptr()),
             ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
@@ -188,6 +202,8 @@ class Plan:
     def run_rows(self, imgs, iy_begin, iy_end, out=None, stream=None):
         """Only reference-grid rows [iy_begin, iy_end) (row-band sharding)."""
         imgs = self._check_img(imgs)
+        if out is not None:
+            out = self._check_out(out, imgs.shape[0], max(0, iy_end - iy_begin) * self.nx, True)
         idx, dist = out if out is not None else self.alloc_out(imgs.shape[0], (iy_begin, iy_end))
         _check("sc_bm_run_rows", self._lib.sc_bm_run_rows(
             self._h, ctypes.c_void_p(imgs.data_ptr()), imgs.shape[0], iy_begin, iy_end,
@@ -200,14 +216,16 @@ class Plan:
         t = imgs if isinstance(imgs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(imgs))
         if t.dim() == 3:
             t = t.unsqueeze(0)
-        if t.is_cuda or not t.is_contiguous():
-            raise ValueError("run_host expects a contiguous host tensor/array")
+        want = torch.uint8 if self.dtype == "u8" else torch.float32
+        if t.is_cuda or not t.is_contiguous() or t.dtype != want or t.dim() != 4 or \
+                tuple(t.shape[1:]) != (self.C, self.H, self.W):
+            raise ValueError(f"run_host expects a contiguous host {want} tensor/array [N, {self.C}, {self.H}, {self.W}]")
         n = t.shape[0]
         if out is None:
             idx = torch.empty((n, self.n_refs, self.K), dtype=torch.int32)
             dist = torch.empty((n, self.n_refs, self.K), dtype=self._dist_dtype())
         else:
-            idx, dist = out
+            idx, dist = self._check_out(out, n, self.n_refs, False)
         _check("sc_bm_run_host", self._lib.sc_bm_run_host(
             self._h, ctypes.c_void_p(t.data_ptr()), n, ctypes.c_void_p(idx.data_ptr()),
             ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))

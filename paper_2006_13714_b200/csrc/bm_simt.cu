@@ -287,7 +287,8 @@ __device__ __forceinline__ void process_ref(const SimtArgs& a, int f, int ref_ba
   if (a.dense) {
     if (a.nlm_inv_h2 > 0.f) {  // fused NLM epilogue: the warp's own row, just written (L2-hot)
       __syncwarp();
-      nlm_normalize_row<T>(dense_row, a.Wn * a.Wn, a.nlm_inv_h2, lane);
+      const NlmRowGeom gm{ry, rx, a.H - b, a.W - b, a.Wn, a.lo};
+      nlm_normalize_row<T>(dense_row, gm, a.nlm_inv_h2, lane);
     }
     return;
   }

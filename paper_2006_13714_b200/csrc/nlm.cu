@@ -20,11 +20,14 @@ namespace scbm {
 namespace {
 
 template <typename T>
-__global__ void __launch_bounds__(256) nlm_normalize(void* rows, long long n_refs, int slots, float inv_h2) {
+__global__ void __launch_bounds__(256) nlm_normalize(void* rows, long long n_refs, int nx, int s, int cy_max,
+                                                     int cx_max, int Wn, int lo, float inv_h2) {
   const int lane = threadIdx.x & 31;
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_refs; r += nw)
-    nlm_normalize_row<T>(static_cast<T*>(rows) + r * slots, slots, inv_h2, lane);
+  for (long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n_refs; r += nw) {
+    const NlmRowGeom gm{int(r / nx) * s, int(r % nx) * s, cy_max, cx_max, Wn, lo};
+    nlm_normalize_row<T>(static_cast<T*>(rows) + r * Wn * Wn, gm, inv_h2, lane);
+  }
 }
 
 }  // namespace
@@ -36,10 +39,14 @@ cudaError_t launch_nlm_normalize(const sc_bm_plan_s& p, void* rows, float h, cud
   const float inv_h2 = 1.f / (h * h);
   const long long blocks = std::min<long long>((n_refs + 7) / 8, (long long)p.sm_count * 16);
   if (launches) *launches += 1;
+  const int lo = -(g.Wn / 2);
+  (void)slots;
   if (g.dtype == SC_DTYPE_U8)
-    nlm_normalize<int32_t><<<unsigned(blocks), 256, 0, st>>>(rows, n_refs, slots, inv_h2);
+    nlm_normalize<int32_t><<<unsigned(blocks), 256, 0, st>>>(rows, n_refs, g.nx, g.s, g.H - g.b, g.W - g.b, g.Wn, lo,
+                                                             inv_h2);
   else
-    nlm_normalize<float><<<unsigned(blocks), 256, 0, st>>>(rows, n_refs, slots, inv_h2);
+    nlm_normalize<float><<<unsigned(blocks), 256, 0, st>>>(rows, n_refs, g.nx, g.s, g.H - g.b, g.W - g.b, g.Wn, lo,
+                                                           inv_h2);
   return cudaGetLastError();
 }
 

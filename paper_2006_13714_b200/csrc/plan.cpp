@@ -267,6 +267,8 @@ sc_status_t sc_bm_run_rows(sc_bm_plan_t p, const void* imgs, int64_t n_images, i
   if (!p || !imgs || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
   if (iy_begin < 0 || iy_end > p->g.ny || iy_end < iy_begin) return SC_ERR_INVALID_ARGUMENT;
+  // temporal search reports batch-global idx = frame * H * W + pixel, which must stay int32
+  if (p->T > 0 && n_images * int64_t(p->g.H) * p->g.W > (int64_t(1) << 31)) return SC_ERR_INVALID_ARGUMENT;
   sc_status_t s = check_device(p);
   if (s != SC_OK) return s;
   if (n_images == 0 || iy_end == iy_begin) return SC_OK;
@@ -484,6 +486,11 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
 sc_status_t sc_bm_set_temporal(sc_bm_plan_t p, int32_t T) {
   if (!p || T < 0) return SC_ERR_INVALID_ARGUMENT;
   if (T > 0 && !box_temporal_supported(p->g, T)) return SC_ERR_UNSUPPORTED;
+  if (T > 0 && p->T == 0) p->kernel_before_T = p->kernel;
+  if (T == 0 && p->T > 0 && p->kernel_before_T >= 0) {  // back to the matcher the plan had
+    p->kernel = p->kernel_before_T;
+    p->kernel_before_T = -1;
+  }
   p->T = T;
   if (T > 0) p->kernel = SC_KERNEL_BOX;  // the only matcher with a temporal window
   return SC_OK;

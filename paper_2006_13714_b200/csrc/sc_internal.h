@@ -73,6 +73,7 @@ struct sc_bm_plan_s {
   scbm::Timing timing;
   int64_t launches = 0;
   int T = 0;                          // temporal search radius (sc_bm_set_temporal)
+  int kernel_before_T = -1;           // the matcher T > 0 replaced (restored by T = 0)
   float nlm_inv_h2 = 0.f;             // > 0 while sc_bm_nlm_weights / sc_bm_nlm_average run
   void* nlm_avg_out = nullptr;        // set while sc_bm_nlm_average runs (float [refs][C][b][b])
   const void* batch_base = nullptr;   // temporal search: the run's whole batch ...

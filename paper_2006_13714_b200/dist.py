@@ -183,18 +183,27 @@ class PeerTables:
         return (self.idx, self.dist) if self.rank == self.root else None
 
 
-def temporal_halo(local, rank: int, world: int, T: int, group=None):
+def temporal_halo(local, rank: int, world: int, T: int, group=None, n_frames=None):
     """The one real data exchange of the method: 3D / temporal search on
     frame shards needs, for the references of a rank's first and last frames, the T neighbouring
     frames held by the adjacent ranks. Every rank sends its first T frames to rank-1 and its last
     T to rank+1 (point-to-point NCCL over NVLink on GPUs; gloo in the CPU tests) and returns the
     extended buffer [left halo | own frames | right halo] plus the halo sizes (0 at the ends).
-    T must not exceed the shard size (each halo comes from one neighbour)."""
+    T must not exceed the SMALLEST shard (each halo comes from one neighbour); the check uses a
+    value every rank shares -- n_frames // world when n_frames is given, else the all-reduced
+    minimum shard size -- so all ranks raise together before any point-to-point op starts."""
     import torch
     import torch.distributed as dist
     n = local.shape[0]
-    if T > n and world > 1:
-        raise ValueError("temporal_halo: T larger than the frame shard")
+    if world > 1 and T > 0:
+        if n_frames is not None:
+            min_shard = n_frames // world
+        else:
+            t = torch.tensor([n], dtype=torch.int64, device=local.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            min_shard = int(t.item())
+        if T > min_shard:
+            raise ValueError(f"temporal_halo: T = {T} larger than the smallest frame shard ({min_shard})")
     left = T if rank > 0 else 0
     right = T if rank < world - 1 else 0
     if world == 1 or T == 0:
@@ -222,5 +231,5 @@ def run_temporal_sharded(run_window: Callable, local, rank: int, world: int, n_f
     a, b = frame_shard(n_frames, rank, world)
     if local.shape[0] != b - a:
         raise ValueError("run_temporal_sharded: expected this rank's frame shard")
-    ext, left, _ = temporal_halo(local, rank, world, T, group)
+    ext, left, _ = temporal_halo(local, rank, world, T, group, n_frames=n_frames)
     return run_window(ext, left, left + (b - a), a - left)

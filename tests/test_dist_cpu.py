@@ -137,3 +137,40 @@ def test_temporal_halo_equals_single_process(world):
         assert p.exitcode == 0
     res = sorted(q.get(timeout=5) for _ in range(world))
     assert all(ok for _, ok in res), res
+
+
+def _halo_reject_worker(rank, world, port, use_n, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_frames, T = 5, 3  # shards 3 and 2: T fits rank 0's shard but not rank 1's
+        a, e = sdist.frame_shard(n_frames, rank, world)
+        local = torch.zeros((e - a, 1, 4, 4), dtype=torch.uint8)
+        try:
+            sdist.temporal_halo(local, rank, world, T, n_frames=n_frames if use_n else None)
+            q.put((rank, "no error"))
+        except ValueError:
+            q.put((rank, "raised"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("use_n", [True, False])
+def test_temporal_halo_rejects_on_every_rank(use_n):
+    """A T larger than the smallest shard raises on EVERY rank before any point-to-point op
+    (a rank-local check would let the larger shards block in batch_isend_irecv forever)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_reject_worker, args=(r, 2, port, use_n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert res == [(0, "raised"), (1, "raised")], res
