@@ -451,7 +451,7 @@ def main():
     ap.add_argument("--temporal", type=int, default=0,
                     help="3D / temporal search radius T: candidates in frames f-T..f+T of the batch")
     ap.add_argument("--nlm-h", type=float, default=0.0, help="NLM bandwidth (default: 1.0 * sqrt(b^2 C) * value scale)")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf"],
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "warp", "tc", "box", "boxf", "tcf"],
                     help="force the matching kernel (default: the plan's choice)")
     ap.add_argument("--selftest-cpu", action="store_true",
                     help="CPU check of the multi-rank plumbing (gloo, stand-in step); prints no measurement")
@@ -491,7 +491,7 @@ def main():
     if args.temporal > 0:
         plan.set_temporal(args.temporal)
     if args.kernel != "auto":
-        plan.set_kernel({"simt": 0, "tc": 1, "warp": 2, "box": 3, "boxf": 4}[args.kernel])
+        plan.set_kernel({"simt": 0, "tc": 1, "warp": 2, "box": 3, "boxf": 4, "tcf": 5}[args.kernel])
     info = plan.info()
     idx, dst = plan.alloc_out(nloc)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -590,14 +590,20 @@ def main():
     # kernel correlates one s-column strip per reference and offset, b s C per pair. Both are
     # reported (frac_executed = the executed MACs at the same peak).
     mac_pair = cfg.b * cfg.b * cfg.C
-    mac_exec = {3: cfg.s * cfg.s * cfg.C, 4: cfg.b * cfg.s * cfg.C}.get(info["kernel"], mac_pair)
+    mac_exec = {3: cfg.s * cfg.s * cfg.C, 4: cfg.b * cfg.s * cfg.C,
+                5: 3 * cfg.C * cfg.b * 8}.get(info["kernel"], mac_pair)  # 3xTF32: 3 MMAs of K = 8 b
     pairs_rank = pairs_rank_t if args.temporal > 0 else pairs_per_image * nloc
     macs_launch = pairs_rank * mac_pair  # algorithmic MACs per rank-step
     macs_direct = pairs_rank * cfg.b * cfg.b * cfg.C
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    tf32x3_peak = 0.5 * peaks["bf16_tflops"] / 3.0  # tf32 = 1/2 bf16 (guide ratio, tools/tc_peaks.cu), 3 MMAs per MAC
     if info["kernel"] == 1:
         peak = 2.0 * peaks["bf16_tflops"]  # int8 tcgen05 = 2x the measured bf16 (guide's nominal ratio)
         bound, unit, peak_note = "tensor", "TOP/s", "int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json x guide ratio)"
+    elif info["kernel"] == 5:
+        peak = tf32x3_peak
+        bound, unit, peak_note = "tensor", "TFLOP/s", ("3xTF32: tf32 dense = 1/2 x measured bf16 burst (MEASURED_PEAKS.json x "
+                                                       "guide ratio, confirmed by tools/tc_peaks.cu) / 3 MMAs per product")
     elif cfg.dtype == "u8":
         # dp4a: 64 lanes/SM/clk (half rate, measured by tools/peaks.cu) x 4 MACs x 2 ops
         peak = 148 * 64 * 4 * 2 * sm_mhz * 1e6 / 1e12
@@ -608,9 +614,13 @@ def main():
     achieved = 2.0 * macs_launch / (match_ms / 1e3) / 1e12 if match_ms > 0 else None
     traffic, traffic_src = None, None
     kname = {0: "bm_lanes_kernel", 1: "bm_tc_i8_kernel", 2: "bm_simt_kernel", 3: "bm_box_kernel",
-             4: "bm_boxf_kernel"}[info["kernel"]]
-    prof = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{kname.replace('_kernel', '')}_{cfg.name}_metrics.json")
-    if os.path.exists(prof):
+             4: "bm_boxf_kernel", 5: "bm_tcf_kernel"}[info["kernel"]]
+    # the ncu capture of THIS kernel, config, metric and temporal mode (newest round first)
+    tag = f"{kname.replace('_kernel', '')}{'_ncc' if args.metric == 'ncc' else ''}_{cfg.name}" + \
+        (f"_t{args.temporal}" if args.temporal else "")
+    prof = next((c for c in (os.path.join(ROOT, "profiles", r, f"ncu_full_{tag}_metrics.json")
+                             for r in ("r02", "r01", os.path.join("r01", "next"))) if os.path.exists(c)), "")
+    if prof:
         m = json.load(open(prof))
         mb = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
         traffic = sum(float(m[k]["value"]) * mb.get(m[k]["unit"], 1.0) for k in
@@ -635,6 +645,10 @@ def main():
     t_mac, t_hbm = macs_direct / mac_peak, io_bytes / (peaks["hbm_gbs"] * 1e9)
     roof["north_star"] = {"t_roof_ms": 1e3 * max(t_mac, t_hbm), "t_mac_ms": 1e3 * t_mac, "t_hbm_ms": 1e3 * t_hbm,
                           "mac_unit": mac_unit, "frac": (1e3 * max(t_mac, t_hbm)) / ms if ms > 0 else None}
+    if cfg.dtype != "u8":  # the best-available float unit too, so the unit choice cannot inflate the number
+        t_best = max(macs_direct / (tf32x3_peak * 1e12 / 2.0), t_hbm)
+        roof["north_star"]["best_unit"] = {"unit": "3xTF32 tcgen05 (tf32 = 1/2 measured bf16, / 3)",
+                                           "t_roof_ms": 1e3 * t_best, "frac": 1e3 * t_best / ms if ms > 0 else None}
 
     # end-to-end through the public API with host buffers (pinned), copies inside the timing
     e2e = None

@@ -101,6 +101,7 @@ typedef struct {
 #define SC_KERNEL_SIMT_WARP 2  /* CUDA-core matcher, one warp per reference (lanes = candidates) */
 #define SC_KERNEL_BOX 3        /* box-sum matcher: 4x4 block sums of the shifted product image
                                   (u8, b = 8, stride 4, C = 1, K <= 32; default where supported) */
+#define SC_KERNEL_TC_F32 5     /* tcgen05 3xTF32 cross term (TMEM) + fused top-K (f32, C = 1, b <= 8) */
 #define SC_KERNEL_BOXF 4       /* float box-sum matcher (f32, C = 1, (stride, b) in {(3,8), (1,7),
                                   (4,8), (2,8)}, K + m <= 80; default where supported) */
 

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SCBM_LIB") or os.path.join(_HERE, "libscbm.so")  # SCBM_LIB: tuning builds
 
 SC_DTYPE_U8, SC_DTYPE_F32 = 0, 1
-SC_KERNEL_SIMT, SC_KERNEL_TC_I8, SC_KERNEL_SIMT_WARP, SC_KERNEL_BOX, SC_KERNEL_BOXF = 0, 1, 2, 3, 4
+SC_KERNEL_SIMT, SC_KERNEL_TC_I8, SC_KERNEL_SIMT_WARP, SC_KERNEL_BOX, SC_KERNEL_BOXF, SC_KERNEL_TC_F32 = 0, 1, 2, 3, 4, 5
 STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_UNSUPPORTED",
           3: "SC_ERR_OUT_OF_MEMORY", 4: "SC_ERR_CUDA", 5: "SC_ERR_WRONG_DEVICE"}
 

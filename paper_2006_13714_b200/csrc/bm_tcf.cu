@@ -1,0 +1,586 @@
+// bm_tcf.cu -- the tensor-core float matcher (SC_KERNEL_TC_F32): f32 images, one channel, patch
+// side b <= 8, any reference stride: steps a0, a2-a6 fused in one kernel, a1 from the norm map.
+//
+// a2 (the Self-Convolution cross term, Eq. 5) runs on the 5th-generation tensor
+// cores as a 3xTF32 GEMM  D[ref][cand] = sum_k A[ref][k] B[cand][k]  with fp32 accumulation in TMEM:
+// every operand is split x = hi + lo (hi = x with the 13 low mantissa bits cleared, exactly
+// representable in tf32; lo = x - hi, exact in fp32) and D = A_hi B_hi + A_hi B_lo + A_lo B_hi, which
+// keeps the products to ~2^-21 relative (fp32-class; bf16x3 would not meet the 1e-5 rule).
+//   * A (M = 128 references of an 8 x 16 reference block; TMEM lane quadrant q = a 4 x 8 sub-block)
+//     is K-major in shared memory: per reference the centred patch x' = x - 0.5 as K = 8 b floats,
+//     k = 8 u + v (patch row u, column v; v >= b is zero), in canonical 8-row x 16-byte core matrices.
+//   * B (N = 128 candidates: an 8-row x 16-column block of candidate top-left positions) is K-major
+//     straight out of a "shift-expanded" tile E[y][jg][kc][j][t] = x'(cy0 + y, cx0 + 8 jg + j + 4 kc + t):
+//     an 8-candidate group (8 consecutive columns jg of candidate row i) x 16 B of K (4 shifts v)
+//     is one canonical core matrix, the K-group of patch row u of candidate row i is tile row i + u,
+//     so ONE descriptor per patch row (start + 512 u, LBO = 128, SBO = 256) addresses the whole block --
+//     no im2col; the tile is 8 + b - 1 rows x 512 B per copy (hi, lo). (MN-major B, which would need
+//     no shifted copies along K, does not work for kind::tf32: tools/tf32_layout_test.cu.)
+//   * per candidate tile, 3 b MMAs (tcgen05.mma.cta_group::1.kind::tf32, K = 8) into one of two
+//     128 x 128 fp32 TMEM accumulators (double-buffered: the MMAs of tile t+1 overlap the epilogue
+//     of tile t), issued by one thread, committed to mbarriers; three producer warps stage the E
+//     tiles of a 3-slot ring from the CTA's staged image region.
+// Epilogue (4 warps, one per TMEM lane quadrant; lane = reference, its list stays in registers or
+// in its shared-memory heap for the whole kernel): tcgen05.ld 32 columns (two candidate rows),
+// d' = n_c - 2 C (Lemma 2; n_c from the fp64-SAT norm map), slack = thr - d',
+// sign bits packed into a fail mask (one SHF per pair), the window mask, and the u8 box kernel's
+// branch-free survivor rounds into the reference's top-(K+m) of 32-bit keys (a4, Theorem 1,
+// PAPER.md:322-330). Tiles are visited by distance to the block (thresholds tighten early); a warp
+// skips tiles / candidate rows outside its quadrant's window union. a5 + a6 as in the float box
+// kernel: the kept keys re-scored by direct differences, sorted, written; references whose kept
+// keys cannot decide the K-th go to the exact fix-up (fixup.cu).
+#include <algorithm>
+
+#include "regtopk.cuh"
+#include "sc_internal.h"
+#include "sm100.cuh"
+#include "topk.cuh"
+
+namespace scbm {
+namespace {
+
+constexpr int kTfEpi = 4;                       // epilogue warps = TMEM lane quadrants
+constexpr int kTfProd = 3;                      // E-tile producer warps
+constexpr int kTfWarps = kTfEpi + kTfProd + 1;  // + the MMA warp
+constexpr int kTfThreads = kTfWarps * 32;
+constexpr int kRBY = 8, kRBX = 16;  // reference block (M = 128)
+constexpr int kTR = 8, kTC = 16;    // candidate tile (N = 128)
+constexpr int kES = 3;              // E ring slots
+constexpr int kScrPitch = 36;       // epilogue scratch words per lane (32 staged + pad; 16-B rows)
+constexpr float kTcfErr = 2e-5f;    // bound on the 3xTF32 identity's error, relative to n_r + d
+
+struct TcfArgs {
+  const float* imgs;   // [F][H][W]
+  const float* norm;   // norm map interior of frame 0 (centred, fp32), pitch Mx, frame stride nfs
+  int32_t* idx_out;    // [F][band refs][K]
+  float* dist_out;
+  float* dense;        // debug: every window distance [refs][Wn^2] (nullptr: block matching)
+  int H, W, s, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
+  int Mx;
+  long long nfs;
+  int rb;              // window-relative index bits of the 32-bit keys (rel + 1, 0 = sentinel)
+  int RH, RWp;         // staged region rows / row pitch (floats)
+  uint32_t off_raw, off_A, off_E, off_heap, off_scr, off_order, off_nc;
+  int hp;              // heap pitch (words per reference)
+  int scr;             // epilogue scratch words per warp
+  int* fix_count;
+  int* fix_list;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
+
+template <int BK, int KR, bool DENSE>
+__global__ void __launch_bounds__(kTfThreads, 1) bm_tcf_kernel(TcfArgs a) {
+  constexpr bool HEAP = KR > 48;
+  constexpr int ER = kTR + BK - 1;                  // E tile rows
+  constexpr uint32_t kEBytes = uint32_t(ER) * 512;  // one copy (hi or lo) of an E tile
+  constexpr uint32_t kAGroup = 2 * BK * 128;        // bytes per 8-reference group of A (K = 8 b floats)
+  constexpr uint32_t kIdesc = sm100::idesc_tf32(128, 128, /*a_mn=*/false, /*b_mn=*/false);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int f = blockIdx.y;
+  const int by = blockIdx.x / a.tiles_x, bx = blockIdx.x - by * a.tiles_x;
+  const int iy_first = a.iy_begin + by * kRBY;
+  const int iy_last = min(a.iy_end, iy_first + kRBY) - 1;
+  const int ix_first = bx * kRBX;
+  const int ix_last = min(a.nx, ix_first + kRBX) - 1;
+  const int s = a.s, H = a.H, W = a.W;
+  const int cyA = max(0, iy_first * s + a.lo), cyB = min(H - BK, iy_last * s + a.hi);
+  // (tile columns start at a multiple of 4: the norm-map loads are 16-byte vectors)
+  const int cxA = max(0, ix_first * s + a.lo) & ~3, cxB = min(W - BK, ix_last * s + a.hi);
+  const int NTI = (cyB - cyA) / kTR + 1;  // candidate tile rows / columns of the block's window union
+  const int NTC = (cxB - cxA) / kTC + 1;
+  const int ntiles = NTI * NTC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar_full = sbase, bar_empty = sbase + 16, bar_ef = sbase + 32, bar_ee = sbase + 56;
+  const uint32_t tmem_slot = sbase + 80, bar_nc = sbase + 96;  // bar_nc[2]: the tile's candidate norms staged
+  float* raw = reinterpret_cast<float*>(smem + a.off_raw);
+  const uint32_t sA = sbase + a.off_A, sE = sbase + a.off_E;
+  const uint32_t aLo = uint32_t(kRBY * kRBX / 8) * kAGroup;  // A_lo follows A_hi
+
+  if (warp == kTfWarps - 1) {
+    sm100::tmem_alloc(tmem_slot, 256);
+    sm100::tmem_relinquish();
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(bar_full + 8 * i, 1);
+      sm100::mbar_init(bar_empty + 8 * i, kTfEpi);
+    }
+    for (int i = 0; i < kES; ++i) {
+      sm100::mbar_init(bar_ef + 8 * i, kTfProd * 32);
+      sm100::mbar_init(bar_ee + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) sm100::mbar_init(bar_nc + 8 * i, 32);
+    sm100::fence_barrier_init();
+  }
+
+  // ---- the block's image region as stored (0 outside the image): the A / E staging centres it
+  // (a0: x' = x - 0.5), the a5 re-score reads the raw values
+  const float* img = a.imgs + size_t(f) * H * W;
+  const int RH = NTI * kTR + BK - 1, RW = NTC * kTC + 7;
+  for (int e = threadIdx.x; e < RH * RW; e += kTfThreads) {
+    const int r = e / RW, c = e - r * RW;
+    const int y = cyA + r, x = cxA + c;
+    raw[r * a.RWp + c] = (y < H && x < W) ? __ldg(img + size_t(y) * W + x) : 0.5f;
+  }
+  __syncthreads();
+  // A: reference m = 32 q + l -> (iy_first + 4 (q >> 1) + l / 8, ix_first + 8 (q & 1) + l % 8)
+  for (int e = threadIdx.x; e < 128 * 2 * BK; e += kTfThreads) {
+    const int m = e / (2 * BK), kc = e - m * (2 * BK);
+    const int q = m >> 5, l = m & 31;
+    const int iy = iy_first + 4 * (q >> 1) + (l >> 3), ix = ix_first + 8 * (q & 1) + (l & 7);
+    const int u = kc >> 1, v0 = 4 * (kc & 1);
+    uint4 hi = make_uint4(0, 0, 0, 0), lo = make_uint4(0, 0, 0, 0);
+    if (iy <= iy_last && ix <= ix_last) {
+      const float* src = raw + (iy * s - cyA + u) * a.RWp + (ix * s - cxA) + v0;
+      uint32_t h[4], o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float x = (v0 + t < BK) ? src[t] - 0.5f : 0.f;
+        h[t] = tf32_hi(x);
+        o[t] = __float_as_uint(x - __uint_as_float(h[t]));
+      }
+      hi = make_uint4(h[0], h[1], h[2], h[3]);
+      lo = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    const uint32_t off = uint32_t(m >> 3) * kAGroup + uint32_t(kc) * 128 + uint32_t(m & 7) * 16;
+    *reinterpret_cast<uint4*>(smem + a.off_A + off) = hi;
+    *reinterpret_cast<uint4*>(smem + a.off_A + aLo + off) = lo;
+  }
+  // tile order: by L1 gap to the reference block's rectangle (every reference meets its own
+  // neighbourhood first), ties by index
+  int16_t* order = reinterpret_cast<int16_t*>(smem + a.off_order);
+  {
+    const int ry0 = iy_first * s, ry1 = iy_last * s, rx0 = ix_first * s, rx1 = ix_last * s;
+    auto dist_of = [&](int t) {
+      const int tr = t / NTC, tc = t - (t / NTC) * NTC;
+      const int y0 = cyA + kTR * tr, y1 = y0 + kTR - 1, x0 = cxA + kTC * tc, x1 = x0 + kTC - 1;
+      return max(0, max(ry0 - y1, y0 - ry1)) + max(0, max(rx0 - x1, x0 - rx1));
+    };
+    for (int t = threadIdx.x; t < ntiles; t += kTfThreads) {
+      const int dt = dist_of(t);
+      int rank = 0;
+      for (int u = 0; u < ntiles; ++u) {
+        const int du = dist_of(u);
+        rank += (du < dt || (du == dt && u < t)) ? 1 : 0;
+      }
+      order[rank] = int16_t(t);
+    }
+  }
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + 80);
+
+  if (warp == kTfWarps - 1) {
+    // ---------------- MMA issuer (one elected thread) + norm producer (all 32 lanes): once the
+    // TMEM buffer of tile t is free, the warp stages the tile's 8 x 16 candidate norms (a1, from the
+    // L2-resident norm map) into ring slot t & 1 and arrives on bar_nc[slot]; lane 0 issues the MMAs
+    float* ncring = reinterpret_cast<float*>(smem + a.off_nc);  // [2][8][16]
+    const float* nsrc = a.norm + size_t(f) * a.nfs;
+    for (int t = 0; t < ntiles; ++t) {
+      const int sl = t % kES, buf = t & 1;
+      if (t >= 2) sm100::mbar_wait_sleep(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1), 32);
+      {
+        const int ot = order[t];
+        const int tr = ot / NTC, tc = ot - tr * NTC;
+        const int rr = lane >> 2, cq = lane & 3;
+        const int cy = min(cyA + kTR * tr + rr, H - BK);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(nsrc + size_t(cy) * a.Mx + cxA + kTC * tc) + cq);
+        reinterpret_cast<float4*>(ncring + (buf * kTR + rr) * kTC)[cq] = v;
+        sm100::mbar_arrive(bar_nc + 8 * buf);
+      }
+      if (lane == 0) {
+        sm100::mbar_wait_sleep(bar_ef + 8 * sl, uint32_t((t / kES) & 1), 32);
+        sm100::tc_fence_after();
+        const uint32_t eh = sE + uint32_t(sl) * 2 * kEBytes, el = eh + kEBytes;
+#pragma unroll 1
+        for (int u = 0; u < BK; ++u) {
+          const uint64_t ah = sm100::smem_desc(sA + 256u * u, 128u, kAGroup);
+          const uint64_t al = sm100::smem_desc(sA + aLo + 256u * u, 128u, kAGroup);
+          const uint64_t bh = sm100::smem_desc(eh + 512u * u, 128u, 256u);
+          const uint64_t bl = sm100::smem_desc(el + 512u * u, 128u, 256u);
+          const uint32_t d = tmem + 128u * buf;
+          sm100::mma_tf32(d, ah, bh, kIdesc, u > 0);
+          sm100::mma_tf32(d, ah, bl, kIdesc, 1);
+          sm100::mma_tf32(d, al, bh, kIdesc, 1);
+        }
+        sm100::mma_commit(bar_full + 8 * buf);
+        sm100::mma_commit(bar_ee + 8 * sl);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= kTfEpi) {
+    // ---------------- E-tile producers: E[y][jg][kc][j][t] = x'(cy0 + y, cx0 + 8 jg + j + 4 kc + t), hi and lo
+    const int pt = threadIdx.x - kTfEpi * 32;
+    for (int t = 0; t < ntiles; ++t) {
+      const int sl = t % kES;
+      if (t >= kES) sm100::mbar_wait_sleep(bar_ee + 8 * sl, uint32_t(((t / kES) - 1) & 1), 64);
+      const int ot = order[t];
+      const int tr = ot / NTC, tc = ot - tr * NTC;
+      const float* src0 = raw + (kTR * tr) * a.RWp + kTC * tc;
+      uint8_t* eh = smem + a.off_E + size_t(sl) * 2 * kEBytes;
+      for (int e = pt; e < ER * 32; e += kTfProd * 32) {
+        const int y = e >> 5, jg = (e >> 4) & 1, kc = (e >> 3) & 1, j = e & 7;
+        const float* sp = src0 + y * a.RWp + 8 * jg + j + 4 * kc;
+        uint32_t h[4], o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float x = sp[q] - 0.5f;
+          h[q] = tf32_hi(x);
+          o[q] = __float_as_uint(x - __uint_as_float(h[q]));
+        }
+        *reinterpret_cast<uint4*>(eh + e * 16) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(eh + kEBytes + e * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      sm100::fence_proxy_async_smem();
+      sm100::mbar_arrive(bar_ef + 8 * sl);
+    }
+  } else {
+    // ---------------- epilogue: warp q = TMEM lanes 32q..32q+31 = references of a 4 x 8 sub-block
+    const int q = warp;
+    const int wiy0 = iy_first + 4 * (q >> 1), wix0 = ix_first + 8 * (q & 1);
+    const int iy = wiy0 + (lane >> 3), ix = wix0 + (lane & 7);
+    const bool valid = iy <= iy_last && ix <= ix_last;
+    const bool wvalid = wiy0 <= iy_last && wix0 <= ix_last;
+    const int wiy1 = min(iy_last, wiy0 + 3), wix1 = min(ix_last, wix0 + 7);
+    const int wy_lo = wiy0 * s + a.lo, wy_hi = wiy1 * s + a.hi;  // the quadrant's window union
+    const int wx_lo = wix0 * s + a.lo, wx_hi = wix1 * s + a.hi;
+    const int ry = iy * s, rx = ix * s;
+    const float nr = valid ? __ldg(a.norm + size_t(f) * a.nfs + size_t(ry) * a.Mx + rx) : 0.f;  // ||X_i||^2 (centred)
+    const int rb = a.rb;
+    const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
+    const size_t ref_band = size_t(iy - a.iy_begin) * a.nx + ix;
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + a.off_scr) + warp * a.scr;
+    RegTopK32<HEAP ? 1 : KR> rt;
+    if constexpr (!HEAP) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
+    }
+    uint32_t* heap = reinterpret_cast<uint32_t*>(smem + a.off_heap) + (warp * 32 + lane) * a.hp;
+    if constexpr (HEAP) {
+      for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
+      heap[a.KP + 1] = 0u;  // padding child: never the larger one
+    }
+    if constexpr (DENSE) {
+      if (valid)
+        for (int k = 0; k < a.Wn * a.Wn; ++k) a.dense[ref_band * a.Wn * a.Wn + k] = -1.f;
+    }
+    float thr = __int_as_float(0x7f800000);  // largest d' that may still enter the top-KP
+    const uint32_t tq = tmem + (uint32_t(32 * q) << 16);
+    const uint32_t sc_s = smem_u32(scratch + lane * kScrPitch);
+
+    for (int t = 0; t < ntiles; ++t) {
+      const int buf = t & 1;
+      sm100::mbar_wait(bar_full + 8 * buf, uint32_t((t >> 1) & 1));
+      sm100::mbar_wait(bar_nc + 8 * buf, uint32_t((t >> 1) & 1));
+      sm100::tc_fence_after();
+      const float4* ncr = reinterpret_cast<const float4*>(smem + a.off_nc) + buf * kTR * 4;
+      const int ot = order[t];
+      const int tr = ot / NTC, tc = ot - tr * NTC;
+      const int cy0 = cyA + kTR * tr, cx0 = cxA + kTC * tc;
+      const bool xrel = wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo;
+      if (xrel) {
+        // this lane's window columns inside the tile (a 16-bit mask), the same for every row
+        const int jlo = max(0, max(0, rx + a.lo) - cx0), jhi = min(15, min(W - BK, rx + a.hi) - cx0);
+        const uint32_t cols = (valid && jhi >= jlo) ? (((2u << jhi) - 1u) & ~((1u << jlo) - 1u)) : 0u;
+#pragma unroll 1
+        for (int i2 = 0; i2 < kTR; i2 += 2) {
+          const int cyp = cy0 + i2;
+          const bool r0 = cyp >= wy_lo && cyp <= wy_hi && cyp <= cyB;
+          const bool r1 = cyp + 1 >= wy_lo && cyp + 1 <= wy_hi && cyp + 1 <= cyB;
+          if (!r0 && !r1) continue;  // warp-uniform
+          uint32_t cv[32];
+          sm100::tmem_ld32(tq + 128u * buf + 16u * i2, cv);
+          // candidate norms of the two rows (staged by the MMA warp; rows past the map are masked below)
+          float4 nq[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) nq[v] = ncr[i2 * 4 + v];
+          sm100::tmem_wait_ld();
+          const uint32_t m0 = (r0 && cyp - ry >= a.lo && cyp - ry <= a.hi) ? cols : 0u;
+          const uint32_t m1 = (r1 && cyp + 1 - ry >= a.lo && cyp + 1 - ry <= a.hi) ? cols : 0u;
+          const uint32_t wmask = m0 | (m1 << 16);
+          float dp[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float4 n4 = nq[j >> 2];
+            const float nc = (j & 3) == 0 ? n4.x : (j & 3) == 1 ? n4.y : (j & 3) == 2 ? n4.z : n4.w;
+            dp[j] = fmaf(-2.f, __uint_as_float(cv[j]), nc);  // d' = n_c - 2 C
+          }
+          if constexpr (DENSE) {
+            const int rel0 = (cyp - ry - a.lo) * a.Wn + (cx0 - rx - a.lo);
+            float* drow = a.dense + ref_band * a.Wn * a.Wn;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if ((wmask >> j) & 1u) drow[rel0 + (j >> 4) * a.Wn + (j & 15)] = dp[j] + nr;
+            continue;
+          }
+          uint32_t fails = 0u;
+#pragma unroll
+          for (int j = 31; j >= 0; --j) fails = __funnelshift_l(__float_as_uint(thr - dp[j]), fails, 1);
+          uint32_t bits = ~fails & wmask;
+          if (!__any_sync(0xffffffffu, bits != 0u)) continue;
+          // stage the distances d = d' + ||X_i||^2 (>= 0) of the two rows, then insert one survivor per
+          // lane per round (branch-free; lanes without one insert the no-op key ~0)
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 o = make_float4(fmaxf(dp[j] + nr, 0.f), fmaxf(dp[j + 1] + nr, 0.f),
+                                         fmaxf(dp[j + 2] + nr, 0.f), fmaxf(dp[j + 3] + nr, 0.f));
+            *reinterpret_cast<float4*>(scratch + lane * kScrPitch + j) = o;
+          }
+          __syncwarp();
+          const int rel1b = (cyp - ry - a.lo) * a.Wn + (cx0 - rx - a.lo) + 1;
+          while (__any_sync(0xffffffffu, bits != 0u)) {
+            const int i = 31 - __clz(bits | 1u);
+            uint32_t d;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sc_s + 4u * uint32_t(i)));
+            const uint32_t qd = d >> (rb - 1);
+            const int rel1 = rel1b + (i >> 4) * a.Wn + (i & 15);
+            const uint32_t key = bits ? (qd << rb) | uint32_t(rel1) : 0xffffffffu;
+            bits &= ~(1u << i);
+            if constexpr (HEAP) {
+              if (key < heap[1]) {  // replace the root, sift down (children of h: 2h, 2h+1)
+                int h = 1;
+                for (int c = 2; c <= a.KP; c = 2 * h) {
+                  const uint2 vv = *reinterpret_cast<const uint2*>(heap + c);
+                  const int cb = vv.y > vv.x ? c + 1 : c;
+                  const uint32_t big = max(vv.x, vv.y);
+                  if (big <= key) break;
+                  heap[h] = big;
+                  h = cb;
+                }
+                heap[h] = key;
+              }
+            } else {
+              rt.insert(key);
+            }
+          }
+          const uint32_t kth = HEAP ? heap[1] : rt.r[KR - 1];
+          if (kth != 0xffffffffu) {
+            // largest distance whose key can still tie the KP-th key, plus a rounding margin
+            const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
+            thr = fmaf(dmax, 1.0f + 1e-6f, -nr) + 1e-30f;
+          }
+          __syncwarp();
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(bar_empty + 8 * buf);
+    }
+
+    if constexpr (!DENSE) {  // hand the reference norms and register lists to the a5 stage
+      float* nrs = reinterpret_cast<float*>(smem + a.off_E);
+      uint32_t* lists = reinterpret_cast<uint32_t*>(smem + a.off_E) + 128;
+      nrs[32 * warp + lane] = nr;
+      if constexpr (!HEAP) {
+#pragma unroll
+        for (int k = 0; k < KR; ++k) lists[(32 * warp + lane) * (KR + 1) + k] = rt.r[k];
+      }
+    }
+  }
+
+  if constexpr (!DENSE) {
+    // ---- a5 + a6, all warps: per reference (one warp each), the KP kept keys re-scored by direct
+    // differences from the staged region (the input values as stored), sorted by (distance, idx),
+    // K written; references whose kept keys cannot decide the K-th go to the exact fix-up.
+    __syncthreads();  // every tile's MMAs and epilogue are done: the E ring holds the handed-over lists
+    const float* nrs = reinterpret_cast<const float*>(smem + a.off_E);
+    const uint32_t* lists = reinterpret_cast<const uint32_t*>(smem + a.off_E) + 128;
+    const uint32_t* heaps = reinterpret_cast<const uint32_t*>(smem + a.off_heap);
+    const int rb = a.rb;
+    const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
+    constexpr int NJ = (KR + 31) / 32;
+    for (int m = warp; m < 128; m += kTfWarps) {
+      const int q = m >> 5, l = m & 31;
+      const int iyj = iy_first + 4 * (q >> 1) + (l >> 3), ixj = ix_first + 8 * (q & 1) + (l & 7);
+      if (iyj > iy_last || ixj > ix_last) continue;  // warp-uniform
+      const int ryj = iyj * s, rxj = ixj * s;
+      const size_t row = size_t(f) * band_refs + size_t(iyj - a.iy_begin) * a.nx + ixj;
+      const float* pr = raw + (ryj - cyA) * a.RWp + (rxj - cxA);
+      WarpTopK<NJ> top;
+      top.init();
+#pragma unroll
+      for (int sl = 0; sl < NJ; ++sl) {
+        const int k = sl * 32 + lane;
+        uint64_t key = kKeyInf;
+        uint32_t kk;
+        if constexpr (HEAP) kk = k < a.KP ? heaps[m * a.hp + 1 + k] : 0xffffffffu;
+        else kk = k < KR ? lists[m * (KR + 1) + k] : 0xffffffffu;
+        if (kk != 0u && kk != 0xffffffffu) {
+          const int rel = int(kk & ((1u << rb) - 1u)) - 1;
+          const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+          const int cy = ryj + dyy + a.lo, cx = rxj + dxx + a.lo;
+          const float* pc = raw + (cy - cyA) * a.RWp + (cx - cxA);
+          float d = 0.f;
+#pragma unroll
+          for (int r = 0; r < BK; ++r)
+#pragma unroll
+            for (int c = 0; c < BK; ++c) {
+              const float df = pr[r * a.RWp + c] - pc[r * a.RWp + c];
+              d = fmaf(df, df, d);
+            }
+          key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * W + cx);
+        }
+        top.merge(key, lane);
+      }
+      {  // worst kept key vs the exact K-th distance: the filter's error could hide a candidate
+        uint64_t kv = kKeyInf;
+#pragma unroll
+        for (int sl = 0; sl < NJ; ++sl)
+          if (sl == (a.K - 1) / 32) kv = top.v[sl];
+        kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
+        const float nrj = nrs[m];
+        const uint32_t klast = HEAP ? heaps[m * a.hp + 1] : lists[m * (KR + 1) + KR - 1];  // heap root / last
+        if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf) {
+          const float dK = __uint_as_float(uint32_t(kv >> 32));
+          const float smin = __uint_as_float((klast >> rb) << (rb - 1));
+          if (smin <= fmaf(dK, 1.0f + 1e-5f, kTcfErr * (nrj + dK))) {
+            const int pos = atomicAdd(a.fix_count, 1);
+            a.fix_list[pos] = int(row);
+          }
+        }
+      }
+#pragma unroll
+      for (int sl = 0; sl < NJ; ++sl) {
+        const int k = sl * 32 + lane;
+        if (k < a.K) {
+          const uint64_t key = top.v[sl];
+          const bool none = key == kKeyInf;
+          a.idx_out[row * a.K + k] = none ? -1 : int32_t(uint32_t(key));
+          a.dist_out[row * a.K + k] = none ? __int_as_float(0x7f800000) : __uint_as_float(uint32_t(key >> 32));
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == kTfWarps - 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, 256);
+  }
+}
+
+struct TcfLayout {
+  int RHmax, RWp, NTImax, NTCmax, hp, scr;
+  uint32_t off_order, off_raw, off_A, off_E, off_heap, off_scr, off_nc, bytes;
+};
+
+int tcf_kr(const Geometry& g) {
+  return g.KP <= 24 ? 24 : g.KP <= 32 ? 32 : g.KP <= 40 ? 40 : g.KP <= 48 ? 48 : g.KP <= 80 ? 80 : 0;
+}
+
+int tcf_rel_bits(int Wn) {  // bits of rel + 1 (values 1 .. Wn^2; 0 = sentinel)
+  int rb = 1;
+  while ((1 << rb) <= Wn * Wn) ++rb;
+  return rb;
+}
+
+TcfLayout tcf_layout(const Geometry& g) {
+  TcfLayout L{};
+  const int kr = tcf_kr(g);
+  L.NTImax = ((kRBY - 1) * g.s + g.Wn - 1) / kTR + 1;
+  L.NTCmax = ((kRBX - 1) * g.s + g.Wn - 1 + 3) / kTC + 1;  // + the alignment of cxA
+  L.RHmax = L.NTImax * kTR + g.b - 1;
+  L.RWp = L.NTCmax * kTC + 7 + 1;
+  L.hp = ((g.KP + 2 + 1) & ~3) + 2;  // = 2 (mod 4): 8-byte aligned rows, spread bank pairs
+  L.scr = std::max(32 * kScrPitch, kr > 48 ? 0 : 32 * (kr + 1));
+  uint32_t off = 128;  // barriers + TMEM slot
+  L.off_order = off;
+  off += uint32_t(L.NTImax * L.NTCmax) * 2;
+  off = (off + 15) & ~15u;
+  L.off_raw = off;
+  off += uint32_t(L.RHmax * L.RWp) * 4;
+  off = (off + 1023) & ~1023u;
+  L.off_A = off;
+  off += 2u * 16u * uint32_t(2 * g.b * 128);  // A_hi, A_lo
+  L.off_E = off;  // the E ring; after the last tile the a5 stage's norms + register lists
+  off += std::max(uint32_t(kES) * 2u * uint32_t(kTR + g.b - 1) * 512u, uint32_t(128 + 128 * (kr + 1)) * 4u);
+  L.off_nc = off;  // candidate-norm ring [2][8][16]
+  off += 2u * kTR * kTC * 4u;
+  L.off_heap = off;
+  if (kr > 48) off += 128u * uint32_t(L.hp) * 4u;
+  L.off_scr = off;
+  off += uint32_t(kTfEpi * L.scr) * 4u;
+  L.bytes = off;
+  return L;
+}
+
+template <int BK, int KR, bool DENSE>
+cudaError_t launch_tcf_t(const TcfArgs& a, int F, size_t smem, cudaStream_t st) {
+  const int tiles_y = (a.iy_end - a.iy_begin + kRBY - 1) / kRBY;
+  auto k = bm_tcf_kernel<BK, KR, DENSE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k<<<dim3(a.tiles_x * tiles_y, F), kTfThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tcf_supported(const Geometry& g) {
+  if (g.dtype != SC_DTYPE_F32 || g.metric != SC_METRIC_L2 || g.C != 1) return false;
+  if (g.b < 1 || g.b > 8 || tcf_kr(g) == 0) return false;
+  if (tcf_rel_bits(g.Wn) > 12) return false;  // keeps >= 20 distance bits in the 32-bit keys
+  if (g.W - g.b + 1 < 16 && g.W < 24) return false;  // (tiles read 16 norm columns; tiny widths use others)
+  return tcf_layout(g).bytes <= 227 * 1024;
+}
+
+cudaError_t launch_bm_tcf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                          int32_t* idx_out, void* dist_out, void* dense, cudaStream_t st, int64_t* launches) {
+  const Geometry& g = p.g;
+  const TcfLayout L = tcf_layout(g);
+  TcfArgs a{};
+  a.imgs = static_cast<const float*>(imgs);
+  a.norm = static_cast<const float*>(p.ws.norm);
+  a.idx_out = idx_out;
+  a.dist_out = static_cast<float*>(dist_out);
+  a.dense = static_cast<float*>(dense);
+  a.H = g.H; a.W = g.W; a.s = g.s; a.Wn = g.Wn; a.K = g.K; a.KP = g.KP; a.lo = g.lo; a.hi = g.hi; a.nx = g.nx;
+  a.iy_begin = iy_begin; a.iy_end = iy_end;
+  a.tiles_x = (g.nx + kRBX - 1) / kRBX;
+  a.Mx = g.Mxp;
+  a.nfs = g.NFS;
+  a.rb = tcf_rel_bits(g.Wn);
+  a.RH = L.RHmax; a.RWp = L.RWp;
+  a.off_raw = L.off_raw; a.off_A = L.off_A; a.off_E = L.off_E; a.off_heap = L.off_heap; a.off_scr = L.off_scr;
+  a.off_order = L.off_order;
+  a.off_nc = L.off_nc;
+  a.hp = L.hp;
+  a.scr = L.scr;
+  a.fix_count = p.ws.fix_count;
+  a.fix_list = p.ws.fix_list;
+  const int kr = tcf_kr(g);
+  cudaError_t e = cudaSuccess;
+  if (!dense) e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  if (launches) *launches += 1;
+#define SCBM_TCF_B(B_)                                                                 \
+  if (g.b == B_) {                                                                     \
+    if (dense) return launch_tcf_t<B_, 24, true>(a, F, L.bytes, st);                   \
+    if (kr == 24) e = launch_tcf_t<B_, 24, false>(a, F, L.bytes, st);                  \
+    else if (kr == 32) e = launch_tcf_t<B_, 32, false>(a, F, L.bytes, st);             \
+    else if (kr == 40) e = launch_tcf_t<B_, 40, false>(a, F, L.bytes, st);             \
+    else if (kr == 48) e = launch_tcf_t<B_, 48, false>(a, F, L.bytes, st);             \
+    else e = launch_tcf_t<B_, 80, false>(a, F, L.bytes, st);                           \
+  }
+  SCBM_TCF_B(8)
+  else SCBM_TCF_B(7)
+  else SCBM_TCF_B(6)
+  else SCBM_TCF_B(5)
+  else SCBM_TCF_B(4)
+  else SCBM_TCF_B(3)
+  else SCBM_TCF_B(2)
+  else SCBM_TCF_B(1)
+#undef SCBM_TCF_B
+  if (e != cudaSuccess) return e;
+  if (launches) *launches += 1;
+  return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
+}
+
+}  // namespace scbm

@@ -115,6 +115,8 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, nullptr, st, &p->launches);
     else if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
       e = launch_bm_tc(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
+    else if (p->kernel == SC_KERNEL_TC_F32)
+      e = launch_bm_tcf(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
     else if (p->kernel == SC_KERNEL_BOX && dense == nullptr)
       e = launch_bm_box(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_BOXF && dense == nullptr)
@@ -504,8 +506,9 @@ sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_BOX && !box_supported(p->g)) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_BOXF && !boxf_supported(p->g)) return SC_ERR_UNSUPPORTED;
+  if (kernel == SC_KERNEL_TC_F32 && !tcf_supported(p->g)) return SC_ERR_UNSUPPORTED;
   if (kernel != SC_KERNEL_SIMT && kernel != SC_KERNEL_SIMT_WARP && kernel != SC_KERNEL_TC_I8 &&
-      kernel != SC_KERNEL_BOX && kernel != SC_KERNEL_BOXF)
+      kernel != SC_KERNEL_BOX && kernel != SC_KERNEL_BOXF && kernel != SC_KERNEL_TC_F32)
     return SC_ERR_UNSUPPORTED;
   p->kernel = kernel;
   return SC_OK;

@@ -115,6 +115,12 @@ cudaError_t launch_bm_tc(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
                          int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
 size_t lanes_smem_bytes(const Geometry& g, int nwy);
 
+// bm_tcf.cu: the tensor-core float matcher (SC_KERNEL_TC_F32; f32, C = 1, b <= 8, 3xTF32 on tcgen05).
+// dense != nullptr: the debug mode writing every window distance [refs][Wn^2] (-1 in clipped slots).
+bool tcf_supported(const Geometry& g);
+cudaError_t launch_bm_tcf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
+                          int32_t* idx_out, void* dist_out, void* dense, cudaStream_t st, int64_t* launches);
+
 // bm_box.cu: the box-sum matcher (SC_KERNEL_BOX; u8, b = 8, s = 4, C = 1, K <= 32).
 bool box_supported(const Geometry& g);
 bool box_temporal_supported(const Geometry& g, int T);

@@ -32,6 +32,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (++spins > (1ll << 26)) __trap();
   }
 }
+// Same, backing off with nanosleep between polls (producer / issuer warps: frees issue slots for
+// the compute warps sharing their scheduler).
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t done = 0;
+  long long spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (++spins > (1ll << 24)) __trap();
+    __nanosleep(ns);
+  }
+}
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -66,6 +84,16 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem], tf32 x tf32 -> f32 (K = 8 per instruction), issued by ONE thread.
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -118,6 +146,18 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_mn, bool b_
   return (2u << 4)                     // c_format = S32
          | (1u << 7)                   // a_format = signed int8
          | (1u << 10)                  // b_format = signed int8
+         | (uint32_t(a_mn) << 15)      // a_major
+         | (uint32_t(b_mn) << 16)      // b_major
+         | (uint32_t(N >> 3) << 17)    // n_dim
+         | (uint32_t(M >> 4) << 24);   // m_dim
+}
+
+// Instruction descriptor for kind::tf32: D f32, A/B tf32 (format 2), A K-major or MN-major (a_mn),
+// B likewise (b_mn).
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                     // c_format = F32
+         | (2u << 7)                   // a_format = TF32
+         | (2u << 10)                  // b_format = TF32
          | (uint32_t(a_mn) << 15)      // a_major
          | (uint32_t(b_mn) << 16)      // b_major
          | (uint32_t(N >> 3) << 17)    // n_dim

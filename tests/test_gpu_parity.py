@@ -1073,3 +1073,80 @@ def test_temporal_batch_idx_range_checked():
         p.run_rows(x, 0, 1, out=out)
     with pytest.raises(ScError):
         p.run(x)
+
+
+# ------------------------------------------------------------------ tensor-core float matcher (3xTF32)
+def _tcf(x, b, s, Wn, K, where):
+    from paper_2006_13714_b200.bm import SC_KERNEL_TC_F32
+    N, C, H, W = x.shape
+    p = _plan((H, W, C, b, s, Wn, K), "f32")
+    p.set_kernel(SC_KERNEL_TC_F32)
+    gi, gd = _run(p, x)
+    oi, od = oracle.bm(x, b, s, Wn, K)
+    for n in range(N):
+        check_f32(x[n], b, s, Wn, K, gi[n], gd[n], oi[n], od[n], where=f"{where} img{n}")
+    return p
+
+
+@pytest.mark.parametrize("H,W,b,s,Wn", [(40, 52, 8, 3, 17), (37, 45, 7, 1, 13), (33, 61, 5, 2, 21), (50, 40, 8, 4, 9)])
+def test_tcf_dense_cross_term(H, W, b, s, Wn):
+    """Steps a2 + a3 on the tensor cores (3xTF32, MN-major shift-expanded B): every window
+    distance of the identity against the oracle's direct differences."""
+    from paper_2006_13714_b200.bm import SC_KERNEL_TC_F32
+    rng = np.random.Generator(np.random.PCG64(H * W + b))
+    x = synth.random_image(rng, 1, 1, H, W, "f32")[0]
+    p = _plan((H, W, 1, b, s, Wn, 1), "f32")
+    p.set_kernel(SC_KERNEL_TC_F32)
+    got = p.dense_debug(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+    want = oracle.bm_dense(x, b, s, Wn)
+    np.testing.assert_array_equal(got == -1, want == -1)
+    m = want >= 0
+    scale = b * b * 0.25
+    assert np.max(np.abs(got[m] - want[m])) <= 4e-6 * scale + 1e-5 * np.max(want[m])
+
+
+def _tcf_cases(n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = []
+    while len(out) < n:
+        b = int(rng.integers(1, 9))
+        s = int(rng.integers(1, 5))
+        H = int(rng.integers(b + 4, b + 70))
+        W = int(rng.integers(max(b + 4, 24), b + 90))
+        Wn = int(rng.integers(1, 46))
+        K = int(rng.choice([1, 5, 16, 30, 45, 70]))
+        out.append((b, s, H, W, Wn, K))
+    return out
+
+
+@pytest.mark.parametrize("case", _tcf_cases(24, 77))
+def test_tcf_random_sweep(case):
+    b, s, H, W, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 2, 1, H, W, "f32")
+    _tcf(x, b, s, Wn, K, f"tcf {case}")
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_tcf_configs_full(name):
+    cfg = synth.CONFIGS[name]
+    x = synth.make_input(cfg)
+    _tcf(x, cfg.b, cfg.s, cfg.Wn, cfg.K, f"tcf {name}")
+
+
+@pytest.mark.parametrize("kind", ["constant", "periodic", "binary", "smooth"])
+def test_tcf_ties_and_extremes(kind):
+    rng = np.random.Generator(np.random.PCG64(15))
+    if kind == "constant":
+        x = np.full((1, 1, 60, 90), 0.3, dtype=np.float32)
+    elif kind == "periodic":
+        x = np.tile(rng.random((8, 8), dtype=np.float32), (8, 12))[None, None].copy()
+    elif kind == "binary":
+        x = rng.integers(0, 2, size=(1, 1, 60, 90)).astype(np.float32)
+    else:
+        yy, xx = np.mgrid[0:64, 0:96]
+        x = (0.5 + 0.4 * np.sin(yy / 7.0) * np.cos(xx / 9.0)).astype(np.float32)[None, None].copy()
+    for (s, b, K) in [(3, 8, 30), (1, 7, 70)]:
+        p = _tcf(x, b, s, 21, K, f"tcf {kind} s{s} b{b}")
+        if kind == "constant":
+            assert p.debug_fix_count() == p.n_refs  # every reference ties: exact fix-up
