@@ -113,9 +113,10 @@ typedef struct {
 sc_status_t sc_bm_plan(int H, int W, int C, int b, int stride, int window, int K,
                        sc_dtype_t dtype, sc_bm_plan_t* plan_out);
 
-/* Same with an explicit metric. SC_METRIC_NCC runs on the box-sum kernels: uint8 with stride 4,
- * b = 8, one channel on the dp4a kernel; otherwise the float kernel, which needs (stride, b) in
- * {(3,8), (1,7), (4,8), (2,8)}; K <= 30 for uint8, K <= 28 for float (else SC_ERR_UNSUPPORTED). */
+/* Same with an explicit metric. SC_METRIC_NCC (Eq. 4) runs on the box-sum
+ * kernels: uint8 with stride 4, b = 8, one channel on the dp4a kernel; otherwise the float kernel,
+ * which needs (stride, b) in {(3,8), (1,7), (4,8), (2,8)}, any channel count; K <= 30 for uint8
+ * (exact 128-bit ordering of the kept keys), K <= 76 for float (else SC_ERR_UNSUPPORTED). */
 sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, int K,
                           sc_dtype_t dtype, sc_metric_t metric, sc_bm_plan_t* plan_out);
 

@@ -47,6 +47,8 @@ def lib():
         L.sco_norm_map.argtypes = [vp, ci, ci, ci, ci, ci, dp]
         L.sco_selfconv.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, dp]
         L.sco_pair_dist.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
+        L.sco_pair_ncc.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
+        L.sco_bm3d.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, vp, ci]
         L.sco_num_threads.restype = ci
         L.sco_ncc_rows.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, dp, ci]
         L.sco_bm_temporal.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, vp, ci]
@@ -139,6 +141,27 @@ def bm_temporal(img: np.ndarray, b: int, s: int, Wn: int, K: int, T: int, nthrea
     return idx, dist
 
 
+def bm3d(vol: np.ndarray, d: int, b: int, s: int, sz: int, Wn: int, c: int, K: int, nthreads: int = 0):
+    """3D block matching over the planes of a volume [P,H,W] (channels of one image or frames of a
+    video): d-plane patches, references at planes 0, sz, ... <= P - d, candidates
+    at plane offsets [-floor(c/2), c-1-floor(c/2)] x the clipped spatial window. Returns (idx int32,
+    dist int32 (uint8) / float64) [n_zref, n_refs, K], idx = (z * H + y) * W + x."""
+    a = np.ascontiguousarray(vol)
+    if a.ndim == 4:
+        a = a.reshape((-1,) + a.shape[2:])
+    P, H, W = a.shape
+    ny, nx = grid(H, W, b, s)
+    nz = (P - d) // sz + 1
+    code = _dtype_code(a)
+    idx = np.empty((nz, ny * nx, K), dtype=np.int32)
+    dist = np.empty((nz, ny * nx, K), dtype=np.int32 if code == U8 else np.float64)
+    rc = lib().sco_bm3d(a.ctypes.data, code, P, H, W, d, b, s, sz, Wn, c, K,
+                        idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), dist.ctypes.data, nthreads)
+    if rc != 0:
+        raise ValueError("oracle.bm3d: invalid arguments")
+    return idx, dist
+
+
 def nlm_weights(img: np.ndarray, b: int, s: int, Wn: int, h: float, nthreads: int = 0) -> np.ndarray:
     """NLM weights (Eq. 2) over each reference's clipped window, one image [C,H,W]:
     [refs, Wn*Wn] float64, 0 in clipped slots, rows summing to 1."""
@@ -220,6 +243,24 @@ def selfconv(img: np.ndarray, b: int, ry: int, rx: int) -> np.ndarray:
                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     if rc != 0:
         raise ValueError("oracle.selfconv: invalid arguments")
+    return out
+
+
+def pair_ncc(img: np.ndarray, b: int, ry, rx, cy, cx) -> np.ndarray:
+    """-NCC (Eq. 4) of explicit (ref, candidate) pairs of one image [C,H,W]."""
+    a = np.ascontiguousarray(img)
+    if a.ndim == 2:
+        a = a[None]
+    C, H, W = a.shape
+    arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.int32).ravel()) for v in (ry, rx, cy, cx)]
+    n = arrs[0].size
+    out = np.empty(n, dtype=np.float64)
+    P = ctypes.POINTER(ctypes.c_int32)
+    rc = lib().sco_pair_ncc(a.ctypes.data, _dtype_code(a), C, H, W, b, n,
+                            *[x.ctypes.data_as(P) for x in arrs],
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if rc != 0:
+        raise ValueError("oracle.pair_ncc: invalid arguments")
     return out
 
 

@@ -273,6 +273,36 @@ int sco_pair_dist(const void* img, int dtype, int C, int H, int W, int b, long l
 }
 
 /*
+ * -NCC of explicit (reference, candidate) pairs (Eq. 4, on the raw values,
+ * channels summed; NCC := 0 when a norm is 0, R15), double -- the same arithmetic as
+ * sco_ncc_rows' reported value, for full-size checks of sampled or selected pairs.
+ */
+int sco_pair_ncc(const void* img, int dtype, int C, int H, int W, int b, long long n,
+                 const int32_t* ry, const int32_t* rx, const int32_t* cy, const int32_t* cx,
+                 double* out) {
+    if (!img || !out || b < 1 || H < b || W < b) return -1;
+    for (long long k = 0; k < n; ++k) {
+        if (ry[k] < 0 || rx[k] < 0 || cy[k] < 0 || cx[k] < 0 || ry[k] > H - b || cy[k] > H - b ||
+            rx[k] > W - b || cx[k] > W - b)
+            return -1;
+        double nr = 0.0, nc = 0.0, cc = 0.0;
+        for (int c = 0; c < C; ++c)
+            for (int l = 0; l < b; ++l)
+                for (int m = 0; m < b; ++m) {
+                    const size_t base = (size_t)c * H * W;
+                    const double vr = px(img, dtype, base + (size_t)(ry[k] + l) * W + rx[k] + m);
+                    const double vc = px(img, dtype, base + (size_t)(cy[k] + l) * W + cx[k] + m);
+                    cc += vr * vc;
+                    nr += vr * vr;
+                    nc += vc * vc;
+                }
+        const double den = sqrt(nr * nc);
+        out[k] = den > 0.0 ? -(cc / den) : 0.0;
+    }
+    return 0;
+}
+
+/*
  * NCC block matching (the "next" row): Eq. 4,
  *   S_i = argmin_{|S| <= K} sum_{j in S} d_NCC(X_j, X_i),
  *   d_NCC(X_j, X_i) = - vec(X_j)^T vec(X_i) / (||X_j||_F ||X_i||_F)
@@ -509,4 +539,78 @@ int sco_num_threads(void) {
 #else
     return 1;
 #endif
+}
+
+/*
+ * 3D block matching (the "next" row SURVEY.md 8f rank 4): the paper's 3D Self-Convolution
+ * (patches Y_i of sqrt(n) x sqrt(n) x d with d < p, searched "across channels" by a
+ * 3D FFT instead of the channel sum S(.)) and its video setting (SALT: 6 x 6 x 1 patches in a
+ * 30 x 30 x c window, c = 9 frames). A volume V[P][H][W] of planes (the channels of
+ * one image, or the frames of a video); a patch is d consecutive planes x b x b; references start at
+ * planes z in {0, sz, 2 sz, ...} <= P - d and on the usual spatial grid; the candidates of a
+ * reference at plane z are the patches starting at planes z + dz, dz in [lo_z, hi_z]
+ * (lo_z = -floor(c/2), hi_z = c - 1 - floor(c/2), reading R4 for even c), clipped to [0, P - d],
+ * and at the clipped spatial window positions (footnote 2);
+ *     d(r, c) = sum_{t < d} sum_{l, m} (V[z_r + t][ry + l][rx + m] - V[z_c + t][cy + l][cx + m])^2
+ * by direct differences (int64 for uint8, double otherwise), idx = (z_c H + cy) W + cx (the volume
+ * raster of the candidate's first voxel), ties by (d, idx), output [n_zref][n_refs][K] with
+ * n_zref = floor((P - d) / sz) + 1. d = P, c = 1 is multi-channel 2D BM; d = 1, c = 2T + 1,
+ * sz = 1 is the temporal search of sco_bm_temporal.
+ */
+int sco_bm3d(const void* vol, int dtype, int P, int H, int W, int d, int b, int s, int sz, int Wn, int c,
+             int K, int32_t* idx_out, void* dist_out, int nthreads) {
+    if (!vol || !idx_out || !dist_out || P < 1 || d < 1 || d > P || b < 1 || s < 1 || sz < 1 || Wn < 1 ||
+        c < 1 || K < 1 || H < b || W < b)
+        return -1;
+    const int ny = grid_n(H, b, s), nx = grid_n(W, b, s), nz = (P - d) / sz + 1;
+    const int lo = -(Wn / 2), hi = Wn - 1 - Wn / 2, loz = -(c / 2), hiz = c - 1 - c / 2;
+    const long long refs2d = (long long)ny * nx, total = refs2d * nz;
+    const size_t plane = (size_t)H * W;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+#pragma omp parallel
+    {
+        sco_key* keys = (sco_key*)malloc(sizeof(sco_key) * (size_t)Wn * (size_t)Wn * (size_t)c);
+#pragma omp for schedule(dynamic, 16)
+        for (long long t = 0; t < total; ++t) {
+            const int zr = (int)(t / refs2d) * sz;
+            const long long j = t % refs2d;
+            const int ry = (int)(j / nx) * s, rx = (int)(j % nx) * s;
+            const int cy0 = ry + lo < 0 ? 0 : ry + lo, cy1 = ry + hi > H - b ? H - b : ry + hi;
+            const int cx0 = rx + lo < 0 ? 0 : rx + lo, cx1 = rx + hi > W - b ? W - b : rx + hi;
+            int cnt = 0;
+            for (int zc = zr + loz; zc <= zr + hiz; ++zc) {
+                if (zc < 0 || zc > P - d) continue;
+                for (int cy = cy0; cy <= cy1; ++cy)
+                    for (int cx = cx0; cx <= cx1; ++cx) {
+                        int64_t acc = 0;
+                        double accd = 0.0;
+                        for (int q = 0; q < d; ++q)
+                            for (int l = 0; l < b; ++l)
+                                for (int m = 0; m < b; ++m) {
+                                    const double vr = px(vol, dtype, (size_t)(zr + q) * plane + (size_t)(ry + l) * W + rx + m);
+                                    const double vc = px(vol, dtype, (size_t)(zc + q) * plane + (size_t)(cy + l) * W + cx + m);
+                                    accd += (vr - vc) * (vr - vc);
+                                    if (dtype == SCO_U8) acc += (int64_t)(vr - vc) * (int64_t)(vr - vc);
+                                }
+                        keys[cnt].di = acc;
+                        keys[cnt].d = accd;
+                        keys[cnt].idx = (int32_t)(((long long)zc * H + cy) * W + cx);
+                        ++cnt;
+                    }
+            }
+            qsort(keys, (size_t)cnt, sizeof(sco_key), dtype == SCO_U8 ? cmp_key_int : cmp_key_dbl);
+            const long long o = t * K;
+            for (int k = 0; k < K; ++k) {
+                idx_out[o + k] = k < cnt ? keys[k].idx : -1;
+                if (dtype == SCO_U8) ((int32_t*)dist_out)[o + k] = k < cnt ? (int32_t)keys[k].di : INT32_MAX;
+                else ((double*)dist_out)[o + k] = k < cnt ? keys[k].d : INFINITY;
+            }
+        }
+        free(keys);
+    }
+    return 0;
 }

@@ -46,6 +46,7 @@ struct BoxfArgs {
   int nblk;         // dy blocks of VY offsets
   int scr;          // per-warp scratch words (survivor staging [+ output staging | + heaps])
   int hp;           // heap pitch (words per reference) when the top-KP lives in shared heaps
+  int lofs;         // WS = 2: word offset of the per-row list area (0: the staged region, reused)
   int rb;           // window-relative index bits of the 32-bit keys
   int* fix_count;   // references the key quantisation leaves open -> exact fix-up (fixup.cu)
   int* fix_list;
@@ -71,8 +72,14 @@ __device__ __forceinline__ float hcombine(float ef, float ep) {
   }
 }
 
-template <int S, int BK, int VY, int KR, bool C1, bool NCC, typename TIN>
-__global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
+// WS = 2 (window split): two warps per reference row, each visiting half of the window's dx pairs
+// (alternating, so both start near the reference), with their own top-KP lists and a shared filter
+// threshold (the smaller of the two published KP-th keys: each list holds KP real candidates of the
+// reference, so the KP-th best of their union can only be smaller -- a valid superset bound); the
+// second half's list is merged into the first's before a5. Doubles the warps per staged region
+// where the grid or the shared memory leaves the SMs half empty (c2: 132 CTAs; c4: 216 KB, 1 CTA/SM).
+template <int S, int BK, int VY, int KR, bool C1, bool NCC, typename TIN, int WS = 1>
+__global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_kernel(BoxfArgs a) {
   constexpr int NS = (BK + S - 1) / S;   // strips per patch
   constexpr int WL = BK - (NS - 1) * S;  // width of the last strip
   constexpr int RX = 33 - NS;            // references per warp (lanes RX..31: helper strips)
@@ -83,6 +90,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const int iy_first = a.iy_begin + ty * kFWarps;
   const int ix_first = tx * RX;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = warp % kFWarps, hh = warp / kFWarps;  // reference row of the warp, window half (WS = 2)
   const int Ybase = iy_first * S + a.lo, Xbase = ix_first * S + a.lo;
 
   // ---- a0: the staged region of every channel (0 outside the image): L2 centres x' = x - 0.5
@@ -98,10 +106,14 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     smf[e] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
                  ? float(__ldg(img + c * plane + size_t(yy) * a.W + xx)) - shift : 0.f;
   }
+  // published KP-th keys of the two window halves (WS = 2), +inf until a list fills
+  uint32_t* pub = reinterpret_cast<uint32_t*>(smf + ((nch * a.PL + 1) & ~1)) + kFWarps * WS * a.scr;
+  if (WS == 2) pub[warp * 32 + lane] = 0xffffffffu;
   __syncthreads();
 
-  const int iy0 = iy_first + warp;
-  if (iy0 >= a.iy_end) return;
+  const int iy0 = iy_first + wr;
+  const bool wact = iy0 < a.iy_end;  // warp-uniform
+  if (WS == 1 && !wact) return;
   const int ix = ix_first + lane;
   const bool lane_ok = lane < RX && ix < a.nx;
   const int rx = ix * S, ry = iy0 * S;
@@ -147,6 +159,8 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   // (helper lanes RX..31 never insert; they alias lane RX-1's heap for the root reads)
   uint32_t* const scr0 = reinterpret_cast<uint32_t*>(smf + ((nch * a.PL + 1) & ~1));  // 8-byte aligned
   uint32_t* heap = scr0 + warp * a.scr + 64 * VY + min(lane, RX - 1) * a.hp;
+  uint32_t* const pub_own = pub + warp * 32 + lane;
+  const uint32_t* const pub_other = pub + ((1 - hh) * kFWarps + wr) * 32 + lane;
   if constexpr (HEAP) {
     if (lane < RX)
       for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
@@ -160,10 +174,23 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const int span = max(-a.lo, a.hi);
   unsigned pend = 0u;  // survivor bits of the staged group(s)
   int rel1p = 0;
+  auto set_thr = [&](uint32_t kth) {
+    if (kth != 0xffffffffu) {
+      // largest distance whose key can still tie the KP-th key, plus a rounding margin
+      const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
+      thr = fmaf(dmax, 1.0f + (NCC ? 1e-5f : 1e-6f), -nadd) + 1e-30f;
+    }
+  };
   auto flush = [&](int rel1c) {
     unsigned bits = pend;
     pend = 0u;
-    if (!__any_sync(0xffffffffu, bits != 0u)) return;
+    if (!__any_sync(0xffffffffu, bits != 0u)) {
+      if constexpr (WS == 2) {  // the partner half may have tightened the shared threshold
+        const uint32_t own = HEAP ? heap[1] : rt.r[KR - 1];
+        set_thr(min(own, *pub_other));
+      }
+      return;
+    }
     const uint32_t* sc = scratch + lane;
     while (__any_sync(0xffffffffu, bits != 0u)) {
       const int i = 31 - __clz(bits | 1u);
@@ -191,10 +218,11 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
       }
     }
     const uint32_t kth = HEAP ? heap[1] : rt.r[KR - 1];
-    if (kth != 0xffffffffu) {
-      // largest distance whose key can still tie the KP-th key, plus a rounding margin
-      const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
-      thr = fmaf(dmax, 1.0f + (NCC ? 1e-5f : 1e-6f), -nadd) + 1e-30f;
+    if constexpr (WS == 2) {
+      *pub_own = kth;
+      set_thr(min(kth, *pub_other));
+    } else {
+      set_thr(kth);
     }
     __syncwarp();
   };
@@ -202,6 +230,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   // the uint8 box kernel: thresholds tighten sooner; measured on c2 / c4). Heap lists (c3, K = 70)
   // measured slower with the split: one phase.
   const int kNearPairs = HEAP ? span + 1 : 5;
+  if (wact) {  // (WS = 2: an inactive warp still joins the merge barrier below)
   for (int ph = 0; ph < 2; ++ph) {
   const int j_begin = ph == 0 ? 0 : kNearPairs, j_end = ph == 0 ? min(kNearPairs, span + 1) : span + 1;
   for (int kb = 0; kb < 2 * a.nblk; ++kb) {
@@ -292,6 +321,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     // dx centre-out (0, 1, -1, 2, -2, ...): pairs (-j, j+1) staged in the two halves and
     // flushed together (a round lasts as long as the busiest lane); a lone group flushes alone
     for (int j = j_begin; j < j_end; ++j) {
+      if (WS == 2 && (j & 1) != hh) continue;  // the other half's dx pair
       const bool va = -j >= a.lo, vb = j + 1 <= a.hi;
       if (!va && !vb) continue;  // warp-uniform
       rel1p = group(va ? -j : j + 1, std::integral_constant<int, 0>{});
@@ -299,10 +329,33 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
     }
   }
   }  // phases
+  }  // wact
+
+  if constexpr (WS == 2) {
+    // merge the second half's list into the first's (0 sentinels skipped), then only the first
+    // half's warps go on to a5
+    // (the lists go to a per-row area -- by default the staged region, free once every warp is done)
+    uint32_t* ml = reinterpret_cast<uint32_t*>(smf) + a.lofs + wr * RX * (KR + 1);
+    __syncthreads();
+    if (hh == 1 && wact && lane < RX) {
+#pragma unroll
+      for (int k = 0; k < KR; ++k) ml[lane * (KR + 1) + k] = rt.r[k];
+    }
+    __syncthreads();
+    if (hh == 1 || !wact) return;
+    if (lane < RX) {
+#pragma unroll 1
+      for (int k = 0; k < KR; ++k) {
+        const uint32_t x = ml[lane * (KR + 1) + k];
+        rt.insert(x == 0u ? 0xffffffffu : x);
+      }
+    }
+  }
 
   // ---- a5 + a6: stage each reference's KP keys (register lists; the heaps already are in shared
   // memory), then per reference (warp-cooperative) re-score them by direct differences from the
   // input, sort the (distance, idx) keys and write K.
+  if constexpr (WS == 2) scratch = reinterpret_cast<uint32_t*>(smf) + a.lofs + wr * RX * (KR + 1);
   if constexpr (!HEAP) {
     if (lane_ok) {
 #pragma unroll
@@ -314,7 +367,85 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
   const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
   const size_t row0 = size_t(f) * band_refs + size_t(iy0 - a.iy_begin) * a.nx + ix_first;
   constexpr int NJ = (KR + 31) / 32;
-  if constexpr (NCC) {
+  if constexpr (NCC && KR > 32) {
+    // a5 (NCC, float input, K + m > 32: lists of 40 / 48 keys or the shared-memory heaps): per
+    // reference the kept candidates' NCC recomputed in double from the input (Eq. 4), ranked by
+    // (float32 d_NCC = -NCC, idx) -- the reported value, as the f32 rule compares -- with the warp's
+    // 64-bit key lists (topk.cuh), K written; a reference whose worst kept key's quantum could still
+    // hold a score as good as the exact K-th one goes to the exact fix-up
+    static_assert(sizeof(TIN) == 4, "wide NCC lists serve float input (uint8 NCC keeps K + m <= 32)");
+    constexpr int NJ = (KR + 31) / 32;
+    for (int j = 0; j < nref; ++j) {
+      const int rxj = (ix_first + j) * S;
+      const size_t rowj = row0 + j;
+      WarpTopK<NJ> top;
+      top.init();
+      double nrq = 0.0;
+#pragma unroll
+      for (int sl = 0; sl < NJ; ++sl) {
+        const int k = sl * 32 + lane;
+        uint32_t kk;
+        if constexpr (HEAP) kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
+        else kk = k < a.KP ? scratch[j * (KR + 1) + (KR - a.KP) + k] : 0xffffffffu;  // skip 0 sentinels
+        const bool have = kk != 0u && kk != 0xffffffffu;
+        double nrd = 0.0, cd = 0.0, ncd = 0.0;
+        int cy = ry, cx = rxj;
+        if (have) {
+          const int rel = int(kk & ((1u << rb) - 1u)) - 1;
+          const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+          cy = ry + dyy + a.lo;
+          cx = rxj + dxx + a.lo;
+        }
+        for (int c = 0; c < nch; ++c) {
+          const TIN* pr = img + c * plane + size_t(ry) * a.W + rxj;
+          const TIN* pc = img + c * plane + size_t(cy) * a.W + cx;
+          for (int l = 0; l < BK; ++l)
+#pragma unroll
+            for (int m = 0; m < BK; ++m) {
+              const double vr = double(__ldg(pr + l * a.W + m)), vc = double(__ldg(pc + l * a.W + m));
+              nrd = fma(vr, vr, nrd);
+              cd = fma(vr, vc, cd);
+              ncd = fma(vc, vc, ncd);
+            }
+        }
+        nrq = nrd;  // the same for every slot (the reference's own norm)
+        uint64_t key = kKeyInf;
+        if (have) {
+          const double den = sqrt(nrd * ncd);
+          const float dn = -float(den > 0.0 ? cd / den : 0.0);  // the reported d_NCC
+          key = (uint64_t(ord_f32(dn)) << 32) | uint32_t(cy * a.W + cx);
+        }
+        top.merge(key, lane);
+      }
+      uint64_t kv = kKeyInf;
+#pragma unroll
+      for (int sl = 0; sl < NJ; ++sl)
+        if (sl == (a.K - 1) / 32) kv = top.v[sl];
+      kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
+      const uint32_t klast = HEAP ? heap[(j - min(lane, RX - 1)) * a.hp + 1] : scratch[j * (KR + 1) + KR - 1];
+      nrq = __shfl_sync(0xffffffffu, nrq, 0);
+      if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf && nrq > 0.0) {
+        const double fK = -double(unord_f32(uint32_t(kv >> 32)));  // exact K-th NCC (float32)
+        const float smin = __uint_as_float((klast >> rb) << (rb - 1));  // quantum minimum
+        const double nrs_d = sqrt(nrq), scK = nrs_d * (1.0 - fK);    // exact K-th filter score
+        if (double(smin) <= scK * (1.0 + 1e-5) + 1e-6 * nrs_d) {
+          const int pos = atomicAdd(a.fix_count, 1);
+          a.fix_list[pos] = int(rowj);
+        }
+      }
+#pragma unroll
+      for (int sl = 0; sl < NJ; ++sl) {
+        const int k = sl * 32 + lane;
+        if (k < a.K) {
+          const uint64_t key = top.v[sl];
+          const bool none = key == kKeyInf;
+          a.idx_out[rowj * a.K + k] = none ? -1 : int32_t(uint32_t(key));
+          a.dist_out[rowj * a.K + k] = none ? __int_as_float(0x7f800000) : unord_f32(uint32_t(key >> 32));
+        }
+      }
+    }
+    return;
+  } else if constexpr (NCC) {
     // a5 (NCC): exact cross terms / norms of the KP (<= 32) kept candidates, which arrive in key
     // order; exact neighbour checks + odd-even repair (128-bit comparisons for uint8, ncc.cuh),
     // write K (idx, d_NCC = -NCC)
@@ -451,7 +582,23 @@ __global__ void __launch_bounds__(kFWarps * 32, 2) bm_boxf_kernel(BoxfArgs a) {
 
 constexpr int kFVY = 8;
 
-size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) {
+// window split (WS = 2) where one 8-warp CTA per SM would be all the SM gets: several channel
+// planes (the staged region takes the SM's shared memory) or fewer CTAs than 2 per SM; register
+// lists only (the c3-style shared heaps keep WS = 1)
+size_t boxf_bytes(const Geometry& g, int KR, int ws, BoxfArgs* a);
+
+int boxf_ws(const Geometry& g, int KR) {
+  if (KR > 48 || g.metric != SC_METRIC_L2) return 1;
+  const int ns = (g.b + g.s - 1) / g.s, rx = 33 - ns;
+  const long long ctas = (long long)((g.nx + rx - 1) / rx) * ((g.ny + kFWarps - 1) / kFWarps);
+  if (!(g.C > 1 || ctas < 2 * 148)) return 1;
+  BoxfArgs t{};
+  return boxf_bytes(g, KR, 2, &t) <= 227 * 1024 ? 2 : 1;  // (else the plain layout)
+}
+
+size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) { return boxf_bytes(g, KR, boxf_ws(g, KR), a); }
+
+size_t boxf_bytes(const Geometry& g, int KR, int ws, BoxfArgs* a) {
   const int ns = (g.b + g.s - 1) / g.s, rx = 33 - ns;
   a->nblk = (g.Wn + kFVY - 1) / kFVY;
   a->RH = (kFWarps - 1) * g.s + a->nblk * kFVY + g.b;
@@ -460,8 +607,14 @@ size_t boxf_layout(const Geometry& g, int KR, BoxfArgs* a) {
   // heap pitch: 1-indexed heap + a padding child, = 2 (mod 4) words: 8-byte aligned rows whose
   // 64-bit child loads hit distinct bank pairs across a half-warp
   a->hp = ((g.KP + 2 + 1) & ~3) + 2;
-  a->scr = KR > 48 ? 64 * kFVY + rx * a->hp : std::max(64 * kFVY, rx * (KR + 1));  // 2 staged groups
-  return size_t(((g.C * a->PL + 1) & ~1) + kFWarps * a->scr) * 4;  // scratch 8-byte aligned
+  // per warp: two staged offset groups (+ the heaps, or the output lists with WS = 1)
+  a->scr = KR > 48 ? 64 * kFVY + rx * a->hp : ws == 2 ? 64 * kFVY : std::max(64 * kFVY, rx * (KR + 1));
+  const size_t region = size_t((g.C * a->PL + 1) & ~1);
+  const size_t base = region + size_t(kFWarps) * ws * a->scr + (ws == 2 ? 2 * kFWarps * 32 : 0);
+  // WS = 2: the per-row list areas reuse the staged region when it is large enough
+  const size_t lists = size_t(kFWarps) * rx * (KR + 1);
+  a->lofs = ws == 2 && lists > region ? int(base) : 0;
+  return (base + (ws == 2 && lists > region ? lists : 0)) * 4;
 }
 
 // key bits of the window-relative index + 1 (values 1 .. Wn^2; 0 is the sentinel)
@@ -477,11 +630,15 @@ int boxf_kr(const Geometry& g) {
 }
 
 template <int S, int BK, int KR, bool NCC = false, typename TIN = float>
-cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st) {
+cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st, int ws = 1) {
   const int tiles_y = (a.iy_end - a.iy_begin + kFWarps - 1) / kFWarps;
   auto k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN> : bm_boxf_kernel<S, BK, kFVY, KR, false, NCC, TIN>;
+  if constexpr (KR <= 48 && !NCC) {
+    if (ws == 2) k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN, 2>
+                              : bm_boxf_kernel<S, BK, kFVY, KR, false, NCC, TIN, 2>;
+  }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  k<<<dim3(a.tiles_x * tiles_y, F), kFWarps * 32, smem, st>>>(a);
+  k<<<dim3(a.tiles_x * tiles_y, F), kFWarps * 32 * ws, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -490,7 +647,8 @@ cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st
 bool boxf_supported(const Geometry& g) {
   // L2: float images (uint8 L2 has the dp4a box kernel); NCC: both dtypes, K + m <= 32
   if (g.metric == SC_METRIC_L2 && g.dtype != SC_DTYPE_F32) return false;
-  if (g.metric == SC_METRIC_NCC && g.KP > 32) return false;
+  // NCC: uint8 keeps the exact 128-bit re-rank of <= 32 kept keys; float input takes wider lists
+  if (g.metric == SC_METRIC_NCC && g.KP > (g.dtype == SC_DTYPE_U8 ? 32 : 80)) return false;
   const bool shape = (g.s == 3 && g.b == 8) || (g.s == 1 && g.b == 7) || (g.s == 4 && g.b == 8) ||
                      (g.s == 2 && g.b == 8);
   if (!shape) return false;
@@ -498,8 +656,8 @@ bool boxf_supported(const Geometry& g) {
   if (kr == 0) return false;
   if (boxf_rel_bits(g.Wn) > 12) return false;  // keeps >= 20 distance bits in the 32-bit keys
   BoxfArgs a{};
-  // one channel: 2 CTAs per SM; several channels (c4): the staged planes may take the whole SM
-  return boxf_layout(g, kr, &a) <= (g.C == 1 ? 113 : 227) * 1024;
+  // up to the whole SM's shared memory (one channel with register lists normally fits two CTAs)
+  return boxf_layout(g, kr, &a) <= 227 * 1024;
 }
 
 namespace {
@@ -520,14 +678,18 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
   const int kr = boxf_kr(g);  // the layout and the instantiation use the same list size
   const size_t smem = boxf_layout(g, kr, &a);
   if (launches) *launches += 1;
-  if (g.metric == SC_METRIC_NCC) {  // KP <= 32: register lists, exact re-rank
+  if (g.metric == SC_METRIC_NCC) {  // uint8: K + m <= 32, exact re-rank; float: lists up to 80
 #define SCBM_NCC_CASE(S_, B_)                                                                          \
   if (g.s == S_ && g.b == B_) {                                                                        \
     if (kr == 24)                                                                                      \
       return g.dtype == SC_DTYPE_U8 ? launch_boxf_t<S_, B_, 24, true, uint8_t>(a, F, smem, st)         \
                                     : launch_boxf_t<S_, B_, 24, true, float>(a, F, smem, st);          \
-    return g.dtype == SC_DTYPE_U8 ? launch_boxf_t<S_, B_, 32, true, uint8_t>(a, F, smem, st)           \
-                                  : launch_boxf_t<S_, B_, 32, true, float>(a, F, smem, st);            \
+    if (kr == 32)                                                                                      \
+      return g.dtype == SC_DTYPE_U8 ? launch_boxf_t<S_, B_, 32, true, uint8_t>(a, F, smem, st)         \
+                                    : launch_boxf_t<S_, B_, 32, true, float>(a, F, smem, st);          \
+    if (kr == 40) return launch_boxf_t<S_, B_, 40, true, float>(a, F, smem, st);                       \
+    if (kr == 48) return launch_boxf_t<S_, B_, 48, true, float>(a, F, smem, st);                       \
+    return launch_boxf_t<S_, B_, 80, true, float>(a, F, smem, st);                                     \
   }
     SCBM_NCC_CASE(3, 8)
     SCBM_NCC_CASE(1, 7)
@@ -536,12 +698,13 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
 #undef SCBM_NCC_CASE
     return cudaErrorInvalidValue;
   }
+  const int ws = boxf_ws(g, kr);
 #define SCBM_BOXF_CASE(S_, B_)                                                    \
   if (g.s == S_ && g.b == B_) {                                                   \
-    if (kr == 24) return launch_boxf_t<S_, B_, 24>(a, F, smem, st);               \
-    if (kr == 32) return launch_boxf_t<S_, B_, 32>(a, F, smem, st);               \
-    if (kr == 40) return launch_boxf_t<S_, B_, 40>(a, F, smem, st);               \
-    if (kr == 48) return launch_boxf_t<S_, B_, 48>(a, F, smem, st);               \
+    if (kr == 24) return launch_boxf_t<S_, B_, 24>(a, F, smem, st, ws);           \
+    if (kr == 32) return launch_boxf_t<S_, B_, 32>(a, F, smem, st, ws);           \
+    if (kr == 40) return launch_boxf_t<S_, B_, 40>(a, F, smem, st, ws);           \
+    if (kr == 48) return launch_boxf_t<S_, B_, 48>(a, F, smem, st, ws);           \
     return launch_boxf_t<S_, B_, 80>(a, F, smem, st);                             \
   }
   SCBM_BOXF_CASE(3, 8)

@@ -44,6 +44,46 @@ __device__ void fixup_ncc_ref(const FixArgs& a, int code, int lane) {
   const int ncols = cx1 - cx0 + 1, nwin = (cy1 - cy0 + 1) * ncols;
   const size_t plane = size_t(a.H) * a.W;
   const TIN* img = static_cast<const TIN*>(a.imgs) + size_t(a.frame0 + f) * a.C * plane;
+  if constexpr (!EXACT) {
+    if (a.K > 32) {  // float input with K > 32 (wide lists): (float32 d_NCC, idx) 64-bit keys, K <= 128
+      WarpTopK<4> top;
+      top.init();
+      for (int base = 0; base < nwin; base += 32) {
+        const int k = base + lane;
+        uint64_t key = kKeyInf;
+        if (k < nwin) {
+          const int cy = cy0 + k / ncols, cx = cx0 + k % ncols;
+          double cd = 0.0, ncd = 0.0, nrd = 0.0;
+          for (int c = 0; c < a.C; ++c)
+            for (int l = 0; l < a.b; ++l) {
+              const TIN* pr = img + c * plane + size_t(ry + l) * a.W + rx;
+              const TIN* pc = img + c * plane + size_t(cy + l) * a.W + cx;
+              for (int m = 0; m < a.b; ++m) {
+                cd = fma(double(pr[m]), double(pc[m]), cd);
+                ncd = fma(double(pc[m]), double(pc[m]), ncd);
+                nrd = fma(double(pr[m]), double(pr[m]), nrd);
+              }
+            }
+          const double den = sqrt(nrd * ncd);
+          const float dn = -float(den > 0.0 ? cd / den : 0.0);
+          key = (uint64_t(ord_f32(dn)) << 32) | uint32_t(cy * a.W + cx);
+        }
+        top.merge(key, lane);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = lane + 32 * j;
+        if (k < a.K) {
+          const uint64_t key = top.v[j];
+          const bool none = key == kKeyInf;
+          const size_t o = size_t(code) * a.K + k;
+          a.idx_out[o] = none ? -1 : int32_t(uint32_t(key));
+          static_cast<float*>(a.dist_out)[o] = none ? __int_as_float(0x7f800000) : unord_f32(uint32_t(key >> 32));
+        }
+      }
+      return;
+    }
+  }
   NccItem best;
   best.c = 0; best.n = 1; best.f = 0.0; best.idx = -1;
   for (int base = 0; base < nwin; base += 32) {

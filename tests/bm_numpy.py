@@ -88,3 +88,35 @@ def ncc_np(img: np.ndarray, b: int, s: int, Wn: int, K: int):
                 d_out[r, k] = -f
             r += 1
     return idx_out, d_out
+
+
+def bm3d_np(vol: np.ndarray, d: int, b: int, s: int, sz: int, Wn: int, c: int, K: int):
+    """Independent 3D brute force: every d-plane patch of the volume [P,H,W] materialised with
+    sliding_window_view over (plane, y, x), distances to ALL patch positions, the (plane offset,
+    row, column) window applied as a mask, lexsort by (distance, volume index)."""
+    integer = np.issubdtype(vol.dtype, np.integer)
+    x = vol.astype(np.int64 if integer else np.float64)
+    P, H, W = x.shape
+    pt = sliding_window_view(x, (d, b, b))  # [P-d+1, H-b+1, W-b+1, d, b, b]
+    Z, My, Mx = pt.shape[:3]
+    flat = pt.reshape(Z, My, Mx, d * b * b)
+    lo, hi, loz, hiz = -(Wn // 2), Wn - 1 - Wn // 2, -(c // 2), c - 1 - c // 2
+    zz, yy, xx = np.meshgrid(np.arange(Z), np.arange(My), np.arange(Mx), indexing="ij")
+    vidx = ((zz * H + yy) * W + xx).ravel()
+    out_i, out_d = [], []
+    big = np.iinfo(np.int32).max if integer else np.inf
+    for zr in range(0, P - d + 1, sz):
+        for ry in range(0, H - b + 1, s):
+            for rx in range(0, W - b + 1, s):
+                D = ((flat - flat[zr, ry, rx]) ** 2).sum(-1).ravel()
+                m = ((zz - zr >= loz) & (zz - zr <= hiz) & (yy - ry >= lo) & (yy - ry <= hi) &
+                     (xx - rx >= lo) & (xx - rx <= hi)).ravel()
+                o = np.lexsort((vidx[m], D[m]))[:K]
+                ii = np.full(K, -1, np.int64)
+                dd = np.full(K, big, np.int64 if integer else np.float64)
+                ii[:len(o)] = vidx[m][o]
+                dd[:len(o)] = D[m][o]
+                out_i.append(ii)
+                out_d.append(dd)
+    nz = (P - d) // sz + 1
+    return np.array(out_i).reshape(nz, -1, K), np.array(out_d).reshape(nz, -1, K)

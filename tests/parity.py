@@ -112,23 +112,33 @@ def check_ncc(img, b, s, Wn, K, gi, gd, oi, od, exact, iy_range=None, where=""):
     ny, nx = oracle.grid(H, W, b, s)
     iy0, iy1 = iy_range if iy_range is not None else (0, ny)
     refs = (iy1 - iy0) * nx
+    assert gi.shape == (refs, K)
     lo, hi = -(Wn // 2), Wn - 1 - Wn // 2
-    for r in range(refs):
-        ry, rx = (iy0 + r // nx) * s, (r % nx) * s
-        ncand = (min(H - b, ry + hi) - max(0, ry + lo) + 1) * (min(W - b, rx + hi) - max(0, rx + lo) + 1)
-        k = min(ncand, K)
-        g = gi[r, :k]
-        assert (gi[r, k:] == -1).all() and len(set(g.tolist())) == k, f"{where}: ref {r} slots"
-        gcy, gcx = g // W, g % W
-        assert ((gcy - ry >= lo) & (gcy - ry <= hi) & (gcx - rx >= lo) & (gcx - rx <= hi)).all()
-        D = pair_ncc(img, b, [ry] * k, [rx] * k, gcy, gcx)
-        assert np.max(np.abs(gd[r, :k] - D)) <= NCC_ATOL, f"{where}: ref {r} d_NCC off"
-        d = gd[r, :k].astype(np.float64)
-        assert ((d[1:] > d[:-1]) | ((d[1:] == d[:-1]) & (g[1:] > g[:-1]))).all(), f"{where}: ref {r} order"
-        gs, os_ = set(g.tolist()), set(oi[r, :k].tolist())
-        if gs != os_:
-            dK = od[r, k - 1]
-            dmap = dict(zip(oi[r, :k].tolist(), od[r, :k].tolist()))
-            dmap.update(zip(g.tolist(), D.tolist()))
-            for c in gs ^ os_:
-                assert abs(dmap[c] - dK) <= NCC_ATOL, f"{where}: ref {r} set differs beyond tolerance"
+    t = np.arange(refs)
+    ry, rx = (iy0 + t // nx) * s, (t % nx) * s
+    ncand = (np.minimum(H - b, ry + hi) - np.maximum(0, ry + lo) + 1) * \
+        (np.minimum(W - b, rx + hi) - np.maximum(0, rx + lo) + 1)
+    kk = np.minimum(ncand, K)
+    valid = np.arange(K)[None, :] < kk[:, None]
+    assert ((gi == -1) == ~valid).all(), f"{where}: padding slots"
+    gcy, gcx = np.where(valid, gi // W, 0), np.where(valid, gi % W, 0)
+    RY, RX = np.broadcast_to(ry[:, None], gi.shape), np.broadcast_to(rx[:, None], gi.shape)
+    inwin = (gcy - RY >= lo) & (gcy - RY <= hi) & (gcx - RX >= lo) & (gcx - RX <= hi)
+    assert (inwin | ~valid).all(), f"{where}: candidate outside its window"
+    srt = np.sort(np.where(valid, gi, -1 - np.arange(K)[None, :]), axis=1)
+    assert (np.diff(srt, axis=1) != 0).all(), f"{where}: duplicate indices"
+    D = np.zeros(gi.shape)
+    D[valid] = oracle.pair_ncc(img, b, RY[valid], RX[valid], gcy[valid], gcx[valid])
+    assert np.max(np.abs(gd[valid] - D[valid]), initial=0) <= NCC_ATOL, f"{where}: d_NCC off"
+    d = gd.astype(np.float64)
+    ok = (d[:, 1:] > d[:, :-1]) | ((d[:, 1:] == d[:, :-1]) & (gi[:, 1:] > gi[:, :-1])) | ~valid[:, 1:]
+    assert ok.all(), f"{where}: row not sorted by (d_NCC, idx)"
+    same = (np.sort(gi, axis=1) == np.sort(oi, axis=1)).all(axis=1)
+    for r in np.flatnonzero(~same):
+        k = int(kk[r])
+        gs, os_ = set(gi[r, :k].tolist()), set(oi[r, :k].tolist())
+        dK = od[r, k - 1]
+        dmap = dict(zip(oi[r, :k].tolist(), od[r, :k].tolist()))
+        dmap.update(zip(gi[r, :k].tolist(), D[r, :k].tolist()))
+        for c in gs ^ os_:
+            assert abs(dmap[c] - dK) <= NCC_ATOL, f"{where}: ref {r} set differs beyond tolerance"

@@ -464,7 +464,7 @@ def _boxf_fits(s, b, Wn, K, C=1):
     pl = (7 * s + nblk * 8 + b) * (32 * s + Wn)
     hp = ((kp + 3) & ~3) + 2
     scr = 512 + (33 - ns) * hp if kr == 80 else max(512, (33 - ns) * (kr + 1))
-    return (((C * pl + 1) & ~1) + 8 * scr) * 4 <= (113 if C == 1 else 227) * 1024
+    return (((C * pl + 1) & ~1) + 8 * scr) * 4 <= 227 * 1024
 
 
 def _boxf_cases(n, seed):
@@ -1150,3 +1150,62 @@ def test_tcf_ties_and_extremes(kind):
         p = _tcf(x, b, s, 21, K, f"tcf {kind} s{s} b{b}")
         if kind == "constant":
             assert p.debug_fix_count() == p.n_refs  # every reference ties: exact fix-up
+
+
+# ------------------------------------------------------------------ NCC with wide lists (round 2)
+def _ncc_wide_cases(n, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shapes = [(3, 8), (1, 7), (4, 8), (2, 8)]
+    out = []
+    while len(out) < n:
+        s, b = shapes[len(out) % 4]
+        H, W = int(rng.integers(b + 8, 80)), int(rng.integers(b + 8, 110))
+        Wn, K = int(rng.integers(9, 46)), int(rng.integers(29, 77))
+        C = int(rng.choice([1, 1, 2, 4]))
+        if ((H - b) // s + 1) * ((W - b) // s + 1) * Wn * Wn * C > 2e7:
+            continue
+        out.append((s, b, C, H, W, Wn, K))
+    return out
+
+
+@pytest.mark.parametrize("case", _ncc_wide_cases(12, 909))
+def test_ncc_f32_wide_lists(case):
+    """NCC (Eq. 4) with K + m > 32 on float input: register lists of 40 / 48 keys or shared heaps
+    (K up to 76), channels summed, against oracle.ncc under the float NCC rule."""
+    from tests.parity import check_ncc
+    s, b, C, H, W, Wn, K = case
+    rng = np.random.Generator(np.random.PCG64(hash(case) % (1 << 32)))
+    x = synth.random_image(rng, 2, C, H, W, "f32")
+    p, gi, gd = _ncc_run(x, b, s, Wn, K, "f32")
+    oi, od = oracle.ncc(x, b, s, Wn, K)
+    for n in range(2):
+        check_ncc(x[n], b, s, Wn, K, gi[n], gd[n], oi[n], od[n], exact=False, where=f"ncc wide {case} img{n}")
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_ncc_c3_c4_full(name):
+    """The NCC metric on the WNNM-shaped c3 (K = 70) and the 4-channel c4 (K = 32): every reference."""
+    from tests.parity import check_ncc
+    cfg = synth.CONFIGS[name]
+    x = synth.make_input(cfg)
+    p, gi, gd = _ncc_run(x, cfg.b, cfg.s, cfg.Wn, cfg.K, "f32")
+    oi, od = oracle.ncc(x, cfg.b, cfg.s, cfg.Wn, cfg.K)
+    check_ncc(x[0], cfg.b, cfg.s, cfg.Wn, cfg.K, gi[0], gd[0], oi[0], od[0], exact=False, where=f"ncc {name} full")
+
+
+@pytest.mark.parametrize("K", [40, 70])
+def test_ncc_wide_lists_fixup(K):
+    """A constant / tiny-noise image ties every NCC: the wide-list references go to the exact fix-up,
+    whose float path ranks (float32 d_NCC, idx) 64-bit keys for K > 32."""
+    from tests.parity import check_ncc
+    H, W, b, s, Wn = 40, 56, 8, 3, 15
+    rng = np.random.Generator(np.random.PCG64(31))
+    for kind in ("constant", "tiny_noise"):
+        x = np.full((1, 1, H, W), 0.7, dtype=np.float32)
+        if kind == "tiny_noise":
+            x += (rng.standard_normal(x.shape) * 1e-3).astype(np.float32)
+        p, gi, gd = _ncc_run(x, b, s, Wn, K, "f32")
+        if kind == "constant":  # (references whose window holds fewer than K + m candidates keep all)
+            assert p.debug_fix_count() >= p.n_refs * 9 // 10
+        oi, od = oracle.ncc(x, b, s, Wn, K)
+        check_ncc(x[0], b, s, Wn, K, gi[0], gd[0], oi[0], od[0], exact=False, where=f"ncc wide fixup {kind} K{K}")

@@ -17,7 +17,7 @@ import pytest
 
 import oracle
 from paper_2006_13714_b200 import synth
-from tests.bm_numpy import all_patches as _all_patches, bm_np, ncc_np
+from tests.bm_numpy import all_patches as _all_patches, bm_np, ncc_np, bm3d_np
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "worked_3x3.json")
 
@@ -411,6 +411,32 @@ def test_ncc_invariants(dtype):
     np.testing.assert_allclose(d1, d2, atol=1e-12)
 
 
+def test_pair_ncc_pins():
+    """oracle.pair_ncc (explicit pairs, the full-size parity checks' D): the worked example's hand
+    NCC values (Lemma 1), an independent numpy loop, and the d_NCC oracle.ncc reports
+    for the pairs it selects."""
+    from tests.parity import pair_ncc as pair_ncc_np
+    g = json.load(open(GOLD))
+    img = np.array(g["image"], dtype=np.uint8)
+    Cm, nm = np.array(g["C"], float), np.array(g["norms"], float)
+    want = -(Cm / np.sqrt(nm[0, 0] * nm)).ravel()
+    got = oracle.pair_ncc(img[None], 2, [0] * 4, [0] * 4, [0, 0, 1, 1], [0, 1, 0, 1])
+    np.testing.assert_allclose(got, want, rtol=1e-15)
+    rng = _rng(77)
+    for dtype in ("u8", "f32"):
+        x = synth.random_image(rng, 1, 3, 19, 23, dtype)[0]
+        b, s, Wn, K = 5, 2, 9, 12
+        idx, dist = oracle.ncc(x, b, s, Wn, K)
+        ny, nx = oracle.grid(19, 23, b, s)
+        t = np.repeat(np.arange(ny * nx), K)
+        ry, rx = (t // nx) * s, (t % nx) * s
+        ii = idx[0].ravel()
+        d = oracle.pair_ncc(x, b, ry, rx, ii // 23, ii % 23)
+        np.testing.assert_allclose(d, dist[0].ravel(), atol=1e-14)
+        np.testing.assert_allclose(d[:200], pair_ncc_np(x, b, ry[:200], rx[:200], ii[:200] // 23, ii[:200] % 23),
+                                   atol=1e-12)
+
+
 # ---------------------------------------------------------------- NLM weights (Eq. 2, Prop. 1)
 def test_nlm_worked_example():
     """Eq. 2 on the hand-worked distances d = [0, 4, 36, 64] of ref (0,0) (worked_3x3.json) with
@@ -522,3 +548,62 @@ def test_temporal_translated_video():
         # frame 1's content at (y, x) is frame 0's at (y + 2, x + 1): frame 1 ref -> frame 0 (ry+2, rx+1)
         want = 0 * 30 * 32 + (ry + 2) * 32 + rx + 1
         assert want in idx[1, r].tolist() and dist[1, r, 0] == 0
+
+
+# ---------------------------------------------------------------- 3D search
+@pytest.mark.parametrize("dtype", ["u8", "f32"])
+@pytest.mark.parametrize("P,d,b,s,sz,Wn,c,K", [(4, 1, 3, 2, 1, 5, 3, 6), (6, 3, 3, 1, 1, 5, 2, 9),
+                                                (5, 2, 4, 3, 2, 7, 4, 11), (3, 3, 2, 1, 1, 3, 1, 4),
+                                                (7, 1, 2, 2, 3, 4, 9, 20)])
+def test_bm3d_vs_numpy_bruteforce(dtype, P, d, b, s, sz, Wn, c, K):
+    rng = _rng(800 + P * 11 + d + Wn)
+    x = synth.random_image(rng, 1, P, 11, 12, dtype)[0]
+    if dtype == "u8":
+        x[1:, :4, :4] = x[0, :4, :4]  # repeated content across planes: exact ties
+    gi, gd = oracle.bm3d(x, d, b, s, sz, Wn, c, K)
+    ni, nd = bm3d_np(x, d, b, s, sz, Wn, c, K)
+    np.testing.assert_array_equal(gi, ni)
+    if dtype == "u8":
+        np.testing.assert_array_equal(gd, nd)
+    else:
+        np.testing.assert_allclose(gd, nd, rtol=1e-12, atol=1e-12)
+
+
+def test_bm3d_special_cases():
+    """d = P, c = 1: multi-channel 2D BM (Eq. 12's channel sum); d = 1, c = 2T + 1: the temporal
+    search over the frames; c = 1, d = 1: per-plane 2D BM with the plane offset in idx."""
+    rng = _rng(901)
+    x = synth.random_image(rng, 1, 4, 19, 21, "f32")[0]
+    i3, d3 = oracle.bm3d(x, 4, 5, 2, 1, 7, 1, 9)
+    i2, d2 = oracle.bm(x, 5, 2, 7, 9)
+    np.testing.assert_array_equal(i3, i2)
+    np.testing.assert_array_equal(d3, d2)
+    it, dt = oracle.bm_temporal(x[:, None], 5, 2, 7, 9, 1)
+    i3, d3 = oracle.bm3d(x, 1, 5, 2, 1, 7, 3, 9)
+    np.testing.assert_array_equal(i3, it)
+    np.testing.assert_array_equal(d3, dt)
+    i3, d3 = oracle.bm3d(x, 1, 5, 2, 1, 7, 1, 9)
+    for z in range(4):
+        i2, d2 = oracle.bm(x[z], 5, 2, 7, 9)
+        np.testing.assert_array_equal(i3[z], i2[0] + z * 19 * 21)
+        np.testing.assert_array_equal(d3[z], d2[0])
+
+
+def test_bm3d_translated_volume():
+    """Planes that are one canvas shifted by (2, -3) per plane: every reference away from the
+    borders has an exact d = 0 match in the next plane at offset (+2, -3) (and the previous at
+    (-2, +3)); with c = 3 and a window covering the motion the K-th list holds both."""
+    rng = _rng(902)
+    canvas = synth.random_image(rng, 1, 1, 60, 60, "f32")[0, 0]
+    P, H, W, b = 4, 24, 24, 4
+    vol = np.stack([canvas[20 + 2 * z:20 + 2 * z + H, 20 - 3 * z:20 - 3 * z + W] for z in range(P)]).astype(np.float32)
+    idx, dist = oracle.bm3d(vol, 1, b, 4, 1, 9, 3, 3)
+    ny, nx = oracle.grid(H, W, b, 4)
+    for z in range(1, P - 1):
+        for r in range(ny * nx):
+            ry, rx = (r // nx) * 4, (r % nx) * 4
+            if not (2 <= ry <= H - b - 2 and 3 <= rx <= W - b - 3):
+                continue
+            want = {((z + 1) * H + ry - 2) * W + rx + 3, ((z - 1) * H + ry + 2) * W + rx - 3}
+            assert want <= set(idx[z, r].tolist())
+            assert (dist[z, r] == 0).all()  # self + the two motion-compensated matches
