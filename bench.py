@@ -306,6 +306,131 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def _pairs_3d(cfg, info, n_planes):
+    """Candidate pairs of one 3D step: per reference plane, the valid plane offsets x the 2D pairs."""
+    nz = (n_planes - cfg.d) // cfg.sz + 1
+    zlo, zhi = -(cfg.zwin // 2), cfg.zwin - 1 - cfg.zwin // 2
+    zc = [min(n_planes - cfg.d, z * cfg.sz + zhi) - max(0, z * cfg.sz + zlo) + 1 for z in range(nz)]
+    return nz, sum(zc) * info["total_candidates"]
+
+
+def _oracle_3d_sample(cfg, vol, n_sub):
+    """The oracle on the first n_sub planes (reference planes whose plane window lies inside them
+    see exactly the full volume's candidates)."""
+    import oracle
+    zhi = cfg.zwin - 1 - cfg.zwin // 2
+    t0 = time.perf_counter()
+    oi, od = oracle.bm3d(vol[:n_sub], cfg.d, cfg.b, cfg.s, cfg.sz, cfg.Wn, cfg.zwin, cfg.K)
+    dt = time.perf_counter() - t0
+    n_exact = max(0, (n_sub - cfg.d - zhi) // cfg.sz + 1)  # reference planes unaffected by the crop
+    return oi, od, dt, n_exact
+
+
+def bench_3d(args, cfg):
+    """3D search: one volume per step through sc_bm_run3d on the float box-sum
+    kernel with a plane loop; metric candidate distances/s; parity of the sampled reference planes."""
+    import torch
+    from paper_2006_13714_b200.bm import Plan3D
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    vol_h = synth_input = None
+    from paper_2006_13714_b200 import synth
+    vol_h = np.ascontiguousarray(synth.make_input(cfg)[0])
+    vol = torch.from_numpy(vol_h).cuda()
+    plan = Plan3D(cfg.H, cfg.W, cfg.d, cfg.b, cfg.s, cfg.Wn, cfg.sz, cfg.zwin, cfg.K)
+    info = plan.info()
+    P = vol_h.shape[0]
+    nz, pairs = _pairs_3d(cfg, info, P)
+    idx, dst = plan.alloc_out(nz)
+    for _ in range(args.warmup):
+        plan.run(vol, out=(idx, dst))
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = plan.info()["launches"]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            starts[k].record(stream)
+            plan.run(vol, out=(idx, dst))
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    ms = float(np.mean(step_ms))
+    peaks = _peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    macs = pairs * cfg.b * cfg.b * cfg.d
+    ffma = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    achieved = 2.0 * macs / (ms / 1e3) / 1e12
+    line = {"metric": METRIC, "value": pairs / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_min": float(np.min(step_ms)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "planes": P, "H": cfg.H, "W": cfg.W, "patch": [cfg.b, cfg.b, cfg.d],
+                       "stride": cfg.s, "window": [cfg.Wn, cfg.Wn, cfg.zwin], "plane_stride": cfg.sz, "K": cfg.K,
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "candidate_pairs_per_step": pairs, "ref_patches_per_s": nz * info["n_refs"] / (ms / 1e3),
+            "roofline": {"bound": "alu", "kernel": "bm_boxf_kernel (Z3)", "achieved": achieved, "peak": ffma,
+                         "unit": "TFLOP/s", "frac": achieved / ffma, "traffic": None,
+                         "algorithmic_flops_per_step": 2.0 * macs, "macs_per_pair": cfg.b * cfg.b * cfg.d,
+                         "peak_source": "FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz"},
+            "gpu_launches": int(plan.info()["launches"] - launches0), "clocks": clk.summary()}
+    if not args.no_cpu:
+        import oracle
+        n_sub = min(P, cfg.d + (cfg.zwin - 1 - cfg.zwin // 2) + 2 * cfg.sz)
+        oi, od, dt, n_exact = _oracle_3d_sample(cfg, vol_h, n_sub)
+        sub = Plan3D(cfg.H, cfg.W, cfg.d, cfg.b, cfg.s, cfg.Wn, cfg.sz, cfg.zwin, cfg.K)
+        _, p_sub = _pairs_3d(cfg, info, n_sub)
+        line["cpu_baseline"] = {"value": p_sub / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                                "sample": f"{cfg.name} planes 0:{n_sub} ({p_sub} candidate pairs), {dt:.2f} s"}
+        del sub
+        from tests.parity import check_f32_3d
+        gi, gd = idx[:n_exact].cpu().numpy(), dst[:n_exact].cpu().numpy()
+        what = f"reference planes 0:{n_exact} ({n_exact * info['n_refs']} references)"
+        try:
+            check_f32_3d(vol_h, cfg.d, cfg.b, cfg.s, cfg.sz, cfg.Wn, cfg.zwin, cfg.K, gi, gd, oi[:n_exact],
+                         od[:n_exact], "bench")
+            line["parity"] = {"checked": what, "rule": "f32 rule in 3D (tests/parity.py check_f32_3d)", "result": "pass"}
+        except AssertionError as e:
+            line["parity"] = {"checked": what, "result": "FAIL", "detail": str(e)[:300]}
+    print(json.dumps(line), flush=True)
+
+
+def run_reference_3d(args, cfg):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from paper_2006_13714_b200 import synth
+    vol = np.ascontiguousarray(synth.make_input(cfg)[0])
+    oracle.build()
+    n_sub = min(vol.shape[0], cfg.d + (cfg.zwin - 1 - cfg.zwin // 2) + 1)
+    for _ in range(args.warmup):
+        _oracle_3d_sample(cfg, vol[:, :64, :64].copy(), n_sub)
+    tot_p, tot_t = 0, 0.0
+    from types import SimpleNamespace
+    H, W = cfg.H, cfg.W
+    ny, nx = (H - cfg.b) // cfg.s + 1, (W - cfg.b) // cfg.s + 1
+    lo, hi = -(cfg.Wn // 2), cfg.Wn - 1 - cfg.Wn // 2
+    tc = sum(min(H - cfg.b, iy * cfg.s + hi) - max(0, iy * cfg.s + lo) + 1 for iy in range(ny)) * \
+        sum(min(W - cfg.b, ix * cfg.s + hi) - max(0, ix * cfg.s + lo) + 1 for ix in range(nx))
+    info = {"total_candidates": tc}
+    for _ in range(args.steps):
+        _, _, dt, _ = _oracle_3d_sample(cfg, vol, n_sub)
+        tot_p += _pairs_3d(cfg, info, n_sub)[1]
+        tot_t += dt
+    value = tot_p / tot_t
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                      "data": "synthetic", "config": {"workload": cfg.name},
+                      "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                                       "sample": f"{cfg.name} planes 0:{n_sub}"},
+                      "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
 def _dtype_name(cfg):
     return "int32" if cfg.dtype == "u8" else "f32"
 
@@ -436,7 +561,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c5")
+    ap.add_argument("--config", default="c5", help="c1..c5 (BASELINE.json configs), v1 / m1 (3D search)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -460,11 +585,15 @@ def main():
     _launch_ranks(args)
 
     from paper_2006_13714_b200 import synth
-    cfg = synth.CONFIGS[args.config]
+    cfg = synth.config_by_name(args.config)
+    if args.impl == "reference" and cfg.d > 0:
+        return run_reference_3d(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
     if args.selftest_cpu:
         return selftest_cpu(args, cfg)
+    if cfg.d > 0:
+        return bench_3d(args, cfg)
 
     import torch
     from paper_2006_13714_b200.bm import Plan

@@ -102,7 +102,7 @@ typedef struct {
 #define SC_KERNEL_BOX 3        /* box-sum matcher: 4x4 block sums of the shifted product image
                                   (u8, b = 8, stride 4, C = 1, K <= 32; default where supported) */
 #define SC_KERNEL_TC_F32 5     /* tcgen05 3xTF32 cross term (TMEM) + fused top-K (f32, C = 1, b <= 8) */
-#define SC_KERNEL_BOXF 4       /* float box-sum matcher (f32, C = 1, (stride, b) in {(3,8), (1,7),
+#define SC_KERNEL_BOXF 4       /* float box-sum matcher (f32, any C, (stride, b) in {(3,8), (1,7), (1,6),
                                   (4,8), (2,8)}, K + m <= 80; default where supported) */
 
 /*
@@ -222,6 +222,28 @@ sc_status_t sc_bm_set_temporal(sc_bm_plan_t plan, int32_t T);
 sc_status_t sc_bm_run_temporal(sc_bm_plan_t plan, const void* imgs, int64_t n_images, int64_t f_begin,
                                int64_t f_end, int64_t frame_offset, int32_t* idx_out, void* dist_out,
                                sc_stream_t stream);
+
+/*
+ * 3D search (3D Self-Convolution "searching across channels" with patches of d < p
+ * channels; the video setting, 6 x 6 x 1 patches in a 30 x 30 x c window, c = 9
+ * frames). A volume vol [n_planes][H][W] (float, device, 16-B aligned) -- the channels of one
+ * multi-channel image or the frames of a video -- is matched in 3D: a patch is d consecutive planes
+ * x b x b; references start at planes 0, z_stride, 2 z_stride, ... <= n_planes - d (n_zref of them)
+ * and on the usual spatial grid; the candidates of a reference at plane z are the patches starting
+ * at planes z + dz, dz in [-floor(z_window/2), z_window - 1 - floor(z_window/2)] (clipped to
+ * [0, n_planes - d]), at every clipped window position; the distance sums the d planes
+ * (oracle.bm3d). Outputs [n_zref][n_refs][K] (idx int32, dist float), idx = (z_c H + cy) W + cx
+ * (the volume raster of the candidate's first voxel), rows sorted by (dist, idx).
+ * sc_bm_plan3d: float only (uint8 video search: sc_bm_set_temporal), z_window <= 64, the float
+ * box-sum kernel's shapes ((stride, b) in {(3,8), (1,7), (4,8), (2,8), (1,6)}), K + 4 <= 48,
+ * z_window Wn^2 < 2^13 (else SC_ERR_UNSUPPORTED). A 3D plan refuses every other run call.
+ * sc_bm_run3d: n_planes >= d and n_planes H W <= 2^31 (SC_ERR_INVALID_ARGUMENT otherwise);
+ * asynchronous on `stream`, never allocates.
+ */
+sc_status_t sc_bm_plan3d(int H, int W, int d, int b, int stride, int window, int z_stride, int z_window, int K,
+                         sc_dtype_t dtype, sc_bm_plan_t* plan_out);
+sc_status_t sc_bm_run3d(sc_bm_plan_t plan, const void* vol, int64_t n_planes, int32_t* idx_out, void* dist_out,
+                        sc_stream_t stream);
 
 /* Plan geometry and bookkeeping. */
 sc_status_t sc_bm_plan_info(sc_bm_plan_t plan, sc_bm_info_t* info);

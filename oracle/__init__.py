@@ -49,6 +49,7 @@ def lib():
         L.sco_pair_dist.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
         L.sco_pair_ncc.argtypes = [vp, ci, ci, ci, ci, ci, ctypes.c_longlong, i32p, i32p, i32p, i32p, dp]
         L.sco_bm3d.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, vp, ci]
+        L.sco_pair_dist3d.argtypes = [vp, ci, ci, ci, ci, ci, ci, ctypes.c_longlong] + [i32p] * 6 + [dp]
         L.sco_num_threads.restype = ci
         L.sco_ncc_rows.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, dp, ci]
         L.sco_bm_temporal.argtypes = [vp, ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, i32p, vp, ci]
@@ -261,6 +262,21 @@ def pair_ncc(img: np.ndarray, b: int, ry, rx, cy, cx) -> np.ndarray:
                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     if rc != 0:
         raise ValueError("oracle.pair_ncc: invalid arguments")
+    return out
+
+
+def pair_dist3d(vol: np.ndarray, d: int, b: int, zr, ry, rx, zc, cy, cx) -> np.ndarray:
+    """Direct distances of explicit 3D pairs (d-plane patches) of a volume [P,H,W] (float64)."""
+    a = np.ascontiguousarray(vol)
+    P, H, W = a.shape
+    arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.int32).ravel()) for v in (zr, ry, rx, zc, cy, cx)]
+    n = arrs[0].size
+    out = np.empty(n, dtype=np.float64)
+    Pt = ctypes.POINTER(ctypes.c_int32)
+    rc = lib().sco_pair_dist3d(a.ctypes.data, _dtype_code(a), P, H, W, d, b, n, *[x.ctypes.data_as(Pt) for x in arrs],
+                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if rc != 0:
+        raise ValueError("oracle.pair_dist3d: invalid arguments")
     return out
 
 

@@ -614,3 +614,27 @@ int sco_bm3d(const void* vol, int dtype, int P, int H, int W, int d, int b, int 
     }
     return 0;
 }
+
+/* Direct distances of explicit 3D pairs (d-plane patches starting at planes zr / zc of a P-plane
+ * volume), double -- the definition of sco_bm3d for full-size parity checks of selected pairs. */
+int sco_pair_dist3d(const void* vol, int dtype, int P, int H, int W, int d, int b, long long n,
+                    const int32_t* zr, const int32_t* ry, const int32_t* rx, const int32_t* zc,
+                    const int32_t* cy, const int32_t* cx, double* out) {
+    if (!vol || !out || d < 1 || d > P || b < 1 || H < b || W < b) return -1;
+    const size_t plane = (size_t)H * W;
+    for (long long k = 0; k < n; ++k) {
+        if (zr[k] < 0 || zc[k] < 0 || zr[k] > P - d || zc[k] > P - d || ry[k] < 0 || rx[k] < 0 || cy[k] < 0 ||
+            cx[k] < 0 || ry[k] > H - b || cy[k] > H - b || rx[k] > W - b || cx[k] > W - b)
+            return -1;
+        double acc = 0.0;
+        for (int q = 0; q < d; ++q)
+            for (int l = 0; l < b; ++l)
+                for (int m = 0; m < b; ++m) {
+                    const double vr = px(vol, dtype, (size_t)(zr[k] + q) * plane + (size_t)(ry[k] + l) * W + rx[k] + m);
+                    const double vc = px(vol, dtype, (size_t)(zc[k] + q) * plane + (size_t)(cy[k] + l) * W + cx[k] + m);
+                    acc += (vr - vc) * (vr - vc);
+                }
+        out[k] = acc;
+    }
+    return 0;
+}

@@ -24,7 +24,7 @@ EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_b
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
             "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group",
             "sc_bm_nlm_weights", "sc_bm_set_temporal", "sc_bm_debug_fix_count", "sc_bm_nlm_average",
-            "sc_bm_run_temporal"]
+            "sc_bm_run_temporal", "sc_bm_plan3d", "sc_bm_run3d"]
 
 
 class ScError(RuntimeError):
@@ -84,6 +84,8 @@ def load_library():
     L.sc_bm_group.argtypes = [vp, vp, i64, vp, vp, vp]
     L.sc_bm_nlm_weights.argtypes = [vp, vp, ctypes.c_float, vp, vp]
     L.sc_bm_set_temporal.argtypes = [vp, i32]
+    L.sc_bm_plan3d.argtypes = [ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ctypes.POINTER(vp)]
+    L.sc_bm_run3d.argtypes = [vp, vp, i64, vp, vp, vp]
     for fn in EXPORTED:
         if fn != "sc_status_string":
             getattr(L, fn).restype = ci
@@ -302,6 +304,43 @@ class Plan:
         n = ctypes.c_int32(0)
         _check("sc_bm_debug_fix_count", self._lib.sc_bm_debug_fix_count(self._h, ctypes.byref(n)))
         return n.value
+
+
+class Plan3D(Plan):
+    """3D block matching over the planes of a float volume (``sc_bm_plan3d`` / ``sc_bm_run3d``):
+    patches of d planes x b x b, references every z_stride planes, candidates at z_window plane
+    offsets x the clipped spatial window. ``run(vol [P,H,W])`` returns
+    (idx, dist) [n_zref, n_refs, K], idx = (z * H + y) * W + x."""
+
+    def __init__(self, H, W, d, b, stride, window, z_stride, z_window, K, dtype="f32"):
+        self._lib = load_library()
+        self.H, self.W, self.C, self.b, self.s, self.Wn, self.K = H, W, d, b, stride, window, K
+        self.d, self.z_stride, self.z_window = d, z_stride, z_window
+        self.dtype, self.metric = dtype, "l2"
+        h = ctypes.c_void_p()
+        _check("sc_bm_plan3d", self._lib.sc_bm_plan3d(H, W, d, b, stride, window, z_stride, z_window, K,
+                                                      {"u8": SC_DTYPE_U8, "f32": SC_DTYPE_F32}[dtype], ctypes.byref(h)))
+        self._h = h
+        inf = self.info()
+        self.ny, self.nx, self.n_refs = inf["n_ref_y"], inf["n_ref_x"], inf["n_refs"]
+
+    def n_zref(self, n_planes: int) -> int:
+        return (n_planes - self.d) // self.z_stride + 1
+
+    def run(self, vol, out=None, stream=None):
+        import torch
+        v = vol.reshape(-1, self.H, self.W) if vol.dim() != 3 else vol
+        if v.dtype != torch.float32 or not v.is_cuda or not v.is_contiguous():
+            raise ValueError("expected a contiguous CUDA float32 volume [P, H, W]")
+        nz = self.n_zref(v.shape[0])
+        if out is None:
+            idx, dist = self.alloc_out(nz)
+        else:
+            idx, dist = self._check_out(out, nz, self.n_refs, True)
+        _check("sc_bm_run3d", self._lib.sc_bm_run3d(self._h, ctypes.c_void_p(v.data_ptr()), v.shape[0],
+                                                    ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
+                                                    _stream_ptr(stream)))
+        return idx, dist
 
 
 def status_string(code: int) -> str:

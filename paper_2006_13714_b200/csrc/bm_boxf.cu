@@ -47,6 +47,10 @@ struct BoxfArgs {
   int scr;          // per-warp scratch words (survivor staging [+ output staging | + heaps])
   int hp;           // heap pitch (words per reference) when the top-KP lives in shared heaps
   int lofs;         // WS = 2: word offset of the per-row list area (0: the staged region, reused)
+  // Z3 (3D search over the planes of a volume, PAPER.md:548 / 697): the launch's reference plane
+  // positions z0 .. z0 + gridDim.y - 1 (first plane (z0 + f) * sz), volume planes P, plane offsets
+  // [zlo, zhi] of the candidates; C = the patch depth d
+  int z0, sz, P, zlo, zhi, zwin;
   int rb;           // window-relative index bits of the 32-bit keys
   int* fix_count;   // references the key quantisation leaves open -> exact fix-up (fixup.cu)
   int* fix_list;
@@ -78,7 +82,10 @@ __device__ __forceinline__ float hcombine(float ef, float ep) {
 // reference, so the KP-th best of their union can only be smaller -- a valid superset bound); the
 // second half's list is merged into the first's before a5. Doubles the warps per staged region
 // where the grid or the shared memory leaves the SMs half empty (c2: 132 CTAs; c4: 216 KB, 1 CTA/SM).
-template <int S, int BK, int VY, int KR, bool C1, bool NCC, typename TIN, int WS = 1>
+// Z3 (3D search): the reference planes are staged once, the candidate planes of every plane offset
+// (centre-out) are restaged into a second region; keys carry (offset index) Wn^2 + slot; idx is the
+// volume raster (z H + y) W + x of the candidate's first voxel.
+template <int S, int BK, int VY, int KR, bool C1, bool NCC, typename TIN, int WS = 1, bool Z3 = false>
 __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_kernel(BoxfArgs a) {
   constexpr int NS = (BK + S - 1) / S;   // strips per patch
   constexpr int WL = BK - (NS - 1) * S;  // width of the last strip
@@ -97,7 +104,10 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   // (halves the identity's cancellation); NCC keeps the raw values (not shift-invariant, Eq. 4)
   const int nch = C1 ? 1 : a.C;
   const size_t plane = size_t(a.H) * a.W;
-  const TIN* img = static_cast<const TIN*>(a.imgs) + size_t(f) * nch * plane;
+  const int zr = Z3 ? (a.z0 + f) * a.sz : 0;  // Z3: the reference patch's first plane
+  const TIN* const vol = static_cast<const TIN*>(a.imgs);
+  const TIN* img = Z3 ? vol + size_t(zr) * plane : vol + size_t(f) * nch * plane;
+  const int regw = (Z3 ? 2 : 1) * nch * a.PL;  // staged floats: reference (+ candidate) planes
   const float shift = NCC ? 0.f : 0.5f;
   for (int e = threadIdx.x; e < nch * a.PL; e += blockDim.x) {
     const int c = e / a.PL, e2 = e - c * a.PL;
@@ -107,13 +117,13 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
                  ? float(__ldg(img + c * plane + size_t(yy) * a.W + xx)) - shift : 0.f;
   }
   // published KP-th keys of the two window halves (WS = 2), +inf until a list fills
-  uint32_t* pub = reinterpret_cast<uint32_t*>(smf + ((nch * a.PL + 1) & ~1)) + kFWarps * WS * a.scr;
+  uint32_t* pub = reinterpret_cast<uint32_t*>(smf + ((regw + 1) & ~1)) + kFWarps * WS * a.scr;
   if (WS == 2) pub[warp * 32 + lane] = 0xffffffffu;
   __syncthreads();
 
   const int iy0 = iy_first + wr;
   const bool wact = iy0 < a.iy_end;  // warp-uniform
-  if (WS == 1 && !wact) return;
+  if (WS == 1 && !Z3 && !wact) return;  // (Z3: every warp joins the restaging barriers)
   const int ix = ix_first + lane;
   const bool lane_ok = lane < RX && ix < a.nx;
   const int rx = ix * S, ry = iy0 * S;
@@ -157,7 +167,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
   }
   // (helper lanes RX..31 never insert; they alias lane RX-1's heap for the root reads)
-  uint32_t* const scr0 = reinterpret_cast<uint32_t*>(smf + ((nch * a.PL + 1) & ~1));  // 8-byte aligned
+  uint32_t* const scr0 = reinterpret_cast<uint32_t*>(smf + ((regw + 1) & ~1));  // 8-byte aligned
   uint32_t* heap = scr0 + warp * a.scr + 64 * VY + min(lane, RX - 1) * a.hp;
   uint32_t* const pub_own = pub + warp * 32 + lane;
   const uint32_t* const pub_other = pub + ((1 - hh) * kFWarps + wr) * 32 + lane;
@@ -230,6 +240,26 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   // the uint8 box kernel: thresholds tighten sooner; measured on c2 / c4). Heap lists (c3, K = 70)
   // measured slower with the split: one phase.
   const int kNearPairs = HEAP ? span + 1 : 5;
+  // Z3: candidate plane offsets centre-out (0, +1, -1, ...), each restaged into the second region
+  float* const creg = smf + (Z3 ? nch * a.PL : 0);
+  for (int kz = 0; kz < (Z3 ? 2 * a.zwin : 1); ++kz) {
+  int relz = 0;
+  if constexpr (Z3) {
+    const int dz = centre_out_f(kz);
+    const int zc = zr + dz;
+    if (dz < a.zlo || dz > a.zhi || zc < 0 || zc > a.P - nch) continue;  // CTA-uniform
+    relz = (dz - a.zlo) * a.Wn * a.Wn;
+    __syncthreads();  // every warp is done with the previous candidate planes
+    const TIN* cimg = vol + size_t(zc) * plane;
+    for (int e = threadIdx.x; e < nch * a.PL; e += blockDim.x) {
+      const int c = e / a.PL, e2 = e - c * a.PL;
+      const int r = e2 / a.RWp, x = e2 - r * a.RWp;
+      const int yy = Ybase + r, xx = Xbase + x;
+      creg[e] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
+                    ? float(__ldg(cimg + c * plane + size_t(yy) * a.W + xx)) - shift : 0.f;
+    }
+    __syncthreads();
+  }
   if (wact) {  // (WS = 2: an inactive warp still joins the merge barrier below)
   for (int ph = 0; ph < 2; ++ph) {
   const int j_begin = ph == 0 ? 0 : kNearPairs, j_end = ph == 0 ? min(kNearPairs, span + 1) : span + 1;
@@ -241,7 +271,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     const int ilo = max(0, -cy0), ihi = min(min(VY - 1, a.hi - dy0), a.H - BK - cy0);
     if (ihi < ilo) continue;  // warp-uniform
     const unsigned rows = ((2u << ihi) - 1u) & ~((1u << ilo) - 1u);
-    const float* cbase = smf + (rr0 + dy0) * a.RWp + rc0;
+    const float* cbase = creg + (rr0 + dy0) * a.RWp + rc0;
     const unsigned rmask = lane_ok ? rows : 0u;
     // one offset group (fixed dx, offsets dy0 .. dy0+VY-1) into staging half H (compile time)
     auto group = [&](int dx, auto hc) -> int {
@@ -316,7 +346,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
         for (int i = 0; i < VY; ++i) sc[32 * i] = __float_as_uint(fmaxf(dpv[i] + nadd, 0.f));
         pend |= bits << (H * VY);
       }
-      return (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
+      return relz + (dy0 - a.lo) * a.Wn + (dx - a.lo) + 1;  // rel + 1 >= 1 (0 = sentinel)
     };
     // dx centre-out (0, 1, -1, 2, -2, ...): pairs (-j, j+1) staged in the two halves and
     // flushed together (a round lasts as long as the busiest lane); a lone group flushes alone
@@ -330,6 +360,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   }
   }  // phases
   }  // wact
+  }  // plane offsets (Z3)
 
   if constexpr (WS == 2) {
     // merge the second half's list into the first's (0 sentinels skipped), then only the first
@@ -529,13 +560,20 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       if constexpr (HEAP) kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
       else kk = k < KR ? scratch[j * (KR + 1) + k] : 0xffffffffu;
       if (kk != 0u && kk != 0xffffffffu) {
-        const int rel = int(kk & ((1u << rb) - 1u)) - 1;
+        int rel = int(kk & ((1u << rb) - 1u)) - 1;
+        int zc = 0;
+        if constexpr (Z3) {  // plane offset index, then the window slot
+          const int zi = rel / (a.Wn * a.Wn);
+          rel -= zi * a.Wn * a.Wn;
+          zc = zr + a.zlo + zi;
+        }
         const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
         const int cy = ry + dyy + a.lo, cx = rxj + dxx + a.lo;
+        const float* cimg = Z3 ? reinterpret_cast<const float*>(vol) + size_t(zc) * plane : img;
         float d = 0.f;
         for (int c = 0; c < nch; ++c) {
           const float* pr = img + c * plane + size_t(ry) * a.W + rxj;
-          const float* pc = img + c * plane + size_t(cy) * a.W + cx;
+          const float* pc = cimg + c * plane + size_t(cy) * a.W + cx;
           for (int l = 0; l < BK; ++l)
 #pragma unroll
             for (int m = 0; m < BK; ++m) {
@@ -543,7 +581,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
               d = fmaf(df, df, d);
             }
         }
-        key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * a.W + cx);
+        key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t((Z3 ? zc * a.H : 0) * a.W + cy * a.W + cx);
       }
       top.merge(key, lane);
     }
@@ -588,7 +626,7 @@ constexpr int kFVY = 8;
 size_t boxf_bytes(const Geometry& g, int KR, int ws, BoxfArgs* a);
 
 int boxf_ws(const Geometry& g, int KR) {
-  if (KR > 48 || g.metric != SC_METRIC_L2) return 1;
+  if (KR > 48 || g.metric != SC_METRIC_L2 || g.z3) return 1;
   const int ns = (g.b + g.s - 1) / g.s, rx = 33 - ns;
   const long long ctas = (long long)((g.nx + rx - 1) / rx) * ((g.ny + kFWarps - 1) / kFWarps);
   if (!(g.C > 1 || ctas < 2 * 148)) return 1;
@@ -609,7 +647,7 @@ size_t boxf_bytes(const Geometry& g, int KR, int ws, BoxfArgs* a) {
   a->hp = ((g.KP + 2 + 1) & ~3) + 2;
   // per warp: two staged offset groups (+ the heaps, or the output lists with WS = 1)
   a->scr = KR > 48 ? 64 * kFVY + rx * a->hp : ws == 2 ? 64 * kFVY : std::max(64 * kFVY, rx * (KR + 1));
-  const size_t region = size_t((g.C * a->PL + 1) & ~1);
+  const size_t region = size_t(((g.z3 ? 2 : 1) * g.C * a->PL + 1) & ~1);  // (3D: + candidate planes)
   const size_t base = region + size_t(kFWarps) * ws * a->scr + (ws == 2 ? 2 * kFWarps * 32 : 0);
   // WS = 2: the per-row list areas reuse the staged region when it is large enough
   const size_t lists = size_t(kFWarps) * rx * (KR + 1);
@@ -618,11 +656,15 @@ size_t boxf_bytes(const Geometry& g, int KR, int ws, BoxfArgs* a) {
 }
 
 // key bits of the window-relative index + 1 (values 1 .. Wn^2; 0 is the sentinel)
-int boxf_rel_bits(int Wn) {
+// key bits of the window-relative index + 1 (values 1 .. n slots; 0 is the sentinel)
+int rel_bits_n(long long n) {
   int rb = 1;
-  while ((1 << rb) <= Wn * Wn) ++rb;
+  while ((1ll << rb) <= n) ++rb;
   return rb;
 }
+int boxf_rel_bits(int Wn) { return rel_bits_n((long long)Wn * Wn); }
+// 3D search: (plane offset, window slot) = zwin Wn^2 slots
+int boxf_rel_bits_g(const Geometry& g) { return rel_bits_n((long long)(g.z3 ? g.zwin : 1) * g.Wn * g.Wn); }
 
 // register list length: the smallest instantiated size >= KP (an insertion costs 2 KR - 1 IMNMX)
 int boxf_kr(const Geometry& g) {
@@ -630,12 +672,16 @@ int boxf_kr(const Geometry& g) {
 }
 
 template <int S, int BK, int KR, bool NCC = false, typename TIN = float>
-cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st, int ws = 1) {
+cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st, int ws = 1, bool z3 = false) {
   const int tiles_y = (a.iy_end - a.iy_begin + kFWarps - 1) / kFWarps;
   auto k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN> : bm_boxf_kernel<S, BK, kFVY, KR, false, NCC, TIN>;
   if constexpr (KR <= 48 && !NCC) {
     if (ws == 2) k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN, 2>
                               : bm_boxf_kernel<S, BK, kFVY, KR, false, NCC, TIN, 2>;
+  }
+  if constexpr (!NCC) {
+    if (z3) k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN, 1, true>
+                         : bm_boxf_kernel<S, BK, kFVY, KR, false, NCC, TIN, 1, true>;
   }
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<dim3(a.tiles_x * tiles_y, F), kFWarps * 32 * ws, smem, st>>>(a);
@@ -650,11 +696,13 @@ bool boxf_supported(const Geometry& g) {
   // NCC: uint8 keeps the exact 128-bit re-rank of <= 32 kept keys; float input takes wider lists
   if (g.metric == SC_METRIC_NCC && g.KP > (g.dtype == SC_DTYPE_U8 ? 32 : 80)) return false;
   const bool shape = (g.s == 3 && g.b == 8) || (g.s == 1 && g.b == 7) || (g.s == 4 && g.b == 8) ||
-                     (g.s == 2 && g.b == 8);
+                     (g.s == 2 && g.b == 8) || (g.s == 1 && g.b == 6);
   if (!shape) return false;
   const int kr = boxf_kr(g);
   if (kr == 0) return false;
-  if (boxf_rel_bits(g.Wn) > 12) return false;  // keeps >= 20 distance bits in the 32-bit keys
+  // keeps >= 20 distance bits in the 32-bit keys (>= 19 with the 3D search's plane offsets)
+  if (boxf_rel_bits_g(g) > (g.z3 ? 13 : 12)) return false;
+  if (g.z3 && (g.metric != SC_METRIC_L2 || kr > 48)) return false;  // 3D: L2 with register lists
   BoxfArgs a{};
   // up to the whole SM's shared memory (one channel with register lists normally fits two CTAs)
   return boxf_layout(g, kr, &a) <= 227 * 1024;
@@ -674,7 +722,13 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
   a.iy_begin = iy_begin; a.iy_end = iy_end;
   const int ns = (g.b + g.s - 1) / g.s;
   a.tiles_x = (g.nx + (33 - ns) - 1) / (33 - ns);
-  a.rb = boxf_rel_bits(g.Wn);
+  a.rb = boxf_rel_bits_g(g);
+  a.z0 = int(p.batch_f0);
+  a.sz = p.zstride;
+  a.P = int(p.n_planes);
+  a.zlo = p.zlo;
+  a.zhi = p.zhi;
+  a.zwin = g.zwin;
   const int kr = boxf_kr(g);  // the layout and the instantiation use the same list size
   const size_t smem = boxf_layout(g, kr, &a);
   if (launches) *launches += 1;
@@ -695,22 +749,25 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
     SCBM_NCC_CASE(1, 7)
     SCBM_NCC_CASE(4, 8)
     SCBM_NCC_CASE(2, 8)
+    SCBM_NCC_CASE(1, 6)
 #undef SCBM_NCC_CASE
     return cudaErrorInvalidValue;
   }
   const int ws = boxf_ws(g, kr);
+  const bool z3 = g.z3 != 0;
 #define SCBM_BOXF_CASE(S_, B_)                                                    \
   if (g.s == S_ && g.b == B_) {                                                   \
-    if (kr == 24) return launch_boxf_t<S_, B_, 24>(a, F, smem, st, ws);           \
-    if (kr == 32) return launch_boxf_t<S_, B_, 32>(a, F, smem, st, ws);           \
-    if (kr == 40) return launch_boxf_t<S_, B_, 40>(a, F, smem, st, ws);           \
-    if (kr == 48) return launch_boxf_t<S_, B_, 48>(a, F, smem, st, ws);           \
+    if (kr == 24) return launch_boxf_t<S_, B_, 24>(a, F, smem, st, ws, z3);       \
+    if (kr == 32) return launch_boxf_t<S_, B_, 32>(a, F, smem, st, ws, z3);       \
+    if (kr == 40) return launch_boxf_t<S_, B_, 40>(a, F, smem, st, ws, z3);       \
+    if (kr == 48) return launch_boxf_t<S_, B_, 48>(a, F, smem, st, ws, z3);       \
     return launch_boxf_t<S_, B_, 80>(a, F, smem, st);                             \
   }
   SCBM_BOXF_CASE(3, 8)
   SCBM_BOXF_CASE(1, 7)
   SCBM_BOXF_CASE(4, 8)
   SCBM_BOXF_CASE(2, 8)
+  SCBM_BOXF_CASE(1, 6)
 #undef SCBM_BOXF_CASE
   return cudaErrorInvalidValue;
 }

@@ -26,6 +26,9 @@ struct FixArgs {
   int T, n_frames, frame0;  // temporal search: frames fref-T..fref+T of the batch at imgs
   int ncc;                  // SC_METRIC_NCC: exact NCC re-rank (K <= 32), dist_out = -NCC (float)
   int idx_foff;             // temporal search: frame offset added to the batch-global idx
+  // 3D search (sc_bm_plan3d): reference plane (frame0 + f) * sz of a P-plane volume at imgs,
+  // candidates at plane offsets [zlo, zhi] (clipped to [0, P - C]), idx = (z H + y) W + x
+  int z3, sz, P, zlo, zhi;
 };
 
 // NCC (Eq. 4): a reference whose kept top-(K+8) could have lost a top-K candidate to the 32-bit
@@ -159,10 +162,14 @@ __global__ void __launch_bounds__(256) fixup_kernel(FixArgs a) {
     const int ncols = cx1 - cx0 + 1, nwin = (cy1 - cy0 + 1) * ncols;
     const size_t plane = size_t(a.H) * a.W;
     const int fref = a.frame0 + f;  // the reference's frame (temporal: index into the batch)
-    const int fa = max(0, fref - a.T), fb = min(a.n_frames - 1, fref + a.T);
+    // candidate frames (planes with the 3D search) fa .. fb; zunit = planes per frame step
+    const int zr = a.z3 ? fref * a.sz : fref;
+    const int fa = a.z3 ? max(0, zr + a.zlo) : max(0, fref - a.T);
+    const int fb = a.z3 ? min(a.P - a.C, zr + a.zhi) : min(a.n_frames - 1, fref + a.T);
+    const int zunit = a.z3 ? 1 : a.C;
     const int ncand = nwin * (fb - fa + 1);
     const TIN* imgs = static_cast<const TIN*>(a.imgs);
-    const TIN* rimg = imgs + size_t(fref) * a.C * plane;
+    const TIN* rimg = imgs + size_t(zr) * zunit * plane;
     WarpTopK<4> top;  // K <= 128
     top.init();
     for (int base = 0; base < ncand; base += 32) {
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(FixArgs a) {
       if (k < ncand) {
         const int fr = fa + k / nwin, kw = k - (k / nwin) * nwin;
         const int cy = cy0 + kw / ncols, cx = cx0 + kw % ncols;
-        const TIN* cimg = imgs + size_t(fr) * a.C * plane;
+        const TIN* cimg = imgs + size_t(fr) * zunit * plane;
         int di = 0;      // uint8: exact integers
         float df = 0.f;  // float: direct differences in fp32 (as the a5 re-score)
         for (int c = 0; c < a.C; ++c)
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(256) fixup_kernel(FixArgs a) {
             }
           }
         // idx: frame-local without temporal search, batch-global with it
-        const int idx = (a.T > 0 ? (fr + a.idx_foff) * int(plane) : 0) + cy * a.W + cx;
+        const int idx = (a.z3 ? fr * int(plane) : a.T > 0 ? (fr + a.idx_foff) * int(plane) : 0) + cy * a.W + cx;
         const uint32_t dbits = U8 ? uint32_t(di) : __float_as_uint(df);  // d >= 0: monotone bits
         key = (uint64_t(dbits) << 32) | uint32_t(idx);
       }
@@ -227,7 +234,12 @@ cudaError_t launch_fixup(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
   a.nx = g.nx; a.iy_begin = iy_begin; a.iy_end = iy_end;
   a.T = p.T;
   a.ncc = g.metric == SC_METRIC_NCC;
-  if (p.T > 0) {  // temporal search: the batch base and the chunk's first frame
+  a.z3 = g.z3;
+  a.sz = p.zstride;
+  a.P = int(p.n_planes);
+  a.zlo = p.zlo;
+  a.zhi = p.zhi;
+  if (p.T > 0 || g.z3) {  // temporal / 3D search: the batch (volume) base and the chunk's first frame
     a.imgs = p.batch_base;
     a.frame0 = int(p.batch_f0);
     a.n_frames = int(p.batch_n);

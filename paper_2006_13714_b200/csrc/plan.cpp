@@ -93,7 +93,8 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
   const int chunk = ((p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF) && dense == nullptr && !avg) ? p->FB : p->F;
   for (int64_t f0 = f_begin; f0 < f_end; f0 += chunk) {
     const int F = int(std::min<int64_t>(chunk, f_end - f0));
-    const void* src = static_cast<const char*>(imgs) + f0 * img_bytes;
+    // (3D search: every launch reads the whole volume; its chunk of reference planes starts at f0)
+    const void* src = g.z3 ? imgs : static_cast<const char*>(imgs) + f0 * img_bytes;
     cudaEvent_t* ev = nullptr;
     Timing& tm = p->timing;
     if (tm.enabled && size_t(tm.n_used + 1) * 3 <= tm.ev.size()) {
@@ -269,6 +270,7 @@ sc_status_t sc_bm_run_rows(sc_bm_plan_t p, const void* imgs, int64_t n_images, i
   if (!p || !imgs || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
   if (iy_begin < 0 || iy_end > p->g.ny || iy_end < iy_begin) return SC_ERR_INVALID_ARGUMENT;
+  if (p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   // temporal search reports batch-global idx = frame * H * W + pixel, which must stay int32
   if (p->T > 0 && n_images * int64_t(p->g.H) * p->g.W > (int64_t(1) << 31)) return SC_ERR_INVALID_ARGUMENT;
   sc_status_t s = check_device(p);
@@ -281,6 +283,7 @@ sc_status_t sc_bm_run_rows(sc_bm_plan_t p, const void* imgs, int64_t n_images, i
 sc_status_t sc_bm_run_temporal(sc_bm_plan_t p, const void* imgs, int64_t n_images, int64_t f_begin,
                                int64_t f_end, int64_t frame_offset, int32_t* idx_out, void* dist_out,
                                sc_stream_t stream) {
+  if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !imgs || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
   if (f_begin < 0 || f_end > n_images || f_end < f_begin) return SC_ERR_INVALID_ARGUMENT;
@@ -297,6 +300,42 @@ sc_status_t sc_bm_run_temporal(sc_bm_plan_t p, const void* imgs, int64_t n_image
   return s;
 }
 
+sc_status_t sc_bm_plan3d(int H, int W, int d, int b, int stride, int window, int z_stride, int z_window, int K,
+                         sc_dtype_t dtype, sc_bm_plan_t* plan_out) {
+  if (!plan_out) return SC_ERR_INVALID_ARGUMENT;
+  *plan_out = nullptr;
+  if (z_stride < 1 || z_window < 1 || z_window > 64) return SC_ERR_INVALID_ARGUMENT;
+  if (dtype != SC_DTYPE_F32) return SC_ERR_UNSUPPORTED;  // (uint8 video: sc_bm_set_temporal)
+  sc_bm_plan_t p = nullptr;
+  sc_status_t st = sc_bm_plan_ex(H, W, d, b, stride, window, K, dtype, SC_METRIC_L2, &p);
+  if (st != SC_OK) return st;
+  p->g.z3 = 1;
+  p->g.zwin = z_window;
+  p->zstride = z_stride;
+  p->zlo = -(z_window / 2);
+  p->zhi = z_window - 1 - z_window / 2;
+  if (!boxf_supported(p->g)) {
+    sc_bm_destroy(p);
+    return SC_ERR_UNSUPPORTED;
+  }
+  p->kernel = SC_KERNEL_BOXF;
+  *plan_out = p;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_run3d(sc_bm_plan_t p, const void* vol, int64_t n_planes, int32_t* idx_out, void* dist_out,
+                        sc_stream_t stream) {
+  if (!p || !vol || !idx_out || !dist_out) return SC_ERR_INVALID_ARGUMENT;
+  if (!p->g.z3) return SC_ERR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(vol) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
+  if (n_planes < p->g.C || n_planes * int64_t(p->g.H) * p->g.W > (int64_t(1) << 31)) return SC_ERR_INVALID_ARGUMENT;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  const int64_t nz = (n_planes - p->g.C) / p->zstride + 1;
+  p->n_planes = n_planes;
+  return enqueue(p, vol, nz, 0, p->g.ny, idx_out, dist_out, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
 sc_status_t sc_bm_run_batch(sc_bm_plan_t p, const void* imgs, int64_t n_images, int32_t* idx_out,
                             void* dist_out, sc_stream_t stream) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
@@ -309,6 +348,7 @@ sc_status_t sc_bm_run(sc_bm_plan_t p, const void* img, int32_t* idx_out, void* d
 }
 
 sc_status_t sc_bm_run_dense_debug(sc_bm_plan_t p, const void* img, void* dist_all, sc_stream_t stream) {
+  if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !img || !dist_all) return SC_ERR_INVALID_ARGUMENT;
   if (p->g.metric != SC_METRIC_L2) return SC_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(img) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
@@ -328,6 +368,7 @@ sc_status_t sc_bm_debug_fix_count(sc_bm_plan_t p, int32_t* count_out) {
 }
 
 sc_status_t sc_bm_nlm_weights(sc_bm_plan_t p, const void* img, float h, float* weights_out, sc_stream_t stream) {
+  if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !img || !weights_out || !(h > 0.f) || !std::isfinite(h)) return SC_ERR_INVALID_ARGUMENT;
   if (p->g.metric != SC_METRIC_L2) return SC_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(img) & 15) != 0 || (reinterpret_cast<uintptr_t>(weights_out) & 3) != 0)
@@ -347,6 +388,7 @@ sc_status_t sc_bm_nlm_weights(sc_bm_plan_t p, const void* img, float h, float* w
 }
 
 sc_status_t sc_bm_nlm_average(sc_bm_plan_t p, const void* img, float h, float* out, sc_stream_t stream) {
+  if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !img || !out || !(h > 0.f) || !std::isfinite(h)) return SC_ERR_INVALID_ARGUMENT;
   if (p->g.metric != SC_METRIC_L2 || p->g.b * p->g.b * p->g.C > 256) return SC_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(img) & 15) != 0 || (reinterpret_cast<uintptr_t>(out) & 3) != 0)
@@ -364,6 +406,7 @@ sc_status_t sc_bm_nlm_average(sc_bm_plan_t p, const void* img, float h, float* o
 }
 
 sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_stream_t stream) {
+  if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !img || !norm_out) return SC_ERR_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(img) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
   sc_status_t s = check_device(p);
@@ -378,6 +421,7 @@ sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_s
 
 sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images, int32_t* h_idx,
                            void* h_dist, sc_stream_t stream) {
+  if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !h_imgs || !h_idx || !h_dist || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
   if (p->T > 0) return SC_ERR_UNSUPPORTED;  // chunked staging has no neighbouring frames
   sc_status_t s = check_device(p);
@@ -457,6 +501,7 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
 
 sc_status_t sc_bm_group(sc_bm_plan_t p, const void* imgs, int64_t n_images, const int32_t* idx,
                         void* groups_out, sc_stream_t stream) {
+  if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !imgs || !idx || !groups_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0 || (reinterpret_cast<uintptr_t>(groups_out) & 15) != 0 ||
       (reinterpret_cast<uintptr_t>(idx) & 3) != 0)
@@ -487,6 +532,7 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
 
 sc_status_t sc_bm_set_temporal(sc_bm_plan_t p, int32_t T) {
   if (!p || T < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (p->g.z3) return SC_ERR_UNSUPPORTED;
   if (T > 0 && !box_temporal_supported(p->g, T)) return SC_ERR_UNSUPPORTED;
   if (T > 0 && p->T == 0) p->kernel_before_T = p->kernel;
   if (T == 0 && p->T > 0 && p->kernel_before_T >= 0) {  // back to the matcher the plan had
@@ -501,6 +547,7 @@ sc_status_t sc_bm_set_temporal(sc_bm_plan_t p, int32_t T) {
 sc_status_t sc_bm_set_kernel(sc_bm_plan_t p, int32_t kernel) {
   if (!p) return SC_ERR_INVALID_ARGUMENT;
   if (p->T > 0 && kernel != SC_KERNEL_BOX) return SC_ERR_UNSUPPORTED;
+  if (p->g.z3 && kernel != SC_KERNEL_BOXF) return SC_ERR_UNSUPPORTED;
   if (p->g.metric == SC_METRIC_NCC && kernel != SC_KERNEL_BOXF && kernel != SC_KERNEL_BOX) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_SIMT && lanes_smem_bytes(p->g, p->lanes_nwy) > 227 * 1024) return SC_ERR_UNSUPPORTED;
   if (kernel == SC_KERNEL_TC_I8 && !tc_supported(p->g)) return SC_ERR_UNSUPPORTED;

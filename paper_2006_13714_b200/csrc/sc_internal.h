@@ -20,6 +20,8 @@ struct Geometry {
   long long NFS;      // norm-map frame stride in elements ((My + 2*NPAD) * Mxp)
   int KP;             // keys kept per ref before output (K, or K+rescore margin for f32 / NCC)
   int metric;         // SC_METRIC_L2 (Eq. 3) or SC_METRIC_NCC (Eq. 4)
+  int z3 = 0;         // 3D search over volume planes (sc_bm_plan3d): C = the patch depth d
+  int zwin = 1;       // 3D: plane offsets per reference (the window depth c)
 };
 
 // Workspace for one chunk of frames.
@@ -80,6 +82,8 @@ struct sc_bm_plan_s {
   int64_t batch_f0 = 0, batch_n = 0;  // ... the current chunk's first frame and the batch size
   int64_t idx_frame_off = 0;          // sc_bm_run_temporal: frame offset of the batch-global idx
   int64_t min_cand = 0, max_cand = 0, total_cand = 0;
+  int zstride = 1, zlo = 0, zhi = 0;  // 3D search: reference plane stride, plane offsets [zlo, zhi]
+  int64_t n_planes = 0;               // 3D search: planes of the volume of the current sc_bm_run3d
 };
 
 namespace scbm {

@@ -17,6 +17,13 @@ these generators stand in with the paper's workload *shapes* (SURVEY.md section 
   noise on RGB only.
 * c5: 64 u8 frames 1080x1920, crops of one large canvas along a seeded random walk
   (integer translation of up to 8 px per frame).
+
+3D search workloads (the next row SURVEY.md 8f rank 4; PAPER.md:696-697's multi-channel task,
+256 x 256 x q data, patch stride 1, 6 x 6 x d patches, 30 x 30 x c windows):
+* v1 (SALT video): 20 float32 frames 256x256 = crops of one canvas along a seeded random walk,
+  /255 + N(0, (25/255)^2); d = 1, c = 9 frames.
+* m1 (Self-MM multi-modality): a 6-plane 256x256 float32 image (gains x luma + independent
+  sinusoids per plane, noise sigma 25/255); d = 3, c = 2.
 """
 from __future__ import annotations
 
@@ -24,7 +31,7 @@ import dataclasses
 
 import numpy as np
 
-__all__ = ["BMConfig", "CONFIGS", "G", "make_input", "config_by_name"]
+__all__ = ["BMConfig", "CONFIGS", "CONFIGS3D", "G", "make_input", "config_by_name"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -42,6 +49,9 @@ class BMConfig:
     seed: int
     noise_seed: int = 0
     sigma: float = 0.0
+    d: int = 0        # 3D search: patch depth in planes (0 = 2D block matching)
+    sz: int = 1       # 3D search: reference plane stride
+    zwin: int = 1     # 3D search: plane offsets per reference (window depth c)
 
     @property
     def shape(self):
@@ -56,9 +66,17 @@ CONFIGS = {
     "c5": BMConfig("c5", "u8", 64, 1, 1080, 1920, 8, 4, 33, 16, seed=5, noise_seed=3005),
 }
 
+# 3D search (volumes of P planes [1, P, H, W]); K = 16 (the paper does not state it)
+CONFIGS3D = {
+    "v1": BMConfig("v1", "f32", 1, 20, 256, 256, 6, 1, 30, 16, seed=6, noise_seed=1006, sigma=25 / 255,
+                   d=1, sz=1, zwin=9),
+    "m1": BMConfig("m1", "f32", 1, 6, 256, 256, 6, 1, 30, 16, seed=7, noise_seed=1007, sigma=25 / 255,
+                   d=3, sz=1, zwin=2),
+}
+
 
 def config_by_name(name: str) -> BMConfig:
-    return CONFIGS[name]
+    return CONFIGS[name] if name in CONFIGS else CONFIGS3D[name]
 
 
 def _sinusoid(rng, H, W, amp_lo, amp_hi, f_lo, f_hi):
@@ -126,8 +144,29 @@ def video_frames(N: int, H: int, W: int, seed: int, walk_seed: int, margin: int 
     return out
 
 
+def _video_f32(cfg: BMConfig) -> np.ndarray:
+    frames = video_frames(cfg.C, cfg.H, cfg.W, cfg.seed, 3000 + cfg.seed, margin=64, max_step=4)
+    rng = np.random.Generator(np.random.PCG64(cfg.noise_seed))
+    v = frames[:, 0].astype(np.float64) / 255.0 + rng.normal(0.0, cfg.sigma, size=(cfg.C, cfg.H, cfg.W))
+    return v.astype(np.float32).reshape(1, cfg.C, cfg.H, cfg.W)
+
+
+def _multimodal(cfg: BMConfig) -> np.ndarray:
+    H, W = cfg.H, cfg.W
+    L = G(H, W, cfg.seed).astype(np.float64) / 255.0
+    rng = np.random.Generator(np.random.PCG64(2000 + cfg.seed))
+    planes = [np.clip(L * rng.uniform(0.6, 1.0), 0.0, 1.0) + _sinusoid(rng, H, W, 0.05, 0.2, 0.01, 0.1)
+              for _ in range(cfg.C)]
+    nrng = np.random.Generator(np.random.PCG64(cfg.noise_seed))
+    v = np.stack(planes) + nrng.normal(0.0, cfg.sigma, size=(cfg.C, H, W))
+    return v.astype(np.float32).reshape(1, cfg.C, H, W)
+
+
 def make_input(cfg: BMConfig, n_frames: int | None = None) -> np.ndarray:
-    """The config's input as a contiguous numpy array [N, C, H, W] (uint8 or float32)."""
+    """The config's input as a contiguous numpy array [N, C, H, W] (uint8 or float32); the 3D
+    configs return one volume [1, P, H, W]."""
+    if cfg.d > 0:
+        return _video_f32(cfg) if cfg.name == "v1" else _multimodal(cfg)
     if cfg.name == "c5" or (cfg.dtype == "u8" and cfg.N > 1):
         n = cfg.N if n_frames is None else n_frames
         return video_frames(n, cfg.H, cfg.W, cfg.seed, cfg.noise_seed)

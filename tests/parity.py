@@ -142,3 +142,50 @@ def check_ncc(img, b, s, Wn, K, gi, gd, oi, od, exact, iy_range=None, where=""):
         dmap.update(zip(gi[r, :k].tolist(), D[r, :k].tolist()))
         for c in gs ^ os_:
             assert abs(dmap[c] - dK) <= NCC_ATOL, f"{where}: ref {r} set differs beyond tolerance"
+
+
+def check_f32_3d(vol, d, b, s, sz, Wn, c, K, gi, gd, oi, od, where, rel=1e-5):
+    """The f32 parity rule in 3D: distinct valid candidates of the (plane, y, x) window, distances
+    within rel of the direct ones (self exactly 0), rows sorted by (dist, idx), set differences only
+    at the K-th distance."""
+    P, H, W = vol.shape
+    nz, refs, _ = gi.shape
+    ny, nx = oracle.grid(H, W, b, s)
+    lo, hi, loz, hiz = -(Wn // 2), Wn - 1 - Wn // 2, -(c // 2), c - 1 - c // 2
+    assert gi.shape == oi.shape
+    for zi in range(nz):
+        zr = zi * sz
+        t = np.arange(refs)
+        ry, rx = (t // nx) * s, (t % nx) * s
+        nzc = min(P - d, zr + hiz) - max(0, zr + loz) + 1
+        ncand = nzc * (np.minimum(H - b, ry + hi) - np.maximum(0, ry + lo) + 1) * \
+            (np.minimum(W - b, rx + hi) - np.maximum(0, rx + lo) + 1)
+        valid = np.arange(K)[None, :] < np.minimum(ncand, K)[:, None]
+        g, dd = gi[zi], gd[zi]
+        assert ((g == -1) == ~valid).all(), f"{where}: padding"
+        zc, rem = g // (H * W), g % (H * W)
+        cy, cx = rem // W, rem % W
+        RY, RX = np.broadcast_to(ry[:, None], g.shape), np.broadcast_to(rx[:, None], g.shape)
+        ok = (zc - zr >= loz) & (zc - zr <= hiz) & (zc >= 0) & (zc <= P - d) & (cy - RY >= lo) & \
+            (cy - RY <= hi) & (cx - RX >= lo) & (cx - RX <= hi)
+        assert (ok | ~valid).all(), f"{where}: candidate outside its window"
+        srt = np.sort(np.where(valid, g, -1 - np.arange(K)[None, :]), axis=1)
+        assert (np.diff(srt, axis=1) != 0).all(), f"{where}: duplicates"
+        D = np.zeros(g.shape)
+        D[valid] = oracle.pair_dist3d(vol, d, b, np.full(int(valid.sum()), zr), RY[valid], RX[valid], zc[valid],
+                                      cy[valid], cx[valid])
+        err = np.abs(dd.astype(np.float64) - D)
+        assert (err[valid] <= rel * D[valid]).all(), f"{where}: distance off"
+        self_ = valid & (zc == zr) & (cy == RY) & (cx == RX)
+        assert (dd[self_] == 0).all()
+        d64 = dd.astype(np.float64)
+        order = (d64[:, 1:] > d64[:, :-1]) | ((d64[:, 1:] == d64[:, :-1]) & (g[:, 1:] > g[:, :-1])) | ~valid[:, 1:]
+        assert order.all(), f"{where}: order"
+        same = (np.sort(g, axis=1) == np.sort(oi[zi], axis=1)).all(axis=1)
+        for r in np.flatnonzero(~same):
+            k = int(min(ncand[r], K))
+            dK = od[zi, r, k - 1]
+            dmap = dict(zip(oi[zi, r, :k].tolist(), od[zi, r, :k].tolist()))
+            dmap.update(zip(g[r, :k].tolist(), D[r, :k].tolist()))
+            for cnd in set(g[r, :k].tolist()) ^ set(oi[zi, r, :k].tolist()):
+                assert abs(dmap[cnd] - dK) <= rel * dK, f"{where}: set differs"

@@ -1209,3 +1209,51 @@ def test_ncc_wide_lists_fixup(K):
             assert p.debug_fix_count() >= p.n_refs * 9 // 10
         oi, od = oracle.ncc(x, b, s, Wn, K)
         check_ncc(x[0], b, s, Wn, K, gi[0], gd[0], oi[0], od[0], exact=False, where=f"ncc wide fixup {kind} K{K}")
+
+
+# ------------------------------------------------------------------ 3D search
+def _bm3d_check(vol, d, b, s, sz, Wn, c, K, where):
+    from paper_2006_13714_b200.bm import Plan3D
+    P, H, W = vol.shape
+    p = Plan3D(H, W, d, b, s, Wn, sz, c, K)
+    gi, gd = p.run(torch.from_numpy(vol).cuda())
+    torch.cuda.synchronize()
+    gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
+    oi, od = oracle.bm3d(vol, d, b, s, sz, Wn, c, K)
+    from tests.parity import check_f32_3d
+    check_f32_3d(vol, d, b, s, sz, Wn, c, K, gi, gd, oi, od, where)
+    return p
+
+
+@pytest.mark.parametrize("P,d,s,b,sz,Wn,c,K", [(5, 1, 1, 6, 1, 13, 3, 16), (6, 3, 1, 6, 1, 11, 2, 12),
+                                                (4, 2, 3, 8, 1, 17, 3, 20), (7, 1, 2, 8, 2, 9, 5, 30),
+                                                (3, 1, 1, 7, 1, 15, 1, 16), (6, 1, 4, 8, 3, 21, 4, 8)])
+def test_bm3d_matches_oracle(P, d, s, b, sz, Wn, c, K):
+    rng = np.random.Generator(np.random.PCG64(P * 100 + Wn * 3 + c))
+    vol = synth.random_image(rng, 1, P, 41, 53, "f32")[0]
+    _bm3d_check(vol, d, b, s, sz, Wn, c, K, f"bm3d {(P, d, s, b, sz, Wn, c, K)}")
+
+
+def test_bm3d_translated_video_and_fixup():
+    """A translated video (exact d = 0 motion-compensated matches across planes) and a constant
+    volume (every candidate ties: every reference goes to the exact 3D fix-up)."""
+    rng = np.random.Generator(np.random.PCG64(5))
+    canvas = synth.random_image(rng, 1, 1, 90, 90, "f32")[0, 0]
+    vol = np.stack([canvas[20 + 2 * z:20 + 2 * z + 40, 30 - 3 * z:30 - 3 * z + 44] for z in range(5)]).astype(np.float32)
+    _bm3d_check(vol, 1, 6, 1, 1, 15, 3, 16, "bm3d translated")
+    p = _bm3d_check(np.full((4, 30, 40), 0.25, np.float32), 1, 6, 1, 1, 9, 3, 16, "bm3d constant")
+    assert p.debug_fix_count() > 0
+
+
+def test_bm3d_rejects():
+    from paper_2006_13714_b200.bm import Plan, Plan3D, ScError
+    with pytest.raises(ScError):
+        Plan3D(40, 40, 1, 5, 1, 13, 1, 3, 16)  # (s, b) not a box-kernel shape
+    with pytest.raises(ScError):
+        Plan3D(40, 40, 1, 6, 1, 31, 1, 9, 16)  # 9 * 31^2 window slots > 2^13
+    p = Plan3D(40, 40, 1, 6, 1, 13, 1, 3, 16)
+    with pytest.raises(ScError):
+        p.run(torch.zeros((0, 40, 40), dtype=torch.float32, device="cuda"))
+    x = torch.zeros((1, 1, 40, 40), dtype=torch.float32, device="cuda")
+    with pytest.raises(ScError):
+        Plan.run(p, x)  # a 3D plan refuses 2D runs

@@ -607,3 +607,24 @@ def test_bm3d_translated_volume():
             want = {((z + 1) * H + ry - 2) * W + rx + 3, ((z - 1) * H + ry + 2) * W + rx - 3}
             assert want <= set(idx[z, r].tolist())
             assert (dist[z, r] == 0).all()  # self + the two motion-compensated matches
+
+
+def test_pair_dist3d_matches_bm3d():
+    """oracle.pair_dist3d (the 3D check's D) against the distances oracle.bm3d reports for its own
+    selected pairs, and a numpy patch difference."""
+    rng = _rng(903)
+    x = synth.random_image(rng, 1, 5, 17, 19, "f32")[0]
+    d, b, s, sz, Wn, c, K = 2, 4, 2, 1, 7, 3, 10
+    idx, dist = oracle.bm3d(x, d, b, s, sz, Wn, c, K)
+    ny, nx = oracle.grid(17, 19, b, s)
+    nz = idx.shape[0]
+    zr = np.repeat(np.arange(nz) * sz, ny * nx * K)
+    t = np.tile(np.repeat(np.arange(ny * nx), K), nz)
+    ii = idx.ravel()
+    zc, rem = ii // (17 * 19), ii % (17 * 19)
+    D = oracle.pair_dist3d(x, d, b, zr, (t // nx) * s, (t % nx) * s, zc, rem // 19, rem % 19)
+    np.testing.assert_allclose(D, dist.ravel(), rtol=1e-12)
+    k = 37
+    pr = x[zr[k]:zr[k] + d, (t[k] // nx) * s:(t[k] // nx) * s + b, (t[k] % nx) * s:(t[k] % nx) * s + b].astype(np.float64)
+    pc = x[zc[k]:zc[k] + d, rem[k] // 19:rem[k] // 19 + b, rem[k] % 19:rem[k] % 19 + b].astype(np.float64)
+    assert abs(D[k] - ((pr - pc) ** 2).sum()) < 1e-12
