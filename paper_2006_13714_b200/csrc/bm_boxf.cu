@@ -570,17 +570,24 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
         const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
         const int cy = ry + dyy + a.lo, cx = rxj + dxx + a.lo;
         const float* cimg = Z3 ? reinterpret_cast<const float*>(vol) + size_t(zc) * plane : img;
-        float d = 0.f;
+        // (rows in independent partial sums, 4 in flight: the loads of a row do not wait for the
+        // previous row's FMA chain -- a5 is latency-bound on these L1/L2 reads)
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int c = 0; c < nch; ++c) {
           const float* pr = img + c * plane + size_t(ry) * a.W + rxj;
           const float* pc = cimg + c * plane + size_t(cy) * a.W + cx;
-          for (int l = 0; l < BK; ++l)
+#pragma unroll 4
+          for (int l = 0; l < BK; ++l) {
+            float t = 0.f;
 #pragma unroll
             for (int m = 0; m < BK; ++m) {
               const float df = __ldg(pr + l * a.W + m) - __ldg(pc + l * a.W + m);
-              d = fmaf(df, df, d);
+              t = fmaf(df, df, t);
             }
+            acc[l & 3] += t;
+          }
         }
+        const float d = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t((Z3 ? zc * a.H : 0) * a.W + cy * a.W + cx);
       }
       top.merge(key, lane);

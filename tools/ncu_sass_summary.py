@@ -12,6 +12,7 @@ import sys
 def summarise(hdr, data, top):
     by_op = collections.defaultdict(lambda: [0, 0])
     tot_i = tot_s = 0
+    data = [d for d in data if d.get("Address", "") not in ("-", "")]  # (cuda,sass exports: SASS rows only)
     for d in data:
         try:
             ie = int(d.get("Instructions Executed") or 0)

@@ -20,6 +20,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 
 def main(rep, out, kernel_regex=None):
+    """rep: an .ncu-rep, or the prefix of CSV exports made on the GPU box by tools/prof_f.sh
+    (<prefix>_raw.csv, <prefix>_details.csv, <prefix>_src.csv[.gz] with --print-source cuda,sass)."""
+    if not rep.endswith(".ncu-rep"):
+        return main_csv(rep, out, kernel_regex)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -47,6 +51,41 @@ def main(rep, out, kernel_regex=None):
                           capture_output=True, text=True).stdout
     blocks = subprocess.run([sys.executable, "tools/ncu_blocks.py", "/tmp/_src.csv"], capture_output=True, text=True).stdout
     open(out + "_sass_summary.txt", "w").write(summ + "\n\nby execution count (loop bodies):\n" + blocks)
+    print(json.dumps(m, indent=1)[:1500])
+
+
+def main_csv(prefix, out, kernel_regex=None):
+    import gzip
+    import os
+    raw = open(prefix + "_raw.csv").read()
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    sel = [r for r in rows[2:] if kernel_regex is None or kernel_regex in r[hdr.index("Kernel Name")]]
+    vals = sel[-1]
+    m = {"kernel": vals[hdr.index("Kernel Name")]}
+    for k in KEYS:
+        if k in hdr:
+            m[k] = {"value": vals[hdr.index(k)], "unit": units[hdr.index(k)]}
+    stalls = {}
+    for i, h in enumerate(hdr):
+        if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+            try:
+                stalls[h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = float(vals[i])
+            except ValueError:
+                pass
+    m["stalls_per_issue_active"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:10])
+    json.dump(m, open(out + "_metrics.json", "w"), indent=1)
+    if os.path.exists(prefix + "_details.csv"):
+        open(out + "_details.csv", "w").write(open(prefix + "_details.csv").read())
+    src = prefix + "_src.csv"
+    if os.path.exists(src + ".gz"):
+        open("/tmp/_src.csv", "w").write(gzip.open(src + ".gz", "rt").read())
+        src = "/tmp/_src.csv"
+    if os.path.exists(src):
+        summ = subprocess.run([sys.executable, "tools/ncu_sass_summary.py", src, "30"], capture_output=True,
+                              text=True).stdout
+        lines = subprocess.run([sys.executable, "tools/ncu_lines.py", src, "40"], capture_output=True, text=True).stdout
+        open(out + "_sass_summary.txt", "w").write(summ + "\n\nby CUDA source line:\n" + lines)
     print(json.dumps(m, indent=1)[:1500])
 
 
