@@ -166,7 +166,8 @@ def selftest_cpu(args, cfg):
     from paper_2006_13714_b200.dist import balanced_ranges
     ws, rank, _ = _dist_env()
     if ws > 1:
-        tdist.init_process_group("gloo")
+        import datetime
+        tdist.init_process_group("gloo", timeout=datetime.timedelta(seconds=120))
     shards = balanced_ranges(cfg.N, ws)
     f0, f1 = shards[rank]
     buf = np.random.default_rng(rank).random((max(1, f1 - f0), 1 << 16))
@@ -603,7 +604,11 @@ def main():
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # a bounded collective timeout: a hung peer fails the run instead of blocking it forever
+        # (TORCH_NCCL_ASYNC_ERROR_HANDLING is on by default for NCCL in this torch)
+        import datetime
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=int(os.environ.get("SCBM_NCCL_TIMEOUT_S", "300"))))
 
     # shard frames (strong scaling); single-image configs run as replicas
     if cfg.N > 1:
@@ -654,9 +659,11 @@ def main():
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.fill_(k & 0xFF)  # L2 flush outside the step's events
+            torch.cuda.nvtx.range_push(f"bm_step_{k}")  # (NVTX: step boundaries in an nsys / ncu timeline)
             starts[k].record(stream)
             step()
             ends[k].record(stream)
+            torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
