@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   }  // phases
   }  // wact
   }  // plane offsets (Z3)
+  if (WS == 1 && !wact) return;  // (Z3: reference rows past the band joined the restaging only)
 
   if constexpr (WS == 2) {
     // merge the second half's list into the first's (0 sentinels skipped), then only the first

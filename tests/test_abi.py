@@ -77,3 +77,25 @@ def test_sm100a_code_in_library(lib):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", bm.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("args", [
+    (64, 64, 1, 6, 1, 30, 0, 9, 16, 1),    # z_stride 0
+    (64, 64, 1, 6, 1, 30, 1, 0, 16, 1),    # z_window 0
+    (64, 64, 1, 6, 1, 30, 1, 65, 16, 1),   # z_window > 64
+])
+def test_plan3d_validation(lib, args):
+    h = ctypes.c_void_p(123)
+    assert lib.sc_bm_plan3d(*args, ctypes.byref(h)) == 1 and not h.value
+    assert lib.sc_bm_run3d(None, None, 0, None, None, None) == 1
+
+
+def test_plan3d_no_cpu_fallback_without_gpu(lib):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    h = ctypes.c_void_p()
+    assert lib.sc_bm_plan3d(64, 64, 1, 6, 1, 30, 1, 9, 16, 0, ctypes.byref(h)) == 2  # uint8: unsupported
+    with pytest.raises(bm.ScError) as e:
+        bm.Plan3D(64, 64, 1, 6, 1, 30, 1, 9, 16)
+    assert e.value.code in (2, 4)

@@ -1257,3 +1257,25 @@ def test_bm3d_rejects():
     x = torch.zeros((1, 1, 40, 40), dtype=torch.float32, device="cuda")
     with pytest.raises(ScError):
         Plan.run(p, x)  # a 3D plan refuses 2D runs
+
+
+def test_bm3d_partial_reference_rows_and_guard():
+    """Reference rows that do not fill the last 8-row CTA (ny % 8 != 0) over several planes: every
+    plane's table matches the oracle and nothing is written past the output tables (the idle
+    warps of the last CTA row join the plane restaging but must not reach the output stage)."""
+    from paper_2006_13714_b200.bm import Plan3D
+    from tests.parity import check_f32_3d
+    rng = np.random.Generator(np.random.PCG64(808))
+    for (P, d, H, W, b, s, sz, Wn, c, K) in [(3, 2, 50, 49, 8, 2, 2, 1, 1, 4), (5, 1, 44, 76, 7, 1, 1, 12, 4, 9),
+                                             (6, 2, 25, 32, 8, 3, 1, 13, 2, 30)]:
+        vol = synth.random_image(rng, 1, P, H, W, "f32")[0]
+        p = Plan3D(H, W, d, b, s, Wn, sz, c, K)
+        nz = p.n_zref(P)
+        gi_full = torch.full((nz + 2, p.n_refs, K), -7, dtype=torch.int32, device="cuda")
+        gd_full = torch.full((nz + 2, p.n_refs, K), -7.0, dtype=torch.float32, device="cuda")
+        p.run(torch.from_numpy(vol).cuda(), out=(gi_full[:nz], gd_full[:nz]))
+        torch.cuda.synchronize()
+        assert (gi_full[nz:] == -7).all() and (gd_full[nz:] == -7.0).all(), "write past the tables"
+        oi, od = oracle.bm3d(vol, d, b, s, sz, Wn, c, K)
+        check_f32_3d(vol, d, b, s, sz, Wn, c, K, gi_full[:nz].cpu().numpy(), gd_full[:nz].cpu().numpy(), oi, od,
+                     f"bm3d guard {(P, d, H, W)}")

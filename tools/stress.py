@@ -18,8 +18,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import oracle  # noqa: E402
 from paper_2006_13714_b200 import synth  # noqa: E402
 from paper_2006_13714_b200.bm import (SC_KERNEL_BOX, SC_KERNEL_BOXF, SC_KERNEL_SIMT,  # noqa: E402
-                                      SC_KERNEL_SIMT_WARP, Plan, ScError)
-from parity import check_f32, check_ncc, check_u8  # noqa: E402
+                                      SC_KERNEL_SIMT_WARP, SC_KERNEL_TC_F32, Plan, Plan3D, ScError)
+from parity import check_f32, check_f32_3d, check_ncc, check_u8  # noqa: E402
 
 
 def image(rng, kind, N, C, H, W, dtype):
@@ -36,25 +36,50 @@ def image(rng, kind, N, C, H, W, dtype):
     return np.round(x).astype(np.uint8) if dtype == "u8" else x.astype(np.float32)
 
 
-FOCUS = os.environ.get("STRESS_FOCUS", "")  # "", "ncc" or "box" (u8 b=8 s=4: the dp4a kernels)
+FOCUS = os.environ.get("STRESS_FOCUS", "")  # "", "ncc", "box" (u8 b=8 s=4: the dp4a kernels), "3d"
+
+
+def one3d(rng):
+    """The 3D search (sc_bm_plan3d) against oracle.bm3d on a random volume."""
+    kind = rng.choice(["random", "binary", "smooth", "quantised"])
+    s, b = [(3, 8), (1, 7), (4, 8), (2, 8), (1, 6)][rng.integers(0, 5)]
+    P = int(rng.integers(1, 8))
+    d = int(rng.integers(1, min(P, 3) + 1))
+    H, W = int(rng.integers(b, 60)), int(rng.integers(b, 80))
+    Wn, c, sz = int(rng.integers(1, 24)), int(rng.integers(1, 6)), int(rng.integers(1, 3))
+    K = int(rng.integers(1, 40))
+    vol = image(rng, kind, 1, P, H, W, "f32")[0]
+    desc = f"3d {kind} P{P} d{d} {H}x{W} b{b} s{s} sz{sz} Wn{Wn} c{c} K{K}"
+    try:
+        p = Plan3D(H, W, d, b, s, Wn, sz, c, K)
+    except ScError:
+        return "skip", desc
+    gi, gd = p.run(torch.from_numpy(vol).cuda())
+    torch.cuda.synchronize()
+    oi, od = oracle.bm3d(vol, d, b, s, sz, Wn, c, K)
+    check_f32_3d(vol, d, b, s, sz, Wn, c, K, gi.cpu().numpy(), gd.cpu().numpy(), oi, od, desc)
+    return "ok", desc
 
 
 def one(rng):
+    if FOCUS == "3d" or (FOCUS == "" and rng.random() < 0.15):
+        return one3d(rng)
     metric = "ncc" if FOCUS == "ncc" else rng.choice(["l2", "l2", "l2", "ncc"])
     dtype = "u8" if FOCUS == "box" else rng.choice(["u8", "f32"])
     kind = rng.choice(["random", "binary", "smooth", "quantised"])
     if FOCUS == "box" or (dtype == "u8" and rng.random() < 0.6):  # the dp4a box kernel's geometry
         b, s, C = 8, 4, 1
     elif rng.random() < 0.5:  # the float box kernel's shapes
-        s, b = [(3, 8), (1, 7), (4, 8), (2, 8)][rng.integers(0, 4)]
-        C = int(rng.choice([1, 1, 2, 4])) if metric == "l2" else 1
+        s, b = [(3, 8), (1, 7), (4, 8), (2, 8), (1, 6)][rng.integers(0, 5)]
+        C = int(rng.choice([1, 1, 2, 4]))
     else:
         b, s, C = int(rng.integers(1, 13)), int(rng.integers(1, 6)), int(rng.integers(1, 4))
     H, W = int(rng.integers(b, 90)), int(rng.integers(b, 130))
     Wn = int(rng.integers(1, 40))
-    K = int(rng.integers(1, 25 if metric == "ncc" else 40))
+    K = int(rng.integers(1, (25 if dtype == "u8" else 77) if metric == "ncc" else 72))
     N = int(rng.integers(1, 4))
-    kernel = "box" if FOCUS == "box" and rng.random() < 0.7 else rng.choice(["default", "box", "boxf", "warp", "lanes"])
+    kernel = "box" if FOCUS == "box" and rng.random() < 0.7 else \
+        rng.choice(["default", "box", "boxf", "warp", "lanes", "tcf"])
     T = int(rng.integers(1, 3)) if (metric == "l2" and dtype == "u8" and b == 8 and s == 4 and C == 1
                                     and rng.random() < 0.25) else 0
     x = image(rng, kind, N, C, H, W, dtype)
@@ -65,7 +90,7 @@ def one(rng):
             p.set_temporal(T)
         elif kernel != "default":
             p.set_kernel({"box": SC_KERNEL_BOX, "boxf": SC_KERNEL_BOXF, "warp": SC_KERNEL_SIMT_WARP,
-                          "lanes": SC_KERNEL_SIMT}[kernel])
+                          "lanes": SC_KERNEL_SIMT, "tcf": SC_KERNEL_TC_F32}[kernel])
     except ScError:
         return "skip", desc
     t = torch.from_numpy(x).cuda()
