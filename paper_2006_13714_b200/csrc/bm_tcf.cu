@@ -7,21 +7,24 @@
 // representable in tf32; lo = x - hi, exact in fp32) and D = A_hi B_hi + A_hi B_lo + A_lo B_hi, which
 // keeps the products to ~2^-21 relative (fp32-class; bf16x3 would not meet the 1e-5 rule).
 //   * A (M = 128 references of an 8 x 16 reference block; TMEM lane quadrant q = a 4 x 8 sub-block)
-//     is K-major in shared memory: per reference the centred patch x' = x - 0.5 as K = 8 b floats,
-//     k = 8 u + v (patch row u, column v; v >= b is zero), in canonical 8-row x 16-byte core matrices.
-//   * B (N = 128 candidates: an 8-row x 16-column block of candidate top-left positions) is K-major
+//     lives in TMEM, written once per CTA by tcgen05.st (lane m = reference m): the centred patch
+//     x' = x - 0.5 as K = 8 b tf32 values, k = 8 u + v (patch row u, column v; v >= b is zero),
+//     hi at columns [0, 8b), lo at [8b, 16b) -- so a CTA needs no shared memory for A and two CTAs
+//     (8 epilogue warps) share an SM.
+//   * B (N = 64 candidates: a 4-row x 16-column block of candidate top-left positions) is K-major
 //     straight out of a "shift-expanded" tile E[y][jg][kc][j][t] = x'(cy0 + y, cx0 + 8 jg + j + 4 kc + t):
 //     an 8-candidate group (8 consecutive columns jg of candidate row i) x 16 B of K (4 shifts v)
 //     is one canonical core matrix, the K-group of patch row u of candidate row i is tile row i + u,
 //     so ONE descriptor per patch row (start + 512 u, LBO = 128, SBO = 256) addresses the whole block --
-//     no im2col; the tile is 8 + b - 1 rows x 512 B per copy (hi, lo). (MN-major B, which would need
-//     no shifted copies along K, does not work for kind::tf32: tools/tf32_layout_test.cu.)
-//   * per candidate tile, 3 b MMAs (tcgen05.mma.cta_group::1.kind::tf32, K = 8) into one of two
-//     128 x 128 fp32 TMEM accumulators (double-buffered: the MMAs of tile t+1 overlap the epilogue
-//     of tile t), issued by one thread, committed to mbarriers; three producer warps stage the E
-//     tiles of a 3-slot ring from the CTA's staged image region.
-// Epilogue (4 warps, one per TMEM lane quadrant; lane = reference, its list stays in registers or
-// in its shared-memory heap for the whole kernel): tcgen05.ld 32 columns (two candidate rows),
+//     no im2col; the tile is 4 + b - 1 rows x 512 B per copy (hi, lo). (MN-major B, which would need
+//     no shifted copies along K, does not work for kind::tf32: tools/tf32_layout_test.cu; A from
+//     TMEM: tools/tf32_tmem_a_test.cu.)
+//   * per candidate tile, 3 b MMAs (tcgen05.mma.cta_group::1.kind::tf32 [d], [a_tmem], b_desc, K = 8)
+//     into one of two 128 x 64 fp32 TMEM accumulators (double-buffered: the MMAs of tile t+1 overlap
+//     the epilogue of tile t), issued by one thread, committed to mbarriers; three producer warps
+//     stage the E tiles of a 2-slot ring from the CTA's staged image region.
+// Epilogue (4 warps per CTA, one per TMEM lane quadrant; lane = reference, its list stays in
+// registers or in its shared-memory heap for the whole kernel): tcgen05.ld 32 columns (two candidate rows),
 // d' = n_c - 2 C (Lemma 2; n_c from the fp64-SAT norm map), slack = thr - d',
 // sign bits packed into a fail mask (one SHF per pair), the window mask, and the u8 box kernel's
 // branch-free survivor rounds into the reference's top-(K+m) of 32-bit keys (a4, Theorem 1,
@@ -44,8 +47,11 @@ constexpr int kTfProd = 3;                      // E-tile producer warps
 constexpr int kTfWarps = kTfEpi + kTfProd + 1;  // + the MMA warp
 constexpr int kTfThreads = kTfWarps * 32;
 constexpr int kRBY = 8, kRBX = 16;  // reference block (M = 128)
-constexpr int kTR = 8, kTC = 16;    // candidate tile (N = 128)
-constexpr int kES = 3;              // E ring slots
+constexpr int kTR = 4, kTC = 16;    // candidate tile (N = 64)
+constexpr int kES = 2;              // E ring slots
+// TMEM (256 columns per CTA, two CTAs per SM): A_hi at [0, 8b), A_lo at [8b, 16b) (the reference
+// patches, written once by tcgen05.st), the two N = 64 accumulators at [128, 192) and [192, 256)
+constexpr uint32_t kTmemD = 128;
 constexpr int kScrPitch = 36;       // epilogue scratch words per lane (32 staged + pad; 16-B rows)
 constexpr float kTcfErr = 2e-5f;    // bound on the 3xTF32 identity's error, relative to n_r + d
 
@@ -73,12 +79,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
 
 template <int BK, int KR, bool DENSE>
-__global__ void __launch_bounds__(kTfThreads, 1) bm_tcf_kernel(TcfArgs a) {
+__global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
   constexpr bool HEAP = KR > 48;
   constexpr int ER = kTR + BK - 1;                  // E tile rows
   constexpr uint32_t kEBytes = uint32_t(ER) * 512;  // one copy (hi or lo) of an E tile
-  constexpr uint32_t kAGroup = 2 * BK * 128;        // bytes per 8-reference group of A (K = 8 b floats)
-  constexpr uint32_t kIdesc = sm100::idesc_tf32(128, 128, /*a_mn=*/false, /*b_mn=*/false);
+  constexpr uint32_t kIdesc = sm100::idesc_tf32(128, kTR * kTC, /*a_mn=*/false, /*b_mn=*/false);
+  constexpr uint32_t kKA = 8 * BK;                  // A columns per copy (hi, lo) in TMEM
   extern __shared__ __align__(1024) uint8_t smem[];
   const int f = blockIdx.y;
   const int by = blockIdx.x / a.tiles_x, bx = blockIdx.x - by * a.tiles_x;
@@ -99,8 +105,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) bm_tcf_kernel(TcfArgs a) {
   const uint32_t bar_full = sbase, bar_empty = sbase + 16, bar_ef = sbase + 32, bar_ee = sbase + 56;
   const uint32_t tmem_slot = sbase + 80, bar_nc = sbase + 96;  // bar_nc[2]: the tile's candidate norms staged
   float* raw = reinterpret_cast<float*>(smem + a.off_raw);
-  const uint32_t sA = sbase + a.off_A, sE = sbase + a.off_E;
-  const uint32_t aLo = uint32_t(kRBY * kRBX / 8) * kAGroup;  // A_lo follows A_hi
+  const uint32_t sE = sbase + a.off_E;
 
   if (warp == kTfWarps - 1) {
     sm100::tmem_alloc(tmem_slot, 256);
@@ -129,29 +134,6 @@ __global__ void __launch_bounds__(kTfThreads, 1) bm_tcf_kernel(TcfArgs a) {
     raw[r * a.RWp + c] = (y < H && x < W) ? __ldg(img + size_t(y) * W + x) : 0.5f;
   }
   __syncthreads();
-  // A: reference m = 32 q + l -> (iy_first + 4 (q >> 1) + l / 8, ix_first + 8 (q & 1) + l % 8)
-  for (int e = threadIdx.x; e < 128 * 2 * BK; e += kTfThreads) {
-    const int m = e / (2 * BK), kc = e - m * (2 * BK);
-    const int q = m >> 5, l = m & 31;
-    const int iy = iy_first + 4 * (q >> 1) + (l >> 3), ix = ix_first + 8 * (q & 1) + (l & 7);
-    const int u = kc >> 1, v0 = 4 * (kc & 1);
-    uint4 hi = make_uint4(0, 0, 0, 0), lo = make_uint4(0, 0, 0, 0);
-    if (iy <= iy_last && ix <= ix_last) {
-      const float* src = raw + (iy * s - cyA + u) * a.RWp + (ix * s - cxA) + v0;
-      uint32_t h[4], o[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float x = (v0 + t < BK) ? src[t] - 0.5f : 0.f;
-        h[t] = tf32_hi(x);
-        o[t] = __float_as_uint(x - __uint_as_float(h[t]));
-      }
-      hi = make_uint4(h[0], h[1], h[2], h[3]);
-      lo = make_uint4(o[0], o[1], o[2], o[3]);
-    }
-    const uint32_t off = uint32_t(m >> 3) * kAGroup + uint32_t(kc) * 128 + uint32_t(m & 7) * 16;
-    *reinterpret_cast<uint4*>(smem + a.off_A + off) = hi;
-    *reinterpret_cast<uint4*>(smem + a.off_A + aLo + off) = lo;
-  }
   // tile order: by L1 gap to the reference block's rectangle (every reference meets its own
   // neighbourhood first), ties by index
   int16_t* order = reinterpret_cast<int16_t*>(smem + a.off_order);
@@ -177,6 +159,31 @@ __global__ void __launch_bounds__(kTfThreads, 1) bm_tcf_kernel(TcfArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + 80);
+  // A into TMEM (epilogue warp q writes lanes 32q..32q+31 = its references): row m holds the centred
+  // patch of reference m = 32 q + l -> (iy_first + 4 (q >> 1) + l / 8, ix_first + 8 (q & 1) + l % 8)
+  // as K = 8 b tf32 values k = 8 u + v (v >= b: 0), hi at columns [0, 8b), lo at [8b, 16b)
+  if (warp < kTfEpi) {
+    const int iy = iy_first + 4 * (warp >> 1) + (lane >> 3), ix = ix_first + 8 * (warp & 1) + (lane & 7);
+    const bool ok = iy <= iy_last && ix <= ix_last;
+    const uint32_t ta = tmem + (uint32_t(32 * warp) << 16);
+#pragma unroll 1
+    for (int u = 0; u < BK; ++u) {
+      uint32_t h[8], o[8];
+      const float* src = raw + (iy * s - cyA + u) * a.RWp + (ix * s - cxA);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const float x = (ok && v < BK) ? src[v] - 0.5f : 0.f;
+        h[v] = tf32_hi(x);
+        o[v] = __float_as_uint(x - __uint_as_float(h[v]));
+      }
+      sm100::tmem_st8(ta + 8u * u, h);
+      sm100::tmem_st8(ta + kKA + 8u * u, o);
+    }
+    sm100::tmem_wait_st();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
 
   if (warp == kTfWarps - 1) {
     // ---------------- MMA issuer (one elected thread) + norm producer (all 32 lanes): once the
@@ -184,32 +191,38 @@ __global__ void __launch_bounds__(kTfThreads, 1) bm_tcf_kernel(TcfArgs a) {
     // L2-resident norm map) into ring slot t & 1 and arrives on bar_nc[slot]; lane 0 issues the MMAs
     float* ncring = reinterpret_cast<float*>(smem + a.off_nc);  // [2][8][16]
     const float* nsrc = a.norm + size_t(f) * a.nfs;
+    // the norms of tile t + 1 are loaded while tile t is waited for and issued (their L2 latency
+    // stays off the issue path)
+    const int rr = lane >> 2, cq = lane & 3;
+    auto load_norms = [&](int t) -> float4 {
+      const int ot = order[t];
+      const int tr = ot / NTC, tc = ot - tr * NTC;
+      if (rr >= kTR) return make_float4(0.f, 0.f, 0.f, 0.f);
+      const int cy = min(cyA + kTR * tr + rr, H - BK);
+      return __ldg(reinterpret_cast<const float4*>(nsrc + size_t(cy) * a.Mx + cxA + kTC * tc) + cq);
+    };
+    float4 nv_next = load_norms(0);
     for (int t = 0; t < ntiles; ++t) {
       const int sl = t % kES, buf = t & 1;
-      if (t >= 2) sm100::mbar_wait_sleep(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1), 32);
+      const float4 nv = nv_next;
+      if (t + 1 < ntiles) nv_next = load_norms(t + 1);
+      if (t >= 2) sm100::mbar_wait_sleep(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1), 16);
       {
-        const int ot = order[t];
-        const int tr = ot / NTC, tc = ot - tr * NTC;
-        const int rr = lane >> 2, cq = lane & 3;
-        const int cy = min(cyA + kTR * tr + rr, H - BK);
-        const float4 v = __ldg(reinterpret_cast<const float4*>(nsrc + size_t(cy) * a.Mx + cxA + kTC * tc) + cq);
-        reinterpret_cast<float4*>(ncring + (buf * kTR + rr) * kTC)[cq] = v;
+        if (rr < kTR) reinterpret_cast<float4*>(ncring + (buf * kTR + rr) * kTC)[cq] = nv;
         sm100::mbar_arrive(bar_nc + 8 * buf);
       }
       if (lane == 0) {
-        sm100::mbar_wait_sleep(bar_ef + 8 * sl, uint32_t((t / kES) & 1), 32);
+        sm100::mbar_wait_sleep(bar_ef + 8 * sl, uint32_t((t / kES) & 1), 16);
         sm100::tc_fence_after();
         const uint32_t eh = sE + uint32_t(sl) * 2 * kEBytes, el = eh + kEBytes;
 #pragma unroll 1
         for (int u = 0; u < BK; ++u) {
-          const uint64_t ah = sm100::smem_desc(sA + 256u * u, 128u, kAGroup);
-          const uint64_t al = sm100::smem_desc(sA + aLo + 256u * u, 128u, kAGroup);
           const uint64_t bh = sm100::smem_desc(eh + 512u * u, 128u, 256u);
           const uint64_t bl = sm100::smem_desc(el + 512u * u, 128u, 256u);
-          const uint32_t d = tmem + 128u * buf;
-          sm100::mma_tf32(d, ah, bh, kIdesc, u > 0);
-          sm100::mma_tf32(d, ah, bl, kIdesc, 1);
-          sm100::mma_tf32(d, al, bh, kIdesc, 1);
+          const uint32_t d = tmem + kTmemD + uint32_t(kTR * kTC) * buf;
+          sm100::mma_tf32_ta(d, tmem + 8u * u, bh, kIdesc, u > 0);        // A_hi B_hi
+          sm100::mma_tf32_ta(d, tmem + 8u * u, bl, kIdesc, 1);            // A_hi B_lo
+          sm100::mma_tf32_ta(d, tmem + kKA + 8u * u, bh, kIdesc, 1);      // A_lo B_hi
         }
         sm100::mma_commit(bar_full + 8 * buf);
         sm100::mma_commit(bar_ee + 8 * sl);
@@ -297,7 +310,7 @@ __global__ void __launch_bounds__(kTfThreads, 1) bm_tcf_kernel(TcfArgs a) {
           const bool r1 = cyp + 1 >= wy_lo && cyp + 1 <= wy_hi && cyp + 1 <= cyB;
           if (!r0 && !r1) continue;  // warp-uniform
           uint32_t cv[32];
-          sm100::tmem_ld32(tq + 128u * buf + 16u * i2, cv);
+          sm100::tmem_ld32(tq + kTmemD + uint32_t(kTR * kTC) * buf + 16u * i2, cv);
           // candidate norms of the two rows (staged by the MMA warp; rows past the map are masked below)
           float4 nq[8];
 #pragma unroll
@@ -498,10 +511,11 @@ TcfLayout tcf_layout(const Geometry& g) {
   L.off_raw = off;
   off += uint32_t(L.RHmax * L.RWp) * 4;
   off = (off + 1023) & ~1023u;
-  L.off_A = off;
-  off += 2u * 16u * uint32_t(2 * g.b * 128);  // A_hi, A_lo
+  L.off_A = off;  // (A lives in TMEM)
   L.off_E = off;  // the E ring; after the last tile the a5 stage's norms + register lists
-  off += std::max(uint32_t(kES) * 2u * uint32_t(kTR + g.b - 1) * 512u, uint32_t(128 + 128 * (kr + 1)) * 4u);
+  // (the heaps stay in their own area: only the reference norms are handed over)
+  off += std::max(uint32_t(kES) * 2u * uint32_t(kTR + g.b - 1) * 512u,
+                  uint32_t(128 + (kr > 48 ? 0 : 128 * (kr + 1))) * 4u);
   L.off_nc = off;  // candidate-norm ring [2][8][16]
   off += 2u * kTR * kTC * 4u;
   L.off_heap = off;
@@ -528,7 +542,12 @@ bool tcf_supported(const Geometry& g) {
   if (g.b < 1 || g.b > 8 || tcf_kr(g) == 0) return false;
   if (tcf_rel_bits(g.Wn) > 12) return false;  // keeps >= 20 distance bits in the 32-bit keys
   if (g.W - g.b + 1 < 16 && g.W < 24) return false;  // (tiles read 16 norm columns; tiny widths use others)
+  // two CTAs per SM (4 + 4 epilogue warps) up to 113 KB; larger layouts run one CTA per SM
   return tcf_layout(g).bytes <= 227 * 1024;
+}
+
+bool tcf_preferred(const Geometry& g) {
+  return tcf_supported(g) && g.s == 1 && !g.z3 && tcf_layout(g).bytes <= 113 * 1024;
 }
 
 cudaError_t launch_bm_tcf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,

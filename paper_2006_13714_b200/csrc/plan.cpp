@@ -116,14 +116,15 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, nullptr, st, &p->launches);
     else if (p->kernel == SC_KERNEL_TC_I8 && dense == nullptr)
       e = launch_bm_tc(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
-    else if (p->kernel == SC_KERNEL_TC_F32)
+    else if (p->kernel == SC_KERNEL_TC_F32 && !(dense != nullptr && p->nlm_inv_h2 > 0.f))
       e = launch_bm_tcf(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
     else if (p->kernel == SC_KERNEL_BOX && dense == nullptr)
       e = launch_bm_box(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_BOXF && dense == nullptr)
       e = launch_bm_boxf(*p, src, F, iy_begin, iy_end, io, dd, st, &p->launches);
     else if (p->kernel == SC_KERNEL_SIMT_WARP ||
-             (dense != nullptr && (p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF)))
+             (dense != nullptr && (p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF ||
+                                   p->kernel == SC_KERNEL_TC_F32)))
       // dense tables (NLM weights, debug): one warp per reference, lanes along its window row, so
       // the [refs][Wn^2] rows are written contiguously
       e = launch_bm_simt(*p, src, F, iy_begin, iy_end, io, dd, dense, st, &p->launches);
@@ -232,6 +233,10 @@ sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, in
   // f32, one channel, (s, b) in {(3,8), (1,7), (4,8), (2,8)}, K + 8 <= 80 (c2, c3): the float
   // box-sum matcher
   if (boxf_supported(g)) p->kernel = SC_KERNEL_BOXF;
+  // f32, one channel, stride 1 (c3): the 3xTF32 tensor-core matcher, where its layout leaves two
+  // CTAs per SM -- stride-1 strips cost the float box kernel a 4-shuffle tree per pair (c3: 4.60 vs
+  // 5.02 ms); with larger strides the box kernel's shared strips win (c2)
+  if (metric == SC_METRIC_L2 && tcf_preferred(g)) p->kernel = SC_KERNEL_TC_F32;
   if (metric == SC_METRIC_NCC)  // uint8 stride 4: the dp4a box kernel; else the float one
     p->kernel = (box_supported(g) && (box_ctas >= 16 || !boxf_supported(g))) ? SC_KERNEL_BOX : SC_KERNEL_BOXF;
 
@@ -379,7 +384,8 @@ sc_status_t sc_bm_nlm_weights(sc_bm_plan_t p, const void* img, float h, float* w
   // the window distances of every reference (Self-Convolution identity), written into the output;
   // the one-warp-per-reference dense matcher normalises its own row in its epilogue (nlm.cuh),
   // the lanes matcher (an explicit SC_KERNEL_SIMT choice) is followed by nlm_normalize
-  const bool fused = p->kernel == SC_KERNEL_SIMT_WARP || p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF;
+  const bool fused = p->kernel == SC_KERNEL_SIMT_WARP || p->kernel == SC_KERNEL_BOX || p->kernel == SC_KERNEL_BOXF ||
+                     p->kernel == SC_KERNEL_TC_F32;
   p->nlm_inv_h2 = fused ? 1.f / (h * h) : 0.f;
   s = enqueue(p, img, 1, 0, p->g.ny, nullptr, nullptr, weights_out, st);
   p->nlm_inv_h2 = 0.f;

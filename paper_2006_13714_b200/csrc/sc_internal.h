@@ -122,6 +122,7 @@ size_t lanes_smem_bytes(const Geometry& g, int nwy);
 // bm_tcf.cu: the tensor-core float matcher (SC_KERNEL_TC_F32; f32, C = 1, b <= 8, 3xTF32 on tcgen05).
 // dense != nullptr: the debug mode writing every window distance [refs][Wn^2] (-1 in clipped slots).
 bool tcf_supported(const Geometry& g);
+bool tcf_preferred(const Geometry& g);  // the default matcher where it measured faster (stride 1)
 cudaError_t launch_bm_tcf(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                           int32_t* idx_out, void* dist_out, void* dense, cudaStream_t st, int64_t* launches);
 

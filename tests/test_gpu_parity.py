@@ -515,8 +515,10 @@ def test_boxf_ties_and_extremes(kind, s, b):
 
 def test_boxf_default_and_rejects_unsupported():
     from paper_2006_13714_b200.bm import SC_KERNEL_BOXF, ScError
-    for name in ("c2", "c3", "c4"):
+    from paper_2006_13714_b200.bm import SC_KERNEL_TC_F32
+    for name in ("c2", "c4"):
         assert _plan(synth.CONFIGS[name]).info()["kernel"] == SC_KERNEL_BOXF
+    assert _plan(synth.CONFIGS["c3"]).info()["kernel"] == SC_KERNEL_TC_F32  # stride 1: tensor cores
     for args, dt in [((64, 64, 1, 8, 5, 21, 16), "f32"), ((64, 64, 8, 8, 3, 41, 32), "f32"),
                      ((64, 64, 1, 8, 3, 21, 80), "f32"), ((64, 64, 1, 8, 3, 21, 16), "u8")]:
         p = _plan(args, dt)
