@@ -43,8 +43,7 @@ namespace scbm {
 namespace {
 
 constexpr int kTfEpi = 4;                       // epilogue warps = TMEM lane quadrants
-constexpr int kTfProd = 3;                      // E-tile producer warps
-constexpr int kTfWarps = kTfEpi + kTfProd + 1;  // + the MMA warp
+constexpr int kTfWarps = 8;                     // 4 epilogue + the MMA / producer warp + 3 joining a5 only
 constexpr int kTfThreads = kTfWarps * 32;
 constexpr int kRBY = 8, kRBX = 16;  // reference block (M = 128)
 constexpr int kTR = 4, kTC = 16;    // candidate tile (N = 64)
@@ -102,7 +101,7 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_full = sbase, bar_empty = sbase + 16, bar_ef = sbase + 32, bar_ee = sbase + 56;
+  const uint32_t bar_full = sbase, bar_empty = sbase + 16, bar_ee = sbase + 56;
   const uint32_t tmem_slot = sbase + 80, bar_nc = sbase + 96;  // bar_nc[2]: the tile's candidate norms staged
   float* raw = reinterpret_cast<float*>(smem + a.off_raw);
   const uint32_t sE = sbase + a.off_E;
@@ -117,7 +116,6 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       sm100::mbar_init(bar_empty + 8 * i, kTfEpi);
     }
     for (int i = 0; i < kES; ++i) {
-      sm100::mbar_init(bar_ef + 8 * i, kTfProd * 32);
       sm100::mbar_init(bar_ee + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) sm100::mbar_init(bar_nc + 8 * i, 32);
@@ -185,14 +183,14 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
 
-  if (warp == kTfWarps - 1) {
-    // ---------------- MMA issuer (one elected thread) + norm producer (all 32 lanes): once the
-    // TMEM buffer of tile t is free, the warp stages the tile's 8 x 16 candidate norms (a1, from the
-    // L2-resident norm map) into ring slot t & 1 and arrives on bar_nc[slot]; lane 0 issues the MMAs
-    float* ncring = reinterpret_cast<float*>(smem + a.off_nc);  // [2][8][16]
+  if (warp == kTfEpi) {
+    // ---------------- MMA issuer (one elected thread) + tile producer (all 32 lanes): the warp
+    // stages the E tile of t + 1 (hi and lo, E[y][jg][kc][j][t] = x'(cy0 + y, cx0 + 8 jg + j + 4 kc + t))
+    // while the tensor core runs tile t, and the tile's 4 x 16 candidate norms (a1, from the
+    // L2-resident norm map, loaded one tile ahead) into ring slot t & 1 (bar_nc) once the epilogue
+    // has freed that accumulator; lane 0 issues the MMAs. (One waiting warp instead of four.)
+    float* ncring = reinterpret_cast<float*>(smem + a.off_nc);  // [2][4][16]
     const float* nsrc = a.norm + size_t(f) * a.nfs;
-    // the norms of tile t + 1 are loaded while tile t is waited for and issued (their L2 latency
-    // stays off the issue path)
     const int rr = lane >> 2, cq = lane & 3;
     auto load_norms = [&](int t) -> float4 {
       const int ot = order[t];
@@ -201,18 +199,37 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       const int cy = min(cyA + kTR * tr + rr, H - BK);
       return __ldg(reinterpret_cast<const float4*>(nsrc + size_t(cy) * a.Mx + cxA + kTC * tc) + cq);
     };
+    auto stage = [&](int t) {
+      const int ot = order[t];
+      const int tr = ot / NTC, tc = ot - tr * NTC;
+      const float* src0 = raw + (kTR * tr) * a.RWp + kTC * tc;
+      uint8_t* eh = smem + a.off_E + size_t(t % kES) * 2 * kEBytes;
+      for (int e = lane; e < ER * 32; e += 32) {
+        const int y = e >> 5, jg = (e >> 4) & 1, kc = (e >> 3) & 1, j = e & 7;
+        const float* sp = src0 + y * a.RWp + 8 * jg + j + 4 * kc;
+        uint32_t h[4], o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float x = sp[q] - 0.5f;
+          h[q] = tf32_hi(x);
+          o[q] = __float_as_uint(x - __uint_as_float(h[q]));
+        }
+        *reinterpret_cast<uint4*>(eh + e * 16) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(eh + kEBytes + e * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+      __syncwarp();
+    };
     float4 nv_next = load_norms(0);
+    stage(0);
     for (int t = 0; t < ntiles; ++t) {
       const int sl = t % kES, buf = t & 1;
       const float4 nv = nv_next;
       if (t + 1 < ntiles) nv_next = load_norms(t + 1);
       if (t >= 2) sm100::mbar_wait_sleep(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1), 16);
-      {
-        if (rr < kTR) reinterpret_cast<float4*>(ncring + (buf * kTR + rr) * kTC)[cq] = nv;
-        sm100::mbar_arrive(bar_nc + 8 * buf);
-      }
+      if (rr < kTR) reinterpret_cast<float4*>(ncring + (buf * kTR + rr) * kTC)[cq] = nv;
+      sm100::mbar_arrive(bar_nc + 8 * buf);
       if (lane == 0) {
-        sm100::mbar_wait_sleep(bar_ef + 8 * sl, uint32_t((t / kES) & 1), 16);
         sm100::tc_fence_after();
         const uint32_t eh = sE + uint32_t(sl) * 2 * kEBytes, el = eh + kEBytes;
 #pragma unroll 1
@@ -228,34 +245,12 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
         sm100::mma_commit(bar_ee + 8 * sl);
       }
       __syncwarp();
-    }
-  } else if (warp >= kTfEpi) {
-    // ---------------- E-tile producers: E[y][jg][kc][j][t] = x'(cy0 + y, cx0 + 8 jg + j + 4 kc + t), hi and lo
-    const int pt = threadIdx.x - kTfEpi * 32;
-    for (int t = 0; t < ntiles; ++t) {
-      const int sl = t % kES;
-      if (t >= kES) sm100::mbar_wait_sleep(bar_ee + 8 * sl, uint32_t(((t / kES) - 1) & 1), 64);
-      const int ot = order[t];
-      const int tr = ot / NTC, tc = ot - tr * NTC;
-      const float* src0 = raw + (kTR * tr) * a.RWp + kTC * tc;
-      uint8_t* eh = smem + a.off_E + size_t(sl) * 2 * kEBytes;
-      for (int e = pt; e < ER * 32; e += kTfProd * 32) {
-        const int y = e >> 5, jg = (e >> 4) & 1, kc = (e >> 3) & 1, j = e & 7;
-        const float* sp = src0 + y * a.RWp + 8 * jg + j + 4 * kc;
-        uint32_t h[4], o[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float x = sp[q] - 0.5f;
-          h[q] = tf32_hi(x);
-          o[q] = __float_as_uint(x - __uint_as_float(h[q]));
-        }
-        *reinterpret_cast<uint4*>(eh + e * 16) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4*>(eh + kEBytes + e * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+      if (t + 1 < ntiles) {  // the next tile's slot is free once the MMAs of tile t - 1 are done
+        if (t + 1 >= kES) sm100::mbar_wait_sleep(bar_ee + 8 * ((t + 1) % kES), uint32_t((((t + 1) / kES) - 1) & 1), 16);
+        stage(t + 1);
       }
-      sm100::fence_proxy_async_smem();
-      sm100::mbar_arrive(bar_ef + 8 * sl);
     }
-  } else {
+  } else if (warp < kTfEpi) {
     // ---------------- epilogue: warp q = TMEM lanes 32q..32q+31 = references of a 4 x 8 sub-block
     const int q = warp;
     const int wiy0 = iy_first + 4 * (q >> 1), wix0 = ix_first + 8 * (q & 1);
@@ -417,38 +412,70 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       const int ryj = iyj * s, rxj = ixj * s;
       const size_t row = size_t(f) * band_refs + size_t(iyj - a.iy_begin) * a.nx + ixj;
       const float* pr = raw + (ryj - cyA) * a.RWp + (rxj - cxA);
-      WarpTopK<NJ> top;
-      top.init();
+      // the kept keys re-scored exactly; 128-key sets (K + m > 64) sorted once, 4 per lane
+      // (element e = 4 lane + i), smaller ones through the warp lists
+      auto rescore = [&](uint32_t kk) -> uint64_t {
+        if (kk == 0u || kk == 0xffffffffu) return kKeyInf;
+        const int rel = int(kk & ((1u << rb) - 1u)) - 1;
+        const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+        const int cy = ryj + dyy + a.lo, cx = rxj + dxx + a.lo;
+        const float* pc = raw + (cy - cyA) * a.RWp + (cx - cxA);
+        float d = 0.f;
 #pragma unroll
-      for (int sl = 0; sl < NJ; ++sl) {
-        const int k = sl * 32 + lane;
-        uint64_t key = kKeyInf;
-        uint32_t kk;
-        if constexpr (HEAP) kk = k < a.KP ? heaps[m * a.hp + 1 + k] : 0xffffffffu;
-        else kk = k < KR ? lists[m * (KR + 1) + k] : 0xffffffffu;
-        if (kk != 0u && kk != 0xffffffffu) {
-          const int rel = int(kk & ((1u << rb) - 1u)) - 1;
-          const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
-          const int cy = ryj + dyy + a.lo, cx = rxj + dxx + a.lo;
-          const float* pc = raw + (cy - cyA) * a.RWp + (cx - cxA);
-          float d = 0.f;
+        for (int r = 0; r < BK; ++r)
 #pragma unroll
-          for (int r = 0; r < BK; ++r)
+          for (int c = 0; c < BK; ++c) {
+            const float df = pr[r * a.RWp + c] - pc[r * a.RWp + c];
+            d = fmaf(df, df, d);
+          }
+        return (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * W + cx);
+      };
+      auto kept = [&](int k) -> uint32_t {
+        if constexpr (HEAP) return k < a.KP ? heaps[m * a.hp + 1 + k] : 0xffffffffu;
+        else return k < KR ? lists[m * (KR + 1) + k] : 0xffffffffu;
+      };
+      uint64_t kv;  // the K-th exact key (broadcast)
+      if constexpr (NJ >= 3) {
+        uint64_t v[4];
 #pragma unroll
-            for (int c = 0; c < BK; ++c) {
-              const float df = pr[r * a.RWp + c] - pc[r * a.RWp + c];
-              d = fmaf(df, df, d);
-            }
-          key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * W + cx);
+        for (int i = 0; i < 4; ++i) v[i] = rescore(kept(4 * lane + i));
+        warp_sort128(v, lane);
+        uint64_t kq = v[0];
+#pragma unroll
+        for (int i = 1; i < 4; ++i)
+          if (i == (a.K - 1) % 4) kq = v[i];
+        kv = __shfl_sync(0xffffffffu, kq, (a.K - 1) / 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = 4 * lane + i;
+          if (k < a.K) {
+            const bool none = v[i] == kKeyInf;
+            a.idx_out[row * a.K + k] = none ? -1 : int32_t(uint32_t(v[i]));
+            a.dist_out[row * a.K + k] = none ? __int_as_float(0x7f800000) : __uint_as_float(uint32_t(v[i] >> 32));
+          }
         }
-        top.merge(key, lane);
-      }
-      {  // worst kept key vs the exact K-th distance: the filter's error could hide a candidate
-        uint64_t kv = kKeyInf;
+      } else {
+        WarpTopK<NJ> top;
+        top.init();
+#pragma unroll
+        for (int sl = 0; sl < NJ; ++sl) top.merge(rescore(kept(sl * 32 + lane)), lane);
+        kv = kKeyInf;
 #pragma unroll
         for (int sl = 0; sl < NJ; ++sl)
           if (sl == (a.K - 1) / 32) kv = top.v[sl];
         kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
+#pragma unroll
+        for (int sl = 0; sl < NJ; ++sl) {
+          const int k = sl * 32 + lane;
+          if (k < a.K) {
+            const uint64_t key = top.v[sl];
+            const bool none = key == kKeyInf;
+            a.idx_out[row * a.K + k] = none ? -1 : int32_t(uint32_t(key));
+            a.dist_out[row * a.K + k] = none ? __int_as_float(0x7f800000) : __uint_as_float(uint32_t(key >> 32));
+          }
+        }
+      }
+      {  // worst kept key vs the exact K-th distance: the filter's error could hide a candidate
         const float nrj = nrs[m];
         const uint32_t klast = HEAP ? heaps[m * a.hp + 1] : lists[m * (KR + 1) + KR - 1];  // heap root / last
         if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf) {
@@ -458,16 +485,6 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
             const int pos = atomicAdd(a.fix_count, 1);
             a.fix_list[pos] = int(row);
           }
-        }
-      }
-#pragma unroll
-      for (int sl = 0; sl < NJ; ++sl) {
-        const int k = sl * 32 + lane;
-        if (k < a.K) {
-          const uint64_t key = top.v[sl];
-          const bool none = key == kKeyInf;
-          a.idx_out[row * a.K + k] = none ? -1 : int32_t(uint32_t(key));
-          a.dist_out[row * a.K + k] = none ? __int_as_float(0x7f800000) : __uint_as_float(uint32_t(key >> 32));
         }
       }
     }
