@@ -410,12 +410,9 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     for (int j = 0; j < nref; ++j) {
       const int rxj = (ix_first + j) * S;
       const size_t rowj = row0 + j;
-      WarpTopK<NJ> top;
-      top.init();
       double nrq = 0.0;
-#pragma unroll
-      for (int sl = 0; sl < NJ; ++sl) {
-        const int k = sl * 32 + lane;
+      // kept slot k -> its exact (float32 d_NCC, idx) key (double-precision NCC)
+      auto ncc_key = [&](int k) -> uint64_t {
         uint32_t kk;
         if constexpr (HEAP) kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
         else kk = k < a.KP ? scratch[j * (KR + 1) + (KR - a.KP) + k] : 0xffffffffu;  // skip 0 sentinels
@@ -441,19 +438,38 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
             }
         }
         nrq = nrd;  // the same for every slot (the reference's own norm)
-        uint64_t key = kKeyInf;
-        if (have) {
-          const double den = sqrt(nrd * ncd);
-          const float dn = -float(den > 0.0 ? cd / den : 0.0);  // the reported d_NCC
-          key = (uint64_t(ord_f32(dn)) << 32) | uint32_t(cy * a.W + cx);
-        }
-        top.merge(key, lane);
-      }
-      uint64_t kv = kKeyInf;
+        if (!have) return kKeyInf;
+        const double den = sqrt(nrd * ncd);
+        const float dn = -float(den > 0.0 ? cd / den : 0.0);  // the reported d_NCC
+        return (uint64_t(ord_f32(dn)) << 32) | uint32_t(cy * a.W + cx);
+      };
+      // > 64 kept keys: one warp bitonic sort of 128 (4 per lane, element e = 4 lane + i); fewer:
+      // the warp lists. out(k) -> the k-th smallest key
+      uint64_t sv[4];
+      WarpTopK<NJ> top;
+      if constexpr (NJ >= 3) {
 #pragma unroll
-      for (int sl = 0; sl < NJ; ++sl)
-        if (sl == (a.K - 1) / 32) kv = top.v[sl];
-      kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
+        for (int i = 0; i < 4; ++i) sv[i] = ncc_key(4 * lane + i);
+        warp_sort128(sv, lane);
+      } else {
+        top.init();
+#pragma unroll
+        for (int sl = 0; sl < NJ; ++sl) top.merge(ncc_key(sl * 32 + lane), lane);
+      }
+      uint64_t kv;
+      if constexpr (NJ >= 3) {
+        uint64_t kq = sv[0];
+#pragma unroll
+        for (int i = 1; i < 4; ++i)
+          if (i == (a.K - 1) % 4) kq = sv[i];
+        kv = __shfl_sync(0xffffffffu, kq, (a.K - 1) / 4);
+      } else {
+        kv = kKeyInf;
+#pragma unroll
+        for (int sl = 0; sl < NJ; ++sl)
+          if (sl == (a.K - 1) / 32) kv = top.v[sl];
+        kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
+      }
       const uint32_t klast = HEAP ? heap[(j - min(lane, RX - 1)) * a.hp + 1] : scratch[j * (KR + 1) + KR - 1];
       nrq = __shfl_sync(0xffffffffu, nrq, 0);
       if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf && nrq > 0.0) {
@@ -466,10 +482,10 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
         }
       }
 #pragma unroll
-      for (int sl = 0; sl < NJ; ++sl) {
-        const int k = sl * 32 + lane;
+      for (int sl = 0; sl < (NJ >= 3 ? 4 : NJ); ++sl) {
+        const int k = NJ >= 3 ? 4 * lane + sl : sl * 32 + lane;
         if (k < a.K) {
-          const uint64_t key = top.v[sl];
+          const uint64_t key = NJ >= 3 ? sv[sl] : top.v[sl < NJ ? sl : 0];
           const bool none = key == kKeyInf;
           a.idx_out[rowj * a.K + k] = none ? -1 : int32_t(uint32_t(key));
           a.dist_out[rowj * a.K + k] = none ? __int_as_float(0x7f800000) : unord_f32(uint32_t(key >> 32));
