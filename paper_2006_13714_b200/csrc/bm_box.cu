@@ -66,6 +66,9 @@ __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 
 #ifndef SCBM_BOX_SHFL_OUT
 #define SCBM_BOX_SHFL_OUT 0  // 1: write the output rows through shuffles (no staging scratch)
 #endif
+#ifndef SCBM_BOX_JOINT_ROUNDS
+#define SCBM_BOX_JOINT_ROUNDS 1  // both references of a lane inserted in the same survivor rounds
+#endif
 #ifndef SCBM_BOX_MINB
 #define SCBM_BOX_MINB 2  // CTAs per SM the register allocation targets (tuning builds override)
 #endif
@@ -236,6 +239,40 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
 #pragma unroll
     for (int q = 0; q < NY; ++q) rmask[q] = ref_ok[q] ? rows[q] : 0u;
     auto flush = [&](int rel0c) {
+#if SCBM_BOX_JOINT_ROUNDS
+      if constexpr (!NCC && NY == 2) {
+        // both references of a lane in the same rounds: one survivor of each per round (two insertion
+        // networks), so a round lasts as long as the busiest lane's busier list instead of the
+        // busiest lane of each list in turn (a c5 simulation: ~10 % less round work)
+        unsigned b0 = pend[0], b1 = pend[1];
+        if (__any_sync(0xffffffffu, (b0 | b1) != 0u)) {
+          const uint32_t s0 = uint32_t(__cvta_generic_to_shared(scratch + lane));
+          const uint32_t s1 = s0 + 4u * uint32_t(64 * VY);
+          const int relB = rel0c - VY * Wn;
+          const uint32_t dthr0 = uint32_t(thr[0] + nr[0]), dthr1 = uint32_t(thr[1] + nr[1]);
+          while (__any_sync(0xffffffffu, (b0 | b1) != 0u)) {
+            uint32_t p0, p1, d0, d1;
+            asm("bfind.u32 %0, %1;" : "=r"(p0) : "r"(b0));
+            asm("bfind.u32 %0, %1;" : "=r"(p1) : "r"(b1));
+            const int i0 = int(min(p0, uint32_t(2 * VY - 1))), i1 = int(min(p1, uint32_t(2 * VY - 1)));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d0) : "r"(s0 + 128u * uint32_t(i0)));
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d1) : "r"(s1 + 128u * uint32_t(i1)));
+            const int rel0 = (i0 < VY ? rel0p : relB) + i0 * Wn, rel1 = (i1 < VY ? rel0p : relB) + i1 * Wn;
+            const uint32_t k0 = ((min(dthr0 - d0, dsat) << rbits) | uint32_t(rel0)) | (b0 ? 0u : 0xffffffffu);
+            const uint32_t k1 = ((min(dthr1 - d1, dsat) << rbits) | uint32_t(rel1)) | (b1 ? 0u : 0xffffffffu);
+            b0 &= ~(1u << i0);
+            b1 &= ~(1u << i1);
+            rt[0].insert(k0);
+            rt[1].insert(k1);
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) thr[q] = key32.thr(a.K == KR ? rt[q].r[KR - 1] : rt[q].at(a.K - 1)) - nr[q];
+          __syncwarp();
+        }
+        pend[0] = pend[1] = 0u;
+        return;
+      }
+#endif
 #pragma unroll
       for (int q = 0; q < NY; ++q) {
         unsigned bits = pend[q];
