@@ -366,29 +366,35 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   if constexpr (WS == 2) {
     // merge the second half's list into the first's (0 sentinels skipped), then only the first
     // half's warps go on to a5
-    // (the lists go to a per-row area -- by default the staged region, free once every warp is done)
-    uint32_t* ml = reinterpret_cast<uint32_t*>(smf) + a.lofs + wr * RX * (KR + 1);
-    __syncthreads();
-    if (hh == 1 && wact && lane < RX) {
+    // (in rounds of 16 keys through the second warp's own scratch, [k][lane]: the staged region
+    // stays intact for the a5 re-score)
+    uint32_t* ml = scr0 + (kFWarps + wr) * a.scr;
 #pragma unroll
-      for (int k = 0; k < KR; ++k) ml[lane * (KR + 1) + k] = rt.r[k];
-    }
-    __syncthreads();
-    if (hh == 1 || !wact) return;
-    if (lane < RX) {
-#pragma unroll 1
-      for (int k = 0; k < KR; ++k) {
-        const uint32_t x = ml[lane * (KR + 1) + k];
-        rt.insert(x == 0u ? 0xffffffffu : x);
+    for (int k0 = 0; k0 < KR; k0 += 16) {
+      __syncthreads();
+      if (hh == 1 && wact) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k0 + k < KR) ml[k * 32 + lane] = rt.r[k0 + k < KR ? k0 + k : 0];
+      }
+      __syncthreads();
+      if (hh == 0 && wact && lane < RX) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if (k0 + k < KR) {
+            const uint32_t x = ml[k * 32 + lane];
+            rt.insert(x == 0u ? 0xffffffffu : x);
+          }
+        }
       }
     }
+    if (hh == 1 || !wact) return;
   }
 
   // ---- a5 + a6: stage each reference's KP keys (register lists; the heaps already are in shared
   // memory), then per reference (warp-cooperative) re-score them by direct differences from the
   // input, sort the (distance, idx) keys and write K.
-  if constexpr (WS == 2) scratch = reinterpret_cast<uint32_t*>(smf) + a.lofs + wr * RX * (KR + 1);
-  if constexpr (!HEAP) {
+  if constexpr (!HEAP && WS == 1) {
     if (lane_ok) {
 #pragma unroll
       for (int k = 0; k < KR; ++k) scratch[lane * (KR + 1) + k] = rt.r[k];
@@ -567,6 +573,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   } else {
   for (int j = 0; j < nref; ++j) {
     const int rxj = (ix_first + j) * S;
+    const float nrj_a5 = __shfl_sync(0xffffffffu, nr, j);  // ||X_i||^2 (centred) of reference j
     WarpTopK<NJ> top;
     top.init();
 #pragma unroll
@@ -574,8 +581,20 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       const int k = sl * 32 + lane;
       uint64_t key = kKeyInf;
       uint32_t kk;
-      if constexpr (HEAP) kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
-      else kk = k < KR ? scratch[j * (KR + 1) + k] : 0xffffffffu;
+      if constexpr (HEAP) {
+        kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
+      } else if constexpr (WS == 2) {  // lane j's register list, one key per lane by shuffles
+        kk = 0xffffffffu;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          if (sl * 32 + q < KR) {
+            const uint32_t v = __shfl_sync(0xffffffffu, rt.r[sl * 32 + q < KR ? sl * 32 + q : 0], j);
+            if (lane == q) kk = v;
+          }
+        }
+      } else {
+        kk = k < KR ? scratch[j * (KR + 1) + k] : 0xffffffffu;
+      }
       if (kk != 0u && kk != 0xffffffffu) {
         int rel = int(kk & ((1u << rb) - 1u)) - 1;
         int zc = 0;
@@ -588,23 +607,41 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
         const int cy = ry + dyy + a.lo, cx = rxj + dxx + a.lo;
         const float* cimg = Z3 ? reinterpret_cast<const float*>(vol) + size_t(zc) * plane : img;
         // (rows in independent partial sums, 4 in flight: the loads of a row do not wait for the
-        // previous row's FMA chain -- a5 is latency-bound on these L1/L2 reads)
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int c = 0; c < nch; ++c) {
-          const float* pr = img + c * plane + size_t(ry) * a.W + rxj;
-          const float* pc = cimg + c * plane + size_t(cy) * a.W + cx;
+        // previous row's FMA chain)
+        auto rescore = [&](auto ld_r, auto ld_c) -> float {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int c = 0; c < nch; ++c) {
 #pragma unroll 4
-          for (int l = 0; l < BK; ++l) {
-            float t = 0.f;
+            for (int l = 0; l < BK; ++l) {
+              float t = 0.f;
 #pragma unroll
-            for (int m = 0; m < BK; ++m) {
-              const float df = __ldg(pr + l * a.W + m) - __ldg(pc + l * a.W + m);
-              t = fmaf(df, df, t);
+              for (int m = 0; m < BK; ++m) {
+                const float df = ld_r(c, l, m) - ld_c(c, l, m);
+                t = fmaf(df, df, t);
+              }
+              acc[l & 3] += t;
             }
-            acc[l & 3] += t;
           }
+          return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        };
+        auto from_global = [&]() {
+          return rescore([&](int c, int l, int m) { return __ldg(img + c * plane + size_t(ry + l) * a.W + rxj + m); },
+                         [&](int c, int l, int m) { return __ldg(cimg + c * plane + size_t(cy + l) * a.W + cx + m); });
+        };
+        float d;
+        if constexpr (Z3) {
+          d = from_global();
+        } else {
+          // from the staged region (x' = fl(x - 0.5), shared memory): x' differs from x - 0.5 by at
+          // most 2^-24 |x'|, which moves d by at most 2^-23 sqrt(2 d) (2 sqrt(n_r) + sqrt(d))
+          // (Cauchy-Schwarz) -- below 5e-6 d whenever d >= n_r / 205. Closer pairs (near-duplicate
+          // patches) are re-scored from the input in global memory.
+          const float* prs = smf + (ry - Ybase) * a.RWp + (rxj - Xbase);
+          const float* pcs = smf + (cy - Ybase) * a.RWp + (cx - Xbase);
+          d = rescore([&](int c, int l, int m) { return prs[c * a.PL + l * a.RWp + m]; },
+                      [&](int c, int l, int m) { return pcs[c * a.PL + l * a.RWp + m]; });
+          if (d * 180.f < nrj_a5) d = from_global();
         }
-        const float d = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t((Z3 ? zc * a.H : 0) * a.W + cy * a.W + cx);
       }
       top.merge(key, lane);
@@ -618,11 +655,13 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       const float nrj = __shfl_sync(0xffffffffu, nr, j);
       uint32_t klast;
       if constexpr (HEAP) klast = heap[(j - min(lane, RX - 1)) * a.hp + 1];  // max-heap root
+      else if constexpr (WS == 2) klast = __shfl_sync(0xffffffffu, rt.r[KR - 1], j);
       else klast = scratch[j * (KR + 1) + KR - 1];
       if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf) {
         const float dK = __uint_as_float(uint32_t(kv >> 32));
         const float smin = __uint_as_float((klast >> rb) << (rb - 1));
-        if (smin <= fmaf(dK, 1.0f + 1e-5f, 4e-6f * (nrj + dK))) {
+        // (1.5e-5: the exact K-th distance comes from the staged region, within 5e-6 of the input's)
+        if (smin <= fmaf(dK, 1.0f + 1.5e-5f, 4e-6f * (nrj + dK))) {
           const int pos = atomicAdd(a.fix_count, 1);
           a.fix_list[pos] = int(row0 + j);
         }
