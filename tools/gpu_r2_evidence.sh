@@ -8,7 +8,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 > $O/pytest_gpu.log 2>&1; echo "pytest=$?" >> $O/status.txt
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench_c5.log 2>&1; echo "bench_c5=$?" >> $O/status.txt
 for c in c1 c2 c3 c4; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --graph > $O/bench_$c.log 2>&1; echo "bench_$c=$?" >> $O/status.txt; done
-for c in c2 c3 c4; do timeout 600 python bench.py --config $c --kernel tcf --steps 5 --warmup 3 --no-e2e --no-cpu > $O/bench_tcf_$c.log 2>&1; echo "tcf_$c=$?" >> $O/status.txt; done
+timeout 600 python bench.py --config c2 --kernel tcf --steps 5 --warmup 3 --no-e2e --no-cpu > $O/bench_tcf_c2.log 2>&1; echo "tcf_c2=$?" >> $O/status.txt
+timeout 600 python bench.py --config c3 --kernel boxf --steps 5 --warmup 3 --no-e2e --no-cpu > $O/bench_boxf_c3.log 2>&1; echo "boxf_c3=$?" >> $O/status.txt
+timeout 600 python bench.py --kernel tc --steps 2 --warmup 3 --no-e2e --no-cpu > $O/bench_tc_c5.log 2>&1; echo "tc_c5=$?" >> $O/status.txt
 for c in c5 c2 c3 c4; do timeout 600 python bench.py --config $c --metric ncc --steps 5 --warmup 3 --no-e2e > $O/bench_ncc_$c.log 2>&1; echo "ncc_$c=$?" >> $O/status.txt; done
 for c in v1 m1; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 > $O/bench_$c.log 2>&1; echo "bench_$c=$?" >> $O/status.txt; done
 timeout 600 python bench.py --temporal 1 --steps 5 --warmup 3 --no-cpu > $O/bench_temporal_c5.log 2>&1; echo "temporal=$?" >> $O/status.txt
