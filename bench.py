@@ -597,6 +597,7 @@ def main():
         return bench_3d(args, cfg)
 
     import torch
+    from paper_2006_13714_b200 import bm
     from paper_2006_13714_b200.bm import Plan
 
     ws, rank, local = _dist_env()
@@ -809,6 +810,34 @@ def main():
                "h2d_bytes_per_step": int(xh.numel() * xh.element_size()) * (ws if cfg.N > 1 else 1),
                "d2h_bytes_per_step": int(2 * hi.numel() * 4) * (ws if cfg.N > 1 else 1),
                "steps": e_steps, "timing": "wall clock around sc_bm_run_host (synchronous), max over ranks"}
+        # the same through the packed tables (sc_bm_set_packed: one lossless uint32 word per result,
+        # SURVEY 8e), which halve the PCIe-bound device->host copy; decoded and compared once
+        if cfg.dtype == "u8" and args.metric == "l2" and info["kernel"] == 3:
+            plan.set_packed(max(4096, info["n_refs"] // 4))
+            words, _ = plan.packed_words(nloc)
+            hp = torch.empty(words, dtype=torch.int32).pin_memory()
+            plan.run_host_packed(xh, out=hp)
+            if dist:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(e_steps):
+                plan.run_host_packed(xh, out=hp)
+            p_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+            tp = torch.tensor([p_ms], dtype=torch.float64, device="cuda")
+            if dist:
+                dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+            p_ms = tp.item()
+            body = nloc * info["n_refs"] * cfg.K
+            n_esc = int(hp[body].item())
+            pi, pd = bm.unpack_host(cfg.H, cfg.W, cfg.b, cfg.s, cfg.Wn, cfg.K, hp, nloc)
+            same = bool(np.array_equal(pi, hi.numpy()) and np.array_equal(pd, hd.numpy()))
+            plan.set_packed(0)
+            e2e["packed"] = {"value": pairs_step / (p_ms / 1e3), "unit": UNIT, "ms_per_step": p_ms,
+                             "h2d_bytes_per_step": e2e["h2d_bytes_per_step"],
+                             "d2h_bytes_per_step": int((body + 2 + n_esc * (2 + 2 * cfg.K)) * 4) * (ws if cfg.N > 1 else 1),
+                             "escape_rows": n_esc, "decoded_equals_plain": same,
+                             "what": "sc_bm_run_host with packed tables (uint32 (dist << rb) | window slot, "
+                                     "lossless); host decode sc_bm_unpack_host outside the timed region"}
 
     gather = None
     if dist and (args.gather or (cfg.N > 1 and args.temporal == 0)):  # default at N > 1

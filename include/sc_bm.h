@@ -79,7 +79,8 @@ typedef enum {
     SC_ERR_UNSUPPORTED = 2,      /* valid request this build cannot serve (e.g. no sm_100 device) */
     SC_ERR_OUT_OF_MEMORY = 3,    /* workspace allocation failed */
     SC_ERR_CUDA = 4,             /* CUDA runtime / launch error */
-    SC_ERR_WRONG_DEVICE = 5      /* current device differs from the plan's device */
+    SC_ERR_WRONG_DEVICE = 5,     /* current device differs from the plan's device */
+    SC_ERR_OVERFLOW = 6          /* packed tables: more escape rows than the overflow area holds */
 } sc_status_t;
 
 typedef struct sc_bm_plan_s* sc_bm_plan_t;
@@ -244,6 +245,49 @@ sc_status_t sc_bm_plan3d(int H, int W, int d, int b, int stride, int window, int
                          sc_dtype_t dtype, sc_bm_plan_t* plan_out);
 sc_status_t sc_bm_run3d(sc_bm_plan_t plan, const void* vol, int64_t n_planes, int32_t* idx_out, void* dist_out,
                         sc_stream_t stream);
+
+/*
+ * Packed tables (halve the device->host copy and the gather of the results; a
+ * LOSSLESS re-encoding of the Eq. 3 output, not a different result).
+ * sc_bm_set_packed(plan, cap_rows > 0) switches a uint8 L2 plan with one channel on the box-sum
+ * matcher (SC_KERNEL_BOX; b = 8, stride 4) to writing every (idx, dist) result as ONE uint32 word
+ *     w = (dist << rb) | slot,   slot = (cy - ry - lo) * Wn + (cx - rx - lo)   (the window slot),
+ * rb = ceil(log2(Wn^2)) (>= 2, from sc_bm_packed_words), for every row whose K distances are all
+ * < 2^(32 - rb) - 1 (the matcher's own 32-bit keys: the words ARE its register keys). A row that
+ * does not fit (a distance >= 2^(32-rb) - 1, or fewer than K candidates) is written as K escape
+ * words 0xFFFFFFFF and its exact row goes to the overflow area after the rows. Buffer layout
+ * (uint32 words; sc_bm_packed_words(plan, n_images) gives the total):
+ *     [0, R)          R = n_images * n_refs * K row words, rows in the order of idx_out,
+ *     R + 0           escape rows written by the run (may exceed cap_rows: the excess is lost),
+ *     R + 1           cap_rows,
+ *     R + 2 + r (2 + 2K)   record r < min(count, cap_rows): the row number (n_refs * image +
+ *                     reference; low, high 32 bits), its K idx, its K dist (as sc_bm_run_batch).
+ * In packed mode sc_bm_run / sc_bm_run_batch / sc_bm_run_host take the packed buffer as
+ * idx_out (device / host) and dist_out = NULL (else SC_ERR_INVALID_ARGUMENT); sc_bm_run_rows
+ * over a partial band, sc_bm_run_temporal, T > 0 and any other matcher return SC_ERR_UNSUPPORTED.
+ * cap_rows = 0 restores the plain tables. SC_ERR_UNSUPPORTED for a plan that cannot pack.
+ * Records are in no particular order (device atomics); decoded tables are identical to the plain
+ * run's. run_host allocates its overflow staging on the first packed call.
+ */
+sc_status_t sc_bm_set_packed(sc_bm_plan_t plan, int64_t cap_rows);
+/* Words of a packed buffer for n_images images and the slot bits rb (host pointers). */
+sc_status_t sc_bm_packed_words(sc_bm_plan_t plan, int64_t n_images, int64_t* words_out, int32_t* rel_bits_out);
+/*
+ * Decode a packed buffer of n_images images (device pointers) into idx_out / dist_out
+ * [n_images][n_refs][K] int32 (the plain tables, bit-identical). Reads the overflow count first
+ * (synchronises `stream`): SC_ERR_OVERFLOW when escape rows were lost (re-run unpacked or with a
+ * larger cap_rows); then two kernels, asynchronous on `stream`.
+ */
+sc_status_t sc_bm_unpack(sc_bm_plan_t plan, const uint32_t* packed, int64_t n_images, int32_t* idx_out,
+                         int32_t* dist_out, sc_stream_t stream);
+/*
+ * The same decode on the host (plain C++; no device, no plan: the geometry is passed): for a
+ * packed buffer of n_images images of H x W with patch b, stride, window Wn, K results per row.
+ * SC_ERR_INVALID_ARGUMENT for a bad geometry or a slot outside the window, SC_ERR_OVERFLOW when
+ * escape rows were lost.
+ */
+sc_status_t sc_bm_unpack_host(int H, int W, int b, int stride, int window, int K, const uint32_t* packed,
+                              int64_t n_images, int32_t* idx_out, int32_t* dist_out);
 
 /* Plan geometry and bookkeeping. */
 sc_status_t sc_bm_plan_info(sc_bm_plan_t plan, sc_bm_info_t* info);

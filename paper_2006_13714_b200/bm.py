@@ -17,14 +17,15 @@ LIB_PATH = os.environ.get("SCBM_LIB") or os.path.join(_HERE, "libscbm.so")  # SC
 SC_DTYPE_U8, SC_DTYPE_F32 = 0, 1
 SC_KERNEL_SIMT, SC_KERNEL_TC_I8, SC_KERNEL_SIMT_WARP, SC_KERNEL_BOX, SC_KERNEL_BOXF, SC_KERNEL_TC_F32 = 0, 1, 2, 3, 4, 5
 STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARGUMENT", 2: "SC_ERR_UNSUPPORTED",
-          3: "SC_ERR_OUT_OF_MEMORY", 4: "SC_ERR_CUDA", 5: "SC_ERR_WRONG_DEVICE"}
+          3: "SC_ERR_OUT_OF_MEMORY", 4: "SC_ERR_CUDA", 5: "SC_ERR_WRONG_DEVICE", 6: "SC_ERR_OVERFLOW"}
 
 SC_METRIC_L2, SC_METRIC_NCC = 0, 1
 EXPORTED = ["sc_bm_plan", "sc_bm_plan_ex", "sc_bm_run", "sc_bm_run_batch", "sc_bm_run_rows", "sc_bm_run_host",
             "sc_bm_plan_info", "sc_bm_set_kernel", "sc_bm_destroy", "sc_status_string",
             "sc_bm_norm_map", "sc_bm_run_dense_debug", "sc_bm_set_timing", "sc_bm_get_timing", "sc_bm_group",
             "sc_bm_nlm_weights", "sc_bm_set_temporal", "sc_bm_debug_fix_count", "sc_bm_nlm_average",
-            "sc_bm_run_temporal", "sc_bm_plan3d", "sc_bm_run3d"]
+            "sc_bm_run_temporal", "sc_bm_plan3d", "sc_bm_run3d", "sc_bm_set_packed", "sc_bm_packed_words",
+            "sc_bm_unpack", "sc_bm_unpack_host"]
 
 
 class ScError(RuntimeError):
@@ -86,6 +87,10 @@ def load_library():
     L.sc_bm_set_temporal.argtypes = [vp, i32]
     L.sc_bm_plan3d.argtypes = [ci, ci, ci, ci, ci, ci, ci, ci, ci, ci, ctypes.POINTER(vp)]
     L.sc_bm_run3d.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.sc_bm_set_packed.argtypes = [vp, i64]
+    L.sc_bm_packed_words.argtypes = [vp, i64, ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    L.sc_bm_unpack.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.sc_bm_unpack_host.argtypes = [ci, ci, ci, ci, ci, ci, vp, i64, vp, vp]
     for fn in EXPORTED:
         if fn != "sc_status_string":
             getattr(L, fn).restype = ci
@@ -233,6 +238,66 @@ class Plan:
             ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
         return idx, dist
 
+    # ------------------------------------------------------------------ packed tables (sc_bm_set_packed)
+    def set_packed(self, cap_rows: int):
+        """Packed tables: one uint32 word (dist << rb) | window slot per result, escape rows in an
+        overflow area of cap_rows records (0: plain tables again)."""
+        _check("sc_bm_set_packed", self._lib.sc_bm_set_packed(self._h, int(cap_rows)))
+
+    def packed_words(self, n_images: int):
+        """(words of a packed buffer for n_images images, slot bits rb)."""
+        w, rb = ctypes.c_int64(0), ctypes.c_int32(0)
+        _check("sc_bm_packed_words", self._lib.sc_bm_packed_words(self._h, int(n_images), ctypes.byref(w),
+                                                                  ctypes.byref(rb)))
+        return w.value, rb.value
+
+    def _check_packed(self, buf, words, cuda):
+        import torch
+        if not isinstance(buf, torch.Tensor) or buf.dtype != torch.int32 or buf.is_cuda != cuda or \
+                not buf.is_contiguous() or buf.numel() != words:
+            raise ValueError(f"packed buffer must be a contiguous {'CUDA' if cuda else 'host'} int32 tensor "
+                             f"of {words} words (uint32 bit patterns)")
+        return buf
+
+    def run_packed(self, imgs, out=None, stream=None):
+        """Packed block matching on device tensors: an int32 tensor of packed_words(N) words."""
+        import torch
+        imgs = self._check_img(imgs)
+        words, _ = self.packed_words(imgs.shape[0])
+        buf = self._check_packed(out, words, True) if out is not None else \
+            torch.empty(words, dtype=torch.int32, device=imgs.device)
+        _check("sc_bm_run_batch", self._lib.sc_bm_run_batch(
+            self._h, ctypes.c_void_p(imgs.data_ptr()), imgs.shape[0], ctypes.c_void_p(buf.data_ptr()),
+            None, _stream_ptr(stream)))
+        return buf
+
+    def run_host_packed(self, imgs, out=None, stream=None):
+        """Packed block matching, host buffers in and out (sc_bm_run_host in packed mode)."""
+        import torch
+        t = imgs if isinstance(imgs, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(imgs))
+        if t.dim() == 3:
+            t = t.unsqueeze(0)
+        if t.is_cuda or not t.is_contiguous() or t.dtype != torch.uint8 or t.dim() != 4 or \
+                tuple(t.shape[1:]) != (self.C, self.H, self.W):
+            raise ValueError(f"run_host_packed expects a contiguous host uint8 tensor/array [N, {self.C}, {self.H}, {self.W}]")
+        words, _ = self.packed_words(t.shape[0])
+        buf = self._check_packed(out, words, False) if out is not None else torch.empty(words, dtype=torch.int32)
+        _check("sc_bm_run_host", self._lib.sc_bm_run_host(
+            self._h, ctypes.c_void_p(t.data_ptr()), t.shape[0], ctypes.c_void_p(buf.data_ptr()), None,
+            _stream_ptr(stream)))
+        return buf
+
+    def unpack(self, packed, n_images, out=None, stream=None):
+        """Decode a device packed buffer of n_images images into the plain (idx, dist) tables."""
+        words, _ = self.packed_words(n_images)
+        packed = self._check_packed(packed, words, True)
+        idx, dist = (self._check_out(out, n_images, self.n_refs, True) if out is not None
+                     else self.alloc_out(n_images))
+        _check("sc_bm_unpack", self._lib.sc_bm_unpack(
+            self._h, ctypes.c_void_p(packed.data_ptr()), int(n_images), ctypes.c_void_p(idx.data_ptr()),
+            ctypes.c_void_p(dist.data_ptr()), _stream_ptr(stream)))
+        return idx, dist
+
     def group(self, imgs, idx, out=None, stream=None):
         """Patch groups Y_i of a run's idx table: [N, n_refs, K, C, b, b] (input dtype)."""
         import torch
@@ -341,6 +406,23 @@ class Plan3D(Plan):
                                                     ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(dist.data_ptr()),
                                                     _stream_ptr(stream)))
         return idx, dist
+
+
+def unpack_host(H, W, b, stride, window, K, packed, n_images):
+    """Host decode of a packed buffer (sc_bm_unpack_host; no device): numpy (idx, dist) int32
+    [n_images, n_refs, K]. ``packed``: uint32/int32 numpy array (or host tensor) of the words."""
+    L = load_library()
+    p = np.ascontiguousarray(packed.numpy() if hasattr(packed, "numpy") else packed).view(np.uint32)
+    ny, nx = (H - b) // stride + 1, (W - b) // stride + 1
+    idx = np.empty((n_images, ny * nx, K), dtype=np.int32)
+    dist = np.empty_like(idx)
+    body = n_images * ny * nx * K
+    if p.size < body + 2 or p.size < body + 2 + min(int(p[body]), int(p[body + 1])) * (2 + 2 * K):
+        raise ValueError("packed buffer is shorter than its rows + overflow area")
+    _check("sc_bm_unpack_host", L.sc_bm_unpack_host(H, W, b, stride, window, K, p.ctypes.data_as(ctypes.c_void_p),
+                                                    int(n_images), idx.ctypes.data_as(ctypes.c_void_p),
+                                                    dist.ctypes.data_as(ctypes.c_void_p)))
+    return idx, dist
 
 
 def status_string(code: int) -> str:

@@ -59,6 +59,7 @@ struct BoxArgs {
   uint32_t dsat;   // 32-bit keys: distance saturation value
   int* fix_count;
   int* fix_list;
+  int packed;      // packed tables (sc_bm_set_packed): idx_out receives the row keys themselves
 };
 
 __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 1) : -(k >> 1); }
@@ -521,7 +522,9 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
         const uint32_t v = __shfl_sync(0xffffffffu, rt[q].r[kq], j);
         if (kq == k) kk = v;
       }
-      if (e < nref * a.K) {
+      if (e < nref * a.K && !TEMP && a.packed) {
+        reinterpret_cast<uint32_t*>(a.idx_out)[row0 * a.K + e] = kk;
+      } else if (e < nref * a.K) {
         int rel = key32.rel(kk);
         const int tsl = TEMP ? rel / (Wn * Wn) : 0;  // frame slot tau + T
         rel -= tsl * Wn * Wn;
@@ -541,6 +544,10 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     __syncwarp();
     auto emit = [&](int e, int j, int k) {
       const uint32_t kk = scratch[j * (KR + 1) + k];
+      if (!TEMP && a.packed) {  // the key is the packed word (rows that do not fit: the fix-up's)
+        reinterpret_cast<uint32_t*>(a.idx_out)[row0 * a.K + e] = kk;
+        return;
+      }
       int rel = key32.rel(kk);
       const int tsl = TEMP ? rel / (Wn * Wn) : 0;  // frame slot tau + T
       rel -= tsl * Wn * Wn;
@@ -661,6 +668,7 @@ cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy
     if (e != cudaSuccess) return e;
     return launch_fixup(p, imgs, F, iy_begin, iy_end, idx_out, dist_out, st);
   }
+  a.packed = p.packed_cap > 0 ? 1 : 0;  // (T = 0, L2: the packed run checks)
   cudaError_t e = cudaMemsetAsync(p.ws.fix_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   if (kr == 16 && g.Wn == 33) e = launch_box_t<2, 11, 16, 40, false, 33>(a, F, smem, st);  // c5: all constant

@@ -29,6 +29,13 @@ struct FixArgs {
   // 3D search (sc_bm_plan3d): reference plane (frame0 + f) * sz of a P-plane volume at imgs,
   // candidates at plane offsets [zlo, zhi] (clipped to [0, P - C]), idx = (z H + y) W + x
   int z3, sz, P, zlo, zhi;
+  // packed tables (uint8 L2, K <= 32; packed.cu): idx_out receives the row words
+  // (dist << prb) | slot, rows that do not fit -> escape words + an overflow record in ptail
+  int packed, Wn, prb;
+  uint32_t pdsat;
+  uint32_t* ptail;
+  long long pk_f0;  // image index (in the run) of the chunk's first frame
+  int nref_full;    // references per image
 };
 
 // NCC (Eq. 4): a reference whose kept top-(K+8) could have lost a top-K candidate to the 32-bit
@@ -203,6 +210,36 @@ __global__ void __launch_bounds__(256) fixup_kernel(FixArgs a) {
       top.merge(key, lane);
     }
     const size_t o = size_t(code) * a.K;
+    if (U8 && a.packed) {  // K <= 32: lane k holds rank k
+      const uint64_t key = top.v[0];
+      const bool none = key == kKeyInf;
+      const uint32_t d = uint32_t(key >> 32), ci = uint32_t(key);
+      uint32_t* pk = reinterpret_cast<uint32_t*>(a.idx_out);
+      if (__all_sync(0xffffffffu, lane >= a.K || (!none && d < a.pdsat))) {
+        if (lane < a.K) {
+          const int cy = int(ci) / a.W, cx = int(ci) - (int(ci) / a.W) * a.W;
+          pk[o + lane] = (d << a.prb) | uint32_t((cy - ry - a.lo) * a.Wn + (cx - rx - a.lo));
+        }
+      } else {  // escape row + its exact record
+        if (lane < a.K) pk[o + lane] = 0xffffffffu;
+        uint32_t pos = 0u;
+        if (lane == 0) pos = atomicAdd(a.ptail, 1u);
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (pos < a.ptail[1]) {
+          uint32_t* rec = a.ptail + 2 + size_t(pos) * (2 + 2 * a.K);
+          const long long row = (a.pk_f0 + f) * a.nref_full + (long long)iy * a.nx + ix;
+          if (lane == 0) {
+            rec[0] = uint32_t(row);
+            rec[1] = uint32_t(row >> 32);
+          }
+          if (lane < a.K) {
+            rec[2 + lane] = none ? 0xffffffffu : ci;
+            rec[2 + a.K + lane] = none ? 0x7fffffffu : d;
+          }
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int k = lane + 32 * j;
@@ -249,6 +286,15 @@ cudaError_t launch_fixup(const sc_bm_plan_s& p, const void* imgs, int F, int iy_
     a.n_frames = 1 << 30;
   }
   (void)F;
+  if (p.packed_cap > 0 && g.dtype == SC_DTYPE_U8 && !a.ncc && p.T == 0 && !g.z3) {
+    a.packed = 1;
+    a.Wn = g.Wn;
+    a.prb = packed_rel_bits(g);
+    a.pdsat = uint32_t((uint64_t(1) << (32 - a.prb)) - 1);
+    a.ptail = p.packed_tail;
+    a.pk_f0 = p.packed_f0;
+    a.nref_full = g.ny * g.nx;
+  }
   if (g.dtype == SC_DTYPE_U8) fixup_kernel<uint8_t><<<p.sm_count * 2, 256, 0, st>>>(a);
   else fixup_kernel<float><<<p.sm_count * 2, 256, 0, st>>>(a);
   return cudaGetLastError();

@@ -75,6 +75,7 @@ void free_host(sc_bm_plan_s* p) {
   }
   cudaStreamDestroy(h.copy_in);
   cudaStreamDestroy(h.copy_out);
+  if (h.d_tail) cudaFree(h.d_tail);
   h = HostStaging{};
 }
 
@@ -110,6 +111,7 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
     p->batch_base = imgs;  // temporal search reads the neighbouring frames of the whole batch
     p->batch_f0 = f0;
     p->batch_n = n;
+    p->packed_f0 = p->packed_base + (f0 - f_begin);  // packed tables: overflow records' row numbers
     int32_t* io = idx ? idx + (f0 - f_begin) * out_elems : nullptr;
     void* dd = dist ? static_cast<char*>(dist) + (f0 - f_begin) * out_elems * 4 : nullptr;
     if (avg)
@@ -136,6 +138,9 @@ sc_status_t enqueue(sc_bm_plan_s* p, const void* imgs, int64_t n, int iy_begin, 
   return SC_OK;
 }
 
+// packed tables: the plan can pack now (matcher, temporal radius) -- checked at every packed run
+bool packed_ok(const sc_bm_plan_s* p) { return p->kernel == SC_KERNEL_BOX && p->T == 0; }
+
 }  // namespace
 
 extern "C" {
@@ -148,6 +153,7 @@ const char* sc_status_string(sc_status_t s) {
     case SC_ERR_OUT_OF_MEMORY: return "SC_ERR_OUT_OF_MEMORY";
     case SC_ERR_CUDA: return "SC_ERR_CUDA";
     case SC_ERR_WRONG_DEVICE: return "SC_ERR_WRONG_DEVICE";
+    case SC_ERR_OVERFLOW: return "SC_ERR_OVERFLOW";
   }
   return "SC_ERR_UNKNOWN";
 }
@@ -272,7 +278,10 @@ sc_status_t sc_bm_plan_ex(int H, int W, int C, int b, int stride, int window, in
 
 sc_status_t sc_bm_run_rows(sc_bm_plan_t p, const void* imgs, int64_t n_images, int32_t iy_begin,
                            int32_t iy_end, int32_t* idx_out, void* dist_out, sc_stream_t stream) {
-  if (!p || !imgs || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (!p || !imgs || !idx_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  // packed tables: idx_out is the packed buffer, dist_out NULL, whole images only
+  if ((p->packed_cap > 0) != (dist_out == nullptr)) return SC_ERR_INVALID_ARGUMENT;
+  if (p->packed_cap > 0 && !(packed_ok(p) && iy_begin == 0 && iy_end == p->g.ny)) return SC_ERR_UNSUPPORTED;
   if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
   if (iy_begin < 0 || iy_end > p->g.ny || iy_end < iy_begin) return SC_ERR_INVALID_ARGUMENT;
   if (p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
@@ -280,6 +289,13 @@ sc_status_t sc_bm_run_rows(sc_bm_plan_t p, const void* imgs, int64_t n_images, i
   if (p->T > 0 && n_images * int64_t(p->g.H) * p->g.W > (int64_t(1) << 31)) return SC_ERR_INVALID_ARGUMENT;
   sc_status_t s = check_device(p);
   if (s != SC_OK) return s;
+  if (p->packed_cap > 0) {  // the overflow area follows the rows: header first
+    p->packed_tail = reinterpret_cast<uint32_t*>(idx_out) + size_t(n_images) * p->g.ny * p->g.nx * p->g.K;
+    p->packed_base = 0;
+    cudaError_t e = launch_packed_init(p->packed_tail, p->packed_cap, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_status(e);
+    ++p->launches;
+  }
   if (n_images == 0 || iy_end == iy_begin) return SC_OK;
   return enqueue(p, imgs, n_images, iy_begin, iy_end, idx_out, dist_out, nullptr,
                  reinterpret_cast<cudaStream_t>(stream));
@@ -290,6 +306,7 @@ sc_status_t sc_bm_run_temporal(sc_bm_plan_t p, const void* imgs, int64_t n_image
                                sc_stream_t stream) {
   if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
   if (!p || !imgs || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (p->packed_cap > 0) return SC_ERR_UNSUPPORTED;  // (batch-global idx: plain tables only)
   if ((reinterpret_cast<uintptr_t>(imgs) & 15) != 0) return SC_ERR_INVALID_ARGUMENT;
   if (f_begin < 0 || f_end > n_images || f_end < f_begin) return SC_ERR_INVALID_ARGUMENT;
   if (p->T == 0) return SC_ERR_UNSUPPORTED;  // sc_bm_run_batch on imgs + f_begin frames does it
@@ -428,8 +445,10 @@ sc_status_t sc_bm_norm_map(sc_bm_plan_t p, const void* img, void* norm_out, sc_s
 sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images, int32_t* h_idx,
                            void* h_dist, sc_stream_t stream) {
   if (p && p->g.z3) return SC_ERR_UNSUPPORTED;  // a 3D plan runs volumes (sc_bm_run3d)
-  if (!p || !h_imgs || !h_idx || !h_dist || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (!p || !h_imgs || !h_idx || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if ((p->packed_cap > 0) != (h_dist == nullptr)) return SC_ERR_INVALID_ARGUMENT;  // packed: h_idx only
   if (p->T > 0) return SC_ERR_UNSUPPORTED;  // chunked staging has no neighbouring frames
+  if (p->packed_cap > 0 && !packed_ok(p)) return SC_ERR_UNSUPPORTED;
   sc_status_t s = check_device(p);
   if (s != SC_OK) return s;
   if (n_images == 0) return SC_OK;
@@ -448,9 +467,15 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
 #define SCBM_HOST_STAGE_MB 24
 #endif
     h.F = int(std::max<size_t>(1, std::min<size_t>(size_t(p->F), (size_t(SCBM_HOST_STAGE_MB) << 20) / std::max<size_t>(out_frame, 1))));
+    // packed tables (box matcher only): stages of several frames -- one frame's box launch (c5: 270
+    // CTAs, one partial wave) would take longer than its 8 MB copy
+#ifndef SCBM_HOST_STAGE_MB_PACKED
+#define SCBM_HOST_STAGE_MB_PACKED 40
+#endif
+    h.Fp = int(std::max<size_t>(1, std::min<size_t>(size_t(p->FB), (size_t(SCBM_HOST_STAGE_MB_PACKED) << 20) / std::max<size_t>(out_elems * 4, 1))));
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
-      e = cudaMalloc(&h.d_img[i], img_bytes * h.F);
-      if (e == cudaSuccess) e = cudaMalloc(&h.d_idx[i], out_elems * 4 * h.F);
+      e = cudaMalloc(&h.d_img[i], img_bytes * std::max(h.F, h.Fp));
+      if (e == cudaSuccess) e = cudaMalloc(&h.d_idx[i], out_elems * 4 * std::max(h.F, h.Fp));
       if (e == cudaSuccess) e = cudaMalloc(&h.d_dist[i], out_elems * 4 * h.F);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.ev_in[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h.ev_done[i], cudaEventDisableTiming);
@@ -467,11 +492,32 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
     h.ready = true;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool packed = p->packed_cap > 0;
+  const size_t rec_words = size_t(packed_record_words(g));
+  if (packed) {  // the run's overflow area lives on the device until the end of the run
+    if (h.tail_cap != p->packed_cap) {
+      if (h.d_tail) cudaFree(h.d_tail);
+      h.d_tail = nullptr;
+      h.tail_cap = -1;
+      e = cudaMalloc(&h.d_tail, (2 + size_t(p->packed_cap) * rec_words) * 4);
+      if (e != cudaSuccess) {
+        h.d_tail = nullptr;
+        cudaGetLastError();
+        return cuda_status(e);
+      }
+      h.tail_cap = p->packed_cap;
+    }
+    p->packed_tail = h.d_tail;
+    e = launch_packed_init(h.d_tail, p->packed_cap, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    ++p->launches;
+  }
   // double-buffered pipeline: H2D(chunk k+1) || match(chunk k) || D2H(chunk k-1)
   int64_t k = 0;
-  for (int64_t f0 = 0; f0 < n_images; f0 += h.F, ++k) {
+  const int FS = packed ? h.Fp : h.F;
+  for (int64_t f0 = 0; f0 < n_images; f0 += FS, ++k) {
     const int slot = int(k & 1);
-    const int F = int(std::min<int64_t>(h.F, n_images - f0));
+    const int F = int(std::min<int64_t>(FS, n_images - f0));
     if (k >= 2) cudaStreamWaitEvent(h.copy_in, h.ev_out[slot], 0);  // slot's D2H finished
     e = cudaMemcpyAsync(h.d_img[slot], static_cast<const char*>(h_imgs) + f0 * img_bytes,
                         img_bytes * F, cudaMemcpyHostToDevice, h.copy_in);
@@ -486,14 +532,16 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
     for (int bi = 0; bi < nb; ++bi) {
       const int y0 = int(int64_t(g.ny) * bi / nb), y1 = int(int64_t(g.ny) * (bi + 1) / nb);
       const size_t off = size_t(y0) * row_elems, cnt = (nb == 1 ? out_elems * F : size_t(y1 - y0) * row_elems);
+      p->packed_base = f0;
       s = enqueue(p, h.d_img[slot], F, nb == 1 ? 0 : y0, nb == 1 ? g.ny : y1, h.d_idx[slot] + off,
-                  static_cast<char*>(h.d_dist[slot]) + off * 4, nullptr, st);
+                  packed ? nullptr : static_cast<char*>(h.d_dist[slot]) + off * 4, nullptr, st);
+      p->packed_base = 0;
       if (s != SC_OK) return s;
       cudaEventRecord(h.ev_done[slot], st);
       cudaStreamWaitEvent(h.copy_out, h.ev_done[slot], 0);
       e = cudaMemcpyAsync(h_idx + f0 * out_elems + off, h.d_idx[slot] + off, cnt * 4, cudaMemcpyDeviceToHost,
                           h.copy_out);
-      if (e == cudaSuccess)
+      if (e == cudaSuccess && !packed)
         e = cudaMemcpyAsync(static_cast<char*>(h_dist) + (f0 * out_elems + off) * 4,
                             static_cast<char*>(h.d_dist[slot]) + off * 4, cnt * 4, cudaMemcpyDeviceToHost, h.copy_out);
       if (e != cudaSuccess) return cuda_status(e);
@@ -502,6 +550,13 @@ sc_status_t sc_bm_run_host(sc_bm_plan_t p, const void* h_imgs, int64_t n_images,
   }
   e = cudaStreamSynchronize(h.copy_out);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && packed) {  // the overflow area after the host rows: header, then the records
+    uint32_t* htail = reinterpret_cast<uint32_t*>(h_idx) + size_t(n_images) * out_elems;
+    e = cudaMemcpy(htail, h.d_tail, 8, cudaMemcpyDeviceToHost);
+    const size_t nrec = e == cudaSuccess ? std::min<size_t>(htail[0], size_t(p->packed_cap)) : 0;
+    if (e == cudaSuccess && nrec > 0)
+      e = cudaMemcpy(htail + 2, h.d_tail + 2, nrec * rec_words * 4, cudaMemcpyDeviceToHost);
+  }
   return cuda_status(e);
 }
 
@@ -533,6 +588,86 @@ sc_status_t sc_bm_plan_info(sc_bm_plan_t p, sc_bm_info_t* info) {
   info->launches = p->launches;
   info->kernel = p->kernel;
   info->device = p->device;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_set_packed(sc_bm_plan_t p, int64_t cap_rows) {
+  if (!p || cap_rows < 0 || cap_rows > (int64_t(1) << 30)) return SC_ERR_INVALID_ARGUMENT;
+  const Geometry& g = p->g;
+  if (cap_rows > 0 && (g.dtype != SC_DTYPE_U8 || g.metric != SC_METRIC_L2 || g.z3 || !box_supported(g)))
+    return SC_ERR_UNSUPPORTED;
+  p->packed_cap = cap_rows;
+  return SC_OK;
+}
+
+sc_status_t sc_bm_packed_words(sc_bm_plan_t p, int64_t n_images, int64_t* words_out, int32_t* rel_bits_out) {
+  if (!p || n_images < 0 || !words_out) return SC_ERR_INVALID_ARGUMENT;
+  if (p->packed_cap <= 0) return SC_ERR_UNSUPPORTED;
+  const Geometry& g = p->g;
+  *words_out = n_images * g.ny * g.nx * g.K + 2 + p->packed_cap * packed_record_words(g);
+  if (rel_bits_out) *rel_bits_out = packed_rel_bits(g);
+  return SC_OK;
+}
+
+sc_status_t sc_bm_unpack(sc_bm_plan_t p, const uint32_t* packed, int64_t n_images, int32_t* idx_out,
+                         int32_t* dist_out, sc_stream_t stream) {
+  if (!p || !packed || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (p->packed_cap <= 0) return SC_ERR_UNSUPPORTED;
+  sc_status_t s = check_device(p);
+  if (s != SC_OK) return s;
+  const Geometry& g = p->g;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint32_t hdr[2] = {0u, 0u};
+  cudaError_t e = cudaMemcpyAsync(hdr, packed + size_t(n_images) * g.ny * g.nx * g.K, 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (hdr[0] > hdr[1]) return SC_ERR_OVERFLOW;  // escape rows whose records were lost
+  e = launch_unpack(*p, packed, n_images, int64_t(hdr[0]), idx_out, dist_out, st);
+  p->launches += hdr[0] > 0 ? 2 : 1;
+  return cuda_status(e);
+}
+
+sc_status_t sc_bm_unpack_host(int H, int W, int b, int stride, int window, int K, const uint32_t* packed,
+                              int64_t n_images, int32_t* idx_out, int32_t* dist_out) {
+  if (!packed || !idx_out || !dist_out || n_images < 0) return SC_ERR_INVALID_ARGUMENT;
+  if (H < b || W < b || b < 1 || stride < 1 || window < 1 || window > 255 || K < 1 || K > 128)
+    return SC_ERR_INVALID_ARGUMENT;
+  const int64_t ny = (H - b) / stride + 1, nx = (W - b) / stride + 1, nref = ny * nx;
+  const int lo = -(window / 2), hi = window - 1 - window / 2;
+  int rb = 0;
+  while ((int64_t(1) << rb) < int64_t(window) * window) ++rb;
+  if (rb < 2) rb = 2;
+  const uint32_t mask = (1u << rb) - 1u;
+  const int64_t rows = n_images * nref;
+  for (int64_t r = 0; r < rows; ++r) {
+    const int64_t j = r % nref;
+    const int64_t ry = (j / nx) * stride, rx = (j % nx) * stride;
+    for (int k = 0; k < K; ++k) {
+      const uint32_t w = packed[r * K + k];
+      int32_t idx = -1, dist = 0x7fffffff;
+      if (w != 0xffffffffu) {
+        const int slot = int(w & mask);
+        if (slot >= window * window) return SC_ERR_INVALID_ARGUMENT;
+        const int dy = slot / window + lo, dx = slot % window + lo;
+        if (dy > hi || ry + dy < 0 || ry + dy > H - b || rx + dx < 0 || rx + dx > W - b) return SC_ERR_INVALID_ARGUMENT;
+        idx = int32_t((ry + dy) * W + rx + dx);
+        dist = int32_t(w >> rb);
+      }
+      idx_out[r * K + k] = idx;
+      dist_out[r * K + k] = dist;
+    }
+  }
+  const uint32_t* tail = packed + rows * K;
+  if (tail[0] > tail[1]) return SC_ERR_OVERFLOW;
+  for (uint32_t i = 0; i < tail[0]; ++i) {
+    const uint32_t* rec = tail + 2 + size_t(i) * (2 + 2 * size_t(K));
+    const int64_t row = int64_t(rec[0]) | (int64_t(rec[1]) << 32);
+    if (row < 0 || row >= rows) return SC_ERR_INVALID_ARGUMENT;
+    for (int k = 0; k < K; ++k) {
+      idx_out[row * K + k] = int32_t(rec[2 + k]);
+      dist_out[row * K + k] = int32_t(rec[2 + K + k]);
+    }
+  }
   return SC_OK;
 }
 

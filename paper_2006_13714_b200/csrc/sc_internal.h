@@ -38,11 +38,14 @@ struct Workspace {
 struct HostStaging {
   bool ready = false;
   int F = 0;                 // frames per chunk
+  int Fp = 0;                // frames per chunk with packed tables (half the bytes per frame)
   void* d_img[2] = {nullptr, nullptr};
   int32_t* d_idx[2] = {nullptr, nullptr};
   void* d_dist[2] = {nullptr, nullptr};
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+  uint32_t* d_tail = nullptr;  // packed tables: the run's overflow area (header + records)
+  int64_t tail_cap = -1;       // cap_rows d_tail was allocated for
 };
 
 struct Timing {
@@ -84,6 +87,10 @@ struct sc_bm_plan_s {
   int64_t min_cand = 0, max_cand = 0, total_cand = 0;
   int zstride = 1, zlo = 0, zhi = 0;  // 3D search: reference plane stride, plane offsets [zlo, zhi]
   int64_t n_planes = 0;               // 3D search: planes of the volume of the current sc_bm_run3d
+  int64_t packed_cap = 0;             // sc_bm_set_packed: overflow rows (0: plain tables)
+  uint32_t* packed_tail = nullptr;    // packed run: its overflow area (header word 0 = count)
+  int64_t packed_f0 = 0;              // packed run: image index of the current chunk in the run
+  int64_t packed_base = 0;            // packed run: image index (in the run) of the enqueued batch
 };
 
 namespace scbm {
@@ -131,6 +138,14 @@ bool box_supported(const Geometry& g);
 bool box_temporal_supported(const Geometry& g, int T);
 cudaError_t launch_bm_box(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                           int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches);
+
+// packed.cu: packed tables (sc_bm_set_packed): overflow-area header, device decode.
+// Row words w = (dist << rb) | slot; escape rows (0xFFFFFFFF) come from the overflow records.
+int packed_rel_bits(const Geometry& g);
+int64_t packed_record_words(const Geometry& g);
+cudaError_t launch_packed_init(uint32_t* tail, int64_t cap, cudaStream_t st);
+cudaError_t launch_unpack(const sc_bm_plan_s& p, const uint32_t* packed, int64_t n_images, int64_t n_records,
+                          int32_t* idx_out, int32_t* dist_out, cudaStream_t st);
 
 // nlm.cu: NLM weights (Eq. 2 / Prop. 1) from a dense window-distance table, normalised in place.
 cudaError_t launch_nlm_normalize(const sc_bm_plan_s& p, void* rows, float h, cudaStream_t st, int64_t* launches);
