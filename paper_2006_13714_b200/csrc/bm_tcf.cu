@@ -33,6 +33,7 @@
 // kernel: the kept keys re-scored by direct differences, sorted, written; references whose kept
 // keys cannot decide the K-th go to the exact fix-up (fixup.cu).
 #include <algorithm>
+#include <cstdio>
 
 #include "regtopk.cuh"
 #include "sc_internal.h"
@@ -53,6 +54,15 @@ constexpr int kES = 2;              // E ring slots
 constexpr uint32_t kTmemD = 128;
 constexpr int kScrPitch = 36;       // epilogue scratch words per lane (32 staged + pad; 16-B rows)
 constexpr float kTcfErr = 2e-5f;    // bound on the 3xTF32 identity's error, relative to n_r + d
+#ifndef SCBM_TCF_PROF
+#define SCBM_TCF_PROF 0  // timing experiments only: per-warp cycle counters printed by a few CTAs
+#endif
+#ifndef SCBM_TCF_SIFT
+#define SCBM_TCF_SIFT 1  // 1: branch-free fixed-depth sift-downs, root in a register, next survivor prefetched
+#endif
+#ifndef SCBM_TCF_SKIP
+#define SCBM_TCF_SKIP 0  // timing experiments only: 1 no survivor rounds, 2 no epilogue math, 4 no a5
+#endif
 
 struct TcfArgs {
   const float* imgs;   // [F][H][W]
@@ -80,6 +90,7 @@ __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x)
 template <int BK, int KR, bool DENSE>
 __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
   constexpr bool HEAP = KR > 48;
+  constexpr int kSiftLevels = KR >= 128 ? 7 : KR >= 64 ? 6 : 5;  // sift-down levels below the root: floor(log2(KP))
   constexpr int ER = kTR + BK - 1;                  // E tile rows
   constexpr uint32_t kEBytes = uint32_t(ER) * 512;  // one copy (hi or lo) of an E tile
   constexpr uint32_t kIdesc = sm100::idesc_tf32(128, kTR * kTC, /*a_mn=*/false, /*b_mn=*/false);
@@ -276,6 +287,8 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
       heap[a.KP + 1] = 0u;  // padding child: never the larger one
     }
+    uint32_t root_r = 0xffffffffu;  // heap[1] (SCBM_TCF_SIFT)
+    (void)root_r;
     if constexpr (DENSE) {
       if (valid)
         for (int k = 0; k < a.Wn * a.Wn; ++k) a.dense[ref_band * a.Wn * a.Wn + k] = -1.f;
@@ -284,16 +297,26 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
     const uint32_t tq = tmem + (uint32_t(32 * q) << 16);
     const uint32_t sc_s = smem_u32(scratch + lane * kScrPitch);
 
+#if SCBM_TCF_PROF
+    long long p_wait = 0, p_round = 0, p_dense = 0, n_rounds = 0, n_ins = 0;
+    const long long p_t0 = clock64();
+#endif
     for (int t = 0; t < ntiles; ++t) {
       const int buf = t & 1;
+#if SCBM_TCF_PROF
+      const long long pw0 = clock64();
+#endif
       sm100::mbar_wait(bar_full + 8 * buf, uint32_t((t >> 1) & 1));
       sm100::mbar_wait(bar_nc + 8 * buf, uint32_t((t >> 1) & 1));
       sm100::tc_fence_after();
+#if SCBM_TCF_PROF
+      p_wait += clock64() - pw0;
+#endif
       const float4* ncr = reinterpret_cast<const float4*>(smem + a.off_nc) + buf * kTR * 4;
       const int ot = order[t];
       const int tr = ot / NTC, tc = ot - tr * NTC;
       const int cy0 = cyA + kTR * tr, cx0 = cxA + kTC * tc;
-      const bool xrel = wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo;
+      const bool xrel = wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo && !(SCBM_TCF_SKIP & 2);
       if (xrel) {
         // this lane's window columns inside the tile (a 16-bit mask), the same for every row
         const int jlo = max(0, max(0, rx + a.lo) - cx0), jhi = min(15, min(W - BK, rx + a.hi) - cx0);
@@ -333,6 +356,7 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
 #pragma unroll
           for (int j = 31; j >= 0; --j) fails = __funnelshift_l(__float_as_uint(thr - dp[j]), fails, 1);
           uint32_t bits = ~fails & wmask;
+          if (SCBM_TCF_SKIP & 1) bits = 0u;
           if (!__any_sync(0xffffffffu, bits != 0u)) continue;
           // stage the distances d = d' + ||X_i||^2 (>= 0) of the two rows, then insert one survivor per
           // lane per round (branch-free; lanes without one insert the no-op key ~0)
@@ -344,7 +368,58 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
           }
           __syncwarp();
           const int rel1b = (cyp - ry - a.lo) * a.Wn + (cx0 - rx - a.lo) + 1;
+#if SCBM_TCF_PROF
+          const long long pr0 = clock64();
+          n_ins += __popc(bits);
+#endif
+#if SCBM_TCF_SIFT
+          // one survivor per lane per round, the next one's distance loaded while this one sinks;
+          // the heap root lives in a register (root_r) and the sift-down runs a fixed number of
+          // levels with predicated loads / stores (no divergent early exit)
+          int i = 31 - __clz(bits | 1u);
+          uint32_t d;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sc_s + 4u * uint32_t(i)));
           while (__any_sync(0xffffffffu, bits != 0u)) {
+#if SCBM_TCF_PROF
+            ++n_rounds;
+#endif
+            const int ic = i;
+            const uint32_t qd = d >> (rb - 1);
+            const int rel1 = rel1b + (ic >> 4) * a.Wn + (ic & 15);
+            const uint32_t key = bits ? (qd << rb) | uint32_t(rel1) : 0xffffffffu;
+            bits &= ~(1u << ic);
+            i = 31 - __clz(bits | 1u);
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sc_s + 4u * uint32_t(i)));
+            if constexpr (HEAP) {
+              if (key < root_r) {  // replace the root, sift down (children of h: 2h, 2h+1)
+                int h = 1;
+                bool alive = true;
+                uint32_t nroot = key;
+#pragma unroll
+                for (int lvl = 0; lvl < kSiftLevels; ++lvl) {
+                  const int c = 2 * h;
+                  uint2 vv = make_uint2(0u, 0u);
+                  if (alive && c <= a.KP) vv = *reinterpret_cast<const uint2*>(heap + c);
+                  const int cb = vv.y > vv.x ? c + 1 : c;
+                  const uint32_t big = max(vv.x, vv.y);
+                  const bool mv = big > key;  // (0 for a finished sift or past the last level)
+                  if (mv) heap[h] = big;
+                  if (lvl == 0) nroot = mv ? big : key;
+                  h = mv ? cb : h;
+                  alive = mv;
+                }
+                heap[h] = key;
+                root_r = nroot;
+              }
+            } else {
+              rt.insert(key);
+            }
+          }
+#else
+          while (__any_sync(0xffffffffu, bits != 0u)) {
+#if SCBM_TCF_PROF
+            ++n_rounds;
+#endif
             const int i = 31 - __clz(bits | 1u);
             uint32_t d;
             asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sc_s + 4u * uint32_t(i)));
@@ -369,7 +444,11 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
               rt.insert(key);
             }
           }
-          const uint32_t kth = HEAP ? heap[1] : rt.r[KR - 1];
+#endif
+#if SCBM_TCF_PROF
+          p_round += clock64() - pr0;
+#endif
+          const uint32_t kth = HEAP ? (SCBM_TCF_SIFT ? root_r : heap[1]) : rt.r[KR - 1];
           if (kth != 0xffffffffu) {
             // largest distance whose key can still tie the KP-th key, plus a rounding margin
             const float dmax = __uint_as_float(((kth >> rb) << (rb - 1)) | ((1u << (rb - 1)) - 1u));
@@ -383,6 +462,16 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       if (lane == 0) sm100::mbar_arrive(bar_empty + 8 * buf);
     }
 
+#if SCBM_TCF_PROF
+    {
+      const long long tot = clock64() - p_t0;
+      long long ins = n_ins;
+      for (int o = 16; o; o >>= 1) ins += __shfl_xor_sync(0xffffffffu, ins, o);
+      if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 700 || blockIdx.x == 1500) && blockIdx.y == 0)
+        printf("tcfprof cta %d warp %d tiles %d loop %lld wait %lld rounds_cyc %lld rounds %lld ins %lld\n",
+               blockIdx.x, warp, ntiles, tot, p_wait, p_round, n_rounds, ins);
+    }
+#endif
     if constexpr (!DENSE) {  // hand the reference norms and register lists to the a5 stage
       float* nrs = reinterpret_cast<float*>(smem + a.off_E);
       uint32_t* lists = reinterpret_cast<uint32_t*>(smem + a.off_E) + 128;
@@ -394,18 +483,24 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
     }
   }
 
+#if SCBM_TCF_PROF
+  long long pa0 = 0;
+#endif
   if constexpr (!DENSE) {
     // ---- a5 + a6, all warps: per reference (one warp each), the KP kept keys re-scored by direct
     // differences from the staged region (the input values as stored), sorted by (distance, idx),
     // K written; references whose kept keys cannot decide the K-th go to the exact fix-up.
     __syncthreads();  // every tile's MMAs and epilogue are done: the E ring holds the handed-over lists
+#if SCBM_TCF_PROF
+    pa0 = clock64();
+#endif
     const float* nrs = reinterpret_cast<const float*>(smem + a.off_E);
     const uint32_t* lists = reinterpret_cast<const uint32_t*>(smem + a.off_E) + 128;
     const uint32_t* heaps = reinterpret_cast<const uint32_t*>(smem + a.off_heap);
     const int rb = a.rb;
     const size_t band_refs = size_t(a.iy_end - a.iy_begin) * a.nx;
     constexpr int NJ = (KR + 31) / 32;
-    for (int m = warp; m < 128; m += kTfWarps) {
+    for (int m = warp; m < ((SCBM_TCF_SKIP & 4) ? 0 : 128); m += kTfWarps) {
       const int q = m >> 5, l = m & 31;
       const int iyj = iy_first + 4 * (q >> 1) + (l >> 3), ixj = ix_first + 8 * (q & 1) + (l & 7);
       if (iyj > iy_last || ixj > ix_last) continue;  // warp-uniform
@@ -489,6 +584,12 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       }
     }
   }
+#if SCBM_TCF_PROF
+  if constexpr (!DENSE) {
+    if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 700 || blockIdx.x == 1500) && blockIdx.y == 0)
+      printf("tcfprof cta %d warp %d a5 %lld\n", blockIdx.x, warp, clock64() - pa0);
+  }
+#endif
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == kTfWarps - 1) {

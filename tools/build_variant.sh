@@ -7,6 +7,6 @@ for f in paper_2006_13714_b200/csrc/*.cu paper_2006_13714_b200/csrc/*.cpp; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC \
     -I include --expt-relaxed-constexpr $FLAGS -c $f -o $D/$(basename $f).o &
 done
-wait
+wait; for f in paper_2006_13714_b200/csrc/*.cu paper_2006_13714_b200/csrc/*.cpp; do test -f $D/$(basename $f).o || { echo "compile failed: $f"; exit 1; }; done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $D/libscbm.so $D/*.o -lcudart_static -ldl -lrt -lpthread
 echo $D/libscbm.so

@@ -1,4 +1,7 @@
-mkdir -p gpurun_out
-rm -f gpurun_out/tcf_status.txt
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 -x -k "tcf" > gpurun_out/pytest_tcf.log 2>&1; echo "tcf=$?" >> gpurun_out/tcf_status.txt
-for c in c2 c3; do timeout 300 python bench.py --config $c --kernel tcf --steps 10 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_tcf_$c.log 2>&1; echo "bench_$c=$?" >> gpurun_out/tcf_status.txt; done
+set -x
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/tcf
+rm -f gpurun_out/tcf/*
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "tcf or tc_f32 or c3_c4_full" > gpurun_out/tcf/pytest.log 2>&1; echo "pytest=$?" >> gpurun_out/tcf/status
+timeout 600 python bench.py --config c3 --steps 10 --warmup 3 --no-e2e > gpurun_out/tcf/bench_c3.log 2>&1; echo "c3=$?" >> gpurun_out/tcf/status
+timeout 600 python bench.py --config c2 --kernel tcf --steps 10 --warmup 3 --no-e2e > gpurun_out/tcf/bench_tcf_c2.log 2>&1; echo "c2=$?" >> gpurun_out/tcf/status
