@@ -59,7 +59,8 @@ constexpr float kTcfErr = 2e-5f;    // bound on the 3xTF32 identity's error, rel
 #endif
 #ifndef SCBM_TCF_SIFT
 #define SCBM_TCF_SIFT 2  // 1: branch-free fixed-depth sift-downs, root in a register, next survivor prefetched;
-                         // 2: + the grandchildren loaded one level ahead (one 16-byte load per level)
+                         // 2: + the grandchildren loaded one level ahead (one 16-byte load per level);
+                         // 3: + the great-grandchildren two levels ahead (two 16-byte loads per level)
 #endif
 #ifndef SCBM_TCF_SKIP
 #define SCBM_TCF_SKIP 0  // timing experiments only: 1 no survivor rounds, 2 no epilogue math, 4 no a5
@@ -286,9 +287,7 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
     uint32_t* heap = reinterpret_cast<uint32_t*>(smem + a.off_heap) + (warp * 32 + lane) * a.hp;
     if constexpr (HEAP) {
       for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
-      heap[a.KP + 1] = 0u;  // padding children: never the larger one
-      heap[a.KP + 2] = 0u;
-      heap[a.KP + 3] = 0u;
+      for (int k = a.KP + 1; k <= a.KP + 7; ++k) heap[k] = 0u;  // padding children: never the larger one
     }
     uint32_t root_r = 0xffffffffu;  // heap[1] (SCBM_TCF_SIFT)
     (void)root_r;
@@ -398,7 +397,38 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
                 int h = 1;
                 bool alive = true;
                 uint32_t nroot = key;
-#if SCBM_TCF_SIFT == 2
+#if SCBM_TCF_SIFT == 3
+                // children of h in vv, grandchildren (4h .. 4h+3) in gq, great-grandchildren (8h .. 8h+7) in
+                // g0, g1: a level's loads are consumed two levels later (heap rows 16-byte aligned, nodes
+                // KP+1 .. KP+7 are 0: never the larger child)
+                uint2 vv = *reinterpret_cast<const uint2*>(heap + 2);
+                uint4 gq = *reinterpret_cast<const uint4*>(heap + 4);
+                uint4 g0 = *reinterpret_cast<const uint4*>(heap + 8);
+                uint4 g1 = *reinterpret_cast<const uint4*>(heap + 12);
+#pragma unroll
+                for (int lvl = 0; lvl < kSiftLevels; ++lvl) {
+                  const int c = 2 * h;
+                  const bool right = vv.y > vv.x;
+                  const int cb = right ? c + 1 : c;
+                  const uint32_t big = max(vv.x, vv.y);
+                  const bool mv = alive && big > key;
+                  const uint2 nv = right ? make_uint2(gq.z, gq.w) : make_uint2(gq.x, gq.y);
+                  const uint4 nq = right ? g1 : g0;
+                  if (lvl + 2 < kSiftLevels) {
+                    g0 = g1 = make_uint4(0u, 0u, 0u, 0u);
+                    if (mv && 8 * cb <= a.KP) {
+                      g0 = *reinterpret_cast<const uint4*>(heap + 8 * cb);
+                      g1 = *reinterpret_cast<const uint4*>(heap + 8 * cb + 4);
+                    }
+                  }
+                  if (mv) heap[h] = big;
+                  if (lvl == 0) nroot = mv ? big : key;
+                  h = mv ? cb : h;
+                  alive = mv && 2 * cb <= a.KP;
+                  vv = nv;
+                  gq = nq;
+                }
+#elif SCBM_TCF_SIFT == 2
                 // children of h in vv, grandchildren (nodes 4h .. 4h+3) in gq: the next level's load is
                 // issued before this level's comparison resolves (heap rows are 16-byte aligned, nodes
                 // KP+1 .. KP+3 are 0: never the larger child)
@@ -649,9 +679,10 @@ TcfLayout tcf_layout(const Geometry& g) {
   L.NTCmax = ((kRBX - 1) * g.s + g.Wn - 1 + 3) / kTC + 1;  // + the alignment of cxA
   L.RHmax = L.NTImax * kTR + g.b - 1;
   L.RWp = L.NTCmax * kTC + 7 + 1;
-  // heap pitch: nodes 1 .. KP + 3 (three 0 padding nodes), a multiple of 4 words: 16-byte aligned rows
-  // (the sift-down's grandchild loads)
-  L.hp = (g.KP + 4 + 3) & ~3;
+  // heap pitch: nodes 1 .. KP + 7 (seven 0 padding nodes), a multiple of 4 words: 16-byte aligned rows
+  // (the sift-down's grandchild / great-grandchild loads)
+  L.hp = (g.KP + (SCBM_TCF_SIFT >= 3 ? 8 : 4) + 3) & ~3;
+  if (L.hp % 8 == 0) L.hp += 4;  // = 4 (mod 8): the 32 lanes' 16-byte loads spread over all banks
   L.scr = std::max(32 * kScrPitch, kr > 48 ? 0 : 32 * (kr + 1));
   uint32_t off = 128;  // barriers + TMEM slot
   L.off_order = off;
