@@ -62,6 +62,9 @@ constexpr float kTcfErr = 2e-5f;    // bound on the 3xTF32 identity's error, rel
                          // 2: + the grandchildren loaded one level ahead (one 16-byte load per level);
                          // 3: + the great-grandchildren two levels ahead (two 16-byte loads per level)
 #endif
+#ifndef SCBM_TCF_A5ILP
+#define SCBM_TCF_A5ILP 1  // a5: a lane's 4 kept keys re-scored in one interleaved loop
+#endif
 #ifndef SCBM_TCF_SKIP
 #define SCBM_TCF_SKIP 0  // timing experiments only: 1 no survivor rounds, 2 no epilogue math, 4 no a5
 #endif
@@ -591,8 +594,41 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       uint64_t kv;  // the K-th exact key (broadcast)
       if constexpr (NJ >= 3) {
         uint64_t v[4];
+#if SCBM_TCF_A5ILP
+        {  // the lane's 4 kept keys re-scored together (each reference value loaded once, 4 chains)
+          const float* pc[4];
+          bool ok[4];
+          int cidx[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t kk = kept(4 * lane + i);
+            ok[i] = kk != 0u && kk != 0xffffffffu;
+            const int rel = ok[i] ? int(kk & ((1u << rb) - 1u)) - 1 : 0;
+            const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+            const int cy = ryj + dyy + a.lo, cx = rxj + dxx + a.lo;
+            cidx[i] = cy * W + cx;
+            pc[i] = ok[i] ? raw + (cy - cyA) * a.RWp + (cx - cxA) : pr;
+          }
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int r = 0; r < BK; ++r)
+#pragma unroll
+            for (int c = 0; c < BK; ++c) {
+              const float rv = pr[r * a.RWp + c];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float df = rv - pc[i][r * a.RWp + c];
+                d[i] = fmaf(df, df, d[i]);
+              }
+            }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            v[i] = ok[i] ? (uint64_t(__float_as_uint(d[i])) << 32) | uint32_t(cidx[i]) : kKeyInf;
+        }
+#else
 #pragma unroll
         for (int i = 0; i < 4; ++i) v[i] = rescore(kept(4 * lane + i));
+#endif
         warp_sort128(v, lane);
         uint64_t kq = v[0];
 #pragma unroll
