@@ -37,6 +37,10 @@ namespace {
 
 constexpr int kFWarps = 8;
 
+#ifndef SCBM_BOXF_F2
+#define SCBM_BOXF_F2 0  // 1: packed FFMA2 cross terms (measured: FFMA2 runs at the FFMA FMA rate, 121 /SM/clk, and its pair accumulators spill on c4: c4 2.66 -> 2.74 ms, c2 unchanged)
+#endif
+
 struct BoxfArgs {
   const void* imgs;   // [F][C][H][W] float (or uint8 for the NCC metric)
   int32_t* idx_out;   // [F][band refs][K]
@@ -91,6 +95,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   constexpr int WL = BK - (NS - 1) * S;  // width of the last strip
   constexpr int RX = 33 - NS;            // references per warp (lanes RX..31: helper strips)
   constexpr int NT = BK + VY - 1;        // candidate rows per (dy block, dx)
+  constexpr int kPairs = SCBM_BOXF_F2 ? WL / 2 : 0;  // FFMA2 column pairs of the partial strip
   extern __shared__ __align__(16) float smf[];
   const int f = blockIdx.y;
   const int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
@@ -277,10 +282,16 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     auto group = [&](int dx, auto hc) -> int {
       constexpr int H = decltype(hc)::value;
       const float* col = cbase + dx;
-      // cross terms of the full / partial strip, and running squared-row sums for the norms
+      // cross terms of the full / partial strip, and running squared-row sums for the norms;
+      // the partial strip's column pairs (2p, 2p+1) go through packed FFMA2 (two FMAs per
+      // instruction, __ffma2_rn) into pair accumulators summed at the end
       float Tp[VY], Tr[VY];
+      float2 Tp2[VY];
 #pragma unroll
-      for (int i = 0; i < VY; ++i) Tp[i] = Tr[i] = 0.f;
+      for (int i = 0; i < VY; ++i) {
+        Tp[i] = Tr[i] = 0.f;
+        Tp2[i] = make_float2(0.f, 0.f);
+      }
       float Qp[NT + 1], Qr[NT + 1];
 #pragma unroll
       for (int t = 0; t <= NT; ++t) Qp[t] = Qr[t] = 0.f;
@@ -305,7 +316,11 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
             const int r = t - i;
             if (r >= 0 && r < BK) {
 #pragma unroll
-              for (int m = 0; m < S; ++m) {
+              for (int p = 0; p < kPairs; ++p)
+                Tp2[i] = __ffma2_rn(make_float2(R[r][2 * p], R[r][2 * p + 1]),
+                                    make_float2(cv[2 * p], cv[2 * p + 1]), Tp2[i]);
+#pragma unroll
+              for (int m = 2 * kPairs; m < S; ++m) {
                 if (m < WL) Tp[i] = fmaf(R[r][m], cv[m], Tp[i]);
                 else Tr[i] = fmaf(R[r][m], cv[m], Tr[i]);
               }
@@ -313,6 +328,8 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
           }
         }
       }
+#pragma unroll
+      for (int i = 0; i < VY; ++i) Tp[i] += Tp2[i].x + Tp2[i].y;
 #pragma unroll
       for (int t = 1; t <= NT; ++t) {  // prefix sums over the candidate rows
         Qp[t] += Qp[t - 1];
@@ -640,7 +657,8 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
           const float* pcs = smf + (cy - Ybase) * a.RWp + (cx - Xbase);
           d = rescore([&](int c, int l, int m) { return prs[c * a.PL + l * a.RWp + m]; },
                       [&](int c, int l, int m) { return pcs[c * a.PL + l * a.RWp + m]; });
-          if (d * 180.f < nrj_a5) d = from_global();
+          // (the reference itself, d = 0 exactly, needs no second look)
+          if (d * 180.f < nrj_a5 && (cy != ry || cx != rxj)) d = from_global();
         }
         key = (uint64_t(__float_as_uint(d)) << 32) | uint32_t((Z3 ? zc * a.H : 0) * a.W + cy * a.W + cx);
       }

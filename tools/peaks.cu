@@ -33,6 +33,26 @@ __global__ void k_ffma3(float* out, float a) {  // 3-register form: c varies
   if (s == 1234.5f) out[0] = s;
 }
 
+// packed fp32x2 FMA (sm_100: FFMA2): two FMAs per lane per instruction
+__device__ __forceinline__ void ffma2(float2& x, float2 y, float2 a) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;"
+      : "+l"(*reinterpret_cast<unsigned long long*>(&x))
+      : "l"(*reinterpret_cast<unsigned long long*>(&y)), "l"(*reinterpret_cast<unsigned long long*>(&a)));
+}
+__global__ void k_ffma2(float* out, float a) {
+  float2 x[8], y[8];
+  const float2 a2 = make_float2(a, a);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { x[i] = make_float2(threadIdx.x * 0.001f + i, i); y[i] = make_float2(i * 0.5f, i * 0.25f); }
+  for (int it = 0; it < kIters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ffma2(x[i], y[i], a2);
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i].x + x[i].y;
+  if (s == 1234.5f) out[0] = s;
+}
+
 __global__ void k_imad(int* out, int a) {
   int x[8], y[8];
 #pragma unroll
@@ -93,12 +113,14 @@ int main() {
   dim3 g(sms * 8), b(256);
   const double ffma = rate([&] { k_ffma<<<g, b>>>(fo, 1.0001f, 0.5f); });
   const double ffma3 = rate([&] { k_ffma3<<<g, b>>>(fo, 1.0001f); });
+  const double ffma2 = 2.0 * rate([&] { k_ffma2<<<g, b>>>(fo, 1.0001f); });  // FMAs
   const double imad = rate([&] { k_imad<<<g, b>>>(io, 3); });
   const double dp4a = rate([&] { k_dp4a<<<g, b>>>(io, 0x01010101); });
   const double per = double(sms) * clk * 1e3;  // SM-cycles per second at the reported max clock
   printf("{\"sms\": %d, \"clock_mhz\": %.0f, \"ffma_imm_ops\": %.4g, \"ffma_3reg_ops\": %.4g, "
          "\"imad_ops\": %.4g, \"dp4a_ops\": %.4g, \"ffma_lanes_per_sm_clk\": %.1f, "
-         "\"ffma3_lanes_per_sm_clk\": %.1f, \"imad_lanes_per_sm_clk\": %.1f, \"dp4a_lanes_per_sm_clk\": %.1f}\n",
-         sms, clk / 1e3, ffma, ffma3, imad, dp4a, ffma / per, ffma3 / per, imad / per, dp4a / per);
+         "\"ffma3_lanes_per_sm_clk\": %.1f, \"imad_lanes_per_sm_clk\": %.1f, \"dp4a_lanes_per_sm_clk\": %.1f, "
+         "\"ffma2_fma_per_sm_clk\": %.1f}\n",
+         sms, clk / 1e3, ffma, ffma3, imad, dp4a, ffma / per, ffma3 / per, imad / per, dp4a / per, ffma2 / per);
   return 0;
 }
