@@ -910,6 +910,40 @@ def main():
             pt.finish()
             gather["compute_plus_peer_store_ms"] = tq.item()
             del pt
+        # packed tables through the gather (dist.gather_packed: one uint32 word per result, half the
+        # NVLink bytes of the (idx, dist) all-gather): matcher in packed mode + packed all-gather
+        if cfg.dtype == "u8" and args.metric == "l2" and args.temporal == 0 and info["kernel"] == 3:
+            from paper_2006_13714_b200.dist import balanced_ranges, gather_packed
+            counts = [e_ - s_ for s_, e_ in balanced_ranges(cfg.N, ws)]
+            plan.set_packed(max(4096, info["n_refs"] // 4))
+            words, _ = plan.packed_words(nloc)
+            pbuf = torch.empty(words, dtype=torch.int32, device="cuda")
+            for _ in range(2):
+                plan.run_packed(x, out=pbuf)
+                full = gather_packed(pbuf, counts, info["n_refs"], cfg.K)
+            dist.barrier()
+            torch.cuda.synchronize()
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            k0.record()
+            plan.run_packed(x, out=pbuf)
+            full = gather_packed(pbuf, counts, info["n_refs"], cfg.K)
+            k1.record()
+            torch.cuda.synchronize()
+            tk = torch.tensor([k0.elapsed_time(k1)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tk, op=dist.ReduceOp.MAX)
+            wN, _ = plan.packed_words(cfg.N)  # (the device decoder takes a buffer of the plan's layout)
+            same = False
+            if full.numel() <= wN:
+                padded = torch.zeros(wN, dtype=torch.int32, device="cuda")
+                padded[:full.numel()] = full
+                pi, pd = plan.unpack(padded, cfg.N)
+                same = bool(torch.equal(pi[f0:f0 + nloc], idx) and torch.equal(pd[f0:f0 + nloc], dst))
+                del padded, pi, pd
+            plan.set_packed(0)
+            gather["compute_plus_packed_gather_ms"] = tk.item()
+            gather["packed_gather_bytes_per_rank"] = int(full.numel() * 4)
+            gather["packed_decoded_equals_plain"] = same
+            del pbuf, full
 
     cpu, parity = None, None
     if rank == 0 and ws == 1 and not args.no_cpu:

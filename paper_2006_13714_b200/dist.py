@@ -62,6 +62,59 @@ def gather_tables(tables: Sequence, counts: Sequence[int], group=None):
     return out
 
 
+def gather_packed(buf, counts: Sequence[int], n_refs: int, K: int, group=None):
+    """All-gather PACKED tables of frame shards (sc_bm_set_packed, include/sc_bm.h):
+    one uint32 word per result instead of an (idx, dist) pair, so half the bytes cross NVLink.
+
+    buf: this rank's packed buffer (int32 tensor in the header's layout: its counts[rank] * n_refs
+    rows of K words, the escape-row count, cap_rows, then the records); counts: frames per rank.
+    Returns ONE packed buffer of the whole batch in the same layout: the rows of every rank in
+    frame order (the words are position-relative -- the window slot -- so they need no rewrite),
+    then count = the sum of the ranks' counts, cap = the records kept, and the records of every
+    rank with their row numbers rebased by the rank's first frame. A rank that lost records
+    (count > cap) makes the merged count exceed the merged cap, so the decoders (Plan.unpack,
+    unpack_host) report SC_ERR_OVERFLOW instead of returning a wrong table.
+    """
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if len(counts) != world:
+        raise ValueError("gather_packed: one frame count per rank required")
+    rw = n_refs * K
+    nrow = counts[rank] * rw
+    if buf.dtype != torch.int32 or buf.dim() != 1 or buf.numel() < nrow + 2:
+        raise ValueError("gather_packed: buf must be a 1-D int32 packed buffer of this rank's frames")
+    rows = buf[:nrow].view(-1, K)
+    (rows_all,) = gather_tables([rows], [c * n_refs for c in counts], group)
+    head = buf[nrow:nrow + 2].to(torch.int64)
+    heads = torch.empty(world * 2, dtype=torch.int64, device=buf.device)
+    dist.all_gather_into_tensor(heads, head.contiguous(), group=group)
+    heads = heads.view(world, 2).cpu()
+    rec_words = 2 + 2 * K
+    kept = [min(int(heads[r, 0]), int(heads[r, 1])) for r in range(world)]
+    recs = buf[nrow + 2:nrow + 2 + kept[rank] * rec_words].view(-1, rec_words)
+    parts = []
+    if max(kept) > 0:
+        (recs_all,) = gather_tables([recs], kept, group)
+        first = 0
+        off = 0
+        for r in range(world):
+            part = recs_all[off:off + kept[r]].clone()
+            off += kept[r]
+            if kept[r]:
+                lo = part[:, 0].to(torch.int64) & 0xFFFFFFFF
+                hi = part[:, 1].to(torch.int64) & 0xFFFFFFFF
+                row = (lo | (hi << 32)) + first * n_refs
+                part[:, 0] = (row & 0xFFFFFFFF).to(torch.int32)  # (wraps into int32 bits)
+                part[:, 1] = (row >> 32).to(torch.int32)
+                parts.append(part.view(-1))
+            first += counts[r]
+    tail = torch.tensor([int(heads[:, 0].sum()), sum(kept)], dtype=torch.int64)
+    tail = ((tail + 2**31) % 2**32 - 2**31).to(torch.int32).to(buf.device)
+    return torch.cat([rows_all.reshape(-1), tail] + parts)
+
+
 def run_frames_sharded(run: Callable, frames, rank: int, world: int, gather: bool = True, group=None):
     """Frame-parallel BM. `run(local_frames) -> (idx, dist)` is the local plan's run (the CUDA
     path on GPUs). `frames` is the full batch (each rank slices its range). Returns the local

@@ -174,3 +174,63 @@ def test_temporal_halo_rejects_on_every_rank(use_n):
         assert p.exitcode == 0
     res = sorted(q.get(timeout=5) for _ in range(2))
     assert res == [(0, "raised"), (1, "raised")], res
+
+
+def _packed_worker(rank, world, port, overflow, q):
+    """Each rank encodes its frame shard's oracle tables in the packed format (tests/test_packed.py's
+    restatement of include/sc_bm.h), gather_packed merges them, the host decoder must give the whole
+    batch's oracle tables (escape rows of several ranks included) -- or SC_ERR_OVERFLOW when a rank
+    lost records."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2006_13714_b200 import bm
+    from tests.test_packed import encode
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.Generator(np.random.PCG64(11))
+        H, W, b, s, Wn, K = 37, 45, 8, 4, 9, 5
+        n = 5
+        frames = rng.integers(0, 256, size=(n, 1, H, W), dtype=np.uint8)
+        frames[1, 0, :20] = 0  # constant areas: tie-heavy rows
+        a, e = sdist.frame_shard(n, rank, world)
+        li, ld = oracle.bm(frames[a:e], b, s, Wn, K)
+        nrefs = li.shape[1]
+        esc = {(3 * rank + 2 * j) % (li.shape[0] * nrefs) for j in range(3)} if e > a else set()
+        cap = 1 if (overflow and rank == world - 1) else 8
+        buf, _ = encode(li, ld, H, W, b, s, Wn, cap=cap, escape=esc, rng=rng)
+        counts = [f1 - f0 for f0, f1 in sdist.balanced_ranges(n, world)]
+        full = sdist.gather_packed(torch.from_numpy(buf.view(np.int32)), counts, nrefs, K)
+        wi, wd = oracle.bm(frames, b, s, Wn, K)
+        if overflow:
+            try:
+                bm.unpack_host(H, W, b, s, Wn, K, full, n)
+                ok = False
+            except bm.ScError as err:
+                ok = err.code == 6
+        else:
+            gi, gd = bm.unpack_host(H, W, b, s, Wn, K, full, n)
+            ok = np.array_equal(gi, wi) and np.array_equal(gd, wd) and full.numel() * 2 < 2 * wi.size + 8 * wi.size // K
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("overflow", [False, True])
+@pytest.mark.parametrize("world", [2, 3])
+def test_packed_gather_equals_single_process(world, overflow):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_packed_worker, args=(r, world, port, overflow, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(ok for _, ok in res), res
