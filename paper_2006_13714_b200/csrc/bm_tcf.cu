@@ -49,11 +49,17 @@ constexpr int kTfThreads = kTfWarps * 32;
 constexpr int kRBY = 8, kRBX = 16;  // reference block (M = 128)
 constexpr int kTR = 4, kTC = 16;    // candidate tile (N = 64)
 constexpr int kES = 2;              // E ring slots
+#ifndef SCBM_TCF_STAGERS
+#define SCBM_TCF_STAGERS 4  // warps staging the E tiles (warp kTfEpi issues the MMAs; the others idle until
+                            // a5). c3: 3.33 ms with 4, 3.35 with 1
+#endif
+constexpr int kStg = SCBM_TCF_STAGERS;
 // TMEM (256 columns per CTA, two CTAs per SM): A_hi at [0, 8b), A_lo at [8b, 16b) (the reference
 // patches, written once by tcgen05.st), the two N = 64 accumulators at [128, 192) and [192, 256)
 constexpr uint32_t kTmemD = 128;
 constexpr int kScrPitch = 36;       // epilogue scratch words per lane (32 staged + pad; 16-B rows)
 constexpr float kTcfErr = 2e-5f;    // bound on the 3xTF32 identity's error, relative to n_r + d
+constexpr int kBinBase = (127 - 6) << 4;  // BOUND histogram: bin 0 = float bits >> 19 of 2^-6
 #ifndef SCBM_TCF_PROF
 #define SCBM_TCF_PROF 0  // timing experiments only: per-warp cycle counters printed by a few CTAs
 #endif
@@ -64,6 +70,11 @@ constexpr float kTcfErr = 2e-5f;    // bound on the 3xTF32 identity's error, rel
 #endif
 #ifndef SCBM_TCF_A5ILP
 #define SCBM_TCF_A5ILP 1  // a5: a lane's 4 kept keys re-scored in one interleaved loop
+#endif
+#ifndef SCBM_TCF_BOUND
+#define SCBM_TCF_BOUND 0  // 1: heap lists (K + m > 48) get a first sweep over the tiles that bounds the
+                          // (K+m)-th distance (measured on c3: 42 % fewer insertions, 23 % fewer survivor
+                          // rounds, but the extra sweep costs more than they save: 4.12 vs 3.33 ms; off)
 #endif
 #ifndef SCBM_TCF_SKIP
 #define SCBM_TCF_SKIP 0  // timing experiments only: 1 no survivor rounds, 2 no epilogue math, 4 no a5
@@ -100,6 +111,15 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
   constexpr uint32_t kEBytes = uint32_t(ER) * 512;  // one copy (hi or lo) of an E tile
   constexpr uint32_t kIdesc = sm100::idesc_tf32(128, kTR * kTC, /*a_mn=*/false, /*b_mn=*/false);
   constexpr uint32_t kKA = 8 * BK;                  // A columns per copy (hi, lo) in TMEM
+  // BOUND: the tiles are swept twice. Sweep 1 only counts, per reference, the minimum distance of
+  // every 2 x 16 group of window candidates in a histogram of 1/16-octave bins over [2^-6, 2^10)
+  // (u8 counters in the reference's heap row); the upper edge of the bin where the count reaches
+  // K + m bounds the (K+m)-th smallest distance from above (K + m group minima are distinct
+  // candidates below it), so sweep 2 starts with that threshold instead of +inf and the heap sees
+  // far fewer insertions (c3: ~350 -> ~150 per reference). The MMAs of sweep 2 recompute the same
+  // values (deterministic), so the bound holds for the distances sweep 2 filters.
+  constexpr bool BOUND = HEAP && !DENSE && SCBM_TCF_BOUND;
+  constexpr int NSW = BOUND ? 2 : 1;  // sweeps over the tiles
   extern __shared__ __align__(1024) uint8_t smem[];
   const int f = blockIdx.y;
   const int by = blockIdx.x / a.tiles_x, bx = blockIdx.x - by * a.tiles_x;
@@ -199,12 +219,15 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
   __syncthreads();
   sm100::tc_fence_after();
 
-  if (warp == kTfEpi) {
-    // ---------------- MMA issuer (one elected thread) + tile producer (all 32 lanes): the warp
-    // stages the E tile of t + 1 (hi and lo, E[y][jg][kc][j][t] = x'(cy0 + y, cx0 + 8 jg + j + 4 kc + t))
-    // while the tensor core runs tile t, and the tile's 4 x 16 candidate norms (a1, from the
-    // L2-resident norm map, loaded one tile ahead) into ring slot t & 1 (bar_nc) once the epilogue
-    // has freed that accumulator; lane 0 issues the MMAs. (One waiting warp instead of four.)
+  if (warp >= kTfEpi && warp < kTfEpi + kStg) {
+    // ---------------- MMA issuer (one elected thread of warp kTfEpi) + tile producers (kStg warps):
+    // the producers stage the E tile of t + 1 (hi and lo, E[y][jg][kc][j][t] = x'(cy0 + y, cx0 + 8 jg
+    // + j + 4 kc + t)) while the tensor core runs tile t (each warp a share of the tile's entries, then
+    // a named barrier among them); warp kTfEpi also stages the tile's 4 x 16 candidate norms (a1, from
+    // the L2-resident norm map, loaded one tile ahead) into ring slot t & 1 (bar_nc) once the epilogue
+    // has freed that accumulator, and its lane 0 issues the MMAs.
+    const bool issuer = warp == kTfEpi;
+    const int sw = warp - kTfEpi;  // producer index
     float* ncring = reinterpret_cast<float*>(smem + a.off_nc);  // [2][4][16]
     const float* nsrc = a.norm + size_t(f) * a.nfs;
     const int rr = lane >> 2, cq = lane & 3;
@@ -216,11 +239,12 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       return __ldg(reinterpret_cast<const float4*>(nsrc + size_t(cy) * a.Mx + cxA + kTC * tc) + cq);
     };
     auto stage = [&](int t) {
-      const int ot = order[t];
+      const int ot = order[t % ntiles];
+      const int sl_ = t % kES;
       const int tr = ot / NTC, tc = ot - tr * NTC;
       const float* src0 = raw + (kTR * tr) * a.RWp + kTC * tc;
-      uint8_t* eh = smem + a.off_E + size_t(t % kES) * 2 * kEBytes;
-      for (int e = lane; e < ER * 32; e += 32) {
+      uint8_t* eh = smem + a.off_E + size_t(sl_) * 2 * kEBytes;
+      for (int e = sw * 32 + lane; e < ER * 32; e += kStg * 32) {
         const int y = e >> 5, jg = (e >> 4) & 1, kc = (e >> 3) & 1, j = e & 7;
         const float* sp = src0 + y * a.RWp + 8 * jg + j + 4 * kc;
         uint32_t h[4], o[4];
@@ -234,34 +258,37 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
         *reinterpret_cast<uint4*>(eh + kEBytes + e * 16) = make_uint4(o[0], o[1], o[2], o[3]);
       }
       sm100::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-      __syncwarp();
+      if constexpr (kStg > 1) asm volatile("bar.sync 1, %0;" ::"n"(kStg * 32) : "memory");
+      else __syncwarp();
     };
-    float4 nv_next = load_norms(0);
+    float4 nv_next = issuer ? load_norms(0) : make_float4(0.f, 0.f, 0.f, 0.f);
     stage(0);
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = 0; t < NSW * ntiles; ++t) {
       const int sl = t % kES, buf = t & 1;
-      const float4 nv = nv_next;
-      if (t + 1 < ntiles) nv_next = load_norms(t + 1);
-      if (t >= 2) sm100::mbar_wait_sleep(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1), 16);
-      if (rr < kTR) reinterpret_cast<float4*>(ncring + (buf * kTR + rr) * kTC)[cq] = nv;
-      sm100::mbar_arrive(bar_nc + 8 * buf);
-      if (lane == 0) {
-        sm100::tc_fence_after();
-        const uint32_t eh = sE + uint32_t(sl) * 2 * kEBytes, el = eh + kEBytes;
+      if (issuer) {
+        const float4 nv = nv_next;
+        if (t + 1 < NSW * ntiles) nv_next = load_norms((t + 1) % ntiles);
+        if (t >= 2) sm100::mbar_wait_sleep(bar_empty + 8 * buf, uint32_t(((t >> 1) - 1) & 1), 16);
+        if (rr < kTR) reinterpret_cast<float4*>(ncring + (buf * kTR + rr) * kTC)[cq] = nv;
+        sm100::mbar_arrive(bar_nc + 8 * buf);
+        if (lane == 0) {
+          sm100::tc_fence_after();
+          const uint32_t eh = sE + uint32_t(sl) * 2 * kEBytes, el = eh + kEBytes;
 #pragma unroll 1
-        for (int u = 0; u < BK; ++u) {
-          const uint64_t bh = sm100::smem_desc(eh + 512u * u, 128u, 256u);
-          const uint64_t bl = sm100::smem_desc(el + 512u * u, 128u, 256u);
-          const uint32_t d = tmem + kTmemD + uint32_t(kTR * kTC) * buf;
-          sm100::mma_tf32_ta(d, tmem + 8u * u, bh, kIdesc, u > 0);        // A_hi B_hi
-          sm100::mma_tf32_ta(d, tmem + 8u * u, bl, kIdesc, 1);            // A_hi B_lo
-          sm100::mma_tf32_ta(d, tmem + kKA + 8u * u, bh, kIdesc, 1);      // A_lo B_hi
+          for (int u = 0; u < BK; ++u) {
+            const uint64_t bh = sm100::smem_desc(eh + 512u * u, 128u, 256u);
+            const uint64_t bl = sm100::smem_desc(el + 512u * u, 128u, 256u);
+            const uint32_t d = tmem + kTmemD + uint32_t(kTR * kTC) * buf;
+            sm100::mma_tf32_ta(d, tmem + 8u * u, bh, kIdesc, u > 0);        // A_hi B_hi
+            sm100::mma_tf32_ta(d, tmem + 8u * u, bl, kIdesc, 1);            // A_hi B_lo
+            sm100::mma_tf32_ta(d, tmem + kKA + 8u * u, bh, kIdesc, 1);      // A_lo B_hi
+          }
+          sm100::mma_commit(bar_full + 8 * buf);
+          sm100::mma_commit(bar_ee + 8 * sl);
         }
-        sm100::mma_commit(bar_full + 8 * buf);
-        sm100::mma_commit(bar_ee + 8 * sl);
+        __syncwarp();
       }
-      __syncwarp();
-      if (t + 1 < ntiles) {  // the next tile's slot is free once the MMAs of tile t - 1 are done
+      if (t + 1 < NSW * ntiles) {  // the next tile's slot is free once the MMAs of tile t - 1 are done
         if (t + 1 >= kES) sm100::mbar_wait_sleep(bar_ee + 8 * ((t + 1) % kES), uint32_t((((t + 1) / kES) - 1) & 1), 16);
         stage(t + 1);
       }
@@ -288,9 +315,15 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
     }
     uint32_t* heap = reinterpret_cast<uint32_t*>(smem + a.off_heap) + (warp * 32 + lane) * a.hp;
-    if constexpr (HEAP) {
+    auto heap_init = [&]() {
       for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
       for (int k = a.KP + 1; k <= a.KP + 7; ++k) heap[k] = 0u;  // padding children: never the larger one
+    };
+    uint8_t* const hist = reinterpret_cast<uint8_t*>(heap);  // BOUND sweep 1: 256 u8 bins (heap row)
+    if constexpr (BOUND) {
+      for (int k = 0; k < 64; ++k) heap[k] = 0u;
+    } else if constexpr (HEAP) {
+      heap_init();
     }
     uint32_t root_r = 0xffffffffu;  // heap[1] (SCBM_TCF_SIFT)
     (void)root_r;
@@ -306,8 +339,27 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
     long long p_wait = 0, p_round = 0, p_dense = 0, n_rounds = 0, n_ins = 0;
     const long long p_t0 = clock64();
 #endif
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = 0; t < NSW * ntiles; ++t) {
       const int buf = t & 1;
+      const bool sweep1 = BOUND && t < ntiles;
+      if (BOUND && t == ntiles) {
+        // end of sweep 1: the first bin where the cumulative count of group minima reaches K + m
+        int cum = 0, bsel = 256;
+        for (int w = 0; w < 64; ++w) {
+          const uint32_t v = heap[w];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            cum += int((v >> (8 * k)) & 0xffu);
+            if (bsel == 256 && cum >= a.KP) bsel = 4 * w + k;
+          }
+        }
+        __syncwarp();
+        heap_init();
+        if (bsel < 255) {  // (bin 255 also holds everything >= 2^10: no bound)
+          const float edge = __uint_as_float(uint32_t(bsel + kBinBase + 1) << 19);  // the bin's upper edge
+          thr = fmaf(edge, 1.0f + 1e-6f, -nr) + 1e-30f;  // (d' = d - ||X_i||^2; rounding margin)
+        }
+      }
 #if SCBM_TCF_PROF
       const long long pw0 = clock64();
 #endif
@@ -318,7 +370,7 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       p_wait += clock64() - pw0;
 #endif
       const float4* ncr = reinterpret_cast<const float4*>(smem + a.off_nc) + buf * kTR * 4;
-      const int ot = order[t];
+      const int ot = order[t % ntiles];
       const int tr = ot / NTC, tc = ot - tr * NTC;
       const int cy0 = cyA + kTR * tr, cx0 = cxA + kTC * tc;
       const bool xrel = wvalid && cx0 <= wx_hi && cx0 + kTC - 1 >= wx_lo && !(SCBM_TCF_SKIP & 2);
@@ -355,6 +407,18 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if ((wmask >> j) & 1u) drow[rel0 + (j >> 4) * a.Wn + (j & 15)] = dp[j] + nr;
+            continue;
+          }
+          if (sweep1) {  // the group's minimum distance -> its histogram bin
+            float mn = __int_as_float(0x7f800000);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if ((wmask >> j) & 1u) mn = fminf(mn, dp[j]);
+            if (wmask != 0u) {
+              const uint32_t bits = __float_as_uint(fmaxf(mn + nr, 0.f));
+              const int bin = min(255, max(0, int(bits >> 19) - kBinBase));
+              hist[bin] = uint8_t(min(255, int(hist[bin]) + 1));
+            }
             continue;
           }
           uint32_t fails = 0u;
@@ -718,6 +782,7 @@ TcfLayout tcf_layout(const Geometry& g) {
   // heap pitch: nodes 1 .. KP + 7 (seven 0 padding nodes), a multiple of 4 words: 16-byte aligned rows
   // (the sift-down's grandchild / great-grandchild loads)
   L.hp = (g.KP + (SCBM_TCF_SIFT >= 3 ? 8 : 4) + 3) & ~3;
+  if (kr > 48 && SCBM_TCF_BOUND && L.hp < 64) L.hp = 64;  // (the bound sweep's 256 u8 bins share the row)
   if (L.hp % 8 == 0) L.hp += 4;  // = 4 (mod 8): the 32 lanes' 16-byte loads spread over all banks
   L.scr = std::max(32 * kScrPitch, kr > 48 ? 0 : 32 * (kr + 1));
   uint32_t off = 128;  // barriers + TMEM slot
