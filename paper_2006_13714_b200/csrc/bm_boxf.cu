@@ -37,6 +37,9 @@ namespace {
 
 constexpr int kFWarps = 8;
 
+#ifndef SCBM_BOXF_A5SPLIT
+#define SCBM_BOXF_A5SPLIT 1  // a5: the short last key slot re-scored by several lanes per key
+#endif
 #ifndef SCBM_BOXF_F2
 #define SCBM_BOXF_F2 0  // 1: packed FFMA2 cross terms (measured: FFMA2 runs at the FFMA FMA rate, 121 /SM/clk, and its pair accumulators spill on c4: c4 2.66 -> 2.74 ms, c2 unchanged)
 #endif
@@ -96,6 +99,9 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   constexpr int RX = 33 - NS;            // references per warp (lanes RX..31: helper strips)
   constexpr int NT = BK + VY - 1;        // candidate rows per (dy block, dx)
   constexpr int kPairs = SCBM_BOXF_F2 ? WL / 2 : 0;  // FFMA2 column pairs of the partial strip
+  // a5: list entries in the last 32-key slot, and lanes per key there (register lists only)
+  constexpr int kN1 = KR - 32 * (((KR + 31) / 32) - 1);
+  constexpr int kSplitG = (SCBM_BOXF_A5SPLIT && KR > 32 && KR <= 48 && !NCC && !Z3) ? (kN1 <= 8 ? 4 : 2) : 1;
   extern __shared__ __align__(16) float smf[];
   const int f = blockIdx.y;
   const int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
@@ -595,6 +601,74 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     top.init();
 #pragma unroll
     for (int sl = 0; sl < NJ; ++sl) {
+      if constexpr (kSplitG > 1) {
+        if (sl == NJ - 1) {
+          // the last slot holds only kN1 (<= 16) list entries: kSplitG lanes per key, each a strided
+          // share of the patch columns, summed by xor shuffles (instead of a full-length pass with
+          // kN1 of 32 lanes busy)
+          const int kq = lane / kSplitG, part = lane % kSplitG;
+          uint32_t kk = 0xffffffffu;
+          if constexpr (WS == 2) {
+#pragma unroll
+            for (int q = 0; q < kN1; ++q) {
+              const uint32_t v = __shfl_sync(0xffffffffu, rt.r[sl * 32 + q], j);
+              if (kq == q) kk = v;
+            }
+          } else {
+            if (kq < kN1) kk = scratch[j * (KR + 1) + sl * 32 + kq];
+          }
+          const bool have = kq < kN1 && kk != 0u && kk != 0xffffffffu;
+          int cy = ry, cx = rxj;
+          if (have) {
+            const int rel = int(kk & ((1u << rb) - 1u)) - 1;
+            const int dyy = rel / a.Wn, dxx = rel - dyy * a.Wn;
+            cy = ry + dyy + a.lo;
+            cx = rxj + dxx + a.lo;
+          }
+          const float* prs = smf + (ry - Ybase) * a.RWp + (rxj - Xbase);
+          const float* pcs = smf + (cy - Ybase) * a.RWp + (cx - Xbase);
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int c = 0; c < nch; ++c) {
+#pragma unroll 4
+            for (int l = 0; l < BK; ++l) {
+              float t = 0.f;
+#pragma unroll
+              for (int m = 0; m < BK; m += kSplitG) {
+                if (m + part < BK) {
+                  const float df = prs[c * a.PL + l * a.RWp + m + part] - pcs[c * a.PL + l * a.RWp + m + part];
+                  t = fmaf(df, df, t);
+                }
+              }
+              acc[l & 3] += t;
+            }
+          }
+          float d = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+          for (int o = 1; o < kSplitG; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (have && part == 0 && d * 180.f < nrj_a5 && (cy != ry || cx != rxj)) {
+            // near-duplicate pair: re-scored from the input in global memory (as the full-length path)
+            float g[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int c = 0; c < nch; ++c) {
+#pragma unroll 4
+              for (int l = 0; l < BK; ++l) {
+                float t = 0.f;
+#pragma unroll
+                for (int m = 0; m < BK; ++m) {
+                  const float df = __ldg(img + c * plane + size_t(ry + l) * a.W + rxj + m) -
+                                   __ldg(img + c * plane + size_t(cy + l) * a.W + cx + m);
+                  t = fmaf(df, df, t);
+                }
+                g[l & 3] += t;
+              }
+            }
+            d = (g[0] + g[1]) + (g[2] + g[3]);
+          }
+          uint64_t key = (have && part == 0) ? (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * a.W + cx) : kKeyInf;
+          key = __shfl_sync(0xffffffffu, key, min(lane * kSplitG, 31));
+          top.merge(lane < kN1 ? key : kKeyInf, lane);
+          continue;
+        }
+      }
       const int k = sl * 32 + lane;
       uint64_t key = kKeyInf;
       uint32_t kk;
