@@ -603,8 +603,14 @@ def main():
     ws, rank, local = _dist_env()
     torch.cuda.set_device(local)
     dist = None
-    if ws > 1:
+    if ws > 1 or args.gather:  # (--gather at N = 1: a one-rank NCCL group, so the gather paths run too)
         import torch.distributed as dist
+        if ws == 1 and "MASTER_ADDR" not in os.environ:
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(so.getsockname()[1]),
+                                  RANK="0", WORLD_SIZE="1")
         # a bounded collective timeout: a hung peer fails the run instead of blocking it forever
         # (TORCH_NCCL_ASYNC_ERROR_HANDLING is on by default for NCCL in this torch)
         import datetime
@@ -882,6 +888,8 @@ def main():
         from paper_2006_13714_b200.dist import run_frames_pipelined
         chunk = max(1, nloc // 4)
         if nloc % chunk == 0:
+            run_frames_pipelined(lambda fr: plan.run(fr), x, rank, ws, chunk, local=True)  # warm (async NCCL setup)
+            torch.cuda.synchronize()
             dist.barrier()
             p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             p0.record()

@@ -107,6 +107,8 @@ template <int BK, int KR, bool DENSE>
 __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
   constexpr bool HEAP = KR > 48;
   constexpr int kSiftLevels = KR >= 128 ? 7 : KR >= 64 ? 6 : 5;  // sift-down levels below the root: floor(log2(KP))
+  constexpr int kSift4 = KR > 85 ? 4 : 3;  // SIFT 4 (4-ary heap): levels below the root
+  constexpr int kHB = SCBM_TCF_SIFT == 4 ? 3 : 1;  // heap position of the root
   constexpr int ER = kTR + BK - 1;                  // E tile rows
   constexpr uint32_t kEBytes = uint32_t(ER) * 512;  // one copy (hi or lo) of an E tile
   constexpr uint32_t kIdesc = sm100::idesc_tf32(128, kTR * kTC, /*a_mn=*/false, /*b_mn=*/false);
@@ -316,8 +318,13 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
     }
     uint32_t* heap = reinterpret_cast<uint32_t*>(smem + a.off_heap) + (warp * 32 + lane) * a.hp;
     auto heap_init = [&]() {
-      for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
-      for (int k = a.KP + 1; k <= a.KP + 7; ++k) heap[k] = 0u;  // padding children: never the larger one
+      if constexpr (SCBM_TCF_SIFT == 4) {  // nodes at positions 3 .. KP + 2, zeros to the end of the row
+        for (int k = kHB; k < kHB + a.KP; ++k) heap[k] = 0xffffffffu;
+        for (int k = kHB + a.KP; k < a.hp; ++k) heap[k] = 0u;
+      } else {
+        for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
+        for (int k = a.KP + 1; k <= a.KP + 7; ++k) heap[k] = 0u;  // padding children: never the larger one
+      }
     };
     uint8_t* const hist = reinterpret_cast<uint8_t*>(heap);  // BOUND sweep 1: 256 u8 bins (heap row)
     if constexpr (BOUND) {
@@ -495,6 +502,40 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
                   vv = nv;
                   gq = nq;
                 }
+#elif SCBM_TCF_SIFT == 4
+                // 4-ary max-heap: node n at position n + 3, so the children of n (4n+1 .. 4n+4) sit at
+                // positions 4n+4 .. 4n+7 -- one aligned 16-byte load; the children of the four children
+                // (positions 16n+8 .. 16n+23) are loaded one level ahead. Three levels below the root
+                // hold K + m <= 85 keys (binary: six). Positions past the last node are 0.
+                int n = 0;
+                uint4 vv = *reinterpret_cast<const uint4*>(heap + 4);
+                uint4 g0 = *reinterpret_cast<const uint4*>(heap + 8), g1 = *reinterpret_cast<const uint4*>(heap + 12);
+                uint4 g2 = *reinterpret_cast<const uint4*>(heap + 16), g3 = *reinterpret_cast<const uint4*>(heap + 20);
+#pragma unroll
+                for (int lvl = 0; lvl < kSift4; ++lvl) {
+                  const bool r01 = vv.y > vv.x, r23 = vv.w > vv.z;
+                  const uint32_t m01 = max(vv.x, vv.y), m23 = max(vv.z, vv.w);
+                  const bool up = m23 > m01;
+                  const uint32_t big = max(m01, m23);
+                  const int cb = 4 * n + 1 + (up ? (r23 ? 3 : 2) : (r01 ? 1 : 0));
+                  const bool mv = alive && big > key;
+                  const uint4 nv = up ? (r23 ? g3 : g2) : (r01 ? g1 : g0);
+                  if (lvl + 1 < kSift4) {
+                    g0 = g1 = g2 = g3 = make_uint4(0u, 0u, 0u, 0u);
+                    if (mv && 16 * cb + 24 <= a.hp) {
+                      g0 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 8);
+                      g1 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 12);
+                      g2 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 16);
+                      g3 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 20);
+                    }
+                  }
+                  if (mv) heap[3 + n] = big;
+                  if (lvl == 0) nroot = mv ? big : key;
+                  n = mv ? cb : n;
+                  alive = mv && 4 * cb + 1 < a.KP;
+                  vv = nv;
+                }
+                h = 3 + n;
 #elif SCBM_TCF_SIFT == 2
                 // children of h in vv, grandchildren (nodes 4h .. 4h+3) in gq: the next level's load is
                 // issued before this level's comparison resolves (heap rows are 16-byte aligned, nodes
@@ -652,7 +693,7 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
         return (uint64_t(__float_as_uint(d)) << 32) | uint32_t(cy * W + cx);
       };
       auto kept = [&](int k) -> uint32_t {
-        if constexpr (HEAP) return k < a.KP ? heaps[m * a.hp + 1 + k] : 0xffffffffu;
+        if constexpr (HEAP) return k < a.KP ? heaps[m * a.hp + kHB + k] : 0xffffffffu;
         else return k < KR ? lists[m * (KR + 1) + k] : 0xffffffffu;
       };
       uint64_t kv;  // the K-th exact key (broadcast)
@@ -731,7 +772,7 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       }
       {  // worst kept key vs the exact K-th distance: the filter's error could hide a candidate
         const float nrj = nrs[m];
-        const uint32_t klast = HEAP ? heaps[m * a.hp + 1] : lists[m * (KR + 1) + KR - 1];  // heap root / last
+        const uint32_t klast = HEAP ? heaps[m * a.hp + kHB] : lists[m * (KR + 1) + KR - 1];  // heap root / last
         if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf) {
           const float dK = __uint_as_float(uint32_t(kv >> 32));
           const float smin = __uint_as_float((klast >> rb) << (rb - 1));
@@ -781,7 +822,7 @@ TcfLayout tcf_layout(const Geometry& g) {
   L.RWp = L.NTCmax * kTC + 7 + 1;
   // heap pitch: nodes 1 .. KP + 7 (seven 0 padding nodes), a multiple of 4 words: 16-byte aligned rows
   // (the sift-down's grandchild / great-grandchild loads)
-  L.hp = (g.KP + (SCBM_TCF_SIFT >= 3 ? 8 : 4) + 3) & ~3;
+  L.hp = (g.KP + (SCBM_TCF_SIFT == 4 ? 11 : SCBM_TCF_SIFT >= 3 ? 8 : 4) + 3) & ~3;
   if (kr > 48 && SCBM_TCF_BOUND && L.hp < 64) L.hp = 64;  // (the bound sweep's 256 u8 bins share the row)
   if (L.hp % 8 == 0) L.hp += 4;  // = 4 (mod 8): the 32 lanes' 16-byte loads spread over all banks
   L.scr = std::max(32 * kScrPitch, kr > 48 ? 0 : 32 * (kr + 1));

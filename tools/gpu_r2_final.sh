@@ -23,7 +23,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # ncu --set full captures, CSV exports only (gpurun_out <= 64 MiB)
 prof () {  # name config kernel-regex extra
   B="python bench.py --config $2 --steps 1 --warmup 3 --no-e2e --no-cpu $4"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$3" -s 1 -c 1 -o /tmp/prof_$1 $B > $O/ncu_$1.log 2>&1
+  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:"$3" -s 1 -c 1 -o /tmp/prof_$1 $B > $O/ncu_$1.log 2>&1
   echo "ncu_$1=$?" >> $O/status.txt
   ncu -i /tmp/prof_$1.ncu-rep --page raw --csv > $O/prof_$1_raw.csv 2>/dev/null
   ncu -i /tmp/prof_$1.ncu-rep --page details --csv > $O/prof_$1_details.csv 2>/dev/null
