@@ -769,7 +769,7 @@ def main():
         traffic = sum(float(m[k]["value"]) * mb.get(m[k]["unit"], 1.0) for k in
                       ("dram__bytes_read.sum", "dram__bytes_write.sum")) * 1e6
         traffic_src = (f"{os.path.relpath(prof, ROOT)}: dram read+write bytes of one launch "
-                       f"({info['frames_per_chunk']} frames), ncu --set full")
+                       f"({min(info['frames_per_chunk'], cfg.N)} frames), ncu --set full")
     roof = {"bound": bound, "kernel": kname,
             "achieved": achieved, "peak": peak, "unit": unit,
             "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,

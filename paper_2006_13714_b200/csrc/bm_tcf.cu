@@ -64,9 +64,11 @@ constexpr int kBinBase = (127 - 6) << 4;  // BOUND histogram: bin 0 = float bits
 #define SCBM_TCF_PROF 0  // timing experiments only: per-warp cycle counters printed by a few CTAs
 #endif
 #ifndef SCBM_TCF_SIFT
-#define SCBM_TCF_SIFT 2  // 1: branch-free fixed-depth sift-downs, root in a register, next survivor prefetched;
+#define SCBM_TCF_SIFT 4  // 1: branch-free fixed-depth sift-downs, root in a register, next survivor prefetched;
                          // 2: + the grandchildren loaded one level ahead (one 16-byte load per level);
-                         // 3: + the great-grandchildren two levels ahead (two 16-byte loads per level)
+                         // 3: + the great-grandchildren two levels ahead (two 16-byte loads per level);
+                         // 4: a 4-ary heap (three levels for K + m <= 85; the children of the four
+                         //    children loaded one level ahead): c3 3.33 -> 3.13 ms against 2
 #endif
 #ifndef SCBM_TCF_A5ILP
 #define SCBM_TCF_A5ILP 1  // a5: a lane's 4 kept keys re-scored in one interleaved loop
