@@ -37,6 +37,9 @@ namespace {
 
 constexpr int kFWarps = 8;
 
+#ifndef SCBM_BOXF_HEAP4
+#define SCBM_BOXF_HEAP4 1  // K + m > 48: a 4-ary heap with the root in a register (0: the binary heap)
+#endif
 #ifndef SCBM_BOXF_A5SPLIT
 #define SCBM_BOXF_A5SPLIT 1  // a5: the short last key slot re-scored by several lanes per key
 #endif
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
                  ? float(__ldg(img + c * plane + size_t(yy) * a.W + xx)) - shift : 0.f;
   }
   // published KP-th keys of the two window halves (WS = 2), +inf until a list fills
-  uint32_t* pub = reinterpret_cast<uint32_t*>(smf + ((regw + 1) & ~1)) + kFWarps * WS * a.scr;
+  uint32_t* pub = reinterpret_cast<uint32_t*>(smf + ((regw + 3) & ~3)) + kFWarps * WS * a.scr;
   if (WS == 2) pub[warp * 32 + lane] = 0xffffffffu;
   __syncthreads();
 
@@ -178,11 +181,23 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     for (int k = 0; k < KR; ++k) rt.r[k] = k < KR - a.KP ? 0u : 0xffffffffu;
   }
   // (helper lanes RX..31 never insert; they alias lane RX-1's heap for the root reads)
-  uint32_t* const scr0 = reinterpret_cast<uint32_t*>(smf + ((regw + 1) & ~1));  // 8-byte aligned
+  uint32_t* const scr0 = reinterpret_cast<uint32_t*>(smf + ((regw + 3) & ~3));  // 16-byte aligned
   uint32_t* heap = scr0 + warp * a.scr + 64 * VY + min(lane, RX - 1) * a.hp;
   uint32_t* const pub_own = pub + warp * 32 + lane;
   const uint32_t* const pub_other = pub + ((1 - hh) * kFWarps + wr) * 32 + lane;
-  if constexpr (HEAP) {
+  // HEAP4: a 4-ary max-heap, node n at position n + 3 (the children of n, 4n+1 .. 4n+4, are one
+  // aligned 16-byte load at 4n+4), root kept in a register, fixed-depth sift-downs with the children
+  // of the four children loaded one level ahead (as the 3xTF32 matcher's); zeros past the last node
+  constexpr bool HEAP4 = HEAP && SCBM_BOXF_HEAP4;
+  constexpr int kHB = HEAP4 ? 3 : 1;       // heap position of the root
+  constexpr int kSift4 = KR > 85 ? 4 : 3;  // levels below the root
+  uint32_t root_r = 0xffffffffu;           // HEAP4: the root (the KP-th key)
+  if constexpr (HEAP4) {
+    if (lane < RX) {
+      for (int k = kHB; k < kHB + a.KP; ++k) heap[k] = 0xffffffffu;
+      for (int k = kHB + a.KP; k < a.hp; ++k) heap[k] = 0u;
+    }
+  } else if constexpr (HEAP) {
     if (lane < RX)
       for (int k = 1; k <= a.KP; ++k) heap[k] = 0xffffffffu;
     if (lane < RX) heap[a.KP + 1] = 0u;  // padding child: never the larger one
@@ -207,7 +222,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     pend = 0u;
     if (!__any_sync(0xffffffffu, bits != 0u)) {
       if constexpr (WS == 2) {  // the partner half may have tightened the shared threshold
-        const uint32_t own = HEAP ? heap[1] : rt.r[KR - 1];
+        const uint32_t own = HEAP4 ? root_r : HEAP ? heap[1] : rt.r[KR - 1];
         set_thr(min(own, *pub_other));
       }
       return;
@@ -219,7 +234,41 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       const int rel1 = i < VY ? rel1p + i * a.Wn : rel1c + (i - VY) * a.Wn;
       const uint32_t key = bits ? (q << rb) | uint32_t(rel1) : 0xffffffffu;
       bits &= ~(1u << i);
-      if constexpr (HEAP) {
+      if constexpr (HEAP4) {
+        if (key < root_r) {  // replace the root, sift down
+          int n = 0;
+          bool alive = true;
+          uint32_t nroot = key;
+          uint4 vv = *reinterpret_cast<const uint4*>(heap + 4);
+          uint4 g0 = *reinterpret_cast<const uint4*>(heap + 8), g1 = *reinterpret_cast<const uint4*>(heap + 12);
+          uint4 g2 = *reinterpret_cast<const uint4*>(heap + 16), g3 = *reinterpret_cast<const uint4*>(heap + 20);
+#pragma unroll
+          for (int lvl = 0; lvl < kSift4; ++lvl) {
+            const bool r01 = vv.y > vv.x, r23 = vv.w > vv.z;
+            const uint32_t m01 = max(vv.x, vv.y), m23 = max(vv.z, vv.w);
+            const bool up = m23 > m01;
+            const uint32_t big = max(m01, m23);
+            const int cb = 4 * n + 1 + (up ? (r23 ? 3 : 2) : (r01 ? 1 : 0));
+            const bool mv = alive && big > key;
+            const uint4 nv = up ? (r23 ? g3 : g2) : (r01 ? g1 : g0);
+            if (lvl + 1 < kSift4) {
+              g0 = g1 = g2 = g3 = make_uint4(0u, 0u, 0u, 0u);
+              // (each 16-byte block loaded only if it lies inside the row: blocks past the row hold no node)
+              if (mv && 16 * cb + 12 <= a.hp) g0 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 8);
+              if (mv && 16 * cb + 16 <= a.hp) g1 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 12);
+              if (mv && 16 * cb + 20 <= a.hp) g2 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 16);
+              if (mv && 16 * cb + 24 <= a.hp) g3 = *reinterpret_cast<const uint4*>(heap + 16 * cb + 20);
+            }
+            if (mv) heap[3 + n] = big;
+            if (lvl == 0) nroot = mv ? big : key;
+            n = mv ? cb : n;
+            alive = mv && 4 * cb + 1 < a.KP;
+            vv = nv;
+          }
+          heap[3 + n] = key;
+          root_r = nroot;
+        }
+      } else if constexpr (HEAP) {
         if (key < heap[1]) {  // replace the root, sift down (children of i: 2i, 2i+1)
           int h = 1;
           for (int c = 2; c <= a.KP; c = 2 * h) {
@@ -238,7 +287,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
         rt.insert(key);
       }
     }
-    const uint32_t kth = HEAP ? heap[1] : rt.r[KR - 1];
+    const uint32_t kth = HEAP4 ? root_r : HEAP ? heap[1] : rt.r[KR - 1];
     if constexpr (WS == 2) {
       *pub_own = kth;
       set_thr(min(kth, *pub_other));
@@ -443,7 +492,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       // kept slot k -> its exact (float32 d_NCC, idx) key (double-precision NCC)
       auto ncc_key = [&](int k) -> uint64_t {
         uint32_t kk;
-        if constexpr (HEAP) kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
+        if constexpr (HEAP) kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + kHB + k] : 0xffffffffu;
         else kk = k < a.KP ? scratch[j * (KR + 1) + (KR - a.KP) + k] : 0xffffffffu;  // skip 0 sentinels
         const bool have = kk != 0u && kk != 0xffffffffu;
         double nrd = 0.0, cd = 0.0, ncd = 0.0;
@@ -499,7 +548,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
           if (sl == (a.K - 1) / 32) kv = top.v[sl];
         kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
       }
-      const uint32_t klast = HEAP ? heap[(j - min(lane, RX - 1)) * a.hp + 1] : scratch[j * (KR + 1) + KR - 1];
+      const uint32_t klast = HEAP ? heap[(j - min(lane, RX - 1)) * a.hp + kHB] : scratch[j * (KR + 1) + KR - 1];
       nrq = __shfl_sync(0xffffffffu, nrq, 0);
       if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf && nrq > 0.0) {
         const double fK = -double(unord_f32(uint32_t(kv >> 32)));  // exact K-th NCC (float32)
@@ -673,7 +722,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       uint64_t key = kKeyInf;
       uint32_t kk;
       if constexpr (HEAP) {
-        kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + 1 + k] : 0xffffffffu;
+        kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + kHB + k] : 0xffffffffu;
       } else if constexpr (WS == 2) {  // lane j's register list, one key per lane by shuffles
         kk = 0xffffffffu;
 #pragma unroll
@@ -746,7 +795,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       kv = __shfl_sync(0xffffffffu, kv, (a.K - 1) % 32);
       const float nrj = __shfl_sync(0xffffffffu, nr, j);
       uint32_t klast;
-      if constexpr (HEAP) klast = heap[(j - min(lane, RX - 1)) * a.hp + 1];  // max-heap root
+      if constexpr (HEAP) klast = heap[(j - min(lane, RX - 1)) * a.hp + kHB];  // max-heap root
       else if constexpr (WS == 2) klast = __shfl_sync(0xffffffffu, rt.r[KR - 1], j);
       else klast = scratch[j * (KR + 1) + KR - 1];
       if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf) {
@@ -800,9 +849,15 @@ size_t boxf_bytes(const Geometry& g, int KR, int ws, BoxfArgs* a) {
   // heap pitch: 1-indexed heap + a padding child, = 2 (mod 4) words: 8-byte aligned rows whose
   // 64-bit child loads hit distinct bank pairs across a half-warp
   a->hp = ((g.KP + 2 + 1) & ~3) + 2;
+  if (SCBM_BOXF_HEAP4 && KR > 48) {  // 4-ary: nodes at 3 .. KP + 2, zero children and prefetch rows past them
+    // (the last internal node's children end at position 4 ((KP - 2) / 4) + 7; the sift-down guards
+    // each 16-byte prefetch block separately, so the pitch stays minimal: c3 NCC keeps 2 CTAs / SM)
+    a->hp = 4 * ((g.KP - 2) / 4) + 8;
+    if (a->hp % 8 == 0) a->hp += 4;  // = 4 (mod 8): the lanes' 16-byte loads spread over the banks
+  }
   // per warp: two staged offset groups (+ the heaps, or the output lists with WS = 1)
   a->scr = KR > 48 ? 64 * kFVY + rx * a->hp : ws == 2 ? 64 * kFVY : std::max(64 * kFVY, rx * (KR + 1));
-  const size_t region = size_t(((g.z3 ? 2 : 1) * g.C * a->PL + 1) & ~1);  // (3D: + candidate planes)
+  const size_t region = size_t(((g.z3 ? 2 : 1) * g.C * a->PL + 3) & ~3);  // (3D: + candidate planes; 16-B aligned)
   const size_t base = region + size_t(kFWarps) * ws * a->scr + (ws == 2 ? 2 * kFWarps * 32 : 0);
   // WS = 2: the per-row list areas reuse the staged region when it is large enough
   const size_t lists = size_t(kFWarps) * rx * (KR + 1);
