@@ -17,10 +17,22 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 }
 // Wait until the barrier's phase with the given parity has completed. Traps (instead of hanging
 // the GPU) if it never does.
+#ifndef SCBM_MBAR_SUSPEND
+#define SCBM_MBAR_SUSPEND 1  // try_wait with a suspend-time hint: the waiting warp sleeps in hardware
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   long long spins = 0;
   while (true) {
+#if SCBM_MBAR_SUSPEND
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "n"(1000000)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -28,6 +40,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+#endif
     if (done) return;
     if (++spins > (1ll << 26)) __trap();
   }
@@ -47,8 +60,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, u
         : "memory");
     if (done) return;
     if (++spins > (1ll << 24)) __trap();
+#if SCBM_MBAR_SUSPEND
+    (void)ns;
+    mbar_wait(bar, parity);  // (the suspend-time hint replaces the nanosleep back-off)
+    return;
+#else
     __nanosleep(ns);
     ns = ns < 256 ? 2 * ns : ns;  // back off: a waiting warp takes fewer issue slots
+#endif
   }
 }
 __device__ __forceinline__ void fence_barrier_init() {
