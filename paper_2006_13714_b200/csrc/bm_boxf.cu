@@ -40,6 +40,9 @@ constexpr int kFWarps = 8;
 #ifndef SCBM_BOXF_HEAP4
 #define SCBM_BOXF_HEAP4 1  // K + m > 48: a 4-ary heap with the root in a register (0: the binary heap)
 #endif
+#ifndef SCBM_BOXF_A5HALVES
+#define SCBM_BOXF_A5HALVES 1  // WS = 2: both warps of a reference row share a5 (half the references each)
+#endif
 #ifndef SCBM_BOXF_A5SPLIT
 #define SCBM_BOXF_A5SPLIT 1  // a5: the short last key slot re-scored by several lanes per key
 #endif
@@ -460,8 +463,39 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
         }
       }
     }
-    if (hh == 1 || !wact) return;
+    if constexpr (!SCBM_BOXF_A5HALVES) {
+      if (hh == 1 || !wact) return;
+    }
   }
+  // WS = 2, A5HALVES: both warps of a reference row run a5, the first on references [0, nsplit),
+  // the second on [nsplit, nref); the first hands the merged lists of the second half over through
+  // the two warps' scratch (keys < kTS: the second warp's, [j'][25]; the rest: the first warp's,
+  // [j'][KR - kTS + 1]; odd pitches: conflict-free row reads)
+  constexpr int kTS = 24;
+  constexpr int kP1 = KR > kTS ? KR - kTS + 1 : 1;
+  const int nref_all = min(RX, a.nx - ix_first);
+  const int nsplit = (WS == 2 && SCBM_BOXF_A5HALVES) ? (nref_all + 1) / 2 : nref_all;
+  uint32_t* const tb0 = scr0 + (kFWarps + wr) * a.scr;
+  uint32_t* const tb1 = scr0 + wr * a.scr;
+  if constexpr (WS == 2 && SCBM_BOXF_A5HALVES) {
+    __syncwarp();
+    if (hh == 0 && wact && lane >= nsplit && lane < nref_all) {
+      const int jq = lane - nsplit;
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        if (k < kTS) tb0[jq * (kTS + 1) + k] = rt.r[k];
+        else tb1[jq * kP1 + (k - kTS)] = rt.r[k];
+      }
+    }
+    __syncthreads();
+    if (!wact) return;
+  }
+  // key k of reference j taken from the hand-over buffers (second warp, WS = 2)
+  auto handed = [&](int j, int k) -> uint32_t {
+    const int jq = j - nsplit;
+    return k < kTS ? tb0[jq * (kTS + 1) + k] : tb1[jq * kP1 + (k - kTS)];
+  };
+  (void)handed;
 
   // ---- a5 + a6: stage each reference's KP keys (register lists; the heaps already are in shared
   // memory), then per reference (warp-cooperative) re-score them by direct differences from the
@@ -643,7 +677,8 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
     }
     return;
   } else {
-  for (int j = 0; j < nref; ++j) {
+  const int j_lo = (WS == 2 && hh == 1) ? nsplit : 0, j_hi = (WS == 2 && hh == 0) ? nsplit : nref;
+  for (int j = j_lo; j < j_hi; ++j) {
     const int rxj = (ix_first + j) * S;
     const float nrj_a5 = __shfl_sync(0xffffffffu, nr, j);  // ||X_i||^2 (centred) of reference j
     WarpTopK<NJ> top;
@@ -658,10 +693,14 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
           const int kq = lane / kSplitG, part = lane % kSplitG;
           uint32_t kk = 0xffffffffu;
           if constexpr (WS == 2) {
+            if (hh == 0 || !SCBM_BOXF_A5HALVES) {
 #pragma unroll
-            for (int q = 0; q < kN1; ++q) {
-              const uint32_t v = __shfl_sync(0xffffffffu, rt.r[sl * 32 + q], j);
-              if (kq == q) kk = v;
+              for (int q = 0; q < kN1; ++q) {
+                const uint32_t v = __shfl_sync(0xffffffffu, rt.r[sl * 32 + q], j);
+                if (kq == q) kk = v;
+              }
+            } else if (kq < kN1) {
+              kk = handed(j, sl * 32 + kq);
             }
           } else {
             if (kq < kN1) kk = scratch[j * (KR + 1) + sl * 32 + kq];
@@ -725,12 +764,16 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
         kk = k < a.KP ? heap[(j - min(lane, RX - 1)) * a.hp + kHB + k] : 0xffffffffu;
       } else if constexpr (WS == 2) {  // lane j's register list, one key per lane by shuffles
         kk = 0xffffffffu;
+        if (hh == 0 || !SCBM_BOXF_A5HALVES) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          if (sl * 32 + q < KR) {
-            const uint32_t v = __shfl_sync(0xffffffffu, rt.r[sl * 32 + q < KR ? sl * 32 + q : 0], j);
-            if (lane == q) kk = v;
+          for (int q = 0; q < 32; ++q) {
+            if (sl * 32 + q < KR) {
+              const uint32_t v = __shfl_sync(0xffffffffu, rt.r[sl * 32 + q < KR ? sl * 32 + q : 0], j);
+              if (lane == q) kk = v;
+            }
           }
+        } else if (k < KR) {  // (the second warp: from the hand-over buffers)
+          kk = handed(j, k);
         }
       } else {
         kk = k < KR ? scratch[j * (KR + 1) + k] : 0xffffffffu;
@@ -796,7 +839,8 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
       const float nrj = __shfl_sync(0xffffffffu, nr, j);
       uint32_t klast;
       if constexpr (HEAP) klast = heap[(j - min(lane, RX - 1)) * a.hp + kHB];  // max-heap root
-      else if constexpr (WS == 2) klast = __shfl_sync(0xffffffffu, rt.r[KR - 1], j);
+      else if constexpr (WS == 2) klast = (hh == 0 || !SCBM_BOXF_A5HALVES) ? __shfl_sync(0xffffffffu, rt.r[KR - 1], j)
+                                                                           : handed(j, KR - 1);
       else klast = scratch[j * (KR + 1) + KR - 1];
       if (lane == 0 && klast != 0u && klast != 0xffffffffu && kv != kKeyInf) {
         const float dK = __uint_as_float(uint32_t(kv >> 32));
