@@ -75,6 +75,10 @@ __device__ __forceinline__ int centre_out(int k) { return (k & 1) ? ((k + 1) >> 
                          // slack yields a saturated no-op key): no clamp, no per-lane no-op select
                          // (90 instead of 96 instructions per round; c5 8.73 -> 8.65 ms)
 #endif
+#ifndef SCBM_BOX_SORTFILL
+#define SCBM_BOX_SORTFILL 1  // the first flush with survivors builds the (empty) lists by a bitonic sort
+                             // (c5 8.64 -> 8.45 ms: the first flush was 14 % of all survivor rounds)
+#endif
 #ifndef SCBM_BOX_MINB
 #define SCBM_BOX_MINB 2  // CTAs per SM the register allocation targets (tuning builds override)
 #endif
@@ -200,6 +204,7 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
     scratch[kQS + lane] = 0x80000000u;
   }
 
+  bool fresh = true;  // SORTFILL: no survivor inserted yet (warp-uniform)
   const int b0 = (0 - lo) / VY;  // dy block holding dy = 0
   const int span = max(-lo, hi);
   const int nt = TEMP ? 2 * a.T + 1 : 1;
@@ -264,6 +269,42 @@ __global__ void __launch_bounds__(kBoxWarps * 32, NY == 1 ? 3 : SCBM_BOX_MINB) b
             const uint32_t s1 = s0 + 4u * uint32_t(kQS);
             const int relA = rel0p - Wn, relB = rel0c - VY * Wn - Wn;
             const uint32_t dthr0 = uint32_t(thr[0] + nr[0]), dthr1 = uint32_t(thr[1] + nr[1]);
+            if (SCBM_BOX_SORTFILL && fresh) {
+              // the lists are still empty: build them from the staged keys with a bitonic sort of
+              // the first KR keys (absent ones = ~0) and insert the rest (c5: a 16-key network +
+              // 6 insertions per list instead of 22 survivor rounds)
+              const int relB0 = rel0c - VY * Wn;
+              auto fill = [&](RegTopK32<KR>& L, unsigned pb, uint32_t sb, uint32_t dthr) {
+                auto key_at = [&](int i) -> uint32_t {
+                  uint32_t d;
+                  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sb + 128u * uint32_t(i + 1)));
+                  const uint32_t k = (min(dthr - d, dsat) << rbits) | uint32_t((i < VY ? rel0p : relB0) + i * Wn);
+                  return ((pb >> i) & 1u) ? k : 0xffffffffu;
+                };
+#pragma unroll
+                for (int i = 0; i < KR; ++i) L.r[i] = i < 2 * VY ? key_at(i) : 0xffffffffu;
+#pragma unroll
+                for (int k = 2; k <= KR; k <<= 1)
+#pragma unroll
+                  for (int jj = k >> 1; jj > 0; jj >>= 1)
+#pragma unroll
+                    for (int i = 0; i < KR; ++i) {
+                      const int l = i ^ jj;
+                      if (l > i) {
+                        const uint32_t lo_ = min(L.r[i], L.r[l]), hi_ = max(L.r[i], L.r[l]);
+                        const bool asc = (i & k) == 0;
+                        L.r[i] = asc ? lo_ : hi_;
+                        L.r[l] = asc ? hi_ : lo_;
+                      }
+                    }
+#pragma unroll
+                for (int i = KR; i < 2 * VY; ++i) L.insert(key_at(i));
+              };
+              fill(rt[0], pend[0], s0, dthr0);
+              fill(rt[1], pend[1], s1, dthr1);
+              fresh = false;
+              b0 = b1 = 1u;  // (every survivor is in)
+            }
             while (__any_sync(0xffffffffu, (b0 | b1) > 1u)) {
               uint32_t p0, p1, d0, d1;
               asm("bfind.u32 %0, %1;" : "=r"(p0) : "r"(b0));
