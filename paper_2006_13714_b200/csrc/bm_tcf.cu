@@ -70,6 +70,10 @@ constexpr int kBinBase = (127 - 6) << 4;  // BOUND histogram: bin 0 = float bits
                          // 4: a 4-ary heap (three levels for K + m <= 85; the children of the four
                          //    children loaded one level ahead): c3 3.33 -> 3.13 ms against 2
 #endif
+#ifndef SCBM_TCF_FILLUP
+#define SCBM_TCF_FILLUP 0  // 1: 4-ary heap, while not full, keys are appended and sifted up (a divergent loop:
+                           // measured 3.25 ms on c3 against 3.13 with fixed-depth sift-downs only; off)
+#endif
 #ifndef SCBM_TCF_A5ILP
 #define SCBM_TCF_A5ILP 1  // a5: a lane's 4 kept keys re-scored in one interleaved loop
 #endif
@@ -335,6 +339,8 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
       heap_init();
     }
     uint32_t root_r = 0xffffffffu;  // heap[1] (SCBM_TCF_SIFT)
+    constexpr bool kFillUp = SCBM_TCF_FILLUP && SCBM_TCF_SIFT == 4;
+    int hcnt = kFillUp ? 0 : 1 << 30;  // FILLUP: keys in the heap while it fills
     (void)root_r;
     if constexpr (DENSE) {
       if (valid)
@@ -364,6 +370,7 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
         }
         __syncwarp();
         heap_init();
+        if constexpr (kFillUp) hcnt = 0;
         if (bsel < 255) {  // (bin 255 also holds everything >= 2^10: no bound)
           const float edge = __uint_as_float(uint32_t(bsel + kBinBase + 1) << 19);  // the bin's upper edge
           thr = fmaf(edge, 1.0f + 1e-6f, -nr) + 1e-30f;  // (d' = d - ||X_i||^2; rounding margin)
@@ -469,7 +476,21 @@ __global__ void __launch_bounds__(kTfThreads, 2) bm_tcf_kernel(TcfArgs a) {
             i = 31 - __clz(bits | 1u);
             asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d) : "r"(sc_s + 4u * uint32_t(i)));
             if constexpr (HEAP) {
-              if (key < root_r) {  // replace the root, sift down (children of h: 2h, 2h+1)
+              if (kFillUp && key < root_r && hcnt < a.KP) {
+                // the heap is not full yet: the key goes to the next free node and sifts UP (a few
+                // steps on average) instead of replacing the (+inf) root and sinking through every
+                // level; the root register becomes the real maximum once the KP-th key is in
+                int n = hcnt++;
+                while (n > 0) {
+                  const int p = (n - 1) >> 2;
+                  const uint32_t pv = heap[3 + p];
+                  if (pv >= key) break;
+                  heap[3 + n] = pv;
+                  n = p;
+                }
+                heap[3 + n] = key;
+                if (hcnt == a.KP) root_r = heap[3];
+              } else if (key < root_r) {  // replace the root, sift down (children of h: 2h, 2h+1)
                 int h = 1;
                 bool alive = true;
                 uint32_t nroot = key;
