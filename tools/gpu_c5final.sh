@@ -1,5 +1,5 @@
 # c5 evidence after the sentinel rounds: bench (default line), gather paths at N = 1, launch list, ncu capture
-O=gpurun_out/c5f; mkdir -p $O; rm -f $O/*
+O=gpurun_out/c5g; mkdir -p $O; rm -f $O/*
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke=$?" >> $O/status.txt
 timeout 900 python bench.py --steps 10 --warmup 3 > $O/bench_c5.log 2>&1; echo "bench_c5=$?" >> $O/status.txt
 timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu --gather > $O/bench_gather1.log 2>&1; echo "gather1=$?" >> $O/status.txt
@@ -14,3 +14,4 @@ ncu -i /tmp/prof_c5.ncu-rep --page details --csv > $O/prof_c5_details.csv 2>/dev
 ncu -i /tmp/prof_c5.ncu-rep --page source --csv --print-source cuda,sass > $O/prof_c5_src.csv 2>/dev/null
 gzip -f $O/prof_c5_src.csv
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 -x -k "box or c5 or c1 or temporal or packed or peer or ncc" > $O/pytest.log 2>&1; echo "pytest=$?" >> $O/status.txt
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1200 > $O/pytest_gpu_all.log 2>&1; echo "pytest_all=$?" >> $O/status.txt
