@@ -25,6 +25,7 @@
 // K (BASELINE.json north_star tolerance): a true top-K candidate can only
 // be lost if more than KP - K = 8 others lie within one quantum (~1e-4 relative) of it.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "ncc.cuh"
@@ -55,6 +56,8 @@ struct BoxfArgs {
   int32_t* idx_out;   // [F][band refs][K]
   float* dist_out;    // L2: d; NCC: d_NCC = -NCC
   int H, W, C, Wn, K, KP, lo, hi, nx, iy_begin, iy_end, tiles_x;
+  int rows;          // reference rows per CTA (1 .. kFWarps; warps wr >= rows sit idle): the tile height
+                     // that fills the last wave (boxf_rows)
   int RH, RWp, PL;  // staged region rows, row pitch (floats), floats per channel plane
   int nblk;         // dy blocks of VY offsets
   int scr;          // per-warp scratch words (survivor staging [+ output staging | + heaps])
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   extern __shared__ __align__(16) float smf[];
   const int f = blockIdx.y;
   const int ty = blockIdx.x / a.tiles_x, tx = blockIdx.x - ty * a.tiles_x;
-  const int iy_first = a.iy_begin + ty * kFWarps;
+  const int iy_first = a.iy_begin + ty * a.rows;
   const int ix_first = tx * RX;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wr = warp % kFWarps, hh = warp / kFWarps;  // reference row of the warp, window half (WS = 2)
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kFWarps * 32 * WS, WS == 1 ? 2 : 1) bm_boxf_ke
   __syncthreads();
 
   const int iy0 = iy_first + wr;
-  const bool wact = iy0 < a.iy_end;  // warp-uniform
+  const bool wact = wr < a.rows && iy0 < a.iy_end;  // warp-uniform
   if (WS == 1 && !Z3 && !wact) return;  // (Z3: every warp joins the restaging barriers)
   const int ix = ix_first + lane;
   const bool lane_ok = lane < RX && ix < a.nx;
@@ -927,7 +930,7 @@ int boxf_kr(const Geometry& g) {
 
 template <int S, int BK, int KR, bool NCC = false, typename TIN = float>
 cudaError_t launch_boxf_t(const BoxfArgs& a, int F, size_t smem, cudaStream_t st, int ws = 1, bool z3 = false) {
-  const int tiles_y = (a.iy_end - a.iy_begin + kFWarps - 1) / kFWarps;
+  const int tiles_y = (a.iy_end - a.iy_begin + a.rows - 1) / a.rows;
   auto k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN> : bm_boxf_kernel<S, BK, kFVY, KR, false, NCC, TIN>;
   if constexpr (KR <= 48 && !NCC) {
     if (ws == 2) k = a.C == 1 ? bm_boxf_kernel<S, BK, kFVY, KR, true, NCC, TIN, 2>
@@ -963,6 +966,41 @@ bool boxf_supported(const Geometry& g) {
 }
 
 namespace {
+// Tile height (reference rows per CTA): the grid is tiles_x x ceil(rows_in_band / R) CTAs per
+// frame, each of which keeps one SM slot busy for a time ~ R rows; fewer rows than kFWarps pay off
+// where the full-height grid leaves most of its last wave empty (c4: 384 CTAs at 1 CTA / SM =
+// 2.6 waves -> R = 7: 444 CTAs = 3 full waves of 7/8 the work each). Cost model: waves x R.
+int boxf_rows(long long tiles_x, long long band_rows, long long F, int per_sm) {
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      n_sm = v;
+    else
+      n_sm = 148;
+  }
+  const long long slots = (long long)n_sm * per_sm;
+  auto cost = [&](int r) {
+    const long long units = tiles_x * ((band_rows + r - 1) / r) * F;
+    return (double)((units + slots - 1) / slots) * r;
+  };
+  // SC_BM_BOXF_ROWS=r (1 .. kFWarps) forces the tile height (A/B timing, tests of short tiles)
+  static const int forced = [] {
+    const char* e = getenv("SC_BM_BOXF_ROWS");
+    const int v = e ? atoi(e) : 0;
+    return v >= 1 && v <= kFWarps ? v : 0;
+  }();
+  if (forced) return forced;
+  int best = kFWarps;
+  double best_c = cost(kFWarps);
+  // one row fewer only, and only for a >= 8 % modelled gain: the model counts work, but an SM
+  // with fewer active warps also issues less (measured: c4 R = 7 2.446 -> 2.398 ms for 12.5 %
+  // modelled; m1 R = 5, 6 % modelled, 2.10 -> 2.29 ms)
+  const double c = cost(kFWarps - 1);
+  if (c < best_c * 0.92) best = kFWarps - 1;
+  return best;
+}
+
 cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, int iy_begin, int iy_end,
                                int32_t* idx_out, void* dist_out, cudaStream_t st, int64_t* launches) {
   const Geometry& g = p.g;
@@ -986,6 +1024,11 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
   const int kr = boxf_kr(g);  // the layout and the instantiation use the same list size
   const size_t smem = boxf_layout(g, kr, &a);
   if (launches) *launches += 1;
+  const int ws = g.metric == SC_METRIC_NCC ? 1 : boxf_ws(g, kr);
+  // CTAs per SM: 16-warp window-split CTAs (128 registers) take a whole SM; 8-warp CTAs two when
+  // their shared memory fits twice
+  const int per_sm = ws == 2 ? 1 : (2 * (smem + 1024) <= 228 * 1024 ? 2 : 1);
+  a.rows = boxf_rows(a.tiles_x, iy_end - iy_begin, F, per_sm);
   if (g.metric == SC_METRIC_NCC) {  // uint8: K + m <= 32, exact re-rank; float: lists up to 80
 #define SCBM_NCC_CASE(S_, B_)                                                                          \
   if (g.s == S_ && g.b == B_) {                                                                        \
@@ -1007,7 +1050,6 @@ cudaError_t launch_boxf_kernel(const sc_bm_plan_s& p, const void* imgs, int F, i
 #undef SCBM_NCC_CASE
     return cudaErrorInvalidValue;
   }
-  const int ws = boxf_ws(g, kr);
   const bool z3 = g.z3 != 0;
 #define SCBM_BOXF_CASE(S_, B_)                                                    \
   if (g.s == S_ && g.b == B_) {                                                   \

@@ -1281,3 +1281,24 @@ def test_bm3d_partial_reference_rows_and_guard():
         oi, od = oracle.bm3d(vol, d, b, s, sz, Wn, c, K)
         check_f32_3d(vol, d, b, s, sz, Wn, c, K, gi_full[:nz].cpu().numpy(), gd_full[:nz].cpu().numpy(), oi, od,
                      f"bm3d guard {(P, d, H, W)}")
+
+
+# ------------------------------------------------------------------ float box kernel tile heights
+@pytest.mark.parametrize("rows", [3, 7])
+def test_boxf_forced_tile_heights(rows):
+    """The float box kernel's tile height (reference rows per CTA, chosen per launch to fill the
+    last wave: bm_boxf.cu boxf_rows) forced to `rows` through SC_BM_BOXF_ROWS: the boxf parity
+    cases (random sweep, ties, c2 whole image, NCC sweep, 3D search) rerun in a child process
+    (the library reads the variable once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SC_BM_BOXF_ROWS=str(rows))
+    sel = ("boxf_random_sweep or boxf_ties or c2_full or ncc_random_sweep or bm3d_matches_oracle "
+           "or bm3d_translated")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel,
+                        os.path.join(root, "tests", "test_gpu_parity.py")],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
