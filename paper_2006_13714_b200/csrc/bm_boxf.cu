@@ -991,6 +991,9 @@ int boxf_rows(long long tiles_x, long long band_rows, long long F, int per_sm) {
     return v >= 1 && v <= kFWarps ? v : 0;
   }();
   if (forced) return forced;
+  // two CTAs per SM: a part-filled last wave is not idle time (its CTAs run alone on their SMs,
+  // faster) -- the model does not hold there (m1, 2 CTAs / SM: R = 7 2.10 -> 2.30 ms)
+  if (per_sm != 1) return kFWarps;
   int best = kFWarps;
   double best_c = cost(kFWarps);
   // one row fewer only, and only for a >= 8 % modelled gain: the model counts work, but an SM
